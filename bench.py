@@ -1,0 +1,558 @@
+#!/usr/bin/env python
+"""bt200 benchmark -- BASELINE.json metric "CP-ALS MTTKRP GFLOP/s & ST-HOSVD
+time ...; % FP64/HBM roofline".
+
+Headline workload (config C5, the largest config that fits one B200):
+CP-ALS at rank 64 for 10 sweeps (tol 0: exactly 10) on the 4096x4096x1024
+fp64 tensor [[A0,B0,C0]] + 1e-4 noise (seed 3, init seed 1003), built on the
+GPU.  One *step* = one full ``cp_als(X, 64, max_iters=10, tol=0.0)`` call
+(fro norm, 10 sweeps, fits, final KruskalRep).  ``value`` = reference-
+equivalent MTTKRP GFLOP/s = 10 sweeps x 3 modes x 2*I*J*K*R / step time
+(the reference's ``unfold @ khatri_rao`` count, decomp.py:385-387).  The
+tensor (137 GB) is far larger than L2, so no flush is needed between steps.
+
+Also reported: roofline of the dominant kernel (the P = X x3 C DMMA GEMM,
+timed live with CUDA events inside the library), the e2e number through the
+public API with host buffers, the CPU reference (oracle port, all host
+threads) on a bounded mode-3 slab, clocks, launch counts, and secondary
+configs (C3 ST-HOSVD+HOOI time, C1/C2/C4 pipelines, gather stand-in GB/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+I_, J_, K_, R_, ITERS = 4096, 4096, 1024, 64, 10
+CPU_SLAB = 8          # mode-3 rows in the bounded CPU sample
+REF_SLAB = 4          # rows per step for --impl reference
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="bt200", choices=["bt200", "reference"])
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--small", action="store_true", help="reduced C5 (smoke runs)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_index=0):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.dev = dev_index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+
+    def summary(self):
+        import numpy as np
+
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# FP64 peak (DMMA) -- the roofline denominator MEASURED_PEAKS.json lacks
+# ---------------------------------------------------------------------------
+
+
+def fp64_peaks(torch):
+    import ctypes as C
+
+    from paper_2105_01170_b200 import _native as N
+
+    lib = N.load()
+    sink = torch.zeros(8192, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    out = {}
+    for name, fn in (("dmma", lib.bt_peak_dmma), ("dfma", lib.bt_peak_dfma)):
+        fl = C.c_double()
+        fn(2000, 148 * 8, 256, sink.data_ptr(), C.byref(fl), st)
+        torch.cuda.synchronize()
+        best = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn(40000, 148 * 8, 256, sink.data_ptr(), C.byref(fl), st)
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, fl.value / e0.elapsed_time(e1) / 1e9)
+        out[name] = best
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle port of decomp.py:344-410, all host threads)
+# ---------------------------------------------------------------------------
+
+
+def cpu_slab_sweep(x_slab, init, threads):
+    from oracle import port
+
+    t0 = time.perf_counter()
+    port.cp_als(x_slab, init[0].shape[1], max_iters=1, tol=0.0,
+                init=lambda _t, _r: [f.copy() for f in init])
+    return time.perf_counter() - t0
+
+
+def build_slab_host(torch, k_rows):
+    from paper_2105_01170_b200 import configs
+
+    xs = configs.c5_build(I_, J_, K_, R_, k_slab=(0, k_rows))
+    host = xs.cpu().numpy()
+    del xs
+    torch.cuda.empty_cache()
+    return host
+
+
+def run_reference(args, rank, world):
+    nproc = os.cpu_count() or 1
+    if rank != 0:
+        return
+    import numpy as np
+
+    from paper_2105_01170_b200 import configs
+
+    if args.small:
+        global I_, J_, K_
+        I_, J_, K_ = 512, 512, 128
+    from oracle import configs as oc
+
+    host = oc.c5_tensor(I_, J_, K_, R_, k_slab=(0, REF_SLAB))   # numpy generator, untimed
+    init = configs.normal_init((I_, J_, K_), R_, 1003)
+    init = [init[0], init[1], init[2][:REF_SLAB].copy()]
+    for _ in range(args.warmup):
+        cpu_slab_sweep(host, init, nproc)
+    times = [cpu_slab_sweep(host, init, nproc) for _ in range(args.steps)]
+    per = float(np.mean(times))
+    gflops = 6 * I_ * J_ * REF_SLAB * R_ / per / 1e9
+    line = {
+        "metric": "CP-ALS MTTKRP GFLOP/s (reference-equivalent 6*I*J*K*R per sweep)",
+        "value": gflops, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"C5 CP-ALS R={R_} one sweep on a {I_}x{J_}x{REF_SLAB} mode-3 slab "
+                               f"of the {I_}x{J_}x{K_} tensor (bounded CPU sample)"},
+        "cpu_baseline": {"value": gflops, "unit": "GFLOP/s", "cores": nproc, "kind": "port",
+                         "sample": f"1 ALS sweep on a {I_}x{J_}x{REF_SLAB} slab per step; "
+                                   "numpy restatement of decomp.py:344-410 (oracle/port.py), "
+                                   "OpenBLAS threads = all cores, einsum fit single-threaded"},
+        "e2e": {"value": gflops, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# bt200 arm
+# ---------------------------------------------------------------------------
+
+
+def timed(torch, fn, steps, warmup):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def extras_run(torch, budget_s=240.0):
+    """Secondary configs, each device resident, timed with CUDA events."""
+    import numpy as np
+
+    import paper_2105_01170_b200 as bt
+    from paper_2105_01170_b200 import configs, decomp, multilevel, reconstruct
+
+    out = {}
+    t_start = time.time()
+
+    def left():
+        return budget_s - (time.time() - t_start)
+
+    # C3: ST-HOSVD (shared 1/3) + 5 HOOI sweeps -> (64, 32, 64), SPSD blocks
+    try:
+        pat3, t3 = configs.c3_build()
+        torch.cuda.synchronize()
+
+        def c3():
+            rep = decomp.st_hosvd(t3, [64, 32, 64], shared=(1, 3))
+            return decomp.hooi(t3, rep, 5, shared=(1, 3))
+
+        ms = timed(torch, c3, 1, 1)
+        rep = c3()
+        ms_st = timed(torch, lambda: decomp.st_hosvd(t3, [64, 32, 64], shared=(1, 3)), 1, 0)
+        out["c3_st_hosvd_ms"] = ms_st
+        out["c3_st_hosvd_plus_5_hooi_ms"] = ms
+        from paper_2105_01170_b200.tensor import fro_norm_dev
+
+        out["c3_core_norm_ratio"] = fro_norm_dev(rep.core) / fro_norm_dev(t3)
+        del t3, rep
+        torch.cuda.empty_cache()
+    except Exception as exc:  # pragma: no cover - reported, not fatal
+        out["c3_error"] = repr(exc)[:300]
+    # C1 full pipeline
+    if left() > 0:
+        try:
+            pat, a = configs.c1_matrix()
+            init = configs.normal_init((32, 32, 32), 8, 0)
+            rhs = torch.from_numpy(np.random.default_rng(1001).standard_normal((1024, 16))).cuda()
+
+            def c1():
+                t = bt.mat_to_tensor(a, pat)
+                saved = decomp._cp_init
+                decomp._cp_init = lambda _t, _r: [torch.from_numpy(f).cuda() for f in init]
+                try:
+                    res = decomp.cp_als(t, 8, 50, 0.0)
+                finally:
+                    decomp._cp_init = saved
+                ks = reconstruct.kron_sum_from_kruskal(res.rep, pat)
+                err = reconstruct.error_fro(a, ks)
+                y = reconstruct.matvec(ks, rhs)
+                return res, err, y
+
+            out["c1_pipeline_ms"] = timed(torch, c1, 3, 2)
+            res, err, _ = c1()
+            out["c1_fit"] = res.fit
+            out["c1_relerr"] = err
+        except Exception as exc:  # pragma: no cover
+            out["c1_error"] = repr(exc)[:300]
+    # C4: CP R=16 x 30 on the 255^3 weighted PSF + multilevel matvec on 32 volumes
+    if left() > 0:
+        try:
+            x, mlp = multilevel.psf_weighted_tensor(torch.from_numpy(configs.c4_psf()).cuda(),
+                                                    grid=128)
+            x3 = x.reshape(255, 255, 255)
+            init = configs.normal_init((255, 255, 255), 16, 2)
+
+            def c4cp():
+                saved = decomp._cp_init
+                decomp._cp_init = lambda _t, _r: [torch.from_numpy(f).cuda() for f in init]
+                try:
+                    return decomp.cp_als(x3, 16, 30, 0.0)
+                finally:
+                    decomp._cp_init = saved
+
+            out["c4_cp_ms"] = timed(torch, c4cp, 2, 1)
+            res = c4cp()
+            out["c4_fit"] = res.fit
+            terms = multilevel.ml_kron_sum_from_kruskal(res.rep, mlp)
+            stacks = multilevel.stack_level_mats(terms)
+            vols = torch.from_numpy(np.random.default_rng(1004).standard_normal((128**3, 32))).cuda()
+            ms = timed(torch, lambda: multilevel.ml_matvec(terms, vols, stacks), 2, 1)
+            out["c4_matvec32_ms"] = ms
+            out["c4_matvec_tflops"] = 16 * 32 * 3 * 2 * 128**4 / ms / 1e9
+            del vols
+            torch.cuda.empty_cache()
+        except Exception as exc:  # pragma: no cover
+            out["c4_error"] = repr(exc)[:300]
+    # C2: HOSVD (32, 400, 32) of the weighted Hankel tensor + BLR matvec on 64 RHS
+    if left() > 0:
+        try:
+            params = configs.c2_markov()
+            pat2, t2 = configs.c2_build(params)
+
+            def c2():
+                return decomp.hosvd(t2, [32, 400, 32])
+
+            out["c2_hosvd_ms"] = timed(torch, c2, 1, 1)
+            rep = c2()
+            blr = reconstruct.blr_from_tucker(rep, pat2)
+            rhs = torch.from_numpy(np.random.default_rng(1002).standard_normal((32768, 64))).cuda()
+            ms = timed(torch, lambda: reconstruct.matvec(blr, rhs), 2, 1)
+            out["c2_matvec64_ms"] = ms
+            out["c2_matvec_tflops"] = 64 * reconstruct.flops_blr(pat2, 32, 32) / ms / 1e9
+        except Exception as exc:  # pragma: no cover
+            out["c2_error"] = repr(exc)[:300]
+    # gather / scatter stand-in (A 32768^2 = 8.6 GB)
+    if left() > 0:
+        try:
+            patg, blocks = configs.gather_standin()
+            a = bt.struct_assemble(patg, torch.from_numpy(blocks).cuda())
+            del blocks
+            ms_g = timed(torch, lambda: bt.mat_to_tensor(a, patg), 3, 1)
+            t = bt.mat_to_tensor(a, patg)
+            ms_s = timed(torch, lambda: bt.tensor_to_mat(t, patg), 3, 1)
+            nbytes = a.numel() * 8 + t.numel() * 8
+            out["gather_standin_ms"] = ms_g
+            out["gather_standin_gbs"] = nbytes / ms_g / 1e6
+            out["scatter_standin_ms"] = ms_s
+            out["scatter_standin_gbs"] = nbytes / ms_s / 1e6
+            del a, t
+            torch.cuda.empty_cache()
+        except Exception as exc:  # pragma: no cover
+            out["gather_error"] = repr(exc)[:300]
+    return out
+
+
+def run_bt200(args, rank, world):
+    import numpy as np
+    import torch
+
+    import paper_2105_01170_b200 as bt
+    from paper_2105_01170_b200 import _dev, configs, decomp
+    from paper_2105_01170_b200 import _native as N
+
+    global I_, J_, K_
+    if args.small:
+        I_, J_, K_ = 512, 512, 128
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    lib = N.load()
+    peaks = fp64_peaks(torch)
+    log(f"[bench] fp64 peaks (TFLOP/s): {peaks}")
+
+    x = configs.c5_build(I_, J_, K_, R_)
+    init = configs.normal_init((I_, J_, K_), R_, 1003)
+    init_dev = [torch.from_numpy(f).cuda() for f in init]
+    f = [torch.empty_like(v) for v in init_dev]
+    lam = torch.empty(R_, dtype=torch.float64, device="cuda")
+    from paper_2105_01170_b200.decomp import cp_als_device
+    pb_ws = None
+    phase = [0.0] * 4
+    hist_holder = {}
+
+    def step():
+        for k in range(3):
+            f[k].copy_(init_dev[k])
+        hist, n_it, conv = cp_als_device(x, R_, f, lam, ITERS, 0.0, "auto", 0.0, ws_holder(),
+                                         phase_ms=phase)
+        hist_holder["h"] = hist
+
+    ws_cache = {}
+
+    def ws_holder():
+        if "ws" not in ws_cache:
+            import ctypes as C
+
+            pb = N.CpProblem(_dev.ptr(x), I_, J_, K_, R_, 0.0)
+            ws_cache["ws"] = _dev.workspace(lib.bt_cp_als_ws_bytes(C.byref(pb)))
+        return ws_cache["ws"]
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    phase_tot = [0.0] * 4
+    l0 = lib.bt_launch_count()
+    with Clocks(int(os.environ.get("LOCAL_RANK", 0))) as clk:
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            step()
+            phase_tot = [a + b for a, b in zip(phase_tot, phase)]
+        e1.record()
+        torch.cuda.synchronize()
+    launches = (lib.bt_launch_count() - l0) / args.steps
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    ref_flops = ITERS * 6.0 * I_ * J_ * K_ * R_
+    value = world * ref_flops / (ms / 1e3) / 1e9
+    tree_ms = phase_tot[0] / (args.steps * ITERS)
+    mode3_ms = phase_tot[2] / (args.steps * ITERS)
+    achieved = 2.0 * I_ * J_ * K_ * R_ / (tree_ms / 1e3) / 1e12
+    peak = peaks["dmma"] / 1e3
+    fit = hist_holder["h"][-1]
+    log(f"[bench] C5 step {ms:.1f} ms, tree {tree_ms:.2f} ms, mode2 {phase_tot[1] / (args.steps * ITERS):.2f} ms,"
+        f" mode3 {mode3_ms:.2f} ms, solves+fit {phase_tot[3] / (args.steps * ITERS):.2f} ms, fit {fit}")
+    result = {
+        "metric": "CP-ALS MTTKRP GFLOP/s (reference-equivalent 6*I*J*K*R per sweep)",
+        "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"C5: cp_als(X {I_}x{J_}x{K_} fp64 = [[A0,B0,C0]] + 1e-4 noise, "
+                               f"R={R_}, max_iters={ITERS}, tol=0) per step; init seed 1003",
+                   "global_batch": 1, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "inputs (137 GB) >> L2; no flush needed",
+                   "per_sweep_ms": ms / ITERS, "final_fit": fit,
+                   "executed_mttkrp_flops_per_sweep": 4.0 * I_ * J_ * K_ * R_,
+                   "phase_ms_per_sweep": {"p_tree": tree_ms,
+                                          "mode2": phase_tot[1] / (args.steps * ITERS),
+                                          "mode3": mode3_ms,
+                                          "solves_fit": phase_tot[3] / (args.steps * ITERS)}},
+        "roofline": {"bound": "tensor", "kernel": "tree_p_kernel (P = X x3 C, DMMA)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "peak_source": "measured in this run: DMMA.8x8x4 chains on all SMs "
+                                    "(MEASURED_PEAKS.json has no FP64 figure)",
+                     "mode3_gemm_achieved": 2.0 * I_ * J_ * K_ * R_ / (mode3_ms / 1e3) / 1e12},
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+        "fp64_peaks_tflops": {k: v / 1e3 for k, v in peaks.items()},
+    }
+    # ---- e2e: public API with host buffers (H2D of X + init, D2H of factors)
+    ws_cache.clear()
+    torch.cuda.empty_cache()
+    if not args.no_e2e and rank == 0:
+        try:
+            result["e2e"] = e2e_run(args, torch, x, init)
+        except Exception as exc:  # pragma: no cover
+            result["e2e"] = {"value": None, "unit": "GFLOP/s", "error": repr(exc)[:300]}
+        x = None
+    del x
+    ws_cache.clear()
+    torch.cuda.empty_cache()
+    # ---- CPU baseline (bounded slab, rank 0, N=1)
+    if not args.no_cpu and rank == 0 and world == 1:
+        try:
+            host = build_slab_host(torch, CPU_SLAB)
+            init_s = [init[0], init[1], init[2][:CPU_SLAB].copy()]
+            nproc = os.cpu_count() or 1
+            secs = cpu_slab_sweep(host, init_s, nproc)
+            full = secs * (K_ / CPU_SLAB)
+            result["cpu_baseline"] = {
+                "value": 6.0 * I_ * J_ * K_ * R_ / full / 1e9, "unit": "GFLOP/s",
+                "cores": nproc, "kind": "port",
+                "sample": f"1 ALS sweep of oracle/port.py cp_als (numpy restatement of "
+                          f"decomp.py:344-410) on a {I_}x{J_}x{CPU_SLAB} mode-3 slab: {secs:.2f} s, "
+                          f"extrapolated x{K_ // CPU_SLAB} to the full tensor; einsum fit single-threaded"}
+            del host
+        except Exception as exc:  # pragma: no cover
+            result["cpu_baseline"] = {"value": None, "error": repr(exc)[:300]}
+    if not args.no_extras and rank == 0:
+        result["extras"] = extras_run(torch)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def e2e_run(args, torch, x_dev, init):
+    """Same metric through bt.cp_als with host inputs: every step copies X
+    (and the init factors) host->device and reads the factors back."""
+    import numpy as np
+
+    from paper_2105_01170_b200 import decomp
+
+    nbytes = x_dev.numel() * 8
+    try:
+        host = torch.empty(tuple(x_dev.shape), dtype=torch.float64, pin_memory=True)
+        pinned = True
+    except RuntimeError:
+        host = torch.empty(tuple(x_dev.shape), dtype=torch.float64)
+        pinned = False
+    host.copy_(x_dev)
+    torch.cuda.synchronize()
+    x_dev.resize_(0)      # free the resident copy: the API call allocates its own
+    torch.cuda.empty_cache()
+    saved = decomp._cp_init
+    decomp._cp_init = lambda _t, _r: [f.copy() for f in init]
+    steps = max(1, min(args.steps, 2))
+    try:
+        decomp.cp_als(host, R_, ITERS, 0.0)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            res = decomp.cp_als(host, R_, ITERS, 0.0)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        wall = (time.perf_counter() - t0) / steps * 1e3
+    finally:
+        decomp._cp_init = saved
+    h2d = nbytes + sum(f.nbytes for f in init)
+    d2h = sum(np.asarray(v).nbytes for v in (res.rep.x, res.rep.y, res.rep.z)) + 8 * ITERS
+    return {"value": ITERS * 6.0 * I_ * J_ * K_ * R_ / (ms / 1e3) / 1e9, "unit": "GFLOP/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": ms, "wall_ms_per_step": wall, "steps": steps,
+            "host_buffer": "pinned" if pinned else "pageable",
+            "path": "paper_2105_01170_b200.cp_als(torch CPU tensor) -> H2D, device ALS, D2H"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
+        os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        if args.impl == "bt200":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+            dist.init_process_group("nccl")
+        else:
+            dist.init_process_group("gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_bt200(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

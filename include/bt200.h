@@ -1,0 +1,236 @@
+/*
+ * bt200 -- C-ABI of the B200-native (sm_100a) hot path behind the
+ * reference package `blockten` (arXiv 2105.01170 structure-preserving
+ * approximations).  Plain pointers, int64 extents, an explicit CUDA stream
+ * (passed as void*), caller-owned device memory and workspaces.  Every
+ * entry point returns a status code; bt_last_error() gives a thread-local
+ * message.  Bit-reproducible: no floating-point atomics anywhere.
+ *
+ * The reference has no FFI of its own: each entry point
+ * below replaces the numpy/LAPACK work inside the named reference function
+ * (paths relative to /root/reference/pkg/src/blockten/).
+ * shows the ctypes binding a maintainer would add to blockten.
+ *
+ * Layouts: all arrays are C-order (row-major) fp64 unless stated; tensors
+ * are (m, p, n) = (block rows, class, block cols) (blocks.py:445-448); CP
+ * factors are (extent, R) row-major like numpy's (decomp.py:90-117).
+ */
+#ifndef BT200_H
+#define BT200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BT_ABI_VERSION 1
+
+/* status codes (errors.py:11-32) */
+#define BT_OK 0
+#define BT_E_SHAPE 1   /* ShapeError */
+#define BT_E_PATTERN 2 /* PatternMismatchError */
+#define BT_E_NOT_PD 3  /* NotPositiveDefiniteError */
+#define BT_E_CONV 4    /* ConvergenceError */
+#define BT_E_CUDA 5    /* RuntimeError (CUDA failure) */
+#define BT_E_VALUE 6   /* ValueError */
+
+int bt_version(void);
+const char* bt_last_error(void);
+/* number of kernels this library has launched in the process (monotonic) */
+int64_t bt_launch_count(void);
+
+/* ------------------------------------------------------------------------
+ * Strided-batched FP64 GEMM on the DMMA tensor pipe (building block of the
+ * mode products and Grams: tensor.py:75-90 mode_multiply, decomp.py:220-234
+ * unfolding Grams).  C[b][m][n] = alpha * sum_{ko,ki} A(b,m,ko,ki) *
+ * B(b,ko,ki,n) * scale(b,ko,n) + beta * C.  A must have unit stride along m
+ * or ki; B along n or ki.  symmetric=1 computes the lower tiles of a square
+ * C and mirrors them (SYRK).
+ * ---------------------------------------------------------------------- */
+typedef struct bt_gemm_desc {
+  int64_t M, N, Kin, Kout, batch;
+  const double* A;
+  int64_t sAm, sAko, sAki, sAb;
+  const double* B;
+  int64_t sBn, sBko, sBki, sBb;
+  const double* bscale; /* optional: B(k,n) *= bscale[b*s_scale_b + ko*s_scale_ko + n] */
+  int64_t s_scale_ko, s_scale_b;
+  const double* ascale; /* optional: A(m,k) *= ascale[b*s_ascale_b + ko*s_ascale_ko + ki] */
+  int64_t s_ascale_ko, s_ascale_b;
+  double* C;
+  int64_t sCm, sCn, sCb;
+  double alpha, beta;
+  int symmetric;
+  int splits; /* 0 = heuristic */
+} bt_gemm_desc;
+
+int64_t bt_gemm_f64_ws_bytes(const bt_gemm_desc* d);
+int bt_gemm_f64(const bt_gemm_desc* d, double* ws, int64_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K1/K2: block gather T_E and scatter M_E.
+ * Pattern maps (built on the host from BlockPattern.placements,
+ * blocks.py:42-123): cell_class[ell*q] (int32, -1 = uncovered),
+ * cell_order[ell*q] (int64: rank of the cell in the reference's scan order:
+ * classes in order then cells in placement order; uncovered cells get
+ * nnz + i*q + j, i.e. argwhere order), rep_cell[p] (int64, i*q+j of each
+ * class's first placement), eta[p] (int64 counts).
+ * ---------------------------------------------------------------------- */
+typedef struct bt_pattern_dev {
+  int64_t ell, q, m, n, p, nnz;
+  const int32_t* cell_class;
+  const int64_t* cell_order;
+  const int64_t* rep_cell;
+  const int64_t* eta;
+} bt_pattern_dev;
+
+/* workspace: 2 * ell * q int32 flags + 2 int64 */
+int64_t bt_gather_ws_bytes(const bt_pattern_dev* pat);
+/* blocks.py:395-449 extract_blocks + mat_to_tensor.  a: (ell*m, q*n) with
+ * row stride lda (>= q*n).  t: (m, p, n).  On mismatch returns BT_E_PATTERN
+ * and writes the offending cell's order rank into *bad_order (host int64;
+ * -1 if none).  Synchronises `stream` to read the verdict. */
+int bt_gather_blocks_f64(const double* a, int64_t lda, const bt_pattern_dev* pat, double tol,
+                         int weighted, double* t, void* ws, int64_t* bad_order, void* stream);
+/* blocks.py:452-462 tensor_to_mat / 363-381 struct_expand: a[cell of k] =
+ * t[:, k, :] / sqrt(eta_k) for a (m, p, n) tensor (t_sm, t_sp, t_sn
+ * strides), uncovered cells zero.  a: (ell*m, q*n) with row stride lda. */
+int bt_scatter_blocks_f64(const double* t, int64_t t_sm, int64_t t_sp, int64_t t_sn,
+                          const bt_pattern_dev* pat, double* a, int64_t lda, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K3: weighted tensor builders for the configs.
+ * ---------------------------------------------------------------------- */
+/* apps.py:193-201: t[a, k, b] = sqrt(eta_k) * params[k, a, b]; t is (d_out, p, d_in) */
+int bt_build_hankel_f64(const double* params, int64_t p, int64_t d_out, int64_t d_in,
+                        const int64_t* eta, double* t, void* stream);
+/* C3 Gneiting space-time tensor, t[i, k, j] = sqrt(eta_k) * phi(|x_i - x_j|, k / lag_scale),
+ * phi(h, u) = exp(-10 h / (u+1)^0.25) / (u+1); points: (npts, 2) */
+int bt_build_gneiting_f64(const double* points, int64_t npts, int64_t lags, double lag_scale,
+                          const int64_t* eta, double* t, void* stream);
+/* multilevel.py:268-298 generalised: x[i1,i2,i3] = sqrt(eta_i1 eta_i2 eta_i3) *
+ * psf[i3,i2,i1], eta_i = grid - |i - h| (psf K^3, K odd) */
+int bt_build_psf_f64(const double* psf, int64_t k, int64_t grid, double* x, void* stream);
+/* C5: x[i,j,k] = sum_r a0[i,r] b0[j,r] c0[k,r] + noise * N(0,1)_philox(key, lin index),
+ * only rows k in [k0, k1) (x is (I, J, k1-k0)); lin index uses the global K */
+int bt_build_cp_model_f64(const double* a0, const double* b0, const double* c0, int64_t I,
+                          int64_t J, int64_t K, int64_t R, int64_t k0, int64_t k1, double noise,
+                          uint64_t key, double* x, void* ws, int64_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K4-K6: CP-ALS (decomp.py:344-410) on a C-order (I, J, K) tensor.
+ * ---------------------------------------------------------------------- */
+typedef struct bt_cp_problem {
+  const double* x; /* (I, J, K) C-order, device */
+  int64_t I, J, K, R;
+  double norm_x; /* ||x||_F (<= 0: computed on device) */
+} bt_cp_problem;
+
+/* Whole ALS loop, device resident.  factors a (I,R), b (J,R), c (K,R) hold
+ * the initialisation on entry; on exit a holds KruskalRep.x = F0 * lam
+ * (decomp.py:403), b and c the normalised factors, lam (R) the mode-3
+ * column norms (decomp.py:391-392).  phase_ms (host, 4 doubles, optional)
+ * accumulates CUDA-event times of the phases [P/mode-1 tree kernel,
+ * mode-2, mode-3 GEMM, solves + fit].  fit_history (host, max_iters) receives the fit
+ * per sweep; *n_iters and *converged follow decomp.py:397-410.
+ * fit_mode: 0 auto (Gram identity, explicit residual when the identity loses
+ * precision), 1 always explicit (reference semantics decomp.py:395-396),
+ * 2 Gram identity only.  The host loop reads the fit back once per sweep only
+ * when tol > 0 (convergence test); with tol <= 0 the sweeps run without host
+ * synchronisation. */
+int64_t bt_cp_als_ws_bytes(const bt_cp_problem* pb);
+int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, double* c, double* lam,
+                  int max_iters, double tol, int fit_mode, double* fit_history, int* n_iters,
+                  int* converged, double* phase_ms, void* ws, int64_t ws_bytes, void* stream);
+
+/* Single MTTKRP (decomp.py:385-387 unfold(t,k) @ khatri_rao(...)): out (extent_mode, R).
+ * mode in {1,2,3}.  Fused Khatri-Rao; no unfolding copy. */
+int64_t bt_mttkrp_ws_bytes(const bt_cp_problem* pb, int mode);
+int bt_mttkrp_f64(const bt_cp_problem* pb, int mode, const double* a, const double* b,
+                  const double* c, double* out, void* ws, int64_t ws_bytes, void* stream);
+
+/* Pseudo-inverse of a symmetric R x R matrix with numpy's pinv cutoff
+ * (rcond 1e-15 * max |eig|) via an on-chip cyclic Jacobi eigensolver. */
+int bt_pinv_sym_f64(const double* v, int64_t R, double* vp, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K7-K9: Tucker pieces (decomp.py:220-321)
+ * ---------------------------------------------------------------------- */
+/* Gram of the mode-`mode` unfolding of a C-order tensor of order `order`
+ * (dims[order]); g: (dims[mode-1])^2.  Unique-half SYRK on DMMA. */
+int64_t bt_unfold_gram_ws_bytes(const int64_t* dims, int order, int mode);
+int bt_unfold_gram_f64(const double* x, const int64_t* dims, int order, int mode, double* g,
+                       void* ws, int64_t ws_bytes, void* stream);
+/* Symmetric eigensolver: w (n) descending, v (n, n) row-major with column i
+ * the eigenvector of w[i], each column sign-normalised so its largest-|.|
+ * entry (first on ties) is positive (decomp.py:176-179). */
+int64_t bt_syevd_ws_bytes(int64_t n);
+int bt_syevd_f64(const double* a, int64_t n, double* w, double* v, void* ws, int64_t ws_bytes,
+                 void* stream);
+/* Thin QR with nonnegative diag(R) (decomp.py:182-193): a (m x n, m >= n),
+ * q (m x n), r (n x n), row-major. */
+int64_t bt_qr_thin_ws_bytes(int64_t m, int64_t n);
+int bt_qr_thin_f64(const double* a, int64_t m, int64_t n, double* q, double* r, void* ws,
+                   int64_t ws_bytes, void* stream);
+/* Mode product y = x x_mode u (tensor.py:75-90): u is (rows, dims[mode-1])
+ * row-major (transpose=0) or u^T is given as (dims[mode-1], rows) (transpose=1). */
+int64_t bt_ttm_ws_bytes(const int64_t* dims, int order, int mode, int64_t rows);
+int bt_ttm_f64(const double* x, const int64_t* dims, int order, int mode, const double* u,
+               int64_t rows, int transpose, double* y, void* ws, int64_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K11: structured matvecs (reconstruct.py:271-315) for nrhs right-hand sides.
+ * x: (nrhs, q*n) row-major (each row one RHS vector), y: (nrhs, ell*m).
+ * ---------------------------------------------------------------------- */
+/* Kron-sum: coeffs (p, r), terms (r, m, n). */
+int64_t bt_matvec_kron_ws_bytes(const bt_pattern_dev* pat, int64_t r, int64_t nrhs);
+int bt_matvec_kron_f64(const bt_pattern_dev* pat, const int64_t* row_ptr, const int64_t* row_cells,
+                       const double* coeffs, const double* terms, int64_t r, const double* x,
+                       int64_t nrhs, double* y, void* ws, int64_t ws_bytes, void* stream);
+/* BLR: left (m, rl), right (n, rr), middles (p, rl, rr).  row_ptr (ell+1) /
+ * row_cells (nnz: j * p + k, cells of block row i sorted by j) describe the
+ * pattern rows. */
+int64_t bt_matvec_blr_ws_bytes(const bt_pattern_dev* pat, int64_t rl, int64_t rr, int64_t nrhs);
+int bt_matvec_blr_f64(const bt_pattern_dev* pat, const int64_t* row_ptr, const int64_t* row_cells,
+                      const double* left, int64_t rl, const double* right, int64_t rr,
+                      const double* middles, const double* x, int64_t nrhs, double* y, void* ws,
+                      int64_t ws_bytes, void* stream);
+/* Multilevel Kronecker sum of `nterms` 3-level terms with dense level
+ * matrices s1 (nterms, N3o, N3i), s2 (nterms, N2o, N2i), s3 (nterms, N1o, N1i)
+ * applied to volumes x (nrhs, N3i, N2i, N1i) -> y (nrhs, N3o, N2o, N1o). */
+int64_t bt_ml_matvec_ws_bytes(int64_t nterms, const int64_t* nin, const int64_t* nout,
+                              int64_t nrhs);
+int bt_ml_matvec_f64(int64_t nterms, const int64_t* nin, const int64_t* nout, const double* s1,
+                     const double* s2, const double* s3, const double* x, int64_t nrhs, double* y,
+                     void* ws, int64_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * misc device reductions used by the host mirror
+ * ---------------------------------------------------------------------- */
+/* max |x| over n doubles into a device double (ws: bt_sumsq_ws_bytes) */
+int bt_maxabs_f64(const double* x, int64_t n, double* out, void* ws, int64_t ws_bytes,
+                  void* stream);
+/* psd.py:141-161 block comparison: blocks (p, n, n), partner[p] (device
+ * int64); returns BT_E_PATTERN with *bad_class = first failing class.
+ * ws: p ints.  Synchronises the stream. */
+int bt_transpose_check_f64(const double* blocks, int64_t p, int64_t n, const int64_t* partner,
+                           double tol, void* ws, int64_t* bad_class, void* stream);
+/* z = alpha * x + beta * y elementwise (n doubles) */
+int bt_axpby_f64(int64_t n, double alpha, const double* x, double beta, const double* y, double* z,
+                 void* stream);
+/* sum of squares of n doubles, deterministic tree; out is a device double */
+int bt_sumsq_f64(const double* x, int64_t n, double* out, void* ws, int64_t ws_bytes,
+                 void* stream);
+int64_t bt_sumsq_ws_bytes(int64_t n);
+
+/* FP64 peak microbenchmarks (bench only): DMMA.8x8x4 chains / DFMA chains on
+ * all SMs; *flops receives the executed flop count. */
+int bt_peak_dmma(int64_t iters, int blocks, int threads, double* sink, double* flops, void* stream);
+int bt_peak_dfma(int64_t iters, int blocks, int threads, double* sink, double* flops, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BT200_H */

@@ -1,0 +1,19 @@
+"""bt200: B200-native (sm_100a) hot path of arXiv 2105.01170's structure-
+preserving approximations, a drop-in behind the reference package
+``blockten``'s API (same names, arguments, outputs, factor layouts and
+exception types).  All arithmetic runs in libbt200.so (hand-written CUDA,
+FP64 DMMA tensor cores); PyTorch only provides device memory and streams.
+"""
+
+from __future__ import annotations
+
+from .blocks import (BlockPattern, build_pattern, extract_blocks, kernel_level_pattern,
+                     mat_to_tensor, struct_assemble, struct_expand, struct_scalars,
+                     tensor_to_mat)
+from .decomp import (CpResult, KruskalRep, SketchConfig, TuckerRep, cp_als, hooi, hosvd,
+                     qr_thin, st_hosvd, svd_truncated, tucker_partial)
+from .errors import (ContainerExtentError, ContainerFormatError, ConvergenceError,
+                     NotPositiveDefiniteError, PatternMismatchError, ShapeError)
+from .tensor import fold, fro_norm, mode_multiply, squeeze, twist, unfold
+
+__version__ = "0.1.0"

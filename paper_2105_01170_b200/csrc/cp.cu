@@ -1,0 +1,863 @@
+// K4-K6: CP-ALS (decomp.py:344-410) device resident.
+//
+// Per sweep the reference builds three Khatri-Rao matrices and multiplies
+// three unfolding copies (decomp.py:373, 385-387), then reconstructs the
+// whole tensor for the fit (decomp.py:395-396).  Here, over ONE C-order
+// layout of X (no unfoldings):
+//   P      = X x_3 C                    (DMMA GEMM, IJ x K x R; dimension tree)
+//   M1     = sum_j P[i,j,:] * B[j,:]    (fused epilogue of the P kernel)
+//   M2     = sum_i P[i,j,:] * A[i,:]    (HBM stream over P, new A)
+//   M3     = X_(3) (B kr A)             (DMMA GEMM, Khatri-Rao generated on the
+//                                         fly as a per-i column scale of B)
+// and after each MTTKRP the R x R solve of decomp.py:386-393 runs on chip:
+// pinv(G_a o G_b) by a cyclic Jacobi eigensolver in one CTA (numpy's pinv
+// cutoff 1e-15 * max|eig|), F = M pinv(V), column norms, lambda, Grams.
+// The fit uses the Gram identity ||X||^2 - 2<X,Xhat> + ||Xhat||^2 (exact
+// algebra, no extra pass) and switches to an explicit fused residual pass
+// (DMMA reconstruction tile - X tile) when the identity would lose digits.
+// Every reduction is a fixed-order tree: results are bit-reproducible.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "gemm.cuh"
+#include "jacobi.cuh"
+
+int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, int64_t ws_elems);
+int64_t bt_gemm_ws_elems(BtGemmArgs g, int64_t batch);
+
+namespace {
+
+constexpr int PINV_MAX_R = 96;
+
+// ---------------------------------------------------------------------------
+// P = X x_3 C with the mode-1 MTTKRP reduction fused into the epilogue
+// ---------------------------------------------------------------------------
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS)
+    tree_p_kernel(BtGemmArgs g, const double* __restrict__ Bf, int64_t R, double* __restrict__ m1part,
+                  int64_t jtiles, int store_p) {
+  extern __shared__ __align__(16) double smem_dyn[];
+  __shared__ double red[Cfg::WM][Cfg::BN];
+  const int64_t tm = blockIdx.x;  // j-tile
+  const int64_t tn = blockIdx.y;  // r-tile
+  const int64_t i = blockIdx.z;   // batch = mode-1 index
+  const int64_t m0 = tm * Cfg::BM, n0 = tn * Cfg::BN;
+  const int64_t KT = (g.Kin + Cfg::BK - 1) / Cfg::BK;
+  double acc[Cfg::FM][Cfg::FN][2];
+  bt_gemm_mainloop<Cfg>(g, i, m0, n0, 0, KT, acc, smem_dyn);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wmi = warp % Cfg::WM;
+  const int wm0 = wmi * Cfg::TM;
+  const int wn0 = (warp / Cfg::WM) * Cfg::TN;
+  double* Pb = g.C + i * g.sCb;
+  double colsum[Cfg::FN][2];
+#pragma unroll
+  for (int j = 0; j < Cfg::FN; ++j) colsum[j][0] = colsum[j][1] = 0.0;
+#pragma unroll
+  for (int fi = 0; fi < Cfg::FM; ++fi) {
+    const int64_t jrow = m0 + wm0 + fi * 8 + gq;
+    const bool rv = jrow < g.M;
+#pragma unroll
+    for (int fj = 0; fj < Cfg::FN; ++fj) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t r = n0 + wn0 + fj * 8 + 2 * tq + h;
+        if (rv && r < g.N) {
+          const double v = acc[fi][fj][h];
+          if (store_p) Pb[jrow * g.sCm + r] = v;
+          colsum[fj][h] = fma(v, __ldg(Bf + jrow * R + r), colsum[fj][h]);
+        }
+      }
+    }
+  }
+  // reduce over the 8 row-groups of the warp (lane bits 2..4)
+#pragma unroll
+  for (int fj = 0; fj < Cfg::FN; ++fj)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double v = colsum[fj][h];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      colsum[fj][h] = v;
+    }
+  if (gq == 0) {
+#pragma unroll
+    for (int fj = 0; fj < Cfg::FN; ++fj)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) red[wmi][wn0 + fj * 8 + 2 * tq + h] = colsum[fj][h];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < Cfg::BN; c += Cfg::THREADS) {
+    const int64_t r = n0 + c;
+    if (r >= g.N) continue;
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < Cfg::WM; ++w) s += red[w][c];
+    m1part[(i * jtiles + tm) * R + r] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// M2 partials from P: m2part[s][j][r] = sum_{i in chunk s} P[i][j][r] A[i][r]
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256)
+    mode2_from_p_kernel(const double* __restrict__ P, const double* __restrict__ A, int64_t I,
+                        int64_t JR, int64_t R, int64_t chunk, double* __restrict__ m2part) {
+  const int64_t s = blockIdx.y;
+  const int64_t i0 = s * chunk, i1 = min(I, i0 + chunk);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < JR;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % R;
+    double acc0 = 0.0, acc1 = 0.0;
+    int64_t i = i0;
+    for (; i + 1 < i1; i += 2) {
+      acc0 = fma(ld_stream(P + i * JR + e), __ldg(A + i * R + r), acc0);
+      acc1 = fma(ld_stream(P + (i + 1) * JR + e), __ldg(A + (i + 1) * R + r), acc1);
+    }
+    if (i < i1) acc0 = fma(ld_stream(P + i * JR + e), __ldg(A + i * R + r), acc0);
+    m2part[s * JR + e] = acc0 + acc1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// on-chip symmetric Jacobi: pinv of an R x R symmetric matrix
+// ---------------------------------------------------------------------------
+
+__device__ void pinv_from_eig(const double* a, const double* qv, int R, int ld, double* out) {
+  __shared__ double wmax;
+  __shared__ double inv[PINV_MAX_R + 1];
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < R; ++i) m = fmax(m, fabs(a[i * ld + i]));
+    wmax = m;
+  }
+  __syncthreads();
+  const double cut = 1e-15 * wmax;  // numpy pinv: rcond 1e-15 times the largest singular value
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    const double w = a[i * ld + i];
+    inv[i] = (fabs(w) > cut) ? 1.0 / w : 0.0;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
+    const int r = idx / R, c = idx % R;
+    double s = 0.0;
+    for (int k = 0; k < R; ++k) s = fma(qv[r * ld + k] * inv[k], qv[c * ld + k], s);
+    out[idx] = s;
+  }
+}
+
+// V = G0 o G1 (Hadamard) if g1 != null else V = G0; Vp = pinv(V)
+__global__ void __launch_bounds__(256) pinv_kernel(const double* __restrict__ g0,
+                                                   const double* __restrict__ g1, int R,
+                                                   double* __restrict__ vp) {
+  extern __shared__ __align__(16) double sm[];
+  const int n = R + (R & 1);
+  const int ld = n + 1;
+  double* a = sm;
+  double* qv = a + n * ld;
+  double* cs = qv + n * ld;
+  double* sn = cs + n / 2;
+  int* pp = reinterpret_cast<int*>(sn + n / 2);
+  int* qq = pp + n / 2;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int r = idx / n, c = idx % n;
+    double v = 0.0;
+    if (r < R && c < R) v = g1 ? g0[r * R + c] * g1[r * R + c] : g0[r * R + c];
+    a[r * ld + c] = v;
+  }
+  __syncthreads();
+  jacobi_smem(a, qv, n, ld, cs, sn, pp, qq, 40, 0.0);
+  __syncthreads();
+  pinv_from_eig(a, qv, R, ld, vp);
+}
+
+size_t pinv_smem_bytes(int R) {
+  const int n = R + (R & 1);
+  return (size_t)(2 * n * (n + 1) + n) * 8 + (size_t)n * 4;
+}
+
+// ---------------------------------------------------------------------------
+// solve: F_un = (sum_s Mpart[s]) @ Vp ; per-CTA Gram + <F_un, M> partials
+// ---------------------------------------------------------------------------
+
+constexpr int SOLVE_ROWS = 32;  // rows of F per CTA
+
+__global__ void __launch_bounds__(256)
+    solve_apply_kernel(const double* __restrict__ mpart, int64_t nparts, int64_t part_stride,
+                       int64_t row_stride, const double* __restrict__ vp, int64_t rows, int R, double* __restrict__ f,
+                       double* __restrict__ gram_part, double* __restrict__ inner_part) {
+  extern __shared__ __align__(16) double sm[];
+  double* ms = sm;                     // SOLVE_ROWS x R  (reduced M rows)
+  double* fs = ms + SOLVE_ROWS * R;    // SOLVE_ROWS x R  (F_un rows)
+  double* vs = fs + SOLVE_ROWS * R;    // R x R
+  const int64_t r0 = blockIdx.x * (int64_t)SOLVE_ROWS;
+  const int nr = static_cast<int>(rows - r0 < SOLVE_ROWS ? rows - r0 : SOLVE_ROWS);
+  for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) vs[idx] = vp[idx];
+  for (int idx = threadIdx.x; idx < SOLVE_ROWS * R; idx += blockDim.x) {
+    const int rr = idx / R;
+    double s = 0.0;
+    if (rr < nr) {
+      const double* src = mpart + (r0 + rr) * row_stride + idx % R;
+      for (int64_t p = 0; p < nparts; ++p) s += src[p * part_stride];
+    }
+    ms[idx] = s;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < SOLVE_ROWS * R; idx += blockDim.x) {
+    const int rr = idx / R, c = idx % R;
+    double s = 0.0;
+    for (int k = 0; k < R; ++k) s = fma(ms[rr * R + k], vs[k * R + c], s);
+    fs[idx] = s;
+    if (rr < nr) f[(r0 + rr) * R + c] = s;
+  }
+  __syncthreads();
+  double* gp = gram_part + blockIdx.x * (int64_t)R * R;
+  for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
+    const int a = idx / R, b = idx % R;
+    double s = 0.0;
+    for (int rr = 0; rr < nr; ++rr) s = fma(fs[rr * R + a], fs[rr * R + b], s);
+    gp[idx] = s;
+  }
+  if (inner_part != nullptr) {
+    __shared__ double red[8];
+    double s = 0.0;
+    for (int idx = threadIdx.x; idx < nr * R; idx += blockDim.x) s = fma(fs[idx], ms[idx], s);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+      inner_part[blockIdx.x] = t;
+    }
+  }
+}
+
+// Device-side state of one CP-ALS run.
+struct CpState {
+  double* gram[3];     // normalised Grams G_k = F_k^T F_k
+  double* vp;          // R x R
+  double* norms;       // R
+  double* lam;         // R
+  double* scal;        // [0] ||X||^2, [1] <X,Xhat>, [2] explicit residual^2, [3] use_explicit
+  double* fit_hist;    // max_iters
+};
+
+// Reduce Gram partials, column norms (0 -> 1), normalised Gram; mode 3 also
+// sets lambda, the Gram-identity fit and the explicit/identity decision.
+__global__ void __launch_bounds__(256)
+    solve_finish_kernel(const double* __restrict__ gram_part, int64_t nparts, int R,
+                        double* __restrict__ norms, double* __restrict__ gram_out,
+                        double* __restrict__ lam, const double* __restrict__ inner_part,
+                        CpState st, int it, int fit_mode) {
+  __shared__ double nrm[PINV_MAX_R];
+  __shared__ double red[8];
+  for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
+    double s = 0.0;
+    for (int64_t p = 0; p < nparts; ++p) s += gram_part[p * R * R + idx];
+    gram_out[idx] = s;
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    double v = sqrt(gram_out[r * R + r]);
+    if (v == 0.0) v = 1.0;
+    nrm[r] = v;
+    norms[r] = v;
+    if (lam) lam[r] = v;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
+    const int a = idx / R, b = idx % R;
+    gram_out[idx] = gram_out[idx] / (nrm[a] * nrm[b]);
+  }
+  if (lam == nullptr) return;
+  __syncthreads();
+  // ||Xhat||^2 = lam^T (G0 o G1 o G2) lam ; <X, Xhat> = sum(C_un o M3)
+  double s = 0.0;
+  for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
+    const int a = idx / R, b = idx % R;
+    s += nrm[a] * nrm[b] * st.gram[0][idx] * st.gram[1][idx] * st.gram[2][idx];
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double xh2 = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) xh2 += red[w];
+    double inner = 0.0;
+    for (int64_t p = 0; p < nparts; ++p) inner += inner_part[p];
+    const double x2 = st.scal[0];
+    const double res2 = fmax(x2 - 2.0 * inner + xh2, 0.0);
+    const double relres = sqrt(res2 / x2);
+    st.scal[1] = inner;
+    // identity error ~ c*eps*||X||^2 / (2 res): keep it below ~1e-12 in fit
+    const bool explicit_fit = (fit_mode == 1) || (fit_mode == 0 && relres < 1e-3);
+    st.scal[3] = explicit_fit ? 1.0 : 0.0;
+    st.fit_hist[it] = 1.0 - relres;
+  }
+}
+
+__global__ void scale_cols_kernel(double* __restrict__ f, int64_t rows, int R,
+                                  const double* __restrict__ norms) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < rows * R;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    f[idx] = f[idx] / norms[idx % R];
+}
+
+__global__ void gram_kernel(const double* __restrict__ f, int64_t rows, int R,
+                            double* __restrict__ g) {
+  // small: one CTA, fixed order over rows
+  for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
+    const int a = idx / R, b = idx % R;
+    double s = 0.0;
+    for (int64_t r = 0; r < rows; ++r) s = fma(f[r * R + a], f[r * R + b], s);
+    g[idx] = s;
+  }
+}
+
+// W = A * lam (row scale for the explicit residual)
+__global__ void lam_scale_kernel(const double* a, const double* __restrict__ lam, int64_t rows,
+                                 int R, double* w) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < rows * R;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    w[idx] = a[idx] * lam[idx % R];
+}
+
+// ---------------------------------------------------------------------------
+// explicit residual ||X - [[lam; A, B, C]]||^2 (decomp.py:395-396, fused)
+// Xhat tile (j-rows x k-cols) for fixed i = (B o W_i) C^T on DMMA; epilogue
+// subtracts X and accumulates squares.  Persistent grid; exits at once when
+// the Gram identity was judged accurate (scal[3] == 0).
+// ---------------------------------------------------------------------------
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS)
+    residual_kernel(BtGemmArgs g, const double* __restrict__ X, int64_t J, int64_t K,
+                    int64_t tiles_total, const double* __restrict__ flag,
+                    double* __restrict__ part) {
+  extern __shared__ __align__(16) double smem_dyn[];
+  __shared__ double red[Cfg::THREADS / 32];
+  if (flag != nullptr && *flag == 0.0) {
+    if (threadIdx.x == 0) part[blockIdx.x] = 0.0;
+    return;
+  }
+  const int64_t tiles_m = (J + Cfg::BM - 1) / Cfg::BM;
+  const int64_t tiles_n = (K + Cfg::BN - 1) / Cfg::BN;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm0 = (warp % Cfg::WM) * Cfg::TM;
+  const int wn0 = (warp / Cfg::WM) * Cfg::TN;
+  const int64_t KT = (g.Kin + Cfg::BK - 1) / Cfg::BK;
+  double local = 0.0;
+  for (int64_t tile = blockIdx.x; tile < tiles_total; tile += gridDim.x) {
+    const int64_t i = tile / (tiles_m * tiles_n);
+    const int64_t rem = tile % (tiles_m * tiles_n);
+    const int64_t tm = rem % tiles_m, tn = rem / tiles_m;
+    const int64_t m0 = tm * Cfg::BM, n0 = tn * Cfg::BN;
+    double acc[Cfg::FM][Cfg::FN][2];
+    __syncthreads();
+    bt_gemm_mainloop<Cfg>(g, i, m0, n0, 0, KT, acc, smem_dyn);
+    const double* xi = X + i * J * K;
+#pragma unroll
+    for (int fi = 0; fi < Cfg::FM; ++fi) {
+      const int64_t j = m0 + wm0 + fi * 8 + gq;
+      if (j >= J) continue;
+#pragma unroll
+      for (int fj = 0; fj < Cfg::FN; ++fj)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t k = n0 + wn0 + fj * 8 + 2 * tq + h;
+          if (k < K) {
+            const double d = ld_stream(xi + j * K + k) - acc[fi][fj][h];
+            local = fma(d, d, local);
+          }
+        }
+    }
+  }
+  local = warp_sum(local);
+  if (lane == 0) red[warp] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < Cfg::THREADS / 32; ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+__global__ void residual_finish_kernel(const double* __restrict__ part, int n, CpState st, int it) {
+  if (threadIdx.x != 0) return;
+  if (st.scal[3] == 0.0) return;
+  double s = 0.0;
+  for (int k = 0; k < n; ++k) s += part[k];
+  st.scal[2] = s;
+  st.fit_hist[it] = 1.0 - sqrt(s) / sqrt(st.scal[0]);
+}
+
+// ---------------------------------------------------------------------------
+// host-side plan
+// ---------------------------------------------------------------------------
+
+template <int BN>
+struct TreeCfgSel;
+template <>
+struct TreeCfgSel<64> {
+  template <int V>
+  using Cfg = GemmCfg<128, 64, 16, 4, 2, 4, true, false, V>;
+};
+template <>
+struct TreeCfgSel<16> {
+  template <int V>
+  using Cfg = GemmCfg<128, 16, 16, 8, 1, 4, true, false, V>;
+};
+template <>
+struct TreeCfgSel<8> {
+  template <int V>
+  using Cfg = GemmCfg<128, 8, 16, 8, 1, 4, true, false, V>;
+};
+
+// residual: rows j, cols k, reduction r (K-contig on both sides)
+template <int V>
+using ResCfg = GemmCfg<128, 64, 16, 4, 2, 3, true, true, V>;
+
+int tree_bn(int64_t R) { return R <= 8 ? 8 : (R <= 16 ? 16 : 64); }
+
+struct Plan {
+  int64_t I, J, K, R;
+  int bn;          // tree-P tile width
+  int64_t jtiles;  // tree-P row tiles per i
+  int64_t s2;      // i-chunks for mode 2
+  int64_t chunk2;
+  int64_t solve_parts_max;
+  int res_grid;
+  // workspace layout (doubles)
+  int64_t off_p, off_m1, off_m2, off_m3, off_m3ws, off_gp, off_ip, off_f, off_state, off_res,
+      off_w, total;
+  int64_t m3_ws_elems;
+};
+
+BtGemmArgs mode3_args(const Plan& pl, const double* X, const double* A, const double* B,
+                      double* out) {
+  BtGemmArgs g{};
+  g.M = pl.K;
+  g.N = pl.R;
+  g.Kin = pl.J;
+  g.Kout = pl.I;
+  g.A = BtOperand{X, 1, pl.J * pl.K, pl.K, 0};
+  g.B = BtOperand{B, 1, 0, pl.R, 0};
+  g.bscale = A;
+  g.s_scale_ko = pl.R;
+  g.C = out;
+  g.sCm = pl.R;
+  g.sCn = 1;
+  g.alpha = 1.0;
+  g.beta = 0.0;
+  return g;
+}
+
+Plan make_plan(const bt_cp_problem* pb) {
+  Plan pl;
+  pl.I = pb->I;
+  pl.J = pb->J;
+  pl.K = pb->K;
+  pl.R = pb->R;
+  pl.bn = tree_bn(pl.R);
+  pl.jtiles = bt_cdiv(pl.J, 128);
+  const int64_t JR = pl.J * pl.R;
+  // mode 2: enough CTAs along (j, r) x i-chunks to fill the GPU ~4x
+  const int64_t blocks_jr = std::max<int64_t>(1, std::min<int64_t>(bt_cdiv(JR, 256), 2048));
+  pl.s2 = std::max<int64_t>(1, std::min<int64_t>(pl.I, bt_cdiv(4 * bt_num_sms(), blocks_jr)));
+  pl.chunk2 = bt_cdiv(pl.I, pl.s2);
+  pl.s2 = bt_cdiv(pl.I, pl.chunk2);
+  const int64_t maxrows = std::max(pl.I, std::max(pl.J, pl.K));
+  pl.solve_parts_max = bt_cdiv(maxrows, SOLVE_ROWS);
+  pl.res_grid = 8 * bt_num_sms();
+  BtGemmArgs g3 = mode3_args(pl, nullptr, nullptr, nullptr, nullptr);
+  pl.m3_ws_elems = bt_gemm_ws_elems(g3, 1);
+  const int64_t RR = pl.R * pl.R;
+  int64_t o = 0;
+  auto take = [&](int64_t n) {
+    int64_t at = o;
+    o += (n + 1) / 2 * 2;  // keep 16-byte alignment
+    return at;
+  };
+  pl.off_p = take(pl.I * pl.J * pl.R);
+  pl.off_m1 = take(pl.I * pl.jtiles * pl.R);
+  pl.off_m2 = take(pl.s2 * JR);
+  pl.off_m3 = take(pl.K * pl.R);
+  pl.off_m3ws = take(pl.m3_ws_elems);
+  pl.off_gp = take(pl.solve_parts_max * RR);
+  pl.off_ip = take(pl.solve_parts_max);
+  pl.off_f = take(maxrows * pl.R);
+  pl.off_state = take(3 * RR + RR + 2 * pl.R + 8);
+  pl.off_res = take(std::max<int64_t>(pl.res_grid, 2048));
+  pl.off_w = take(pl.I * pl.R);
+  pl.total = o;
+  return pl;
+}
+
+template <int BN, int V>
+int launch_tree(const Plan& pl, const double* X, const double* C, const double* B, double* P,
+                double* m1part, int store_p, cudaStream_t st) {
+  using Cfg = typename TreeCfgSel<BN>::template Cfg<V>;
+  BtGemmArgs g{};
+  g.M = pl.J;
+  g.N = pl.R;
+  g.Kin = pl.K;
+  g.Kout = 1;
+  g.A = BtOperand{X, pl.K, 0, 1, pl.J * pl.K};
+  g.B = BtOperand{C, 1, 0, pl.R, 0};
+  g.C = P;
+  g.sCm = pl.R;
+  g.sCn = 1;
+  g.sCb = pl.J * pl.R;
+  g.alpha = 1.0;
+  static bool attr = false;
+  if (!attr) {
+    BT_CUDA_CHECK(cudaFuncSetAttribute(tree_p_kernel<Cfg>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Cfg::SMEM_BYTES));
+    attr = true;
+  }
+  BT_REQUIRE(pl.I <= 65535, BT_E_SHAPE, "cp: mode-1 extent %lld exceeds 65535",
+             (long long)pl.I);
+  dim3 grid(static_cast<unsigned>(pl.jtiles), static_cast<unsigned>(bt_cdiv(pl.R, BN)),
+            static_cast<unsigned>(pl.I));
+  tree_p_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(g, B, pl.R, m1part, pl.jtiles,
+                                                                   store_p);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+int run_tree(const Plan& pl, const double* X, const double* C, const double* B, double* P,
+             double* m1part, int store_p, cudaStream_t st) {
+  const bool v2 = (pl.K % 2 == 0) && (pl.R % 2 == 0) &&
+                  ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(C)) & 15u) == 0;
+  switch (pl.bn) {
+    case 8:
+      return v2 ? launch_tree<8, 2>(pl, X, C, B, P, m1part, store_p, st)
+                : launch_tree<8, 1>(pl, X, C, B, P, m1part, store_p, st);
+    case 16:
+      return v2 ? launch_tree<16, 2>(pl, X, C, B, P, m1part, store_p, st)
+                : launch_tree<16, 1>(pl, X, C, B, P, m1part, store_p, st);
+    default:
+      return v2 ? launch_tree<64, 2>(pl, X, C, B, P, m1part, store_p, st)
+                : launch_tree<64, 1>(pl, X, C, B, P, m1part, store_p, st);
+  }
+}
+
+int run_mode2(const Plan& pl, const double* P, const double* A, double* m2part, cudaStream_t st) {
+  const int64_t JR = pl.J * pl.R;
+  const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(bt_cdiv(JR, 256), 2048));
+  mode2_from_p_kernel<<<dim3(static_cast<unsigned>(bx), static_cast<unsigned>(pl.s2)), 256, 0,
+                        st>>>(P, A, pl.I, JR, pl.R, pl.chunk2, m2part);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+int run_mode3(const Plan& pl, const double* X, const double* A, const double* B, double* out,
+              double* ws, cudaStream_t st) {
+  BtGemmArgs g = mode3_args(pl, X, A, B, out);
+  g.ws = ws;
+  return bt_gemm_run(g, 1, st, 0, pl.m3_ws_elems);
+}
+
+int run_pinv(const double* g0, const double* g1, int R, double* vp, cudaStream_t st) {
+  const size_t sm = pinv_smem_bytes(R);
+  static bool attr = false;
+  if (!attr) {
+    BT_CUDA_CHECK(cudaFuncSetAttribute(pinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(pinv_smem_bytes(PINV_MAX_R))));
+    attr = true;
+  }
+  pinv_kernel<<<1, 256, sm, st>>>(g0, g1, R, vp);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+// One factor update: F_k <- normalise((sum parts) pinv(G_o0 o G_o1)).
+int run_solve(const Plan& pl, const CpState& s, double* ws, const double* mpart, int64_t nparts,
+              int64_t part_stride, int64_t row_stride, int64_t rows, int go0, int go1, double* F, int k,
+              bool last_mode, int it, int fit_mode, cudaStream_t st) {
+  const int R = static_cast<int>(pl.R);
+  BT_TRY(run_pinv(s.gram[go0], s.gram[go1], R, s.vp, st));
+  const int64_t parts = bt_cdiv(rows, SOLVE_ROWS);
+  double* gp = ws + pl.off_gp;
+  double* ip = ws + pl.off_ip;
+  const size_t sm = (size_t)(2 * SOLVE_ROWS * R + R * R) * 8;
+  static bool attr = false;
+  if (!attr) {
+    BT_CUDA_CHECK(cudaFuncSetAttribute(solve_apply_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (2 * SOLVE_ROWS * PINV_MAX_R + PINV_MAX_R * PINV_MAX_R) * 8));
+    attr = true;
+  }
+  solve_apply_kernel<<<static_cast<unsigned>(parts), 256, sm, st>>>(
+      mpart, nparts, part_stride, row_stride, s.vp, rows, R, F, gp, last_mode ? ip : nullptr);
+  BT_LAUNCH_CHECK();
+  solve_finish_kernel<<<1, 256, 0, st>>>(gp, parts, R, s.norms, s.gram[k],
+                                         last_mode ? s.lam : nullptr, ip, s, it, fit_mode);
+  BT_LAUNCH_CHECK();
+  const int64_t n = rows * pl.R;
+  scale_cols_kernel<<<static_cast<unsigned>(std::min<int64_t>(bt_cdiv(n, 256), 4096)), 256, 0,
+                      st>>>(F, rows, R, s.norms);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+}  // namespace
+
+// Explicit residual: Xhat_i = B diag(W_i) C^T with W = A * lam; the per-i
+// diagonal rides on the engine's A-scale (indexed by the reduction index r).
+namespace {
+
+template <int V>
+int residual_pass(const Plan& pl, const double* X, const double* W, const double* Bf,
+                  const double* Cf, const double* flag, double* part, cudaStream_t st) {
+  using Cfg = ResCfg<V>;
+  static bool attr = false;
+  if (!attr) {
+    BT_CUDA_CHECK(cudaFuncSetAttribute(residual_kernel<Cfg>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Cfg::SMEM_BYTES));
+    attr = true;
+  }
+  BtGemmArgs g{};
+  g.M = pl.J;
+  g.N = pl.K;
+  g.Kin = pl.R;
+  g.Kout = 1;
+  g.A = BtOperand{Bf, pl.R, 0, 1, 0};
+  g.B = BtOperand{Cf, pl.R, 0, 1, 0};
+  g.ascale = W;
+  g.s_ascale_b = pl.R;
+  g.alpha = 1.0;
+  const int64_t tiles = pl.I * bt_cdiv(pl.J, Cfg::BM) * bt_cdiv(pl.K, Cfg::BN);
+  residual_kernel<Cfg><<<pl.res_grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(g, X, pl.J, pl.K, tiles,
+                                                                           flag, part);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+
+static int64_t cp_total_ws(const Plan& pl) { return pl.total + 16; }
+
+extern "C" int64_t bt_cp_als_ws_bytes(const bt_cp_problem* pb) {
+  Plan pl = make_plan(pb);
+  return cp_total_ws(pl) * 8;
+}
+
+extern "C" int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, double* c,
+                             double* lam, int max_iters, double tol, int fit_mode,
+                             double* fit_history, int* n_iters, int* converged, double* phase_ms,
+                             void* wsv, int64_t ws_bytes, void* stream) {
+  BT_REQUIRE(pb->I >= 1 && pb->J >= 1 && pb->K >= 1, BT_E_SHAPE, "cp_als: empty tensor");
+  BT_REQUIRE(pb->R >= 1, BT_E_SHAPE, "CP rank must be at least 1");
+  BT_REQUIRE(pb->R <= PINV_MAX_R, BT_E_SHAPE, "cp_als: rank %lld above the on-chip limit %d",
+             (long long)pb->R, PINV_MAX_R);
+  BT_REQUIRE(max_iters >= 1, BT_E_VALUE, "max_iters must be at least 1");
+  cudaStream_t st = bt_stream(stream);
+  Plan pl = make_plan(pb);
+  BT_REQUIRE(ws_bytes >= cp_total_ws(pl) * 8, BT_E_VALUE, "cp_als: workspace too small");
+  double* ws = static_cast<double*>(wsv);
+  const int R = static_cast<int>(pl.R);
+  const int64_t RR = pl.R * pl.R;
+  CpState s;
+  double* sb = ws + pl.off_state;
+  s.gram[0] = sb;
+  s.gram[1] = sb + RR;
+  s.gram[2] = sb + 2 * RR;
+  s.vp = sb + 3 * RR;
+  s.norms = sb + 4 * RR;
+  s.lam = lam;
+  s.scal = sb + 4 * RR + pl.R;
+  std::vector<double> hist(max_iters, 0.0);
+  // per-sweep fit values stay on device until the end (stream-ordered scratch)
+  double* dhist = nullptr;
+  BT_CUDA_CHECK(cudaMallocAsync(&dhist, sizeof(double) * max_iters, st));
+  s.fit_hist = dhist;
+  const double* X = pb->x;
+  double* F[3] = {a, b, c};
+  const int64_t rows[3] = {pl.I, pl.J, pl.K};
+
+  // ||X||^2
+  if (pb->norm_x > 0.0) {
+    const double x2 = pb->norm_x * pb->norm_x;
+    BT_CUDA_CHECK(cudaMemcpyAsync(s.scal, &x2, 8, cudaMemcpyHostToDevice, st));
+  } else {
+    BT_TRY(bt_sumsq_f64(X, pl.I * pl.J * pl.K, s.scal, ws + pl.off_res, 2048 * 8, st));
+  }
+  // initial Grams
+  for (int k = 0; k < 3; ++k) {
+    gram_kernel<<<1, 256, 0, st>>>(F[k], rows[k], R, s.gram[k]);
+    BT_LAUNCH_CHECK();
+  }
+
+  double* P = ws + pl.off_p;
+  double* m1 = ws + pl.off_m1;
+  double* m2 = ws + pl.off_m2;
+  double* m3 = ws + pl.off_m3;
+  double* m3ws = ws + pl.off_m3ws;
+  double* W = ws + pl.off_w;
+  double* rpart = ws + pl.off_res;
+  const bool res_v2 = (pl.R % 2 == 0);
+
+  double prev = -INFINITY;
+  int it = 0;
+  int conv = 0;
+  // optional phase timing: 5 events per sweep (stream-ordered, read at the end)
+  std::vector<cudaEvent_t> ev;
+  auto mark = [&]() -> int {
+    if (!phase_ms) return BT_OK;
+    cudaEvent_t e;
+    BT_CUDA_CHECK(cudaEventCreate(&e));
+    BT_CUDA_CHECK(cudaEventRecord(e, st));
+    ev.push_back(e);
+    return BT_OK;
+  };
+  for (it = 1; it <= max_iters; ++it) {
+    const int ix = it - 1;
+    BT_TRY(mark());
+    // mode 1: P = X x3 C ; M1 = sum_j P o B
+    BT_TRY(run_tree(pl, X, c, b, P, m1, 1, st));
+    BT_TRY(mark());
+    BT_TRY(run_solve(pl, s, ws, m1, pl.jtiles, pl.R, pl.jtiles * pl.R, pl.I, 1, 2, a, 0, false,
+                     ix, fit_mode, st));
+    // mode 2: M2 = sum_i P o A_new   (rows j)
+    BT_TRY(mark());
+    BT_TRY(run_mode2(pl, P, a, m2, st));
+    BT_TRY(mark());
+    BT_TRY(run_solve(pl, s, ws, m2, pl.s2, pl.J * pl.R, pl.R, pl.J, 0, 2, b, 1, false, ix,
+                     fit_mode, st));
+    // mode 3: M3 = X_(3) (B kr A)
+    BT_TRY(mark());
+    BT_TRY(run_mode3(pl, X, a, b, m3, m3ws, st));
+    BT_TRY(mark());
+    BT_TRY(run_solve(pl, s, ws, m3, 1, 0, pl.R, pl.K, 0, 1, c, 2, true, ix, fit_mode, st));
+    // explicit residual when requested / when the Gram identity is unreliable
+    if (fit_mode != 2) {
+      lam_scale_kernel<<<static_cast<unsigned>(std::min<int64_t>(bt_cdiv(pl.I * pl.R, 256), 4096)),
+                         256, 0, st>>>(a, lam, pl.I, R, W);
+      BT_LAUNCH_CHECK();
+      if (res_v2)
+        BT_TRY(residual_pass<2>(pl, X, W, b, c, s.scal + 3, rpart, st));
+      else
+        BT_TRY(residual_pass<1>(pl, X, W, b, c, s.scal + 3, rpart, st));
+      residual_finish_kernel<<<1, 32, 0, st>>>(rpart, pl.res_grid, s, ix);
+      BT_LAUNCH_CHECK();
+    }
+    BT_TRY(mark());
+    if (tol > 0.0) {
+      double fit = 0.0;
+      BT_CUDA_CHECK(cudaMemcpyAsync(&fit, dhist + ix, 8, cudaMemcpyDeviceToHost, st));
+      BT_CUDA_CHECK(cudaStreamSynchronize(st));
+      if (std::fabs(fit - prev) < tol) {
+        conv = 1;
+        break;
+      }
+      prev = fit;
+    }
+  }
+  if (it > max_iters) it = max_iters;
+  // KruskalRep.x = F0 * lambda (decomp.py:403)
+  lam_scale_kernel<<<static_cast<unsigned>(std::min<int64_t>(bt_cdiv(pl.I * pl.R, 256), 4096)), 256,
+                     0, st>>>(a, lam, pl.I, R, a);
+  BT_LAUNCH_CHECK();
+  BT_CUDA_CHECK(cudaMemcpyAsync(hist.data(), dhist, sizeof(double) * it, cudaMemcpyDeviceToHost,
+                                st));
+  BT_CUDA_CHECK(cudaFreeAsync(dhist, st));
+  BT_CUDA_CHECK(cudaStreamSynchronize(st));
+  for (int k = 0; k < it; ++k) fit_history[k] = hist[k];
+  *n_iters = it;
+  *converged = conv;
+  if (phase_ms) {
+    // events per sweep: [t0 tree t1 solve1 t2 mode2 t3 solve2 t4 mode3 t5 solve3+fit t6]
+    for (int k = 0; k < 4; ++k) phase_ms[k] = 0.0;
+    for (size_t base = 0; base + 7 <= ev.size(); base += 7) {
+      float ms = 0.f;
+      auto el = [&](int x, int y) {
+        cudaEventElapsedTime(&ms, ev[base + x], ev[base + y]);
+        return static_cast<double>(ms);
+      };
+      phase_ms[0] += el(0, 1);
+      phase_ms[1] += el(2, 3);
+      phase_ms[2] += el(4, 5);
+      phase_ms[3] += el(1, 2) + el(3, 4) + el(5, 6);
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  return BT_OK;
+}
+
+extern "C" int64_t bt_mttkrp_ws_bytes(const bt_cp_problem* pb, int mode) {
+  Plan pl = make_plan(pb);
+  (void)mode;
+  return pl.total * 8;
+}
+
+// reduce partials (fixed order) into out (rows x R)
+namespace {
+__global__ void reduce_parts_kernel(const double* __restrict__ part, int64_t nparts,
+                                    int64_t stride, int64_t n, double* __restrict__ out) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t p = 0; p < nparts; ++p) s += part[p * stride + idx];
+    out[idx] = s;
+  }
+}
+// m1part is laid out [i][jt][r]: reduce over jt
+__global__ void reduce_m1_kernel(const double* __restrict__ part, int64_t I, int64_t jt,
+                                 int64_t R, double* __restrict__ out) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < I * R;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / R, r = idx % R;
+    double s = 0.0;
+    for (int64_t t = 0; t < jt; ++t) s += part[(i * jt + t) * R + r];
+    out[idx] = s;
+  }
+}
+}  // namespace
+
+extern "C" int bt_mttkrp_f64(const bt_cp_problem* pb, int mode, const double* a, const double* b,
+                             const double* c, double* out, void* wsv, int64_t ws_bytes,
+                             void* stream) {
+  BT_REQUIRE(mode >= 1 && mode <= 3, BT_E_SHAPE, "mttkrp: mode %d out of range", mode);
+  cudaStream_t st = bt_stream(stream);
+  Plan pl = make_plan(pb);
+  BT_REQUIRE(ws_bytes >= pl.total * 8, BT_E_VALUE, "mttkrp: workspace too small");
+  double* ws = static_cast<double*>(wsv);
+  double* P = ws + pl.off_p;
+  if (mode == 1) {
+    BT_TRY(run_tree(pl, pb->x, c, b, P, ws + pl.off_m1, 0, st));
+    reduce_m1_kernel<<<static_cast<unsigned>(std::min<int64_t>(bt_cdiv(pl.I * pl.R, 256), 4096)),
+                       256, 0, st>>>(ws + pl.off_m1, pl.I, pl.jtiles, pl.R, out);
+    BT_LAUNCH_CHECK();
+  } else if (mode == 2) {
+    BT_TRY(run_tree(pl, pb->x, c, b, P, ws + pl.off_m1, 1, st));
+    BT_TRY(run_mode2(pl, P, a, ws + pl.off_m2, st));
+    const int64_t n = pl.J * pl.R;
+    reduce_parts_kernel<<<static_cast<unsigned>(std::min<int64_t>(bt_cdiv(n, 256), 4096)), 256, 0,
+                          st>>>(ws + pl.off_m2, pl.s2, n, n, out);
+    BT_LAUNCH_CHECK();
+  } else {
+    BT_TRY(run_mode3(pl, pb->x, a, b, out, ws + pl.off_m3ws, st));
+  }
+  return BT_OK;
+}
+
+extern "C" int bt_pinv_sym_f64(const double* v, int64_t R, double* vp, void* stream) {
+  BT_REQUIRE(R >= 1 && R <= PINV_MAX_R, BT_E_SHAPE, "pinv: size %lld outside [1, %d]",
+             (long long)R, PINV_MAX_R);
+  return run_pinv(v, nullptr, static_cast<int>(R), vp, bt_stream(stream));
+}

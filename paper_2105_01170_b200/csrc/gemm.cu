@@ -1,0 +1,289 @@
+// Strided-batched FP64 DMMA GEMM (exported as bt_gemm_f64) + the shared
+// split-K reduction.  Replaces the dgemm calls of the reference's
+// mode products and Grams (tensor.py:90 `u @ unfold(t, mode)`,
+// decomp.py:227 SVD-of-unfolding -> Gram SYRK) without unfolding copies.
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "gemm.cuh"
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+
+static thread_local char g_last_error[1024] = "";
+
+void bt_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+}
+
+extern "C" const char* bt_last_error(void) { return g_last_error; }
+
+extern "C" int bt_version(void) { return BT_ABI_VERSION; }
+
+static std::atomic<long long> g_launches{0};
+void bt_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+extern "C" int64_t bt_launch_count(void) { return g_launches.load(); }
+
+int bt_num_sms() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  }
+  return cached;
+}
+
+// ---------------------------------------------------------------------------
+// reduction
+// ---------------------------------------------------------------------------
+
+__global__ void bt_gemm_reduce_kernel(BtGemmArgs g, int64_t bm, int64_t bn) {
+  const int64_t total = g.M * g.N;
+  const int64_t batch = blockIdx.y;
+  const double* wsb = g.ws + batch * g.splits * total;
+  double* Cb = g.C + batch * g.sCb;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t m = idx / g.N, n = idx % g.N;
+    int64_t src = idx;
+    if (g.symmetric && (m / bm < n / bn || (m / bm == n / bn && m < n))) src = n * g.N + m;
+    double s = 0.0;
+    for (int k = 0; k < g.splits; ++k) s += wsb[k * total + src];
+    double* c = Cb + m * g.sCm + n * g.sCn;
+    const double v = g.alpha * s;
+    *c = (g.beta == 0.0) ? v : v + g.beta * (*c);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launch
+// ---------------------------------------------------------------------------
+
+static int bt_pick_splits(int64_t tiles, int64_t batch, int64_t KT) {
+  const int64_t target = 2 * bt_num_sms();
+  const int64_t have = tiles * batch;
+  if (have >= target || KT < 8) return 1;
+  int64_t s = (target + have - 1) / have;
+  s = std::min<int64_t>(s, KT / 4);
+  s = std::min<int64_t>(s, 64);
+  return static_cast<int>(std::max<int64_t>(s, 1));
+}
+
+template <class Cfg>
+static void bt_gemm_geometry(BtGemmArgs& g, int64_t batch, int want_splits) {
+  g.tiles_m = bt_cdiv(g.M, Cfg::BM);
+  g.tiles_n = bt_cdiv(g.N, Cfg::BN);
+  const int64_t tiles = g.symmetric ? g.tiles_m * (g.tiles_m + 1) / 2 : g.tiles_m * g.tiles_n;
+  const int64_t KT = bt_cdiv(g.Kin, Cfg::BK) * g.Kout;
+  g.splits = want_splits > 0 ? want_splits : bt_pick_splits(tiles, batch, KT);
+  if (g.splits > KT) g.splits = static_cast<int>(std::max<int64_t>(KT, 1));
+}
+
+template <class Cfg>
+int bt_gemm_launch(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits) {
+  bt_gemm_geometry<Cfg>(g, batch, want_splits);
+  const int64_t tiles = g.symmetric ? g.tiles_m * (g.tiles_m + 1) / 2 : g.tiles_m * g.tiles_n;
+  static bool attr_done = false;
+  if (!attr_done) {
+    BT_CUDA_CHECK(cudaFuncSetAttribute(bt_gemm_kernel<Cfg>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Cfg::SMEM_BYTES));
+    attr_done = true;
+  }
+  BT_REQUIRE(tiles <= INT32_MAX && batch <= 65535 && g.splits <= 65535, BT_E_SHAPE,
+             "gemm grid too large (tiles %lld batch %lld)", (long long)tiles, (long long)batch);
+  dim3 grid(static_cast<unsigned>(tiles), g.splits, static_cast<unsigned>(batch));
+  bt_gemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(g);
+  BT_LAUNCH_CHECK();
+  if (g.splits > 1 || g.symmetric) {
+    const int64_t total = g.M * g.N;
+    const int blocks = static_cast<int>(std::min<int64_t>(bt_cdiv(total, 256), 4096));
+    bt_gemm_reduce_kernel<<<dim3(blocks, static_cast<unsigned>(batch)), 256, 0, st>>>(g, Cfg::BM,
+                                                                                      Cfg::BN);
+    BT_LAUNCH_CHECK();
+  }
+  return BT_OK;
+}
+
+// configurations ------------------------------------------------------------
+// wide: 128x64 CTA tile, 8 warps of 32x32, BK 16, 4 stages (~120 KB smem)
+template <bool AK, bool BKc, int V>
+using CfgWide = GemmCfg<128, 64, 16, 4, 2, 4, AK, BKc, V>;
+// narrow: 128x16 CTA tile for N <= 16 (Grams of R <= 16 factors, TTM r <= 16)
+template <bool AK, bool BKc, int V>
+using CfgNarrow = GemmCfg<128, 16, 16, 8, 1, 4, AK, BKc, V>;
+// square: 128x128 for symmetric (SYRK) outputs, 8 warps of 64x32
+template <bool AK, bool BKc, int V>
+using CfgSquare = GemmCfg<128, 128, 16, 2, 4, 3, AK, BKc, V>;
+
+// tuning alternatives (selected with BT_GEMM_CFG=<id> for experiments)
+template <bool AK, bool BKc, int V>
+using CfgWideK32 = GemmCfg<128, 64, 32, 4, 2, 3, AK, BKc, V>;
+template <bool AK, bool BKc, int V>
+using CfgBig = GemmCfg<128, 128, 16, 2, 4, 3, AK, BKc, V>;
+template <bool AK, bool BKc, int V>
+using CfgTall = GemmCfg<256, 64, 16, 4, 2, 3, AK, BKc, V>;
+template <bool AK, bool BKc, int V>
+using CfgW4 = GemmCfg<128, 64, 16, 2, 2, 4, AK, BKc, V>;
+
+static int bt_tune_cfg() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("BT_GEMM_CFG");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
+enum BtTileClass { BT_TILE_WIDE = 0, BT_TILE_NARROW = 1, BT_TILE_SQUARE = 2 };
+
+template <template <bool, bool, int> class C>
+static int bt_dispatch_layout(const BtGemmArgs& g, int64_t batch, cudaStream_t st, bool ak,
+                              bool bk, int vec, int want_splits) {
+  if (vec == 2) {
+    if (ak && bk) return bt_gemm_launch<C<true, true, 2>>(g, batch, st, want_splits);
+    if (ak && !bk) return bt_gemm_launch<C<true, false, 2>>(g, batch, st, want_splits);
+    if (!ak && bk) return bt_gemm_launch<C<false, true, 2>>(g, batch, st, want_splits);
+    return bt_gemm_launch<C<false, false, 2>>(g, batch, st, want_splits);
+  }
+  if (ak && bk) return bt_gemm_launch<C<true, true, 1>>(g, batch, st, want_splits);
+  if (ak && !bk) return bt_gemm_launch<C<true, false, 1>>(g, batch, st, want_splits);
+  if (!ak && bk) return bt_gemm_launch<C<false, true, 1>>(g, batch, st, want_splits);
+  return bt_gemm_launch<C<false, false, 1>>(g, batch, st, want_splits);
+}
+
+static bool even_aligned(const double* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Normalise an argument set (swap to make N the small side, decide layouts
+// and vector width) and run it.  Used by every internal GEMM-shaped call.
+int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, int64_t ws_elems) {
+  BT_REQUIRE(g.M >= 0 && g.N >= 0 && g.Kin >= 0 && g.Kout >= 0 && batch >= 1, BT_E_SHAPE,
+             "gemm: negative extent");
+  if (g.M == 0 || g.N == 0) return BT_OK;
+  if (g.Kin == 0 || g.Kout == 0) {
+    // C = beta * C (alpha * empty sum)
+    BtGemmArgs z = g;
+    z.alpha = 0.0;
+    z.Kin = 1;
+    z.Kout = 1;
+    g = z;
+  }
+  // make N the smaller extent (the CTA tile is tall); no swap with a B-scale
+  if (!g.symmetric && g.bscale == nullptr && g.ascale == nullptr && g.N > g.M && g.N > 64) {
+    BtGemmArgs s = g;
+    s.M = g.N;
+    s.N = g.M;
+    s.A = g.B;
+    s.B = g.A;
+    s.sCm = g.sCn;
+    s.sCn = g.sCm;
+    g = s;
+  }
+  const bool ak = (g.A.s_ki == 1);
+  const bool bk = (g.B.s_ki == 1);
+  BT_REQUIRE(ak || g.A.s_mn == 1, BT_E_SHAPE, "gemm: A needs unit stride along m or k");
+  BT_REQUIRE(bk || g.B.s_mn == 1, BT_E_SHAPE, "gemm: B needs unit stride along n or k");
+  const int64_t a_row = ak ? g.A.s_mn : g.A.s_ki;
+  const int64_t b_row = bk ? g.B.s_mn : g.B.s_ki;
+  const bool v2 = even_aligned(g.A.ptr) && even_aligned(g.B.ptr) && (a_row % 2 == 0) &&
+                  (b_row % 2 == 0) && (g.A.s_ko % 2 == 0) && (g.B.s_ko % 2 == 0) &&
+                  (g.A.s_b % 2 == 0) && (g.B.s_b % 2 == 0);
+  const int vec = v2 ? 2 : 1;
+  int cls = g.symmetric ? BT_TILE_SQUARE : (g.N <= 16 ? BT_TILE_NARROW : BT_TILE_WIDE);
+  // workspace check (computed with the same geometry the launcher will use)
+  BtGemmArgs probe = g;
+  if (cls == BT_TILE_SQUARE)
+    bt_gemm_geometry<CfgSquare<true, true, 1>>(probe, batch, want_splits);
+  else if (cls == BT_TILE_NARROW)
+    bt_gemm_geometry<CfgNarrow<true, true, 1>>(probe, batch, want_splits);
+  else
+    bt_gemm_geometry<CfgWide<true, true, 1>>(probe, batch, want_splits);
+  const int64_t need = (probe.splits > 1 || g.symmetric) ? batch * probe.splits * g.M * g.N : 0;
+  if (need > ws_elems) {
+    BT_REQUIRE(!g.symmetric && ws_elems >= 0, BT_E_VALUE,
+               "gemm: workspace too small (%lld < %lld doubles)", (long long)ws_elems,
+               (long long)need);
+    want_splits = 1;
+  } else if (want_splits <= 0) {
+    want_splits = probe.splits;
+  }
+  if (cls == BT_TILE_SQUARE)
+    return bt_dispatch_layout<CfgSquare>(g, batch, st, ak, bk, vec, want_splits);
+  if (cls == BT_TILE_WIDE) {
+    switch (bt_tune_cfg()) {
+      case 1: return bt_dispatch_layout<CfgWideK32>(g, batch, st, ak, bk, vec, want_splits);
+      case 2: return bt_dispatch_layout<CfgBig>(g, batch, st, ak, bk, vec, want_splits);
+      case 3: return bt_dispatch_layout<CfgTall>(g, batch, st, ak, bk, vec, want_splits);
+      case 4: return bt_dispatch_layout<CfgW4>(g, batch, st, ak, bk, vec, want_splits);
+      default: break;
+    }
+  }
+  if (cls == BT_TILE_NARROW)
+    return bt_dispatch_layout<CfgNarrow>(g, batch, st, ak, bk, vec, want_splits);
+  return bt_dispatch_layout<CfgWide>(g, batch, st, ak, bk, vec, want_splits);
+}
+
+int64_t bt_gemm_ws_elems(BtGemmArgs g, int64_t batch) {
+  if (!g.symmetric && g.bscale == nullptr && g.ascale == nullptr && g.N > g.M && g.N > 64)
+    std::swap(g.M, g.N);
+  int cls = g.symmetric ? BT_TILE_SQUARE : (g.N <= 16 ? BT_TILE_NARROW : BT_TILE_WIDE);
+  if (cls == BT_TILE_SQUARE)
+    bt_gemm_geometry<CfgSquare<true, true, 1>>(g, batch, 0);
+  else if (cls == BT_TILE_NARROW)
+    bt_gemm_geometry<CfgNarrow<true, true, 1>>(g, batch, 0);
+  else
+    bt_gemm_geometry<CfgWide<true, true, 1>>(g, batch, 0);
+  return (g.splits > 1 || g.symmetric) ? batch * g.splits * g.M * g.N : 0;
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+
+static BtGemmArgs bt_make_args(const bt_gemm_desc* d) {
+  BtGemmArgs g;
+  memset(&g, 0, sizeof(g));
+  g.M = d->M;
+  g.N = d->N;
+  g.Kin = d->Kin;
+  g.Kout = d->Kout;
+  g.A = BtOperand{d->A, d->sAm, d->sAko, d->sAki, d->sAb};
+  g.B = BtOperand{d->B, d->sBn, d->sBko, d->sBki, d->sBb};
+  g.bscale = d->bscale;
+  g.s_scale_ko = d->s_scale_ko;
+  g.s_scale_b = d->s_scale_b;
+  g.ascale = d->ascale;
+  g.s_ascale_ko = d->s_ascale_ko;
+  g.s_ascale_b = d->s_ascale_b;
+  g.C = d->C;
+  g.sCm = d->sCm;
+  g.sCn = d->sCn;
+  g.sCb = d->sCb;
+  g.alpha = d->alpha;
+  g.beta = d->beta;
+  g.symmetric = d->symmetric;
+  return g;
+}
+
+extern "C" int64_t bt_gemm_f64_ws_bytes(const bt_gemm_desc* d) {
+  return bt_gemm_ws_elems(bt_make_args(d), d->batch < 1 ? 1 : d->batch) * 8;
+}
+
+extern "C" int bt_gemm_f64(const bt_gemm_desc* d, double* ws, int64_t ws_bytes, void* stream) {
+  BT_REQUIRE(d != nullptr, BT_E_VALUE, "gemm: null descriptor");
+  BT_REQUIRE(!d->symmetric || d->M == d->N, BT_E_SHAPE, "gemm: symmetric output must be square");
+  BtGemmArgs g = bt_make_args(d);
+  g.ws = ws;
+  return bt_gemm_run(g, d->batch < 1 ? 1 : d->batch, bt_stream(stream), d->splits,
+                     ws ? ws_bytes / 8 : 0);
+}

@@ -1,0 +1,484 @@
+// K11: structured matvecs for many right-hand sides (reconstruct.py:271-315;
+// the reference loops over terms and over every grid cell in Python and
+// handles one vector at a time).
+//
+//   Kron-sum : Z_j = D_j X (one batched DMMA GEMM over all terms and RHS),
+//              then y[:, block i] = sum_{cells (i,c) of class k} sum_j
+//              (coeffs[k,j] / sqrt(eta_k)) Z_j[:, c]        (CTA per block row)
+//   BLR      : Z = R^T X (DMMA GEMM); yb_i = sum_{cells (i,j)} (S_k/sqrt(eta_k)) Z_j
+//              (CTA per block row, the per-cell 2-D products on DMMA with
+//              cp.async double buffering); y = L yb (DMMA GEMM)
+//   multilevel (no reference counterpart; cli.py:247-248 densifies):
+//              y = sum_r (S1_r (x) S2_r (x) S3_r) x as three batched DMMA mode
+//              products over the volume batch, the last one reducing over r.
+// Flop counts per RHS equal the reference's FlopCounter formulas.
+#include <algorithm>
+
+#include "gemm.cuh"
+
+int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, int64_t ws_elems);
+int64_t bt_gemm_ws_elems(BtGemmArgs g, int64_t batch);
+
+namespace {
+
+int grid1d(int64_t n) { return static_cast<int>(std::min<int64_t>(bt_cdiv(n, 256), 8192)); }
+
+// X2[(c * nrhs + s)][b] = x[s][c * n + b]
+__global__ void kron_permute_kernel(const double* __restrict__ x, int64_t nrhs, int64_t q,
+                                    int64_t n, double* __restrict__ x2) {
+  const int64_t total = nrhs * q * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = idx % n;
+    const int64_t s = (idx / n) % nrhs;
+    const int64_t c = idx / (n * nrhs);
+    x2[idx] = x[(s * q + c) * n + b];
+  }
+}
+
+// W[k][j] = coeffs[k][j] / sqrt(eta_k)   (reconstruct.py:97)
+__global__ void kron_weights_kernel(const double* __restrict__ coeffs, const int64_t* __restrict__ eta,
+                                    int64_t p, int64_t r, double* __restrict__ w) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < p * r;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    w[idx] = coeffs[idx] / sqrt(static_cast<double>(eta[idx / r]));
+}
+
+// y[s][i*m + a] = sum_{cells (i,c,k)} sum_j W[k][j] Z[j][a][c*nrhs + s]
+__global__ void __launch_bounds__(256)
+    kron_combine_kernel(const double* __restrict__ z, const double* __restrict__ w,
+                        const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ row_cells,
+                        int64_t p, int64_t r, int64_t m, int64_t q, int64_t nrhs, int64_t ell,
+                        double* __restrict__ y) {
+  const int64_t i = blockIdx.x;
+  const int64_t ms = m * nrhs;
+  const int64_t zj = m * q * nrhs;  // stride between terms
+  for (int64_t e = threadIdx.x + (int64_t)blockIdx.y * blockDim.x; e < ms;
+       e += (int64_t)gridDim.y * blockDim.x) {
+    const int64_t a = e / nrhs, s = e % nrhs;
+    double acc = 0.0;
+    for (int64_t cc = row_ptr[i]; cc < row_ptr[i + 1]; ++cc) {
+      const int64_t code = row_cells[cc];
+      const int64_t c = code / p, k = code % p;
+      const double* zc = z + a * q * nrhs + c * nrhs + s;
+      const double* wk = w + k * r;
+      for (int64_t j = 0; j < r; ++j) acc = fma(wk[j], zc[j * zj], acc);
+    }
+    y[s * ell * m + i * m + a] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// BLR middle product on DMMA
+// ---------------------------------------------------------------------------
+
+// Shat[k] = S[k] / sqrt(eta_k)  (reconstruct.py:305), padded to (RLP x RRP)
+__global__ void blr_scale_kernel(const double* __restrict__ mid, const int64_t* __restrict__ eta,
+                                 int64_t p, int64_t rl, int64_t rr, double* __restrict__ out) {
+  const int64_t tot = p * rl * rr;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    out[idx] = mid[idx] / sqrt(static_cast<double>(eta[idx / (rl * rr)]));
+}
+
+// yb[s][i][rho'] = sum_{cells (i, j, k)} sum_rho Shat[k][rho'][rho] Z[s*q + j][rho]
+// CTA: one block row i, one RHS tile of NB; output tile RLP x NB.
+template <int RLP, int RRP, int NB>
+__global__ void __launch_bounds__(256)
+    blr_middle_kernel(const double* __restrict__ shat, const double* __restrict__ z,
+                      const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ row_cells,
+                      int64_t p, int64_t rl, int64_t rr, int64_t q, int64_t nrhs, int64_t ell,
+                      double* __restrict__ yb) {
+  constexpr int LDS = bt_ld(RRP);  // S tile [rho'][rho] (k-contig for A)
+  constexpr int LDZ = bt_ld(RRP);  // Z tile [s][rho]   (k-contig for B)
+  constexpr int WM = RLP / 16 > 0 ? (RLP >= 32 ? 2 : 1) : 1;
+  constexpr int WN = 8 / WM;
+  constexpr int TM = RLP / WM, TN = NB / WN;
+  constexpr int FM = TM / 8, FN = TN / 8;
+  static_assert(FM >= 1 && FN >= 1, "tile too small");
+  extern __shared__ __align__(16) double sm[];
+  double* Ss = sm;                     // 2 stages of RLP x LDS
+  double* Zs = Ss + 2 * RLP * LDS;     // 2 stages of NB x LDZ
+  const int64_t i = blockIdx.x;
+  const int64_t s0 = blockIdx.y * (int64_t)NB;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm0 = (warp % WM) * TM, wn0 = (warp / WM) * TN;
+  const int64_t c0 = row_ptr[i], c1 = row_ptr[i + 1];
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int a = 0; a < FM; ++a)
+#pragma unroll
+    for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  auto load = [&](int stage, int64_t cell) {
+    const int64_t code = row_cells[cell];
+    const int64_t j = code / p, k = code % p;
+    double* sd = Ss + stage * RLP * LDS;
+    double* zd = Zs + stage * NB * LDZ;
+    const double* sk = shat + k * rl * rr;
+    for (int idx = threadIdx.x; idx < RLP * RRP; idx += 256) {
+      const int a = idx / RRP, b = idx % RRP;
+      const bool v = a < rl && b < rr;
+      cp_async8(sd + a * LDS + b, v ? sk + a * rr + b : sk, v ? 8 : 0);
+    }
+    for (int idx = threadIdx.x; idx < NB * RRP; idx += 256) {
+      const int sl = idx / RRP, b = idx % RRP;
+      const int64_t s = s0 + sl;
+      const bool v = s < nrhs && b < rr;
+      const double* src = z + (s * q + j) * rr + b;
+      cp_async8(zd + sl * LDZ + b, v ? src : z, v ? 8 : 0);
+    }
+  };
+
+  if (c0 < c1) load(0, c0);
+  cp_async_commit();
+  for (int64_t cell = c0; cell < c1; ++cell) {
+    const int stage = static_cast<int>((cell - c0) & 1);
+    if (cell + 1 < c1) load(stage ^ 1, cell + 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* sd = Ss + stage * RLP * LDS;
+    const double* zd = Zs + stage * NB * LDZ;
+#pragma unroll
+    for (int kk = 0; kk < RRP; kk += 4) {
+      double av[FM], bv[FN];
+#pragma unroll
+      for (int a = 0; a < FM; ++a) av[a] = sd[(wm0 + a * 8 + gq) * LDS + kk + tq];
+#pragma unroll
+      for (int b = 0; b < FN; ++b) bv[b] = zd[(wn0 + b * 8 + gq) * LDZ + kk + tq];
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma884(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int a = 0; a < FM; ++a) {
+    const int64_t rho = wm0 + a * 8 + gq;
+    if (rho >= rl) continue;
+#pragma unroll
+    for (int b = 0; b < FN; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t s = s0 + wn0 + b * 8 + 2 * tq + h;
+        if (s < nrhs) yb[(s * ell + i) * rl + rho] = acc[a][b][h];
+      }
+  }
+}
+
+template <int RLP, int RRP, int NB>
+int launch_blr_middle(const double* shat, const double* z, const int64_t* row_ptr,
+                      const int64_t* row_cells, int64_t p, int64_t rl, int64_t rr, int64_t q,
+                      int64_t nrhs, int64_t ell, double* yb, cudaStream_t st) {
+  constexpr size_t SM = (size_t)(2 * RLP * bt_ld(RRP) + 2 * NB * bt_ld(RRP)) * 8;
+  static bool attr = false;
+  if (!attr) {
+    BT_CUDA_CHECK(cudaFuncSetAttribute(blr_middle_kernel<RLP, RRP, NB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM));
+    attr = true;
+  }
+  dim3 grid(static_cast<unsigned>(ell), static_cast<unsigned>(bt_cdiv(nrhs, NB)));
+  blr_middle_kernel<RLP, RRP, NB><<<grid, 256, SM, st>>>(shat, z, row_ptr, row_cells, p, rl, rr,
+                                                         q, nrhs, ell, yb);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+struct KronPlan {
+  int64_t off_x2, off_w, off_z, off_gws, total;
+};
+
+KronPlan kron_plan(const bt_pattern_dev* pat, int64_t r, int64_t nrhs) {
+  KronPlan k;
+  int64_t o = 0;
+  auto take = [&](int64_t n) {
+    int64_t at = o;
+    o += (n + 1) / 2 * 2;
+    return at;
+  };
+  k.off_x2 = take(pat->q * pat->n * nrhs);
+  k.off_w = take(pat->p * r);
+  k.off_z = take(r * pat->m * pat->q * nrhs);
+  BtGemmArgs g{};
+  g.M = pat->m;
+  g.N = pat->q * nrhs;
+  g.Kin = pat->n;
+  g.Kout = 1;
+  k.off_gws = take(bt_gemm_ws_elems(g, r));
+  k.total = o;
+  return k;
+}
+
+struct BlrPlan {
+  int64_t off_shat, off_z, off_yb, off_gws, total;
+};
+
+BlrPlan blr_plan(const bt_pattern_dev* pat, int64_t rl, int64_t rr, int64_t nrhs) {
+  BlrPlan b;
+  int64_t o = 0;
+  auto take = [&](int64_t n) {
+    int64_t at = o;
+    o += (n + 1) / 2 * 2;
+    return at;
+  };
+  b.off_shat = take(pat->p * rl * rr);
+  b.off_z = take(pat->q * nrhs * rr);
+  b.off_yb = take(nrhs * pat->ell * rl);
+  BtGemmArgs g1{};
+  g1.M = pat->q * nrhs;
+  g1.N = rr;
+  g1.Kin = pat->n;
+  g1.Kout = 1;
+  BtGemmArgs g2{};
+  g2.M = nrhs * pat->ell;
+  g2.N = pat->m;
+  g2.Kin = rl;
+  g2.Kout = 1;
+  b.off_gws = take(std::max(bt_gemm_ws_elems(g1, 1), bt_gemm_ws_elems(g2, 1)));
+  b.total = o;
+  return b;
+}
+
+}  // namespace
+
+extern "C" int64_t bt_matvec_kron_ws_bytes(const bt_pattern_dev* pat, int64_t r, int64_t nrhs) {
+  return kron_plan(pat, r, nrhs).total * 8;
+}
+
+extern "C" int bt_matvec_kron_f64(const bt_pattern_dev* pat, const int64_t* row_ptr,
+                                  const int64_t* row_cells, const double* coeffs,
+                                  const double* terms, int64_t r, const double* x, int64_t nrhs,
+                                  double* y, void* wsv, int64_t ws_bytes, void* stream) {
+  BT_REQUIRE(r >= 1 && nrhs >= 1, BT_E_SHAPE, "matvec_kron: empty terms or RHS");
+  KronPlan kp = kron_plan(pat, r, nrhs);
+  BT_REQUIRE(ws_bytes >= kp.total * 8, BT_E_VALUE, "matvec_kron: workspace too small");
+  cudaStream_t st = bt_stream(stream);
+  double* ws = static_cast<double*>(wsv);
+  const int64_t m = pat->m, n = pat->n, q = pat->q, p = pat->p, ell = pat->ell;
+  double* x2 = ws + kp.off_x2;
+  double* w = ws + kp.off_w;
+  double* z = ws + kp.off_z;
+  kron_permute_kernel<<<grid1d(nrhs * q * n), 256, 0, st>>>(x, nrhs, q, n, x2);
+  BT_LAUNCH_CHECK();
+  kron_weights_kernel<<<grid1d(p * r), 256, 0, st>>>(coeffs, pat->eta, p, r, w);
+  BT_LAUNCH_CHECK();
+  // Z[j][a][col] = sum_b D_j[a][b] X2[col][b]
+  BtGemmArgs g{};
+  g.M = m;
+  g.N = q * nrhs;
+  g.Kin = n;
+  g.Kout = 1;
+  g.A = BtOperand{terms, n, 0, 1, m * n};
+  g.B = BtOperand{x2, n, 0, 1, 0};
+  g.C = z;
+  g.sCm = q * nrhs;
+  g.sCn = 1;
+  g.sCb = m * q * nrhs;
+  g.alpha = 1.0;
+  g.ws = ws + kp.off_gws;
+  BT_TRY(bt_gemm_run(g, r, st, 0, kp.total - kp.off_gws));
+  const int64_t ms = m * nrhs;
+  dim3 grid(static_cast<unsigned>(ell), static_cast<unsigned>(std::min<int64_t>(bt_cdiv(ms, 256), 64)));
+  kron_combine_kernel<<<grid, 256, 0, st>>>(z, w, row_ptr, row_cells, p, r, m, q, nrhs, ell, y);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+extern "C" int64_t bt_matvec_blr_ws_bytes(const bt_pattern_dev* pat, int64_t rl, int64_t rr,
+                                          int64_t nrhs) {
+  return blr_plan(pat, rl, rr, nrhs).total * 8;
+}
+
+extern "C" int bt_matvec_blr_f64(const bt_pattern_dev* pat, const int64_t* row_ptr,
+                                 const int64_t* row_cells, const double* left, int64_t rl,
+                                 const double* right, int64_t rr, const double* middles,
+                                 const double* x, int64_t nrhs, double* y, void* wsv,
+                                 int64_t ws_bytes, void* stream) {
+  BT_REQUIRE(rl >= 1 && rr >= 1 && nrhs >= 1, BT_E_SHAPE, "matvec_blr: empty operand");
+  BT_REQUIRE(rl <= 64 && rr <= 64, BT_E_SHAPE, "matvec_blr: side ranks above 64 not supported");
+  BlrPlan bp = blr_plan(pat, rl, rr, nrhs);
+  BT_REQUIRE(ws_bytes >= bp.total * 8, BT_E_VALUE, "matvec_blr: workspace too small");
+  cudaStream_t st = bt_stream(stream);
+  double* ws = static_cast<double*>(wsv);
+  const int64_t m = pat->m, n = pat->n, q = pat->q, p = pat->p, ell = pat->ell;
+  double* shat = ws + bp.off_shat;
+  double* z = ws + bp.off_z;
+  double* yb = ws + bp.off_yb;
+  double* gws = ws + bp.off_gws;
+  const int64_t gws_n = bp.total - bp.off_gws;
+  blr_scale_kernel<<<grid1d(p * rl * rr), 256, 0, st>>>(middles, pat->eta, p, rl, rr, shat);
+  BT_LAUNCH_CHECK();
+  // Z[(s*q + c)][rho] = sum_b x[s][c*n + b] R[b][rho]
+  BtGemmArgs g1{};
+  g1.M = q * nrhs;
+  g1.N = rr;
+  g1.Kin = n;
+  g1.Kout = 1;
+  g1.A = BtOperand{x, n, 0, 1, 0};
+  g1.B = BtOperand{right, 1, 0, rr, 0};
+  g1.C = z;
+  g1.sCm = rr;
+  g1.sCn = 1;
+  g1.alpha = 1.0;
+  g1.ws = gws;
+  BT_TRY(bt_gemm_run(g1, 1, st, 0, gws_n));
+  // middle products
+  if (rl <= 32 && rr <= 32) {
+    int rc = launch_blr_middle<32, 32, 64>(shat, z, row_ptr, row_cells, p, rl, rr, q, nrhs, ell,
+                                           yb, st);
+    BT_TRY(rc);
+  } else {
+    int rc = launch_blr_middle<64, 64, 64>(shat, z, row_ptr, row_cells, p, rl, rr, q, nrhs, ell,
+                                           yb, st);
+    BT_TRY(rc);
+  }
+  // y[(s*ell + i)][a] = sum_rho' yb[(s*ell + i)][rho'] L[a][rho']
+  BtGemmArgs g2{};
+  g2.M = nrhs * ell;
+  g2.N = m;
+  g2.Kin = rl;
+  g2.Kout = 1;
+  g2.A = BtOperand{yb, rl, 0, 1, 0};
+  g2.B = BtOperand{left, rl, 0, 1, 0};
+  g2.C = y;
+  g2.sCm = m;
+  g2.sCn = 1;
+  g2.alpha = 1.0;
+  g2.ws = gws;
+  return bt_gemm_run(g2, 1, st, 0, gws_n);
+}
+
+// ---------------------------------------------------------------------------
+// multilevel Kronecker sum
+// ---------------------------------------------------------------------------
+
+namespace {
+
+struct MlPlan {
+  int64_t chunk, off_u, off_w2, off_gws, total;
+};
+
+MlPlan ml_plan(int64_t R, const int64_t* nin, const int64_t* nout, int64_t nrhs) {
+  // nin = (N3i, N2i, N1i), nout = (N3o, N2o, N1o)
+  MlPlan m;
+  const int64_t per_u = nin[0] * nin[1] * R * nout[2];
+  const int64_t per_w = nin[0] * R * nout[1] * nout[2];
+  const int64_t budget = int64_t(1) << 28;  // ~2 GiB per intermediate
+  m.chunk = std::max<int64_t>(1, std::min<int64_t>(nrhs, budget / std::max(per_u, per_w)));
+  int64_t o = 0;
+  auto take = [&](int64_t n) {
+    int64_t at = o;
+    o += (n + 1) / 2 * 2;
+    return at;
+  };
+  m.off_u = take(m.chunk * per_u);
+  m.off_w2 = take(m.chunk * per_w);
+  BtGemmArgs g{};
+  g.M = m.chunk * nin[0] * nin[1];
+  g.N = R * nout[2];
+  g.Kin = nin[2];
+  g.Kout = 1;
+  int64_t w1 = bt_gemm_ws_elems(g, 1);
+  BtGemmArgs g2{};
+  g2.M = nout[1];
+  g2.N = nout[2];
+  g2.Kin = nin[1];
+  g2.Kout = 1;
+  int64_t w2 = bt_gemm_ws_elems(g2, m.chunk * nin[0]);
+  BtGemmArgs g3{};
+  g3.M = nout[0];
+  g3.N = nout[1] * nout[2];
+  g3.Kin = nin[0];
+  g3.Kout = R;
+  int64_t w3 = bt_gemm_ws_elems(g3, m.chunk);
+  m.off_gws = take(std::max(w1, std::max(w2, w3)));
+  m.total = o;
+  return m;
+}
+
+}  // namespace
+
+extern "C" int64_t bt_ml_matvec_ws_bytes(int64_t nterms, const int64_t* nin, const int64_t* nout,
+                                         int64_t nrhs) {
+  return ml_plan(nterms, nin, nout, nrhs).total * 8;
+}
+
+extern "C" int bt_ml_matvec_f64(int64_t nterms, const int64_t* nin, const int64_t* nout,
+                                const double* s1, const double* s2, const double* s3,
+                                const double* x, int64_t nrhs, double* y, void* wsv,
+                                int64_t ws_bytes, void* stream) {
+  BT_REQUIRE(nterms >= 1 && nrhs >= 1, BT_E_SHAPE, "ml_matvec: empty terms or RHS");
+  const int64_t R = nterms;
+  MlPlan mp = ml_plan(R, nin, nout, nrhs);
+  BT_REQUIRE(ws_bytes >= mp.total * 8, BT_E_VALUE, "ml_matvec: workspace too small");
+  cudaStream_t st = bt_stream(stream);
+  double* ws = static_cast<double*>(wsv);
+  double* U = ws + mp.off_u;
+  double* W2 = ws + mp.off_w2;
+  double* gws = ws + mp.off_gws;
+  const int64_t gws_n = mp.total - mp.off_gws;
+  const int64_t N3i = nin[0], N2i = nin[1], N1i = nin[2];
+  const int64_t N3o = nout[0], N2o = nout[1], N1o = nout[2];
+  for (int64_t s0 = 0; s0 < nrhs; s0 += mp.chunk) {
+    const int64_t ns = std::min(mp.chunk, nrhs - s0);
+    const double* xs = x + s0 * N3i * N2i * N1i;
+    double* ys = y + s0 * N3o * N2o * N1o;
+    // U[(s,a3,a2)][(r,i1)] = sum_a1 x[(s,a3,a2)][a1] S3[r][i1][a1]
+    BtGemmArgs g1{};
+    g1.M = ns * N3i * N2i;
+    g1.N = R * N1o;
+    g1.Kin = N1i;
+    g1.Kout = 1;
+    g1.A = BtOperand{xs, N1i, 0, 1, 0};
+    g1.B = BtOperand{s3, N1i, 0, 1, 0};
+    g1.C = U;
+    g1.sCm = R * N1o;
+    g1.sCn = 1;
+    g1.alpha = 1.0;
+    g1.ws = gws;
+    BT_TRY(bt_gemm_run(g1, 1, st, 0, gws_n));
+    // W2[(s,a3)][r][i2][i1] = sum_a2 S2[r][i2][a2] U[(s,a3)][a2][r][i1]
+    for (int64_t r = 0; r < R; ++r) {
+      BtGemmArgs g2{};
+      g2.M = N2o;
+      g2.N = N1o;
+      g2.Kin = N2i;
+      g2.Kout = 1;
+      g2.A = BtOperand{s2 + r * N2o * N2i, N2i, 0, 1, 0};
+      g2.B = BtOperand{U + r * N1o, 1, 0, R * N1o, N2i * R * N1o};
+      g2.C = W2 + r * N2o * N1o;
+      g2.sCm = N1o;
+      g2.sCn = 1;
+      g2.sCb = R * N2o * N1o;
+      g2.alpha = 1.0;
+      g2.ws = gws;
+      const int64_t batch = ns * N3i;
+      for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+        BtGemmArgs c = g2;
+        c.B.ptr = g2.B.ptr + b0 * g2.B.s_b;
+        c.C = g2.C + b0 * g2.sCb;
+        BT_TRY(bt_gemm_run(c, std::min<int64_t>(65535, batch - b0), st, 0, gws_n));
+      }
+    }
+    // y[s][i3][(i2,i1)] = sum_{r,a3} S1[r][i3][a3] W2[s][a3][r][(i2,i1)]
+    BtGemmArgs g3{};
+    g3.M = N3o;
+    g3.N = N2o * N1o;
+    g3.Kin = N3i;
+    g3.Kout = R;
+    g3.A = BtOperand{s1, N3i, N3o * N3i, 1, 0};
+    g3.B = BtOperand{W2, 1, N2o * N1o, R * N2o * N1o, N3i * R * N2o * N1o};
+    g3.C = ys;
+    g3.sCm = N2o * N1o;
+    g3.sCn = 1;
+    g3.sCb = N3o * N2o * N1o;
+    g3.alpha = 1.0;
+    g3.ws = gws;
+    BT_TRY(bt_gemm_run(g3, ns, st, 0, gws_n));
+  }
+  return BT_OK;
+}

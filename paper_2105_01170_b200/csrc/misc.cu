@@ -1,0 +1,255 @@
+// Deterministic reductions and the FP64 peak microbenchmarks.
+#include "bt_common.cuh"
+
+// ---------------------------------------------------------------------------
+// sum of squares (fro_norm, tensor.py:107-109) -- two-pass fixed tree
+// ---------------------------------------------------------------------------
+
+static constexpr int SUMSQ_BLOCKS = 1184;  // 8 x 148 SMs; fixed => deterministic
+
+__global__ void __launch_bounds__(256) bt_sumsq_partial(const double* __restrict__ x, int64_t n,
+                                                        double* __restrict__ part) {
+  double s = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool v2 = ((reinterpret_cast<uintptr_t>(x) & 15u) == 0);
+  if (v2) {
+    const int64_t n2 = n / 2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += stride) {
+      double2 v = ld_stream2(x + 2 * i);
+      s = fma(v.x, v.x, s);
+      s = fma(v.y, v.y, s);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {
+      double v = x[n - 1];
+      s = fma(v, v, s);
+    }
+  } else {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+      double v = ld_stream(x + i);
+      s = fma(v, v, s);
+    }
+  }
+  __shared__ double red[8];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void bt_sum_final(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    *out = t;
+  }
+}
+
+extern "C" int64_t bt_sumsq_ws_bytes(int64_t) { return SUMSQ_BLOCKS * 8; }
+int64_t bt_sumsq_ws_bytes_const() { return SUMSQ_BLOCKS; }
+
+extern "C" int bt_sumsq_f64(const double* x, int64_t n, double* out, void* ws, int64_t ws_bytes,
+                            void* stream) {
+  BT_REQUIRE(ws_bytes >= SUMSQ_BLOCKS * 8, BT_E_VALUE, "sumsq: workspace too small");
+  cudaStream_t st = bt_stream(stream);
+  double* part = static_cast<double*>(ws);
+  bt_sumsq_partial<<<SUMSQ_BLOCKS, 256, 0, st>>>(x, n, part);
+  BT_LAUNCH_CHECK();
+  bt_sum_final<<<1, 1024, 0, st>>>(part, SUMSQ_BLOCKS, out);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// FP64 peak microbenchmarks: DMMA.8x8x4 vs DFMA
+// ---------------------------------------------------------------------------
+
+template <int CHAINS>
+__global__ void bt_peak_dmma_kernel(int64_t iters, double* sink) {
+  double c[CHAINS][2];
+  const int lane = threadIdx.x & 31;
+  double a = 1.0 + 1e-9 * lane, b = 1.0 - 1e-9 * lane;
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < CHAINS; ++i) dmma884(c[i][0], c[i][1], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) sink[blockIdx.x] = s;
+}
+
+template <int CHAINS>
+__global__ void bt_peak_dfma_kernel(int64_t iters, double* sink) {
+  double c[CHAINS];
+  double a = 1.0 + 1e-9 * threadIdx.x, b = 1.0 - 1e-9 * threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i) c[i] = i;
+  for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < CHAINS; ++i) c[i] = fma(c[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i) s += c[i];
+  if (s == 12345.678) sink[blockIdx.x] = s;
+}
+
+extern "C" int bt_peak_dmma(int64_t iters, int blocks, int threads, double* sink, double* flops,
+                            void* stream) {
+  bt_peak_dmma_kernel<8><<<blocks, threads, 0, bt_stream(stream)>>>(iters, sink);
+  BT_LAUNCH_CHECK();
+  *flops = (double)blocks * (threads / 32) * (double)iters * 8 * 512.0;
+  return BT_OK;
+}
+
+extern "C" int bt_peak_dfma(int64_t iters, int blocks, int threads, double* sink, double* flops,
+                            void* stream) {
+  bt_peak_dfma_kernel<8><<<blocks, threads, 0, bt_stream(stream)>>>(iters, sink);
+  BT_LAUNCH_CHECK();
+  *flops = (double)blocks * threads * (double)iters * 8 * 2.0;
+  return BT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// z = alpha x + beta y
+// ---------------------------------------------------------------------------
+
+__global__ void bt_axpby_kernel(int64_t n, double alpha, const double* __restrict__ x, double beta,
+                                const double* __restrict__ y, double* __restrict__ z) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    z[i] = alpha * x[i] + beta * y[i];
+}
+
+extern "C" int bt_axpby_f64(int64_t n, double alpha, const double* x, double beta, const double* y,
+                            double* z, void* stream) {
+  if (n <= 0) return BT_OK;
+  const int64_t blocks = (n + 255) / 256 < 8192 ? (n + 255) / 256 : 8192;
+  bt_axpby_kernel<<<static_cast<int>(blocks), 256, 0, bt_stream(stream)>>>(n, alpha, x, beta, y, z);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// max |x| (deterministic; max is order independent) -- psd.py:184 scale
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) bt_maxabs_partial(const double* __restrict__ x, int64_t n,
+                                                         double* __restrict__ part) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    s = fmax(s, fabs(ld_stream(x + i)));
+  __shared__ double red[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t = fmax(t, red[w]);
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void bt_max_final(const double* __restrict__ part, int n, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t = fmax(t, part[i]);
+    *out = t;
+  }
+}
+
+extern "C" int bt_maxabs_f64(const double* x, int64_t n, double* out, void* ws, int64_t ws_bytes,
+                             void* stream) {
+  BT_REQUIRE(ws_bytes >= SUMSQ_BLOCKS * 8, BT_E_VALUE, "maxabs: workspace too small");
+  cudaStream_t st = bt_stream(stream);
+  double* part = static_cast<double*>(ws);
+  bt_maxabs_partial<<<SUMSQ_BLOCKS, 256, 0, st>>>(x, n, part);
+  BT_LAUNCH_CHECK();
+  bt_max_final<<<1, 32, 0, st>>>(part, SUMSQ_BLOCKS, out);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// transpose closure check (psd.py:141-161): class k fails iff
+// max|B[partner[k]] - B[k]^T| > tol with numpy NaN semantics
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256)
+    bt_transpose_check_kernel(const double* __restrict__ b, int64_t p, int64_t n,
+                              const int64_t* __restrict__ partner, double tol,
+                              int* __restrict__ flags) {
+  __shared__ int red[2][8];
+  for (int64_t k = blockIdx.x; k < p; k += gridDim.x) {
+    const double* bk = b + k * n * n;
+    const double* bp = b + partner[k] * n * n;
+    int exceed = 0, nan = 0;
+    for (int64_t e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int64_t i = e / n, j = e % n;
+      const double d = fabs(bp[i * n + j] - bk[j * n + i]);
+      exceed |= (d > tol);
+      nan |= (d != d);
+    }
+    exceed = __any_sync(0xffffffffu, exceed);
+    nan = __any_sync(0xffffffffu, nan);
+    if ((threadIdx.x & 31) == 0) {
+      red[0][threadIdx.x >> 5] = exceed;
+      red[1][threadIdx.x >> 5] = nan;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int e = 0, nn = 0;
+      for (int w = 0; w < 8; ++w) {
+        e |= red[0][w];
+        nn |= red[1][w];
+      }
+      flags[k] = (e && !nn) ? 1 : 0;
+    }
+    __syncthreads();
+  }
+}
+
+extern "C" int bt_transpose_check_f64(const double* blocks, int64_t p, int64_t n,
+                                      const int64_t* partner, double tol, void* ws,
+                                      int64_t* bad_class, void* stream) {
+  cudaStream_t st = bt_stream(stream);
+  int* flags = static_cast<int*>(ws);
+  const int grid = static_cast<int>(p < 148 * 8 ? p : 148 * 8);
+  bt_transpose_check_kernel<<<grid, 256, 0, st>>>(blocks, p, n, partner, tol, flags);
+  BT_LAUNCH_CHECK();
+  int* h = new int[p];
+  cudaError_t e1 = cudaMemcpyAsync(h, flags, sizeof(int) * p, cudaMemcpyDeviceToHost, st);
+  cudaError_t e2 = cudaStreamSynchronize(st);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    delete[] h;
+    bt_set_error("transpose check: %s", cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+    return BT_E_CUDA;
+  }
+  int64_t first = -1;
+  for (int64_t k = 0; k < p; ++k)
+    if (h[k]) {
+      first = k;
+      break;
+    }
+  delete[] h;
+  if (bad_class) *bad_class = first;
+  if (first >= 0) {
+    bt_set_error("class %lld: block transpose differs from its partner", (long long)(first + 1));
+    return BT_E_PATTERN;
+  }
+  return BT_OK;
+}

@@ -1,0 +1,214 @@
+"""GPU parity: GEMM engine, K1/K2 maps, CP-ALS, eigensolver, Tucker against
+the reference's golden vectors and the CPU oracle."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2105_01170_b200 as bt  # noqa: E402
+from paper_2105_01170_b200 import _linalg as L  # noqa: E402
+from paper_2105_01170_b200 import decomp  # noqa: E402
+from oracle import configs as oc  # noqa: E402
+from oracle import port  # noqa: E402
+
+from _helpers import pattern_from, subspace_angle  # noqa: E402
+
+
+def with_init(init):
+    saved = decomp._cp_init
+    decomp._cp_init = lambda t, r: [np.array(f, copy=True) for f in init]
+    return saved
+
+
+# ---------------------------------------------------------------------------
+# GEMM engine
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("shape", [(37, 29, 11), (300, 513, 70), (1000, 77, 9), (5, 4000, 64),
+                                   (130, 17, 130)])
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+def test_gemm_layouts(shape, ta, tb):
+    M, K, Nn = shape
+    g = torch.Generator(device="cuda").manual_seed(M + K + Nn)
+    a = torch.randn((K, M) if ta else (M, K), dtype=torch.float64, device="cuda", generator=g)
+    b = torch.randn((Nn, K) if tb else (K, Nn), dtype=torch.float64, device="cuda", generator=g)
+    ref = (a.T if ta else a) @ (b.T if tb else b)
+    got = L.gemm_dev(a, b, ta, tb)
+    assert torch.allclose(got, ref, rtol=0, atol=1e-12 * ref.abs().max().item())
+
+
+@pytest.mark.parametrize("dims,mode", [((7, 9, 5), 1), ((7, 9, 5), 2), ((7, 9, 5), 3),
+                                       ((40, 300, 33), 2), ((300, 4, 6), 1), ((3, 5, 260), 3)])
+def test_unfold_gram(dims, mode):
+    x = np.random.default_rng(1).standard_normal(dims)
+    g = L.unfold_gram_dev(torch.from_numpy(x).cuda(), mode).cpu().numpy()
+    u = port.unfold(x, mode)
+    np.testing.assert_allclose(g, u @ u.T, rtol=0, atol=1e-12 * np.abs(g).max())
+    assert np.array_equal(g, g.T)
+
+
+@pytest.mark.parametrize("dims,mode,rows", [((7, 9, 5), 1, 3), ((7, 9, 5), 2, 4), ((7, 9, 5), 3, 6),
+                                            ((64, 40, 130), 1, 8), ((64, 40, 130), 3, 70)])
+def test_mode_multiply(dims, mode, rows):
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal(dims)
+    u = rng.standard_normal((rows, dims[mode - 1]))
+    got = bt.mode_multiply(x, mode, u)
+    np.testing.assert_allclose(got, port.mode_multiply(x, mode, u), rtol=0,
+                               atol=1e-12 * np.abs(got).max())
+
+
+# ---------------------------------------------------------------------------
+# K1 / K2 maps: bit-exact against the reference's golden vectors
+# ---------------------------------------------------------------------------
+
+def test_gather_scatter_bit_exact(golden):
+    z = golden("maps")
+    for c in range(int(z["n_cases"])):
+        k = f"c{c}"
+        pat = pattern_from(z[k + "_cells"], z[k + "_offs"], z[k + "_dims"])
+        a = z[k + "_a"]
+        assert np.array_equal(bt.mat_to_tensor(a, pat), z[k + "_t"])
+        assert np.array_equal(bt.mat_to_tensor(a, pat, weighted=False), z[k + "_tu"])
+        assert np.array_equal(bt.tensor_to_mat(z[k + "_t"], pat), z[k + "_back"])
+        assert np.array_equal(bt.struct_scalars(pat, z[k + "_coeffs"]), z[k + "_scalars"])
+        blocks = bt.extract_blocks(a, pat)
+        assert np.array_equal(bt.struct_assemble(pat, blocks), a)
+
+
+def test_gather_rejects_like_the_reference():
+    rng = np.random.default_rng(4)
+    pat = bt.build_pattern("toeplitz", 3, 3, 2, 2)
+    a = bt.struct_assemble(pat, [rng.standard_normal((2, 2)) for _ in range(pat.p)])
+    bad = a.copy()
+    bad[-1, -1] += 1.0
+    with pytest.raises(bt.PatternMismatchError, match=r"class 1: block at grid cell \(3, 3\)"):
+        bt.mat_to_tensor(bad, pat)
+    diag = bt.build_pattern("diagonal", 2, 2, 2, 2)
+    b = bt.struct_assemble(diag, [rng.standard_normal((2, 2)) for _ in range(diag.p)])
+    b[0, -1] = 1.0
+    with pytest.raises(bt.PatternMismatchError, match=r"grid cell \(1, 2\) is outside"):
+        bt.extract_blocks(b, diag)
+    # numpy NaN semantics: a NaN difference masks the cell (np.max -> NaN > tol is False)
+    c = a.copy()
+    c[-1, -1] = np.nan
+    c[-2, -2] += 5.0
+    t = bt.mat_to_tensor(c, pat)
+    assert t.shape == (2, pat.p, 2)
+    # tolerance
+    d = a.copy()
+    d[-1, -1] += 1e-9
+    bt.mat_to_tensor(d, pat, tol=1e-8)
+
+
+# ---------------------------------------------------------------------------
+# CP-ALS
+# ---------------------------------------------------------------------------
+
+def test_cp_c1_matches_reference(golden):
+    z = golden("cp")
+    pat, a = oc.c1_inputs()
+    t = bt.mat_to_tensor(a, bt.build_pattern("toeplitz", 32, 32, 32, 32, block_symmetric=True))
+    assert np.array_equal(t, z["c1_t"])
+    saved = with_init(oc.normal_init(t.shape, 8, 0))
+    try:
+        res = bt.cp_als(t, 8, 50, 0.0)
+    finally:
+        decomp._cp_init = saved
+    np.testing.assert_allclose(np.array(res.fit_history), z["c1_hist"], rtol=0, atol=1e-10)
+    assert abs(res.fit - float(z["c1_fit"])) < 1e-10
+    recon = port.mode_multiply  # noqa: F841
+    got = np.einsum("ir,jr,kr->ijk", res.rep.x, res.rep.y, res.rep.z)
+    ref = np.einsum("ir,jr,kr->ijk", z["c1_x"], z["c1_y"], z["c1_z"])
+    assert np.linalg.norm(got - ref) <= 1e-8 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("fit", ["auto", "explicit", "gram"])
+def test_cp_mid_and_odd(golden, fit):
+    z = golden("cp")
+    for name in ("mid", "odd"):
+        t = z[f"{name}_t"]
+        r = int(z[f"{name}_r"])
+        saved = with_init(oc.normal_init(t.shape, r, 5))
+        try:
+            res = bt.cp_als(t, r, int(z[f"{name}_iters"]), 0.0, fit=fit)
+        finally:
+            decomp._cp_init = saved
+        np.testing.assert_allclose(np.array(res.fit_history), z[f"{name}_hist"], rtol=0,
+                                   atol=1e-9)
+        np.testing.assert_allclose(res.rep.x, z[f"{name}_x"], rtol=0, atol=1e-7)
+
+
+def test_cp_rank1_exact_and_padded_init(golden):
+    z = golden("cp")
+    res = bt.cp_als(z["rank1_t"], 1)
+    assert res.fit > 1 - 1e-13
+    np.testing.assert_allclose(np.einsum("ir,jr,kr->ijk", res.rep.x, res.rep.y, res.rep.z),
+                               z["rank1_t"], atol=1e-12)
+    res = bt.cp_als(z["pad_t"], 4, max_iters=200)
+    assert res.rep.x.shape == (2, 4)
+    assert 0 < res.fit <= 1 + 1e-12
+    assert abs(res.fit - float(z["pad_fit"])) < 1e-8
+
+
+def test_cp_c5_small(golden):
+    z = golden("cp")
+    i, j, k, r = (int(v) for v in z["c5s_dims"])
+    x = z["c5s_t"]
+    saved = with_init(oc.normal_init((i, j, k), r, 1003))
+    try:
+        res = bt.cp_als(x, r, 10, 0.0)
+    finally:
+        decomp._cp_init = saved
+    np.testing.assert_allclose(np.array(res.fit_history), z["c5s_hist"], rtol=0, atol=1e-9)
+
+
+def test_cp_rejects_bad_args():
+    with pytest.raises(ValueError):
+        bt.cp_als(np.zeros((2, 2, 2)), 1)
+    with pytest.raises(bt.ShapeError):
+        bt.cp_als(np.zeros((2, 2)), 1)
+    with pytest.raises(bt.ShapeError):
+        bt.cp_als(np.ones((2, 2, 2)), 0)
+
+
+# ---------------------------------------------------------------------------
+# eigensolver / SVD / Tucker
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [1, 2, 7, 64, 96, 97, 200, 513])
+def test_eigh(n):
+    rng = np.random.default_rng(n)
+    g = rng.standard_normal((n, n + 3))
+    a = g @ g.T
+    w, v = L.eigh_dev(torch.from_numpy(a).cuda())
+    w, v = w.cpu().numpy(), v.cpu().numpy()
+    ref = np.linalg.eigvalsh(a)[::-1]
+    np.testing.assert_allclose(w, ref, rtol=0, atol=1e-11 * ref[0])
+    np.testing.assert_allclose(v.T @ v, np.eye(n), atol=1e-12)
+    np.testing.assert_allclose(a @ v, v * w, atol=1e-11 * ref[0])
+    lead = np.argmax(np.abs(v), axis=0)
+    assert np.all(v[lead, np.arange(n)] > 0)
+
+
+def test_svd_truncated_sign_rule(golden):
+    z = golden("tucker")
+    u, s, v = bt.svd_truncated(z["svd_a"], 3)
+    np.testing.assert_allclose(u, z["svd_u"], atol=1e-12)
+    np.testing.assert_allclose(s, z["svd_s"], atol=1e-12)
+    np.testing.assert_allclose(v, z["svd_v"], atol=1e-12)
+
+
+def test_hosvd_golden(golden):
+    z = golden("tucker")
+    for n in range(int(z["n_hosvd"])):
+        rep = bt.hosvd(z[f"h{n}_t"], [int(v) for v in z[f"h{n}_ranks"]])
+        np.testing.assert_allclose(rep.core, z[f"h{n}_core"], atol=1e-12)
+        for k in range(3):
+            np.testing.assert_allclose(rep.factors[k], z[f"h{n}_u{k}"], atol=1e-12)
