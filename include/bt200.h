@@ -216,6 +216,8 @@ int bt_maxabs_f64(const double* x, int64_t n, double* out, void* ws, int64_t ws_
  * ws: p ints.  Synchronises the stream. */
 int bt_transpose_check_f64(const double* blocks, int64_t p, int64_t n, const int64_t* partner,
                            double tol, void* ws, int64_t* bad_class, void* stream);
+/* normalise every column of a row-major (rows x cols) matrix to unit 2-norm */
+int bt_col_normalize_f64(double* x, int64_t rows, int64_t cols, void* stream);
 /* z = alpha * x + beta * y elementwise (n doubles) */
 int bt_axpby_f64(int64_t n, double alpha, const double* x, double beta, const double* y, double* z,
                  void* stream);

@@ -17,6 +17,8 @@
 // (DMMA reconstruction tile - X tile) when the identity would lose digits.
 // Every reduction is a fixed-order tree: results are bit-reproducible.
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 #include <cmath>
 #include <vector>
 
@@ -403,29 +405,62 @@ __global__ void residual_finish_kernel(const double* __restrict__ part, int n, C
 // host-side plan
 // ---------------------------------------------------------------------------
 
-template <int BN>
+template <int BN, int VARIANT = 0>
 struct TreeCfgSel;
-template <>
-struct TreeCfgSel<64> {
+template <int VARIANT>
+struct TreeCfgSel<64, VARIANT> {
+  // variants for tuning (BT_TREE_CFG): 0 default
   template <int V>
-  using Cfg = GemmCfg<128, 64, 16, 4, 2, 4, true, false, V>;
+  using Cfg = typename std::conditional<
+      VARIANT == 1, GemmCfg<128, 64, 16, 4, 2, 3, true, false, V>,
+      typename std::conditional<
+          VARIANT == 2, GemmCfg<128, 64, 32, 4, 2, 3, true, false, V>,
+          typename std::conditional<
+              VARIANT == 3, GemmCfg<128, 64, 32, 4, 2, 2, true, false, V>,
+              typename std::conditional<
+                  VARIANT == 4, GemmCfg<256, 64, 16, 8, 2, 3, true, false, V>,
+                  typename std::conditional<
+                      VARIANT == 5, GemmCfg<64, 64, 16, 2, 2, 4, true, false, V>,
+                      typename std::conditional<
+                          VARIANT == 6, GemmCfg<128, 64, 16, 2, 2, 3, true, false, V>,
+                          typename std::conditional<
+                              VARIANT == 7, GemmCfg<128, 64, 16, 4, 2, 2, true, false, V>,
+                              typename std::conditional<
+                                  VARIANT == 8, GemmCfg<64, 64, 16, 2, 2, 3, true, false, V>,
+                                  GemmCfg<128, 64, 16, 4, 2, 4, true, false, V>>::type>::type>::
+                          type>::type>::type>::type>::type>::type;
 };
-template <>
-struct TreeCfgSel<16> {
+template <int VARIANT>
+struct TreeCfgSel<16, VARIANT> {
   template <int V>
   using Cfg = GemmCfg<128, 16, 16, 8, 1, 4, true, false, V>;
 };
-template <>
-struct TreeCfgSel<8> {
+template <int VARIANT>
+struct TreeCfgSel<8, VARIANT> {
   template <int V>
   using Cfg = GemmCfg<128, 8, 16, 8, 1, 4, true, false, V>;
 };
+
+int tree_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BT_TREE_CFG");
+    v = e ? atoi(e) : 6;  // variant 6 (128x64, 4 warps of 64x32, 3 stages) tuned best
+  }
+  return v;
+}
 
 // residual: rows j, cols k, reduction r (K-contig on both sides)
 template <int V>
 using ResCfg = GemmCfg<128, 64, 16, 4, 2, 3, true, true, V>;
 
 int tree_bn(int64_t R) { return R <= 8 ? 8 : (R <= 16 ? 16 : 64); }
+
+int tree_bm(int bn) {
+  if (bn != 64) return 128;
+  const int v = tree_variant();
+  return v == 4 ? 256 : ((v == 5 || v == 8) ? 64 : 128);
+}
 
 struct Plan {
   int64_t I, J, K, R;
@@ -467,7 +502,7 @@ Plan make_plan(const bt_cp_problem* pb) {
   pl.K = pb->K;
   pl.R = pb->R;
   pl.bn = tree_bn(pl.R);
-  pl.jtiles = bt_cdiv(pl.J, 128);
+  pl.jtiles = bt_cdiv(pl.J, tree_bm(pl.bn));
   const int64_t JR = pl.J * pl.R;
   // mode 2: enough CTAs along (j, r) x i-chunks to fill the GPU ~4x
   const int64_t blocks_jr = std::max<int64_t>(1, std::min<int64_t>(bt_cdiv(JR, 256), 2048));
@@ -501,10 +536,10 @@ Plan make_plan(const bt_cp_problem* pb) {
   return pl;
 }
 
-template <int BN, int V>
+template <int BN, int V, int VAR = 0>
 int launch_tree(const Plan& pl, const double* X, const double* C, const double* B, double* P,
                 double* m1part, int store_p, cudaStream_t st) {
-  using Cfg = typename TreeCfgSel<BN>::template Cfg<V>;
+  using Cfg = typename TreeCfgSel<BN, VAR>::template Cfg<V>;
   BtGemmArgs g{};
   g.M = pl.J;
   g.N = pl.R;
@@ -526,7 +561,7 @@ int launch_tree(const Plan& pl, const double* X, const double* C, const double* 
   }
   BT_REQUIRE(pl.I <= 65535, BT_E_SHAPE, "cp: mode-1 extent %lld exceeds 65535",
              (long long)pl.I);
-  dim3 grid(static_cast<unsigned>(pl.jtiles), static_cast<unsigned>(bt_cdiv(pl.R, BN)),
+  dim3 grid(static_cast<unsigned>(bt_cdiv(pl.J, Cfg::BM)), static_cast<unsigned>(bt_cdiv(pl.R, BN)),
             static_cast<unsigned>(pl.I));
   tree_p_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(g, B, pl.R, m1part, pl.jtiles,
                                                                    store_p);
@@ -546,8 +581,20 @@ int run_tree(const Plan& pl, const double* X, const double* C, const double* B, 
       return v2 ? launch_tree<16, 2>(pl, X, C, B, P, m1part, store_p, st)
                 : launch_tree<16, 1>(pl, X, C, B, P, m1part, store_p, st);
     default:
-      return v2 ? launch_tree<64, 2>(pl, X, C, B, P, m1part, store_p, st)
-                : launch_tree<64, 1>(pl, X, C, B, P, m1part, store_p, st);
+      if (v2) {
+        switch (tree_variant()) {
+          case 1: return launch_tree<64, 2, 1>(pl, X, C, B, P, m1part, store_p, st);
+          case 2: return launch_tree<64, 2, 2>(pl, X, C, B, P, m1part, store_p, st);
+          case 3: return launch_tree<64, 2, 3>(pl, X, C, B, P, m1part, store_p, st);
+          case 4: return launch_tree<64, 2, 4>(pl, X, C, B, P, m1part, store_p, st);
+          case 5: return launch_tree<64, 2, 5>(pl, X, C, B, P, m1part, store_p, st);
+          case 6: return launch_tree<64, 2, 6>(pl, X, C, B, P, m1part, store_p, st);
+          case 7: return launch_tree<64, 2, 7>(pl, X, C, B, P, m1part, store_p, st);
+          case 8: return launch_tree<64, 2, 8>(pl, X, C, B, P, m1part, store_p, st);
+          default: return launch_tree<64, 2>(pl, X, C, B, P, m1part, store_p, st);
+        }
+      }
+      return launch_tree<64, 1>(pl, X, C, B, P, m1part, store_p, st);
   }
 }
 

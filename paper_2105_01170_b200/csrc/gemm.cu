@@ -116,15 +116,17 @@ int bt_gemm_launch(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits
 }
 
 // configurations ------------------------------------------------------------
-// wide: 128x64 CTA tile, 8 warps of 32x32, BK 16, 4 stages (~120 KB smem)
+// (tuned on B200, tools/tune_gemm.py: 2 CTAs per SM with 64x32 warp tiles win)
+// wide: 128x64 CTA tile, 4 warps of 64x32, BK 16, 4 stages (~102 KB smem, 2 CTAs/SM)
 template <bool AK, bool BKc, int V>
-using CfgWide = GemmCfg<128, 64, 16, 4, 2, 4, AK, BKc, V>;
+using CfgWide = GemmCfg<128, 64, 16, 2, 2, 4, AK, BKc, V>;
 // narrow: 128x16 CTA tile for N <= 16 (Grams of R <= 16 factors, TTM r <= 16)
 template <bool AK, bool BKc, int V>
 using CfgNarrow = GemmCfg<128, 16, 16, 8, 1, 4, AK, BKc, V>;
-// square: 128x128 for symmetric (SYRK) outputs, 8 warps of 64x32
+// square: 128x128 for N > 64 and symmetric (SYRK) outputs, 8 warps of 64x32,
+// 2 stages (~78 KB smem, 2 CTAs/SM)
 template <bool AK, bool BKc, int V>
-using CfgSquare = GemmCfg<128, 128, 16, 2, 4, 3, AK, BKc, V>;
+using CfgSquare = GemmCfg<128, 128, 16, 2, 4, 2, AK, BKc, V>;
 
 // tuning alternatives (selected with BT_GEMM_CFG=<id> for experiments)
 template <bool AK, bool BKc, int V>
@@ -135,6 +137,12 @@ template <bool AK, bool BKc, int V>
 using CfgTall = GemmCfg<256, 64, 16, 4, 2, 3, AK, BKc, V>;
 template <bool AK, bool BKc, int V>
 using CfgW4 = GemmCfg<128, 64, 16, 2, 2, 4, AK, BKc, V>;
+template <bool AK, bool BKc, int V>
+using CfgW4s3 = GemmCfg<128, 64, 16, 2, 2, 3, AK, BKc, V>;
+template <bool AK, bool BKc, int V>
+using CfgW4k32 = GemmCfg<128, 64, 32, 2, 2, 2, AK, BKc, V>;
+template <bool AK, bool BKc, int V>
+using CfgBig2 = GemmCfg<128, 128, 16, 2, 4, 2, AK, BKc, V>;
 
 static int bt_tune_cfg() {
   static int v = -2;
@@ -199,7 +207,8 @@ int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, i
                   (b_row % 2 == 0) && (g.A.s_ko % 2 == 0) && (g.B.s_ko % 2 == 0) &&
                   (g.A.s_b % 2 == 0) && (g.B.s_b % 2 == 0);
   const int vec = v2 ? 2 : 1;
-  int cls = g.symmetric ? BT_TILE_SQUARE : (g.N <= 16 ? BT_TILE_NARROW : BT_TILE_WIDE);
+  int cls = g.symmetric ? BT_TILE_SQUARE
+                        : (g.N <= 16 ? BT_TILE_NARROW : (g.N <= 64 ? BT_TILE_WIDE : BT_TILE_SQUARE));
   // workspace check (computed with the same geometry the launcher will use)
   BtGemmArgs probe = g;
   if (cls == BT_TILE_SQUARE)
@@ -225,6 +234,9 @@ int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, i
       case 2: return bt_dispatch_layout<CfgBig>(g, batch, st, ak, bk, vec, want_splits);
       case 3: return bt_dispatch_layout<CfgTall>(g, batch, st, ak, bk, vec, want_splits);
       case 4: return bt_dispatch_layout<CfgW4>(g, batch, st, ak, bk, vec, want_splits);
+      case 5: return bt_dispatch_layout<CfgW4s3>(g, batch, st, ak, bk, vec, want_splits);
+      case 6: return bt_dispatch_layout<CfgW4k32>(g, batch, st, ak, bk, vec, want_splits);
+      case 7: return bt_dispatch_layout<CfgBig2>(g, batch, st, ak, bk, vec, want_splits);
       default: break;
     }
   }
@@ -236,7 +248,8 @@ int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, i
 int64_t bt_gemm_ws_elems(BtGemmArgs g, int64_t batch) {
   if (!g.symmetric && g.bscale == nullptr && g.ascale == nullptr && g.N > g.M && g.N > 64)
     std::swap(g.M, g.N);
-  int cls = g.symmetric ? BT_TILE_SQUARE : (g.N <= 16 ? BT_TILE_NARROW : BT_TILE_WIDE);
+  int cls = g.symmetric ? BT_TILE_SQUARE
+                        : (g.N <= 16 ? BT_TILE_NARROW : (g.N <= 64 ? BT_TILE_WIDE : BT_TILE_SQUARE));
   if (cls == BT_TILE_SQUARE)
     bt_gemm_geometry<CfgSquare<true, true, 1>>(g, batch, 0);
   else if (cls == BT_TILE_NARROW)

@@ -253,3 +253,28 @@ extern "C" int bt_transpose_check_f64(const double* blocks, int64_t p, int64_t n
   }
   return BT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// x[:, c] /= ||x[:, c]||  (row-major rows x cols; one warp per column)
+// ---------------------------------------------------------------------------
+
+__global__ void bt_col_normalize_kernel(double* __restrict__ x, int64_t rows, int64_t cols) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); c < cols;
+       c += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    double s = 0.0;
+    for (int64_t r = lane; r < rows; r += 32) s = fma(x[r * cols + c], x[r * cols + c], s);
+    s = warp_sum(s);
+    const double nrm = sqrt(s);
+    if (nrm > 0.0)
+      for (int64_t r = lane; r < rows; r += 32) x[r * cols + c] = x[r * cols + c] / nrm;
+  }
+}
+
+extern "C" int bt_col_normalize_f64(double* x, int64_t rows, int64_t cols, void* stream) {
+  if (rows <= 0 || cols <= 0) return BT_OK;
+  const int64_t blocks = (cols + 7) / 8 < 1024 ? (cols + 7) / 8 : 1024;
+  bt_col_normalize_kernel<<<static_cast<int>(blocks), 256, 0, bt_stream(stream)>>>(x, rows, cols);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
