@@ -43,7 +43,7 @@ def eigh_dev(gd):
     return w, v
 
 
-RESOLVE_TAU = 1e-8   # eigenvalues above tau * lambda_max are resolved by one Gram pass
+RESOLVE_TAU = 1e-4   # per pass: eigenvectors with lambda > tau * lambda_max are kept (cut accuracy ~eps/tau)
 
 
 def _gram_modes(xd, modes):

@@ -251,23 +251,36 @@ struct CpState {
   double* fit_hist;    // max_iters
 };
 
-// Reduce Gram partials, column norms (0 -> 1), normalised Gram; mode 3 also
-// sets lambda, the Gram-identity fit and the explicit/identity decision.
+// Sum the per-CTA Gram partials (and <F_un, M> partials) of one solve into
+// gbuf = [G_un (R*R), inner, 0] -- the buffer a mode-3-sharded caller sums
+// across ranks before the finish.
 __global__ void __launch_bounds__(256)
-    solve_finish_kernel(const double* __restrict__ gram_part, int64_t nparts, int R,
-                        double* __restrict__ norms, double* __restrict__ gram_out,
-                        double* __restrict__ lam, const double* __restrict__ inner_part,
-                        CpState st, int it, int fit_mode) {
-  __shared__ double nrm[PINV_MAX_R];
-  __shared__ double red[8];
+    gram_reduce_kernel(const double* __restrict__ gram_part, int64_t nparts, int R,
+                       const double* __restrict__ inner_part, double* __restrict__ gbuf) {
   for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
     double s = 0.0;
     for (int64_t p = 0; p < nparts; ++p) s += gram_part[p * R * R + idx];
-    gram_out[idx] = s;
+    gbuf[idx] = s;
   }
-  __syncthreads();
+  if (threadIdx.x == 0) {
+    double inner = 0.0;
+    if (inner_part)
+      for (int64_t p = 0; p < nparts; ++p) inner += inner_part[p];
+    gbuf[R * R] = inner;
+    gbuf[R * R + 1] = 0.0;
+  }
+}
+
+// Column norms (0 -> 1) from the Gram diagonal, normalised Gram; the mode-3
+// update also sets lambda, the Gram-identity fit and the explicit decision.
+__global__ void __launch_bounds__(256)
+    solve_finish_kernel(const double* __restrict__ gbuf, int R, double* __restrict__ norms,
+                        double* __restrict__ gram_out, double* __restrict__ lam, CpState st,
+                        int it, int fit_mode) {
+  __shared__ double nrm[PINV_MAX_R];
+  __shared__ double red[8];
   for (int r = threadIdx.x; r < R; r += blockDim.x) {
-    double v = sqrt(gram_out[r * R + r]);
+    double v = sqrt(gbuf[r * R + r]);
     if (v == 0.0) v = 1.0;
     nrm[r] = v;
     norms[r] = v;
@@ -276,7 +289,7 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
     const int a = idx / R, b = idx % R;
-    gram_out[idx] = gram_out[idx] / (nrm[a] * nrm[b]);
+    gram_out[idx] = gbuf[idx] / (nrm[a] * nrm[b]);
   }
   if (lam == nullptr) return;
   __syncthreads();
@@ -292,13 +305,13 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) {
     double xh2 = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) xh2 += red[w];
-    double inner = 0.0;
-    for (int64_t p = 0; p < nparts; ++p) inner += inner_part[p];
+    const double inner = gbuf[R * R];
     const double x2 = st.scal[0];
     const double res2 = fmax(x2 - 2.0 * inner + xh2, 0.0);
     const double relres = sqrt(res2 / x2);
     st.scal[1] = inner;
-    // identity error ~ c*eps*||X||^2 / (2 res): keep it below ~1e-12 in fit
+    // identity error ~ c*eps*||X||^2 / (2 res): switch to the explicit
+    // residual once the relative residual is small enough to lose digits
     const bool explicit_fit = (fit_mode == 1) || (fit_mode == 0 && relres < 1e-3);
     st.scal[3] = explicit_fit ? 1.0 : 0.0;
     st.fit_hist[it] = 1.0 - relres;
@@ -392,13 +405,24 @@ __global__ void __launch_bounds__(Cfg::THREADS)
   }
 }
 
-__global__ void residual_finish_kernel(const double* __restrict__ part, int n, CpState st, int it) {
+__global__ void residual_reduce_kernel(const double* __restrict__ part, int n,
+                                       double* __restrict__ out) {
   if (threadIdx.x != 0) return;
-  if (st.scal[3] == 0.0) return;
   double s = 0.0;
   for (int k = 0; k < n; ++k) s += part[k];
-  st.scal[2] = s;
-  st.fit_hist[it] = 1.0 - sqrt(s) / sqrt(st.scal[0]);
+  out[0] = s;
+}
+
+__global__ void residual_finish_kernel(const double* __restrict__ res2, CpState st, int it) {
+  if (threadIdx.x != 0) return;
+  if (st.scal[3] == 0.0) return;
+  st.scal[2] = res2[0];
+  st.fit_hist[it] = 1.0 - sqrt(res2[0]) / sqrt(st.scal[0]);
+}
+
+// buf[0] = sum of squares partial result copy (init finish helper)
+__global__ void copy_scalar_kernel(const double* __restrict__ src, double* __restrict__ dst) {
+  if (threadIdx.x == 0) dst[0] = src[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -472,7 +496,7 @@ struct Plan {
   int res_grid;
   // workspace layout (doubles)
   int64_t off_p, off_m1, off_m2, off_m3, off_m3ws, off_gp, off_ip, off_f, off_state, off_res,
-      off_w, total;
+      off_w, off_m1d, off_m2d, off_gbuf, off_init, off_res1, total;
   int64_t m3_ws_elems;
 };
 
@@ -532,6 +556,11 @@ Plan make_plan(const bt_cp_problem* pb) {
   pl.off_state = take(3 * RR + RR + 2 * pl.R + 8);
   pl.off_res = take(std::max<int64_t>(pl.res_grid, 2048));
   pl.off_w = take(pl.I * pl.R);
+  pl.off_m1d = take(pl.I * pl.R);
+  pl.off_m2d = take(pl.J * pl.R);
+  pl.off_gbuf = take(pl.R * pl.R + 2);
+  pl.off_init = take(pl.R * pl.R + 2);
+  pl.off_res1 = take(2);
   pl.total = o;
   return pl;
 }
@@ -627,10 +656,11 @@ int run_pinv(const double* g0, const double* g1, int R, double* vp, cudaStream_t
   return BT_OK;
 }
 
-// One factor update: F_k <- normalise((sum parts) pinv(G_o0 o G_o1)).
-int run_solve(const Plan& pl, const CpState& s, double* ws, const double* mpart, int64_t nparts,
-              int64_t part_stride, int64_t row_stride, int64_t rows, int go0, int go1, double* F, int k,
-              bool last_mode, int it, int fit_mode, cudaStream_t st) {
+// Factor update, local half: Vp = pinv(G_o0 o G_o1), F_un = M Vp (M summed
+// over nparts partials), gbuf = [F_un^T F_un, <F_un, M>] (summed over CTAs).
+int run_solve_rows(const Plan& pl, const CpState& s, double* ws, const double* mpart,
+                   int64_t nparts, int64_t part_stride, int64_t row_stride, int64_t rows, int go0,
+                   int go1, double* F, bool with_inner, double* gbuf, cudaStream_t st) {
   const int R = static_cast<int>(pl.R);
   BT_TRY(run_pinv(s.gram[go0], s.gram[go1], R, s.vp, st));
   const int64_t parts = bt_cdiv(rows, SOLVE_ROWS);
@@ -644,16 +674,29 @@ int run_solve(const Plan& pl, const CpState& s, double* ws, const double* mpart,
                                        (2 * SOLVE_ROWS * PINV_MAX_R + PINV_MAX_R * PINV_MAX_R) * 8));
     attr = true;
   }
-  solve_apply_kernel<<<static_cast<unsigned>(parts), 256, sm, st>>>(
-      mpart, nparts, part_stride, row_stride, s.vp, rows, R, F, gp, last_mode ? ip : nullptr);
+  if (parts > 0) {
+    solve_apply_kernel<<<static_cast<unsigned>(parts), 256, sm, st>>>(
+        mpart, nparts, part_stride, row_stride, s.vp, rows, R, F, gp, with_inner ? ip : nullptr);
+    BT_LAUNCH_CHECK();
+  }
+  gram_reduce_kernel<<<1, 256, 0, st>>>(gp, parts, R, with_inner ? ip : nullptr, gbuf);
   BT_LAUNCH_CHECK();
-  solve_finish_kernel<<<1, 256, 0, st>>>(gp, parts, R, s.norms, s.gram[k],
-                                         last_mode ? s.lam : nullptr, ip, s, it, fit_mode);
+  return BT_OK;
+}
+
+// Factor update, finishing half (after a possible cross-rank sum of gbuf).
+int run_solve_finish(const Plan& pl, const CpState& s, const double* gbuf, int64_t rows,
+                     double* F, int k, bool last_mode, int it, int fit_mode, cudaStream_t st) {
+  const int R = static_cast<int>(pl.R);
+  solve_finish_kernel<<<1, 256, 0, st>>>(gbuf, R, s.norms, s.gram[k], last_mode ? s.lam : nullptr,
+                                         s, it, fit_mode);
   BT_LAUNCH_CHECK();
   const int64_t n = rows * pl.R;
-  scale_cols_kernel<<<static_cast<unsigned>(std::min<int64_t>(bt_cdiv(n, 256), 4096)), 256, 0,
-                      st>>>(F, rows, R, s.norms);
-  BT_LAUNCH_CHECK();
+  if (n > 0) {
+    scale_cols_kernel<<<static_cast<unsigned>(std::min<int64_t>(bt_cdiv(n, 256), 4096)), 256, 0,
+                        st>>>(F, rows, R, s.norms);
+    BT_LAUNCH_CHECK();
+  }
   return BT_OK;
 }
 
@@ -694,176 +737,18 @@ int residual_pass(const Plan& pl, const double* X, const double* W, const double
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// C-ABI
+// CP-ALS state + phase API.  A sweep is
+//   mttkrp(1) -> [sum over ranks] -> solve(1) -> finish(1)
+//   mttkrp(2) -> [sum over ranks] -> solve(2) -> finish(2)
+//   mttkrp(3) ->                     solve(3) -> [sum gbuf]  -> finish(3)
+//   residual  -> [sum over ranks] -> residual_finish
+// where the bracketed sums are the only cross-GPU exchanges when the tensor
+// is sharded along mode 3 (A, B replicated; C row-sharded).  One GPU runs the
+// same phases with the sums skipped (bt_cp_als_f64).
 // ---------------------------------------------------------------------------
 
-static int64_t cp_total_ws(const Plan& pl) { return pl.total + 16; }
-
-extern "C" int64_t bt_cp_als_ws_bytes(const bt_cp_problem* pb) {
-  Plan pl = make_plan(pb);
-  return cp_total_ws(pl) * 8;
-}
-
-extern "C" int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, double* c,
-                             double* lam, int max_iters, double tol, int fit_mode,
-                             double* fit_history, int* n_iters, int* converged, double* phase_ms,
-                             void* wsv, int64_t ws_bytes, void* stream) {
-  BT_REQUIRE(pb->I >= 1 && pb->J >= 1 && pb->K >= 1, BT_E_SHAPE, "cp_als: empty tensor");
-  BT_REQUIRE(pb->R >= 1, BT_E_SHAPE, "CP rank must be at least 1");
-  BT_REQUIRE(pb->R <= PINV_MAX_R, BT_E_SHAPE, "cp_als: rank %lld above the on-chip limit %d",
-             (long long)pb->R, PINV_MAX_R);
-  BT_REQUIRE(max_iters >= 1, BT_E_VALUE, "max_iters must be at least 1");
-  cudaStream_t st = bt_stream(stream);
-  Plan pl = make_plan(pb);
-  BT_REQUIRE(ws_bytes >= cp_total_ws(pl) * 8, BT_E_VALUE, "cp_als: workspace too small");
-  double* ws = static_cast<double*>(wsv);
-  const int R = static_cast<int>(pl.R);
-  const int64_t RR = pl.R * pl.R;
-  CpState s;
-  double* sb = ws + pl.off_state;
-  s.gram[0] = sb;
-  s.gram[1] = sb + RR;
-  s.gram[2] = sb + 2 * RR;
-  s.vp = sb + 3 * RR;
-  s.norms = sb + 4 * RR;
-  s.lam = lam;
-  s.scal = sb + 4 * RR + pl.R;
-  std::vector<double> hist(max_iters, 0.0);
-  // per-sweep fit values stay on device until the end (stream-ordered scratch)
-  double* dhist = nullptr;
-  BT_CUDA_CHECK(cudaMallocAsync(&dhist, sizeof(double) * max_iters, st));
-  s.fit_hist = dhist;
-  const double* X = pb->x;
-  double* F[3] = {a, b, c};
-  const int64_t rows[3] = {pl.I, pl.J, pl.K};
-
-  // ||X||^2
-  if (pb->norm_x > 0.0) {
-    const double x2 = pb->norm_x * pb->norm_x;
-    BT_CUDA_CHECK(cudaMemcpyAsync(s.scal, &x2, 8, cudaMemcpyHostToDevice, st));
-  } else {
-    BT_TRY(bt_sumsq_f64(X, pl.I * pl.J * pl.K, s.scal, ws + pl.off_res, 2048 * 8, st));
-  }
-  // initial Grams
-  for (int k = 0; k < 3; ++k) {
-    gram_kernel<<<1, 256, 0, st>>>(F[k], rows[k], R, s.gram[k]);
-    BT_LAUNCH_CHECK();
-  }
-
-  double* P = ws + pl.off_p;
-  double* m1 = ws + pl.off_m1;
-  double* m2 = ws + pl.off_m2;
-  double* m3 = ws + pl.off_m3;
-  double* m3ws = ws + pl.off_m3ws;
-  double* W = ws + pl.off_w;
-  double* rpart = ws + pl.off_res;
-  const bool res_v2 = (pl.R % 2 == 0);
-
-  double prev = -INFINITY;
-  int it = 0;
-  int conv = 0;
-  // optional phase timing: 5 events per sweep (stream-ordered, read at the end)
-  std::vector<cudaEvent_t> ev;
-  auto mark = [&]() -> int {
-    if (!phase_ms) return BT_OK;
-    cudaEvent_t e;
-    BT_CUDA_CHECK(cudaEventCreate(&e));
-    BT_CUDA_CHECK(cudaEventRecord(e, st));
-    ev.push_back(e);
-    return BT_OK;
-  };
-  for (it = 1; it <= max_iters; ++it) {
-    const int ix = it - 1;
-    BT_TRY(mark());
-    // mode 1: P = X x3 C ; M1 = sum_j P o B
-    BT_TRY(run_tree(pl, X, c, b, P, m1, 1, st));
-    BT_TRY(mark());
-    BT_TRY(run_solve(pl, s, ws, m1, pl.jtiles, pl.R, pl.jtiles * pl.R, pl.I, 1, 2, a, 0, false,
-                     ix, fit_mode, st));
-    // mode 2: M2 = sum_i P o A_new   (rows j)
-    BT_TRY(mark());
-    BT_TRY(run_mode2(pl, P, a, m2, st));
-    BT_TRY(mark());
-    BT_TRY(run_solve(pl, s, ws, m2, pl.s2, pl.J * pl.R, pl.R, pl.J, 0, 2, b, 1, false, ix,
-                     fit_mode, st));
-    // mode 3: M3 = X_(3) (B kr A)
-    BT_TRY(mark());
-    BT_TRY(run_mode3(pl, X, a, b, m3, m3ws, st));
-    BT_TRY(mark());
-    BT_TRY(run_solve(pl, s, ws, m3, 1, 0, pl.R, pl.K, 0, 1, c, 2, true, ix, fit_mode, st));
-    // explicit residual when requested / when the Gram identity is unreliable
-    if (fit_mode != 2) {
-      lam_scale_kernel<<<static_cast<unsigned>(std::min<int64_t>(bt_cdiv(pl.I * pl.R, 256), 4096)),
-                         256, 0, st>>>(a, lam, pl.I, R, W);
-      BT_LAUNCH_CHECK();
-      if (res_v2)
-        BT_TRY(residual_pass<2>(pl, X, W, b, c, s.scal + 3, rpart, st));
-      else
-        BT_TRY(residual_pass<1>(pl, X, W, b, c, s.scal + 3, rpart, st));
-      residual_finish_kernel<<<1, 32, 0, st>>>(rpart, pl.res_grid, s, ix);
-      BT_LAUNCH_CHECK();
-    }
-    BT_TRY(mark());
-    if (tol > 0.0) {
-      double fit = 0.0;
-      BT_CUDA_CHECK(cudaMemcpyAsync(&fit, dhist + ix, 8, cudaMemcpyDeviceToHost, st));
-      BT_CUDA_CHECK(cudaStreamSynchronize(st));
-      if (std::fabs(fit - prev) < tol) {
-        conv = 1;
-        break;
-      }
-      prev = fit;
-    }
-  }
-  if (it > max_iters) it = max_iters;
-  // KruskalRep.x = F0 * lambda (decomp.py:403)
-  lam_scale_kernel<<<static_cast<unsigned>(std::min<int64_t>(bt_cdiv(pl.I * pl.R, 256), 4096)), 256,
-                     0, st>>>(a, lam, pl.I, R, a);
-  BT_LAUNCH_CHECK();
-  BT_CUDA_CHECK(cudaMemcpyAsync(hist.data(), dhist, sizeof(double) * it, cudaMemcpyDeviceToHost,
-                                st));
-  BT_CUDA_CHECK(cudaFreeAsync(dhist, st));
-  BT_CUDA_CHECK(cudaStreamSynchronize(st));
-  for (int k = 0; k < it; ++k) fit_history[k] = hist[k];
-  *n_iters = it;
-  *converged = conv;
-  if (phase_ms) {
-    // events per sweep: [t0 tree t1 solve1 t2 mode2 t3 solve2 t4 mode3 t5 solve3+fit t6]
-    for (int k = 0; k < 4; ++k) phase_ms[k] = 0.0;
-    for (size_t base = 0; base + 7 <= ev.size(); base += 7) {
-      float ms = 0.f;
-      auto el = [&](int x, int y) {
-        cudaEventElapsedTime(&ms, ev[base + x], ev[base + y]);
-        return static_cast<double>(ms);
-      };
-      phase_ms[0] += el(0, 1);
-      phase_ms[1] += el(2, 3);
-      phase_ms[2] += el(4, 5);
-      phase_ms[3] += el(1, 2) + el(3, 4) + el(5, 6);
-    }
-    for (auto e : ev) cudaEventDestroy(e);
-  }
-  return BT_OK;
-}
-
-extern "C" int64_t bt_mttkrp_ws_bytes(const bt_cp_problem* pb, int mode) {
-  Plan pl = make_plan(pb);
-  (void)mode;
-  return pl.total * 8;
-}
-
-// reduce partials (fixed order) into out (rows x R)
 namespace {
-__global__ void reduce_parts_kernel(const double* __restrict__ part, int64_t nparts,
-                                    int64_t stride, int64_t n, double* __restrict__ out) {
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int64_t p = 0; p < nparts; ++p) s += part[p * stride + idx];
-    out[idx] = s;
-  }
-}
-// m1part is laid out [i][jt][r]: reduce over jt
+
 __global__ void reduce_m1_kernel(const double* __restrict__ part, int64_t I, int64_t jt,
                                  int64_t R, double* __restrict__ out) {
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < I * R;
@@ -874,7 +759,334 @@ __global__ void reduce_m1_kernel(const double* __restrict__ part, int64_t I, int
     out[idx] = s;
   }
 }
+
+__global__ void reduce_parts_kernel(const double* __restrict__ part, int64_t nparts,
+                                    int64_t stride, int64_t n, double* __restrict__ out) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t p = 0; p < nparts; ++p) s += part[p * stride + idx];
+    out[idx] = s;
+  }
+}
+
+unsigned grid_n(int64_t n) { return static_cast<unsigned>(std::min<int64_t>(bt_cdiv(n, 256), 4096)); }
+
 }  // namespace
+
+struct bt_cp_state {
+  Plan pl;
+  CpState s;
+  double* ws;
+  double* dhist;
+  int max_iters;
+  int fit_mode;
+  cudaStream_t st;
+  const double* X;
+  double* F[3];
+  double* lam;
+};
+
+static int64_t cp_total_ws(const Plan& pl) { return pl.total + 16; }
+
+extern "C" int64_t bt_cp_als_ws_bytes(const bt_cp_problem* pb) {
+  Plan pl = make_plan(pb);
+  return cp_total_ws(pl) * 8;
+}
+
+extern "C" int64_t bt_cp_state_ws_bytes(const bt_cp_problem* pb) { return bt_cp_als_ws_bytes(pb); }
+
+extern "C" int bt_cp_state_create(const bt_cp_problem* pb, double* a, double* b, double* c,
+                                  double* lam, int max_iters, int fit_mode, void* wsv,
+                                  int64_t ws_bytes, void* stream, void** out) {
+  BT_REQUIRE(pb->I >= 1 && pb->J >= 1 && pb->K >= 0, BT_E_SHAPE, "cp_als: empty tensor");
+  BT_REQUIRE(pb->R >= 1, BT_E_SHAPE, "CP rank must be at least 1");
+  BT_REQUIRE(pb->R <= PINV_MAX_R, BT_E_SHAPE, "cp_als: rank %lld above the on-chip limit %d",
+             (long long)pb->R, PINV_MAX_R);
+  BT_REQUIRE(max_iters >= 1, BT_E_VALUE, "max_iters must be at least 1");
+  auto* S = new bt_cp_state();
+  S->pl = make_plan(pb);
+  if (ws_bytes < cp_total_ws(S->pl) * 8) {
+    delete S;
+    bt_set_error("cp_als: workspace too small");
+    return BT_E_VALUE;
+  }
+  S->ws = static_cast<double*>(wsv);
+  S->st = bt_stream(stream);
+  S->X = pb->x;
+  S->F[0] = a;
+  S->F[1] = b;
+  S->F[2] = c;
+  S->lam = lam;
+  S->max_iters = max_iters;
+  S->fit_mode = fit_mode;
+  const int64_t RR = S->pl.R * S->pl.R;
+  double* sb = S->ws + S->pl.off_state;
+  S->s.gram[0] = sb;
+  S->s.gram[1] = sb + RR;
+  S->s.gram[2] = sb + 2 * RR;
+  S->s.vp = sb + 3 * RR;
+  S->s.norms = sb + 4 * RR;
+  S->s.lam = lam;
+  S->s.scal = sb + 4 * RR + S->pl.R;
+  cudaError_t e = cudaMallocAsync(&S->dhist, sizeof(double) * max_iters, S->st);
+  if (e != cudaSuccess) {
+    delete S;
+    bt_set_error("cp_als: %s", cudaGetErrorString(e));
+    return BT_E_CUDA;
+  }
+  S->s.fit_hist = S->dhist;
+  *out = S;
+  return BT_OK;
+}
+
+extern "C" int bt_cp_state_destroy(void* state) {
+  auto* S = static_cast<bt_cp_state*>(state);
+  if (!S) return BT_OK;
+  cudaFreeAsync(S->dhist, S->st);
+  delete S;
+  return BT_OK;
+}
+
+// Local init contributions: buf = [C^T C (R*R), ||X_local||^2, 0]; A, B Grams are
+// replicated and computed in place.  norm_x > 0 in the problem skips the sum.
+extern "C" int bt_cp_init_local(void* state, double norm_x, double* buf) {
+  auto* S = static_cast<bt_cp_state*>(state);
+  const Plan& pl = S->pl;
+  const int R = static_cast<int>(pl.R);
+  gram_kernel<<<1, 256, 0, S->st>>>(S->F[0], pl.I, R, S->s.gram[0]);
+  BT_LAUNCH_CHECK();
+  gram_kernel<<<1, 256, 0, S->st>>>(S->F[1], pl.J, R, S->s.gram[1]);
+  BT_LAUNCH_CHECK();
+  gram_kernel<<<1, 256, 0, S->st>>>(S->F[2], pl.K, R, buf);
+  BT_LAUNCH_CHECK();
+  if (norm_x > 0.0) {
+    const double x2 = norm_x * norm_x;
+    BT_CUDA_CHECK(cudaMemcpyAsync(buf + pl.R * pl.R, &x2, 8, cudaMemcpyHostToDevice, S->st));
+  } else {
+    BT_TRY(bt_sumsq_f64(S->X, pl.I * pl.J * pl.K, buf + pl.R * pl.R, S->ws + pl.off_res, 2048 * 8,
+                        S->st));
+  }
+  return BT_OK;
+}
+
+__global__ void init_finish_kernel(const double* __restrict__ buf, int R, double* __restrict__ gc,
+                                   double* __restrict__ scal) {
+  for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) gc[idx] = buf[idx];
+  if (threadIdx.x == 0) scal[0] = buf[R * R];
+}
+
+extern "C" int bt_cp_init_finish(void* state, const double* buf) {
+  auto* S = static_cast<bt_cp_state*>(state);
+  init_finish_kernel<<<1, 256, 0, S->st>>>(buf, static_cast<int>(S->pl.R), S->s.gram[2], S->s.scal);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+// MTTKRP of `mode` over the local tensor into out (I x R, J x R, or K_local x R).
+// Modes 1/2 are partial sums over the local mode-3 slab (sum across ranks);
+// mode 3 rows are complete locally.  Mode 1 also (re)computes P = X x3 C.
+extern "C" int bt_cp_mttkrp(void* state, int mode, double* out) {
+  auto* S = static_cast<bt_cp_state*>(state);
+  const Plan& pl = S->pl;
+  double* ws = S->ws;
+  cudaStream_t st = S->st;
+  if (mode == 1) {
+    if (pl.K > 0) {
+      BT_TRY(run_tree(pl, S->X, S->F[2], S->F[1], ws + pl.off_p, ws + pl.off_m1, 1, st));
+      reduce_m1_kernel<<<grid_n(pl.I * pl.R), 256, 0, st>>>(ws + pl.off_m1, pl.I, pl.jtiles, pl.R,
+                                                            out);
+    } else {
+      BT_CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(double) * pl.I * pl.R, st));
+      return BT_OK;
+    }
+    BT_LAUNCH_CHECK();
+  } else if (mode == 2) {
+    if (pl.K > 0) {
+      BT_TRY(run_mode2(pl, ws + pl.off_p, S->F[0], ws + pl.off_m2, st));
+      const int64_t n = pl.J * pl.R;
+      reduce_parts_kernel<<<grid_n(n), 256, 0, st>>>(ws + pl.off_m2, pl.s2, n, n, out);
+      BT_LAUNCH_CHECK();
+    } else {
+      BT_CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(double) * pl.J * pl.R, st));
+    }
+  } else if (mode == 3) {
+    if (pl.K > 0) BT_TRY(run_mode3(pl, S->X, S->F[0], S->F[1], out, ws + pl.off_m3ws, st));
+  } else {
+    bt_set_error("mode %d out of range", mode);
+    return BT_E_SHAPE;
+  }
+  return BT_OK;
+}
+
+// Local solve of `mode` from the (summed) MTTKRP m: gbuf = [F_un^T F_un, <F_un, M>, 0].
+// For mode 3 (row-sharded) gbuf must be summed across ranks before finish.
+extern "C" int bt_cp_solve(void* state, int mode, const double* m, double* gbuf) {
+  auto* S = static_cast<bt_cp_state*>(state);
+  const Plan& pl = S->pl;
+  const int k = mode - 1;
+  const int64_t rows[3] = {pl.I, pl.J, pl.K};
+  const int go0 = (k == 0) ? 1 : 0, go1 = (k == 2) ? 1 : 2;
+  return run_solve_rows(pl, S->s, S->ws, m, 1, 0, pl.R, rows[k], go0, go1, S->F[k], k == 2, gbuf,
+                        S->st);
+}
+
+extern "C" int bt_cp_solve_finish(void* state, int mode, int it, const double* gbuf) {
+  auto* S = static_cast<bt_cp_state*>(state);
+  BT_REQUIRE(it >= 0 && it < S->max_iters, BT_E_VALUE, "sweep index out of range");
+  const Plan& pl = S->pl;
+  const int k = mode - 1;
+  const int64_t rows[3] = {pl.I, pl.J, pl.K};
+  return run_solve_finish(pl, S->s, gbuf, rows[k], S->F[k], k, k == 2, it, S->fit_mode, S->st);
+}
+
+// Explicit residual partial ||X_local - Xhat_local||^2 into res2 (device scalar;
+// writes 0 when the Gram identity was judged accurate).  Sum across ranks.
+extern "C" int bt_cp_residual(void* state, double* res2) {
+  auto* S = static_cast<bt_cp_state*>(state);
+  const Plan& pl = S->pl;
+  if (S->fit_mode == 2 || pl.K == 0) {
+    BT_CUDA_CHECK(cudaMemsetAsync(res2, 0, sizeof(double), S->st));
+    return BT_OK;
+  }
+  double* W = S->ws + pl.off_w;
+  double* rpart = S->ws + pl.off_res;
+  lam_scale_kernel<<<grid_n(pl.I * pl.R), 256, 0, S->st>>>(S->F[0], S->lam, pl.I,
+                                                           static_cast<int>(pl.R), W);
+  BT_LAUNCH_CHECK();
+  if (pl.R % 2 == 0)
+    BT_TRY(residual_pass<2>(pl, S->X, W, S->F[1], S->F[2], S->s.scal + 3, rpart, S->st));
+  else
+    BT_TRY(residual_pass<1>(pl, S->X, W, S->F[1], S->F[2], S->s.scal + 3, rpart, S->st));
+  residual_reduce_kernel<<<1, 32, 0, S->st>>>(rpart, pl.res_grid, res2);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+extern "C" int bt_cp_residual_finish(void* state, int it, const double* res2) {
+  auto* S = static_cast<bt_cp_state*>(state);
+  residual_finish_kernel<<<1, 32, 0, S->st>>>(res2, S->s, it);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+// Synchronous read of the fit of sweep `it` (for the tol > 0 convergence test).
+extern "C" int bt_cp_read_fit(void* state, int it, double* fit) {
+  auto* S = static_cast<bt_cp_state*>(state);
+  BT_CUDA_CHECK(cudaMemcpyAsync(fit, S->dhist + it, 8, cudaMemcpyDeviceToHost, S->st));
+  BT_CUDA_CHECK(cudaStreamSynchronize(S->st));
+  return BT_OK;
+}
+
+// x = F0 * lam (KruskalRep.x, decomp.py:403) and the fit history to the host.
+extern "C" int bt_cp_state_finish(void* state, int n_iters, double* fit_history) {
+  auto* S = static_cast<bt_cp_state*>(state);
+  const Plan& pl = S->pl;
+  lam_scale_kernel<<<grid_n(pl.I * pl.R), 256, 0, S->st>>>(S->F[0], S->lam, pl.I,
+                                                           static_cast<int>(pl.R), S->F[0]);
+  BT_LAUNCH_CHECK();
+  if (n_iters > 0 && fit_history) {
+    BT_CUDA_CHECK(cudaMemcpyAsync(fit_history, S->dhist, sizeof(double) * n_iters,
+                                  cudaMemcpyDeviceToHost, S->st));
+  }
+  BT_CUDA_CHECK(cudaStreamSynchronize(S->st));
+  return BT_OK;
+}
+
+// One-GPU driver over the phase API (no cross-rank sums).
+extern "C" int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, double* c,
+                             double* lam, int max_iters, double tol, int fit_mode,
+                             double* fit_history, int* n_iters, int* converged, double* phase_ms,
+                             void* wsv, int64_t ws_bytes, void* stream) {
+  void* h = nullptr;
+  BT_TRY(bt_cp_state_create(pb, a, b, c, lam, max_iters, fit_mode, wsv, ws_bytes, stream, &h));
+  auto* S = static_cast<bt_cp_state*>(h);
+  const Plan& pl = S->pl;
+  double* ws = S->ws;
+  cudaStream_t st = S->st;
+  double* m1 = ws + pl.off_m1d;
+  double* m2 = ws + pl.off_m2d;
+  double* m3 = ws + pl.off_m3;
+  double* gbuf = ws + pl.off_gbuf;
+  double* res2 = ws + pl.off_res1;
+  int rc = BT_OK;
+  std::vector<cudaEvent_t> ev;
+  auto mark = [&]() -> int {
+    if (!phase_ms) return BT_OK;
+    cudaEvent_t e;
+    BT_CUDA_CHECK(cudaEventCreate(&e));
+    BT_CUDA_CHECK(cudaEventRecord(e, st));
+    ev.push_back(e);
+    return BT_OK;
+  };
+  double prev = -INFINITY;
+  int it = 0, conv = 0;
+  do {
+    if ((rc = bt_cp_init_local(h, pb->norm_x, ws + pl.off_init)) != BT_OK) break;
+    if ((rc = bt_cp_init_finish(h, ws + pl.off_init)) != BT_OK) break;
+    for (it = 1; it <= max_iters; ++it) {
+      const int ix = it - 1;
+      if ((rc = mark()) != BT_OK) break;
+      if ((rc = bt_cp_mttkrp(h, 1, m1)) != BT_OK) break;
+      if ((rc = mark()) != BT_OK) break;
+      if ((rc = bt_cp_solve(h, 1, m1, gbuf)) != BT_OK) break;
+      if ((rc = bt_cp_solve_finish(h, 1, ix, gbuf)) != BT_OK) break;
+      if ((rc = mark()) != BT_OK) break;
+      if ((rc = bt_cp_mttkrp(h, 2, m2)) != BT_OK) break;
+      if ((rc = mark()) != BT_OK) break;
+      if ((rc = bt_cp_solve(h, 2, m2, gbuf)) != BT_OK) break;
+      if ((rc = bt_cp_solve_finish(h, 2, ix, gbuf)) != BT_OK) break;
+      if ((rc = mark()) != BT_OK) break;
+      if ((rc = bt_cp_mttkrp(h, 3, m3)) != BT_OK) break;
+      if ((rc = mark()) != BT_OK) break;
+      if ((rc = bt_cp_solve(h, 3, m3, gbuf)) != BT_OK) break;
+      if ((rc = bt_cp_solve_finish(h, 3, ix, gbuf)) != BT_OK) break;
+      if ((rc = bt_cp_residual(h, res2)) != BT_OK) break;
+      if ((rc = bt_cp_residual_finish(h, ix, res2)) != BT_OK) break;
+      if ((rc = mark()) != BT_OK) break;
+      if (tol > 0.0) {
+        double fit = 0.0;
+        if ((rc = bt_cp_read_fit(h, ix, &fit)) != BT_OK) break;
+        if (std::fabs(fit - prev) < tol) {
+          conv = 1;
+          break;
+        }
+        prev = fit;
+      }
+    }
+    if (rc != BT_OK) break;
+    if (it > max_iters) it = max_iters;
+    rc = bt_cp_state_finish(h, it, fit_history);
+  } while (false);
+  if (rc == BT_OK) {
+    *n_iters = it;
+    *converged = conv;
+    if (phase_ms) {
+      // per sweep: [t0 mttkrp1 t1 solve1 t2 mttkrp2 t3 solve2 t4 mttkrp3 t5 solve3+fit t6]
+      for (int k = 0; k < 4; ++k) phase_ms[k] = 0.0;
+      for (size_t base = 0; base + 7 <= ev.size(); base += 7) {
+        float ms = 0.f;
+        auto el = [&](int x, int y) {
+          cudaEventElapsedTime(&ms, ev[base + x], ev[base + y]);
+          return static_cast<double>(ms);
+        };
+        phase_ms[0] += el(0, 1);
+        phase_ms[1] += el(2, 3);
+        phase_ms[2] += el(4, 5);
+        phase_ms[3] += el(1, 2) + el(3, 4) + el(5, 6);
+      }
+    }
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+  bt_cp_state_destroy(h);
+  return rc;
+}
+
+extern "C" int64_t bt_mttkrp_ws_bytes(const bt_cp_problem* pb, int mode) {
+  Plan pl = make_plan(pb);
+  (void)mode;
+  return pl.total * 8;
+}
 
 extern "C" int bt_mttkrp_f64(const bt_cp_problem* pb, int mode, const double* a, const double* b,
                              const double* c, double* out, void* wsv, int64_t ws_bytes,

@@ -12,6 +12,8 @@
 // Output: eigenvalues descending; eigenvectors as columns, each flipped so
 // its largest-|.| entry (first on ties) is positive (decomp.py:176-179).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -29,6 +31,7 @@ constexpr int ELD = 68;      // smem leading dim, == 4 (mod 16)
 constexpr int SMALL_N = 96;
 constexpr double ABS_TOL = 1e-17;  // rotate only |a_pq| > ABS_TOL * ||A||_F
 constexpr int OFFN_BLOCKS = 296;
+constexpr int INNER_SWEEPS = 2;  // Jacobi sweeps per 64x64 pair subproblem and round
 
 // ---------------------------------------------------------------------------
 // small path
@@ -81,28 +84,94 @@ __device__ __forceinline__ int64_t pair_index(int nb, int rnd, int k, int l) {
   return (l < EB) ? static_cast<int64_t>(P) * EB + l : static_cast<int64_t>(Q) * EB + (l - EB);
 }
 
+// One (or a few) cyclic sweeps of two-sided Jacobi on the 64x64 pair
+// subproblem, specialised for n = 64 and 8 warps: every warp computes all 32
+// rotations of a round redundantly (lane = pair), so only two barriers per
+// round remain (after the row update, after the column + Q update).
+constexpr int SLD = EP + 1;  // 65: conflict-light row/column access
+
+__device__ __forceinline__ void pair_of(int rnd, int k, int& p, int& q) {
+  const int m = EP - 1;
+  if (k == 0) {
+    p = rnd;
+    q = m;
+  } else {
+    p = (rnd + k) % m;
+    q = (rnd - k + m) % m;
+  }
+  if (p > q) {
+    const int t = p;
+    p = q;
+    q = t;
+  }
+}
+
 __global__ void __launch_bounds__(256)
     solve_pairs_kernel(const double* __restrict__ ap, int64_t np, int nb, int rnd,
                        const double* __restrict__ sumsq, double* __restrict__ jout,
-                       int* __restrict__ flag) {
+                       int* __restrict__ flag, int inner_sweeps) {
   extern __shared__ __align__(16) double sm[];
-  constexpr int ld = EP + 1;
   double* s = sm;
-  double* q = s + EP * ld;
-  double* cs = q + EP * ld;
-  double* sn = cs + EP / 2;
-  int* pp = reinterpret_cast<int*>(sn + EP / 2);
-  int* qq = pp + EP / 2;
+  double* q = sm + EP * SLD;
+  __shared__ int rot_any;
   const int k = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int idx = threadIdx.x; idx < EP * EP; idx += blockDim.x) {
     const int r = idx / EP, c = idx % EP;
-    s[r * ld + c] = ap[pair_index(nb, rnd, k, r) * np + pair_index(nb, rnd, k, c)];
+    s[r * SLD + c] = ap[pair_index(nb, rnd, k, r) * np + pair_index(nb, rnd, k, c)];
+    q[r * SLD + c] = (r == c) ? 1.0 : 0.0;
   }
+  if (threadIdx.x == 0) rot_any = 0;
   __syncthreads();
-  const int rot = jacobi_smem(s, q, EP, ld, cs, sn, pp, qq, 40, ABS_TOL * sqrt(*sumsq));
+  const double abs_tol = ABS_TOL * sqrt(*sumsq);
+  int any = 0;
+  for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
+    for (int r = 0; r < EP - 1; ++r) {
+      int p, qq;
+      pair_of(r, lane, p, qq);
+      const double apq = s[p * SLD + qq], app = s[p * SLD + p], aqq = s[qq * SLD + qq];
+      double c = 1.0, sn = 0.0;
+      if (apq != 0.0 && fabs(apq) > abs_tol && fabs(apq) > 1e-18 * sqrt(fabs(app) * fabs(aqq))) {
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        c = 1.0 / sqrt(t * t + 1.0);
+        sn = t * c;
+        any = 1;
+      }
+      // rows p, q: warp w owns columns [8w, 8w + 8)
+      if (sn != 0.0) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int j = warp * 8 + jj;
+          const double x = s[p * SLD + j], y = s[qq * SLD + j];
+          s[p * SLD + j] = c * x - sn * y;
+          s[qq * SLD + j] = sn * x + c * y;
+        }
+      }
+      __syncthreads();
+      // columns p, q of s and q: warp w owns rows [8w, 8w + 8)
+      if (sn != 0.0) {
+#pragma unroll
+        for (int ii = 0; ii < 8; ++ii) {
+          const int i = warp * 8 + ii;
+          double x = s[i * SLD + p], y = s[i * SLD + qq];
+          s[i * SLD + p] = c * x - sn * y;
+          s[i * SLD + qq] = sn * x + c * y;
+          x = q[i * SLD + p];
+          y = q[i * SLD + qq];
+          q[i * SLD + p] = c * x - sn * y;
+          q[i * SLD + qq] = sn * x + c * y;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (any) rot_any = 1;  // benign race: every writer stores 1
+  __syncthreads();
+  const int rot = rot_any;
   double* j = jout + static_cast<int64_t>(k) * EP * EP;
   for (int idx = threadIdx.x; idx < EP * EP; idx += blockDim.x)
-    j[idx] = q[(idx / EP) * ld + idx % EP];
+    j[idx] = q[(idx / EP) * SLD + idx % EP];
   if (threadIdx.x == 0) {
     jout[(int64_t)(nb / 2) * EP * EP + k] = rot ? 1.0 : 0.0;  // per-pair "rotated" mark
     if (rot) *flag = 1;
@@ -364,7 +433,7 @@ extern "C" int bt_syevd_f64(const double* a, int64_t n, double* w, double* v, vo
     if (!attr) {
       BT_CUDA_CHECK(cudaFuncSetAttribute(solve_pairs_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(pair_smem())));
+                                         2 * EP * SLD * 8));
       BT_CUDA_CHECK(cudaFuncSetAttribute(apply_pairs_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(apply_smem())));
@@ -393,7 +462,8 @@ extern "C" int bt_syevd_f64(const double* a, int64_t n, double* w, double* v, vo
     for (int sweep = 0; sweep < 40 && !done; ++sweep) {
       BT_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int), st));
       for (int rnd = 0; rnd < nb - 1; ++rnd) {
-        solve_pairs_kernel<<<pairs, 256, pair_smem(), st>>>(ap, p.np, nb, rnd, ss, jb, flag);
+        solve_pairs_kernel<<<pairs, 256, 2 * EP * SLD * 8, st>>>(ap, p.np, nb, rnd, ss, jb, flag,
+                                                                  INNER_SWEEPS);
         BT_LAUNCH_CHECK();
         apply_pairs_kernel<<<static_cast<unsigned>(tiles), 256, apply_smem(), st>>>(ap, q, p.np,
                                                                                     nb, rnd, jb);
@@ -410,6 +480,9 @@ extern "C" int bt_syevd_f64(const double* a, int64_t n, double* w, double* v, vo
                                     cudaMemcpyDeviceToHost, st));
       BT_CUDA_CHECK(cudaStreamSynchronize(st));
       const double off = sqrt(off2);
+      if (getenv("BT_EIG_DEBUG"))
+        fprintf(stderr, "[syevd n=%lld] sweep %d off/normF %.3e rotated %d\n", (long long)n,
+                sweep, off / normf, h);
       done = (h == 0) || (off <= 2.2e-16 * sqrt(static_cast<double>(n)) * normf) ||
              (off <= 1e-10 * normf && off > 0.5 * prev);
       prev = off;
