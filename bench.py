@@ -363,21 +363,31 @@ def run_bt200(args, rank, world):
     peaks = fp64_peaks(torch)
     log(f"[bench] fp64 peaks (TFLOP/s): {peaks}")
 
-    x = configs.c5_build(I_, J_, K_, R_)
+    from paper_2105_01170_b200.parallel import (NativeCpOps, cp_als_sharded, shard_bounds,
+                                                torch_allreduce)
+
+    k0, k1 = shard_bounds(K_, world, rank)
+    x = configs.c5_build(I_, J_, K_, R_, k_slab=(k0, k1))   # this rank's mode-3 slab
     init = configs.normal_init((I_, J_, K_), R_, 1003)
-    init_dev = [torch.from_numpy(f).cuda() for f in init]
+    init_dev = [torch.from_numpy(init[0]).cuda(), torch.from_numpy(init[1]).cuda(),
+                torch.from_numpy(init[2][k0:k1].copy()).cuda()]
     f = [torch.empty_like(v) for v in init_dev]
     lam = torch.empty(R_, dtype=torch.float64, device="cuda")
     from paper_2105_01170_b200.decomp import cp_als_device
-    pb_ws = None
     phase = [0.0] * 4
     hist_holder = {}
+    allreduce = torch_allreduce()
 
     def step():
         for k in range(3):
             f[k].copy_(init_dev[k])
-        hist, n_it, conv = cp_als_device(x, R_, f, lam, ITERS, 0.0, "auto", 0.0, ws_holder(),
-                                         phase_ms=phase)
+        if world == 1:
+            hist, n_it, conv = cp_als_device(x, R_, f, lam, ITERS, 0.0, "auto", 0.0, ws_holder(),
+                                             phase_ms=phase)
+        else:
+            ops = NativeCpOps(x, R_, f[0], f[1], f[2], ITERS)
+            hist, n_it, conv = cp_als_sharded(ops, ITERS, 0.0, allreduce)
+            ops.close()
         hist_holder["h"] = hist
 
     ws_cache = {}
@@ -386,7 +396,7 @@ def run_bt200(args, rank, world):
         if "ws" not in ws_cache:
             import ctypes as C
 
-            pb = N.CpProblem(_dev.ptr(x), I_, J_, K_, R_, 0.0)
+            pb = N.CpProblem(_dev.ptr(x), I_, J_, k1 - k0, R_, 0.0)
             ws_cache["ws"] = _dev.workspace(lib.bt_cp_als_ws_bytes(C.byref(pb)))
         return ws_cache["ws"]
 
@@ -414,10 +424,22 @@ def run_bt200(args, rank, world):
         ms = float(t.item())
         torch.distributed.barrier()
     ref_flops = ITERS * 6.0 * I_ * J_ * K_ * R_
-    value = world * ref_flops / (ms / 1e3) / 1e9
+    value = ref_flops / (ms / 1e3) / 1e9     # whole job: the global tensor, max-over-ranks time
     tree_ms = phase_tot[0] / (args.steps * ITERS)
     mode3_ms = phase_tot[2] / (args.steps * ITERS)
-    achieved = 2.0 * I_ * J_ * K_ * R_ / (tree_ms / 1e3) / 1e12
+    kloc = k1 - k0
+    if tree_ms == 0.0:
+        # sharded run: time this rank's P / mode-1 and mode-3 kernels separately (CUDA events)
+        for k in range(3):
+            f[k].copy_(init_dev[k])
+        ops = NativeCpOps(x, R_, f[0], f[1], f[2], ITERS)
+        buf = ops.init_local()
+        allreduce(buf)
+        ops.init_finish(buf)
+        tree_ms = timed(torch, lambda: ops.mttkrp(1), 3, 1)
+        mode3_ms = timed(torch, lambda: ops.mttkrp(3), 3, 1)
+        ops.close()
+    achieved = 2.0 * I_ * J_ * kloc * R_ / (tree_ms / 1e3) / 1e12
     peak = peaks["dmma"]
     fit = hist_holder["h"][-1]
     log(f"[bench] C5 step {ms:.1f} ms, tree {tree_ms:.2f} ms, mode2 {phase_tot[1] / (args.steps * ITERS):.2f} ms,"
@@ -426,11 +448,13 @@ def run_bt200(args, rank, world):
         "metric": "CP-ALS MTTKRP GFLOP/s (reference-equivalent 6*I*J*K*R per sweep)",
         "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"C5: cp_als(X {I_}x{J_}x{K_} fp64 = [[A0,B0,C0]] + 1e-4 noise, "
                                f"R={R_}, max_iters={ITERS}, tol=0) per step; init seed 1003",
-                   "global_batch": 1, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "global_batch": 1,
+                   "parallelism": (f"mode-3 sharded x{world} (NCCL allreduce of MTTKRP partials "
+                                   f"and R x R Grams)") if world > 1 else "1 GPU",
                    "l2": "inputs (137 GB) >> L2; no flush needed",
                    "per_sweep_ms": ms / ITERS, "final_fit": fit,
                    "executed_mttkrp_flops_per_sweep": 4.0 * I_ * J_ * K_ * R_,
@@ -443,7 +467,7 @@ def run_bt200(args, rank, world):
                      "frac": achieved / peak, "traffic": None,
                      "peak_source": "measured in this run: DMMA.8x8x4 chains on all SMs "
                                     "(MEASURED_PEAKS.json has no FP64 figure)",
-                     "mode3_gemm_achieved": 2.0 * I_ * J_ * K_ * R_ / (mode3_ms / 1e3) / 1e12},
+                     "mode3_gemm_achieved": 2.0 * I_ * J_ * kloc * R_ / (mode3_ms / 1e3) / 1e12},
         "clocks": clk.summary(),
         "gpu_launches": launches,
         "fp64_peaks_tflops": dict(peaks),
@@ -451,9 +475,9 @@ def run_bt200(args, rank, world):
     # ---- e2e: public API with host buffers (H2D of X + init, D2H of factors)
     ws_cache.clear()
     torch.cuda.empty_cache()
-    if not args.no_e2e and rank == 0:
+    if not args.no_e2e:
         try:
-            result["e2e"] = e2e_run(args, torch, x, init)
+            result["e2e"] = e2e_run(args, torch, x, init, world, rank, k0, k1)
         except Exception as exc:  # pragma: no cover
             result["e2e"] = {"value": None, "unit": "GFLOP/s", "error": repr(exc)[:300]}
         x = None
@@ -483,12 +507,14 @@ def run_bt200(args, rank, world):
         print(json.dumps(result), flush=True)
 
 
-def e2e_run(args, torch, x_dev, init):
-    """Same metric through bt.cp_als with host inputs: every step copies X
-    (and the init factors) host->device and reads the factors back."""
+def e2e_run(args, torch, x_dev, init, world, rank, k0, k1):
+    """Same metric through the public API with host buffers: every step copies
+    this rank's X slab (and the init factors) host->device and reads the
+    factors + fit history back (1 GPU: ``cp_als``; N GPUs:
+    ``parallel.cp_als_distributed`` on mode-3 slabs)."""
     import numpy as np
 
-    from paper_2105_01170_b200 import decomp
+    from paper_2105_01170_b200 import decomp, parallel
 
     nbytes = x_dev.numel() * 8
     try:
@@ -501,30 +527,45 @@ def e2e_run(args, torch, x_dev, init):
     torch.cuda.synchronize()
     x_dev.set_()          # release the resident copy: the API call allocates its own
     torch.cuda.empty_cache()
+    init_l = [init[0], init[1], init[2][k0:k1].copy()]
     saved = decomp._cp_init
-    decomp._cp_init = lambda _t, _r: [f.copy() for f in init]
+    decomp._cp_init = lambda _t, _r: [v.copy() for v in init_l]
+
+    def once():
+        if world == 1:
+            return decomp.cp_als(host, R_, ITERS, 0.0)
+        return parallel.cp_als_distributed(host, R_, ITERS, 0.0, init=init_l)
+
     steps = max(1, min(args.steps, 2))
     try:
-        decomp.cp_als(host, R_, ITERS, 0.0)  # warm-up
+        once()  # warm-up
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(steps):
-            res = decomp.cp_als(host, R_, ITERS, 0.0)
+            res = once()
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
         wall = (time.perf_counter() - t0) / steps * 1e3
     finally:
         decomp._cp_init = saved
-    h2d = nbytes + sum(f.nbytes for f in init)
+    if world > 1:
+        t = torch.tensor([ms, wall], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms, wall = float(t[0]), float(t[1])
+    h2d = nbytes + sum(v.nbytes for v in init_l)
     d2h = sum(np.asarray(v).nbytes for v in (res.rep.x, res.rep.y, res.rep.z)) + 8 * ITERS
     return {"value": ITERS * 6.0 * I_ * J_ * K_ * R_ / (ms / 1e3) / 1e9, "unit": "GFLOP/s",
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
             "ms_per_step": ms, "wall_ms_per_step": wall, "steps": steps,
             "host_buffer": "pinned" if pinned else "pageable",
-            "path": "paper_2105_01170_b200.cp_als(torch CPU tensor) -> H2D, device ALS, D2H"}
+            "path": ("paper_2105_01170_b200.cp_als(torch CPU tensor)" if world == 1 else
+                     "paper_2105_01170_b200.parallel.cp_als_distributed(host slab per rank)") +
+                    " -> H2D, device ALS, D2H of factors + fit history"}
 
 
 def main():

@@ -144,6 +144,31 @@ int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, double* c, doub
                   int max_iters, double tol, int fit_mode, double* fit_history, int* n_iters,
                   int* converged, double* phase_ms, void* ws, int64_t ws_bytes, void* stream);
 
+/* Phase API of the same loop, for a tensor sharded along mode 3 across
+ * ranks (A, B replicated; C and X row-sharded; I, J global, K local).  A sweep:
+ *   bt_cp_mttkrp(1, m1) -> SUM(m1) -> bt_cp_solve(1, m1, g) -> bt_cp_solve_finish(1, it, g)
+ *   bt_cp_mttkrp(2, m2) -> SUM(m2) -> bt_cp_solve(2, m2, g) -> bt_cp_solve_finish(2, it, g)
+ *   bt_cp_mttkrp(3, m3) ->            bt_cp_solve(3, m3, g) -> SUM(g) -> bt_cp_solve_finish(3, it, g)
+ *   bt_cp_residual(r)   -> SUM(r)  -> bt_cp_residual_finish(it, r)
+ * after bt_cp_init_local(buf) -> SUM(buf) -> bt_cp_init_finish(buf).
+ * SUM is the caller's cross-rank sum (NCCL allreduce); with one rank it is
+ * the identity.  Buffers: m1 (I,R), m2 (J,R), m3 (K,R), g and buf (R*R+2),
+ * r (1), all device, caller owned.  bt_cp_state_finish writes x = a * lam. */
+int64_t bt_cp_state_ws_bytes(const bt_cp_problem* pb);
+int bt_cp_state_create(const bt_cp_problem* pb, double* a, double* b, double* c, double* lam,
+                       int max_iters, int fit_mode, void* ws, int64_t ws_bytes, void* stream,
+                       void** state);
+int bt_cp_state_destroy(void* state);
+int bt_cp_init_local(void* state, double norm_x, double* buf);
+int bt_cp_init_finish(void* state, const double* buf);
+int bt_cp_mttkrp(void* state, int mode, double* out);
+int bt_cp_solve(void* state, int mode, const double* m, double* gbuf);
+int bt_cp_solve_finish(void* state, int mode, int it, const double* gbuf);
+int bt_cp_residual(void* state, double* res2);
+int bt_cp_residual_finish(void* state, int it, const double* res2);
+int bt_cp_read_fit(void* state, int it, double* fit);
+int bt_cp_state_finish(void* state, int n_iters, double* fit_history);
+
 /* Single MTTKRP (decomp.py:385-387 unfold(t,k) @ khatri_rao(...)): out (extent_mode, R).
  * mode in {1,2,3}.  Fused Khatri-Rao; no unfolding copy. */
 int64_t bt_mttkrp_ws_bytes(const bt_cp_problem* pb, int mode);

@@ -64,6 +64,19 @@ _SIGS = {
     "bt_cp_als_f64": (C.c_int, [_P(CpProblem), _dp, _dp, _dp, _dp, C.c_int, C.c_double, C.c_int,
                                 _P(C.c_double), _P(C.c_int), _P(C.c_int), _P(C.c_double), _dp,
                                 _i64, _dp]),
+    "bt_cp_state_ws_bytes": (_i64, [_P(CpProblem)]),
+    "bt_cp_state_create": (C.c_int, [_P(CpProblem), _dp, _dp, _dp, _dp, C.c_int, C.c_int, _dp, _i64,
+                                     _dp, _P(C.c_void_p)]),
+    "bt_cp_state_destroy": (C.c_int, [C.c_void_p]),
+    "bt_cp_init_local": (C.c_int, [C.c_void_p, C.c_double, _dp]),
+    "bt_cp_init_finish": (C.c_int, [C.c_void_p, _dp]),
+    "bt_cp_mttkrp": (C.c_int, [C.c_void_p, C.c_int, _dp]),
+    "bt_cp_solve": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp]),
+    "bt_cp_solve_finish": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _dp]),
+    "bt_cp_residual": (C.c_int, [C.c_void_p, _dp]),
+    "bt_cp_residual_finish": (C.c_int, [C.c_void_p, C.c_int, _dp]),
+    "bt_cp_read_fit": (C.c_int, [C.c_void_p, C.c_int, _P(C.c_double)]),
+    "bt_cp_state_finish": (C.c_int, [C.c_void_p, C.c_int, _P(C.c_double)]),
     "bt_mttkrp_ws_bytes": (_i64, [_P(CpProblem), C.c_int]),
     "bt_mttkrp_f64": (C.c_int, [_P(CpProblem), C.c_int, _dp, _dp, _dp, _dp, _dp, _i64, _dp]),
     "bt_pinv_sym_f64": (C.c_int, [_dp, _i64, _dp, _dp]),
