@@ -1,8 +1,9 @@
 """bt200: B200-native (sm_100a) hot path of arXiv 2105.01170's structure-
 preserving approximations, a drop-in behind the reference package
 ``blockten``'s API (same names, arguments, outputs, factor layouts and
-exception types).  All arithmetic runs in libbt200.so (hand-written CUDA,
-FP64 DMMA tensor cores); PyTorch only provides device memory and streams.
+exception types; cf. blockten/__init__.py:12-89).  All arithmetic runs in
+libbt200.so (hand-written CUDA, FP64 DMMA tensor cores); PyTorch only
+provides device memory and streams.
 """
 
 from __future__ import annotations
@@ -14,6 +15,13 @@ from .decomp import (CpResult, KruskalRep, SketchConfig, TuckerRep, cp_als, hooi
                      qr_thin, st_hosvd, svd_truncated, tucker_partial)
 from .errors import (ContainerExtentError, ContainerFormatError, ConvergenceError,
                      NotPositiveDefiniteError, PatternMismatchError, ShapeError)
+from .multilevel import (MlKronTerm, MultilevelPattern, ml_kron_sum_from_kruskal,
+                         ml_kron_sum_from_tucker, ml_matvec, psf_weighted_tensor)
+from .psd import SpsdRep, check_transpose_closed, spsd_compress, spsd_compress_blocks
+from .reconstruct import (BlockLowRankRep, FlopCounter, KronSumRep, TuckerBlockRep,
+                          blr_from_kruskal, blr_from_tucker, densify, error_fro,
+                          kron_sum_from_kruskal, kron_sum_from_tucker, matvec)
 from .tensor import fold, fro_norm, mode_multiply, squeeze, twist, unfold
+from . import decomp, multilevel, parallel, psd, reconstruct  # noqa: F401  (module access)
 
 __version__ = "0.1.0"
