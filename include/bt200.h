@@ -193,6 +193,13 @@ int bt_unfold_gram_f64(const double* x, const int64_t* dims, int order, int mode
 int64_t bt_syevd_ws_bytes(int64_t n);
 int bt_syevd_f64(const double* a, int64_t n, double* w, double* v, void* ws, int64_t ws_bytes,
                  void* stream);
+/* Leading nvec eigenpairs (n >= 3): Householder tridiagonalisation,
+ * bisection, inverse iteration, back-transformation.  w (nvec) descending,
+ * v (n x nvec) row-major, sign rule as bt_syevd_f64.  Eigenvectors are
+ * computed only for w > tau * |w[0]| (tau < 0: all); the other columns are 0. */
+int64_t bt_syevx_ws_bytes(int64_t n, int64_t nvec);
+int bt_syevx_f64(const double* a, int64_t n, int64_t nvec, double tau, double* w, double* v,
+                 void* ws, int64_t ws_bytes, void* stream);
 /* Thin QR with nonnegative diag(R) (decomp.py:182-193): a (m x n, m >= n),
  * q (m x n), r (n x n), row-major. */
 int64_t bt_qr_thin_ws_bytes(int64_t m, int64_t n);
@@ -241,6 +248,8 @@ int bt_maxabs_f64(const double* x, int64_t n, double* out, void* ws, int64_t ws_
  * ws: p ints.  Synchronises the stream. */
 int bt_transpose_check_f64(const double* blocks, int64_t p, int64_t n, const int64_t* partner,
                            double tol, void* ws, int64_t* bad_class, void* stream);
+/* sign rule (decomp.py:176-179) on every column of a row-major matrix */
+int bt_sign_fix_f64(double* x, int64_t rows, int64_t cols, void* stream);
 /* normalise every column of a row-major (rows x cols) matrix to unit 2-norm */
 int bt_col_normalize_f64(double* x, int64_t rows, int64_t cols, void* stream);
 /* z = alpha * x + beta * y elementwise (n doubles) */
@@ -254,6 +263,8 @@ int64_t bt_sumsq_ws_bytes(int64_t n);
 /* FP64 peak microbenchmarks (bench only): DMMA.8x8x4 chains / DFMA chains on
  * all SMs; *flops receives the executed flop count. */
 int bt_peak_dmma(int64_t iters, int blocks, int threads, double* sink, double* flops, void* stream);
+int bt_peak_dmma_chains(int64_t iters, int blocks, int threads, int chains, double* sink,
+                        double* flops, void* stream);
 int bt_peak_dfma(int64_t iters, int blocks, int threads, double* sink, double* flops, void* stream);
 
 #ifdef __cplusplus

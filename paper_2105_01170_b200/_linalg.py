@@ -29,12 +29,26 @@ def unfold_gram_dev(xd, mode: int):
     return g
 
 
-def eigh_dev(gd):
+SMALL_EIG = 96      # one-CTA Jacobi up to this size
+
+
+def eigh_dev(gd, nvec: int | None = None, tau: float = -1.0):
     """(w, V): eigenvalues descending, eigenvectors as columns of V, each
-    sign-normalised (largest-|.| entry positive, first on ties)."""
+    sign-normalised (largest-|.| entry positive, first on ties).  With nvec
+    (< n, n > 96) only the leading nvec pairs are computed (tridiagonal
+    path; vectors only for eigenvalues above tau * |w[0]| when tau >= 0, the
+    rest zero); otherwise the full spectrum (Jacobi)."""
     n = int(gd.shape[0])
     if tuple(gd.shape) != (n, n):
         raise ShapeError("eigh expects a square matrix")
+    if nvec is not None and n > SMALL_EIG and int(nvec) < n:
+        nv = max(1, int(nvec))
+        w = _dev.empty((nv,))
+        v = _dev.empty((n, nv))
+        ws = _dev.workspace(N.load().bt_syevx_ws_bytes(n, nv))
+        N.call("bt_syevx_f64", _dev.ptr(gd.contiguous()), n, nv, float(tau), _dev.ptr(w),
+               _dev.ptr(v), _dev.ptr(ws), int(ws.numel()) * 8, _dev.stream())
+        return w, v
     w = _dev.empty((n,))
     v = _dev.empty((n, n))
     ws = _dev.workspace(N.load().bt_syevd_ws_bytes(n))
@@ -43,7 +57,7 @@ def eigh_dev(gd):
     return w, v
 
 
-RESOLVE_TAU = 1e-4   # per pass: eigenvectors with lambda > tau * lambda_max are kept (cut accuracy ~eps/tau)
+RESOLVE_TAU = 1e-3   # per pass: eigenvectors with lambda > tau * lambda_max are kept (cut accuracy ~eps/tau)
 
 
 def _gram_modes(xd, modes):
@@ -79,54 +93,81 @@ def _orth_normalize(basis, new):
     return out
 
 
-def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_passes: int = 4):
+def _complete(basis, g, need: int, block: int = 32):
+    """``need`` orthonormal columns orthogonal to ``basis``, drawn from the
+    range of g (deterministic sketch g @ Omega), by block classical
+    Gram-Schmidt with reorthogonalisation (two projection + Householder QR
+    passes per 32-column block), sign-normalised.  Used once the remainder
+    is at rounding level, where any orthonormal completion is as good as
+    LAPACK's."""
+    t = _dev.torch()
+    n = int(g.shape[0])
+    rng = np.random.default_rng(12345)
+    y = gemm_dev(g, _dev.to_device(rng.standard_normal((n, need))))
+    cur = basis
+    outs = []
+    for j0 in range(0, need, block):
+        blk = y[:, j0:j0 + block].contiguous()
+        for _ in range(2):
+            if cur is not None:
+                blk = _axpby(1.0, blk, -1.0, gemm_dev(cur, gemm_dev(cur, blk, ta=True)))
+            blk, _ = qr_thin_dev(blk)
+        outs.append(blk)
+        cur = blk if cur is None else t.cat([cur, blk], dim=1).contiguous()
+    out = t.cat(outs, dim=1).contiguous()
+    N.call("bt_sign_fix_f64", _dev.ptr(out), n, int(need), _dev.stream())
+    return out
+
+
+def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_passes: int = 16):
     """Leading r left singular vectors of unfold(x, mode) (decomp.py:220-234),
     sign rule included.  extra_mode: basis of the column concatenation
     [unfold(x, mode), unfold(x, extra_mode)] (tucker_partial
     shared_from="concat"), whose Gram is the sum of the two Grams.
 
-    One Gram + eigensolver pass resolves the directions whose eigenvalue
-    exceeds RESOLVE_TAU * lambda_max (singular values above ~1e-4 sigma_1);
-    Gram rounding (~eps ||G||) blurs the rest.  When r reaches past them the
-    resolved part is deflated out of the tensor and the remainder gets its
-    own Gram pass (repeat), which recovers SVD-grade accuracy for fast
-    decaying spectra (C2's Hankel).  The eigenbasis of the last
-    Gram is complete, which also provides the full_matrices completion when
-    r exceeds the unfolding's column count."""
+    A Gram + eigensolver pass determines eigenvectors to ~eps*lambda_max/gap,
+    so each pass keeps only the directions with lambda > RESOLVE_TAU *
+    lambda_max of the current Gram, deflates them out of the tensor and
+    re-Grams the remainder (SVD-grade accuracy for the fast-decaying spectra
+    of C2/C3).  Once the remainder is at rounding level the
+    basis is completed orthonormally (full_matrices completion, too)."""
     modes = [mode] if extra_mode is None else [mode, extra_mode]
     t = _dev.torch()
-    w, v = eigh_dev(_gram_modes(xd, modes))
-    wh = _dev.to_host(w)
-    k = int(np.sum(wh[:r] > RESOLVE_TAU * max(wh[0], 0.0))) if wh[0] > 0 else 0
-    if k >= r or k == 0:
-        return v[:, :r].contiguous()
-    basis = v[:, :k].contiguous()
-    top = float(wh[0])
-    for _ in range(max_passes - 1):
+    n = int(xd.shape[mode - 1])
+    g = _gram_modes(xd, modes)
+    basis = None
+    top = None
+    for _ in range(max_passes):
+        have = 0 if basis is None else int(basis.shape[1])
+        need = r - have
+        if need <= 0:
+            break
+        w, v = eigh_dev(g, nvec=need, tau=RESOLVE_TAU)
+        wh = _dev.to_host(w)
+        if top is None:
+            top = max(float(wh[0]), 0.0)
+        if top == 0.0 or wh[0] <= 1e-28 * top:
+            break                                   # remainder is rounding noise
+        k = int(np.sum(wh[:need] > RESOLVE_TAU * wh[0]))
+        if basis is None and k >= need:
+            return v[:, :need].contiguous()         # one pass resolved everything
+        k = max(1, min(need, k))
+        new = v[:, :k].contiguous()
+        if basis is not None:
+            new = _orth_normalize(basis, new)
+        basis = new if basis is None else t.cat([basis, new], dim=1).contiguous()
+        if int(basis.shape[1]) >= r:
+            break
         res = [_residual(xd, m, basis) for m in modes]
         g = None
         for m, xr in zip(modes, res):
             gm = unfold_gram_dev(xr, m)
             g = gm if g is None else _axpby(1.0, g, 1.0, gm)
         del res
-        w2, v2 = eigh_dev(g)
-        w2h = _dev.to_host(w2)
-        need = r - int(basis.shape[1])
-        noise = w2h[0] <= 1e-28 * top        # remainder at rounding level: just complete
-        k2 = need if noise else int(np.sum(w2h[:need] > RESOLVE_TAU * max(w2h[0], 0.0)))
-        k2 = max(1, min(need, k2))
-        new = v2[:, :k2].contiguous()
-        # re-orthogonalise against the accepted basis (deflation leaves ~eps
-        # ||X||/||X_r|| leakage) and renormalise column by column
-        new = _orth_normalize(basis, new)
-        basis = t.cat([basis, new], dim=1).contiguous()
-        if int(basis.shape[1]) >= r:
-            break
-        if noise:
-            break
-    if int(basis.shape[1]) < r:     # pass budget exhausted: complete from the last eigenbasis
-        extra = v2[:, k2:k2 + (r - int(basis.shape[1]))].contiguous()
-        basis = t.cat([basis, _orth_normalize(basis, extra)], dim=1).contiguous()
+    have = 0 if basis is None else int(basis.shape[1])
+    if have < r:
+        extra = _complete(basis, g, r - have)
+        basis = extra if basis is None else t.cat([basis, extra], dim=1).contiguous()
     return basis[:, :r].contiguous()
 
 

@@ -84,6 +84,8 @@ _SIGS = {
     "bt_unfold_gram_f64": (C.c_int, [_dp, _P(_i64), C.c_int, C.c_int, _dp, _dp, _i64, _dp]),
     "bt_syevd_ws_bytes": (_i64, [_i64]),
     "bt_syevd_f64": (C.c_int, [_dp, _i64, _dp, _dp, _dp, _i64, _dp]),
+    "bt_syevx_ws_bytes": (_i64, [_i64, _i64]),
+    "bt_syevx_f64": (C.c_int, [_dp, _i64, _i64, C.c_double, _dp, _dp, _dp, _i64, _dp]),
     "bt_qr_thin_ws_bytes": (_i64, [_i64, _i64]),
     "bt_qr_thin_f64": (C.c_int, [_dp, _i64, _i64, _dp, _dp, _dp, _i64, _dp]),
     "bt_ttm_ws_bytes": (_i64, [_P(_i64), C.c_int, C.c_int, _i64]),
@@ -100,11 +102,13 @@ _SIGS = {
                                    _i64, _dp]),
     "bt_maxabs_f64": (C.c_int, [_dp, _i64, _dp, _dp, _i64, _dp]),
     "bt_transpose_check_f64": (C.c_int, [_dp, _i64, _i64, _dp, C.c_double, _dp, _P(_i64), _dp]),
+    "bt_sign_fix_f64": (C.c_int, [_dp, _i64, _i64, _dp]),
     "bt_col_normalize_f64": (C.c_int, [_dp, _i64, _i64, _dp]),
     "bt_axpby_f64": (C.c_int, [_i64, C.c_double, _dp, C.c_double, _dp, _dp, _dp]),
     "bt_sumsq_ws_bytes": (_i64, [_i64]),
     "bt_sumsq_f64": (C.c_int, [_dp, _i64, _dp, _dp, _i64, _dp]),
     "bt_peak_dmma": (C.c_int, [_i64, C.c_int, C.c_int, _dp, _P(C.c_double), _dp]),
+    "bt_peak_dmma_chains": (C.c_int, [_i64, C.c_int, C.c_int, C.c_int, _dp, _P(C.c_double), _dp]),
     "bt_peak_dfma": (C.c_int, [_i64, C.c_int, C.c_int, _dp, _P(C.c_double), _dp]),
 }
 

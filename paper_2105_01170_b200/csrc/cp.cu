@@ -179,6 +179,85 @@ __global__ void __launch_bounds__(256) pinv_kernel(const double* __restrict__ g0
   pinv_from_eig(a, qv, R, ld, vp);
 }
 
+// Fast variant for a compile-time padded size NP (even, <= 96): rotation
+// parameters by the first NP/2 threads, row and column phases as flat loops
+// with constant-size index math; full sweeps until no rotation happens.
+template <int NP>
+__global__ void __launch_bounds__(256) pinv_fast_kernel(const double* __restrict__ g0,
+                                                        const double* __restrict__ g1, int R,
+                                                        double* __restrict__ vp) {
+  constexpr int LD = NP + 1;
+  constexpr int HALF = NP / 2;
+  extern __shared__ __align__(16) double smf[];
+  double* a = smf;
+  double* q = a + NP * LD;
+  __shared__ double cs[HALF], sn[HALF];
+  __shared__ int pp[HALF], qq[HALF];
+  __shared__ int rotated;
+  for (int idx = threadIdx.x; idx < NP * NP; idx += 256) {
+    const int r = idx / NP, c = idx % NP;
+    double v = 0.0;
+    if (r < R && c < R) v = g1 ? g0[r * R + c] * g1[r * R + c] : g0[r * R + c];
+    a[r * LD + c] = v;
+    q[r * LD + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    for (int rnd = 0; rnd < NP - 1; ++rnd) {
+      if (threadIdx.x < HALF) {
+        int p, r2;
+        rr_pair(NP, rnd, threadIdx.x, p, r2);
+        const double apq = a[p * LD + r2], app = a[p * LD + p], aqq = a[r2 * LD + r2];
+        double c = 1.0, sv = 0.0;
+        if (apq != 0.0 && fabs(apq) > 1e-18 * sqrt(fabs(app) * fabs(aqq))) {
+          const double theta = (aqq - app) / (2.0 * apq);
+          const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+          c = 1.0 / sqrt(t * t + 1.0);
+          sv = t * c;
+          rotated = 1;
+        }
+        cs[threadIdx.x] = c;
+        sn[threadIdx.x] = sv;
+        pp[threadIdx.x] = p;
+        qq[threadIdx.x] = r2;
+      }
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < HALF * NP; idx += 256) {
+        const int k = idx / NP, j = idx % NP;
+        const double sv = sn[k];
+        if (sv == 0.0) continue;
+        const double c = cs[k];
+        const int p = pp[k], r2 = qq[k];
+        const double x = a[p * LD + j], y = a[r2 * LD + j];
+        a[p * LD + j] = c * x - sv * y;
+        a[r2 * LD + j] = sv * x + c * y;
+      }
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < HALF * NP; idx += 256) {
+        const int k = idx / NP, i = idx % NP;
+        const double sv = sn[k];
+        if (sv == 0.0) continue;
+        const double c = cs[k];
+        const int p = pp[k], r2 = qq[k];
+        double x = a[i * LD + p], y = a[i * LD + r2];
+        a[i * LD + p] = c * x - sv * y;
+        a[i * LD + r2] = sv * x + c * y;
+        x = q[i * LD + p];
+        y = q[i * LD + r2];
+        q[i * LD + p] = c * x - sv * y;
+        q[i * LD + r2] = sv * x + c * y;
+      }
+      __syncthreads();
+    }
+    const int any = rotated;
+    __syncthreads();
+    if (!any) break;
+  }
+  pinv_from_eig(a, q, R, LD, vp);
+}
+
 size_t pinv_smem_bytes(int R) {
   const int n = R + (R & 1);
   return (size_t)(2 * n * (n + 1) + n) * 8 + (size_t)n * 4;
@@ -550,7 +629,7 @@ Plan make_plan(const bt_cp_problem* pb) {
   pl.off_m2 = take(pl.s2 * JR);
   pl.off_m3 = take(pl.K * pl.R);
   pl.off_m3ws = take(pl.m3_ws_elems);
-  pl.off_gp = take(pl.solve_parts_max * RR);
+  pl.off_gp = take(std::max<int64_t>(pl.solve_parts_max, 64) * RR);  // also Gram split-K partials
   pl.off_ip = take(pl.solve_parts_max);
   pl.off_f = take(maxrows * pl.R);
   pl.off_state = take(3 * RR + RR + 2 * pl.R + 8);
@@ -643,7 +722,26 @@ int run_mode3(const Plan& pl, const double* X, const double* A, const double* B,
   return bt_gemm_run(g, 1, st, 0, pl.m3_ws_elems);
 }
 
+template <int NP>
+int launch_pinv_fast(const double* g0, const double* g1, int R, double* vp, cudaStream_t st) {
+  constexpr int SM = 2 * NP * (NP + 1) * 8;
+  static bool attr = false;
+  if (!attr) {
+    BT_CUDA_CHECK(cudaFuncSetAttribute(pinv_fast_kernel<NP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+    attr = true;
+  }
+  pinv_fast_kernel<NP><<<1, 256, SM, st>>>(g0, g1, R, vp);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
 int run_pinv(const double* g0, const double* g1, int R, double* vp, cudaStream_t st) {
+  if (R <= 8) return launch_pinv_fast<8>(g0, g1, R, vp, st);
+  if (R <= 16) return launch_pinv_fast<16>(g0, g1, R, vp, st);
+  if (R <= 32) return launch_pinv_fast<32>(g0, g1, R, vp, st);
+  if (R <= 64) return launch_pinv_fast<64>(g0, g1, R, vp, st);
+  if (R <= 96) return launch_pinv_fast<96>(g0, g1, R, vp, st);
   const size_t sm = pinv_smem_bytes(R);
   static bool attr = false;
   if (!attr) {
@@ -774,6 +872,29 @@ unsigned grid_n(int64_t n) { return static_cast<unsigned>(std::min<int64_t>(bt_c
 
 }  // namespace
 
+// G = F^T F (R x R) on the DMMA engine (symmetric, split-K over rows)
+static int factor_gram(const Plan& pl, const double* f, int64_t rows, double* g, double* ws,
+                       cudaStream_t st) {
+  if (rows == 0) {
+    BT_CUDA_CHECK(cudaMemsetAsync(g, 0, sizeof(double) * pl.R * pl.R, st));
+    return BT_OK;
+  }
+  BtGemmArgs a{};
+  a.M = pl.R;
+  a.N = pl.R;
+  a.Kin = rows;
+  a.Kout = 1;
+  a.A = BtOperand{f, 1, 0, pl.R, 0};
+  a.B = BtOperand{f, 1, 0, pl.R, 0};
+  a.C = g;
+  a.sCm = pl.R;
+  a.sCn = 1;
+  a.alpha = 1.0;
+  a.symmetric = 1;
+  a.ws = ws;
+  return bt_gemm_run(a, 1, st, 0, std::max<int64_t>(pl.solve_parts_max, 64) * pl.R * pl.R);
+}
+
 struct bt_cp_state {
   Plan pl;
   CpState s;
@@ -854,12 +975,9 @@ extern "C" int bt_cp_init_local(void* state, double norm_x, double* buf) {
   auto* S = static_cast<bt_cp_state*>(state);
   const Plan& pl = S->pl;
   const int R = static_cast<int>(pl.R);
-  gram_kernel<<<1, 256, 0, S->st>>>(S->F[0], pl.I, R, S->s.gram[0]);
-  BT_LAUNCH_CHECK();
-  gram_kernel<<<1, 256, 0, S->st>>>(S->F[1], pl.J, R, S->s.gram[1]);
-  BT_LAUNCH_CHECK();
-  gram_kernel<<<1, 256, 0, S->st>>>(S->F[2], pl.K, R, buf);
-  BT_LAUNCH_CHECK();
+  BT_TRY(factor_gram(pl, S->F[0], pl.I, S->s.gram[0], S->ws + pl.off_gp, S->st));
+  BT_TRY(factor_gram(pl, S->F[1], pl.J, S->s.gram[1], S->ws + pl.off_gp, S->st));
+  BT_TRY(factor_gram(pl, S->F[2], pl.K, buf, S->ws + pl.off_gp, S->st));
   if (norm_x > 0.0) {
     const double x2 = norm_x * norm_x;
     BT_CUDA_CHECK(cudaMemcpyAsync(buf + pl.R * pl.R, &x2, 8, cudaMemcpyHostToDevice, S->st));

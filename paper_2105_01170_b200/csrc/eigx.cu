@@ -1,0 +1,595 @@
+// K8 (leading eigenpairs): Householder tridiagonalisation + bisection +
+// inverse iteration + back-transformation, for the Gram matrices of the
+// Tucker path when only the leading nvec eigenvectors are needed (the
+// reference's LAPACK SVD, decomp.py:172/227, returns them for the leading r).
+//
+//   1. T = Q^T A Q by n-2 Householder reflectors (per step: reflector in one
+//      CTA, SYMV p = tau A22 v by warps-per-row, rank-2 update A22 -= v w^T +
+//      w v^T; the 8-30 MB matrix stays in L2).
+//   2. the nvec largest eigenvalues of T by Sturm-count bisection (one thread
+//      per eigenvalue, absolute accuracy ~eps ||T||).
+//   3. their eigenvectors by inverse iteration on T - lambda I (tridiagonal LU
+//      with partial pivoting), one warp per cluster of close eigenvalues
+//      with modified Gram-Schmidt inside the cluster (LAPACK dstein's rule:
+//      gap <= 1e-3 ||T||).
+//   4. V = Q Y, one warp per vector applying the reflectors in reverse.
+// Output as bt_syevd_f64: eigenvalues descending, vectors sign-normalised
+// (largest-|.| entry positive, first on ties, decomp.py:176-179).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
+
+#include "bt_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+__device__ double block_reduce_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+  return t;
+}
+
+// reflector for column k: x = A[k+1:, k];  H = I - tau v v^T, v[k+1] = 1
+// (LAPACK dlarfg convention).  Writes d[k], e[k], tau[k], V row k.
+__global__ void __launch_bounds__(256)
+    house_kernel(double* __restrict__ a, int64_t n, int64_t k, double* __restrict__ d,
+                 double* __restrict__ e, double* __restrict__ tau, double* __restrict__ vref) {
+  __shared__ double red[8];
+  __shared__ double sh[3];
+  const int64_t m0 = k + 1;
+  double s = 0.0;
+  for (int64_t i = m0 + 1 + threadIdx.x; i < n; i += blockDim.x) {
+    const double x = a[i * n + k];
+    s = fma(x, x, s);
+  }
+  const double tail2 = block_reduce_sum(s, red);
+  if (threadIdx.x == 0) {
+    const double x0 = a[m0 * n + k];
+    d[k] = a[k * n + k];
+    if (tail2 == 0.0) {
+      sh[0] = 0.0;       // tau
+      sh[1] = x0;        // beta
+      sh[2] = 0.0;       // scale
+    } else {
+      const double nrm = sqrt(x0 * x0 + tail2);
+      const double beta = (x0 >= 0.0) ? -nrm : nrm;
+      sh[0] = (beta - x0) / beta;
+      sh[1] = beta;
+      sh[2] = 1.0 / (x0 - beta);
+    }
+    tau[k] = sh[0];
+    e[k] = sh[1];
+  }
+  __syncthreads();
+  const double sc = sh[2];
+  double* v = vref + k * n;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    double val = 0.0;
+    if (i == m0) val = 1.0;
+    else if (i > m0) val = a[i * n + k] * sc;
+    v[i] = val;
+  }
+}
+
+// p[i] = tau * sum_{j > k} A[i][j] v[j] for i > k; part[cta] = sum_i p_i v_i
+__global__ void __launch_bounds__(256)
+    symv_kernel(const double* __restrict__ a, int64_t n, int64_t k,
+                const double* __restrict__ tau, const double* __restrict__ vref,
+                double* __restrict__ p, double* __restrict__ part) {
+  __shared__ double red[8];
+  const double t = tau[k];
+  const double* v = vref + k * n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t m0 = k + 1;
+  double local = 0.0;
+  for (int64_t i = m0 + blockIdx.x * 8 + warp; i < n; i += (int64_t)gridDim.x * 8) {
+    const double* row = a + i * n;
+    double s = 0.0;
+    for (int64_t j = m0 + lane; j < n; j += 32) s = fma(row[j], v[j], s);
+    s = warp_sum(s) * t;
+    if (lane == 0) {
+      p[i] = s;
+      local = fma(s, v[i], local);
+    }
+  }
+  const double tot = block_reduce_sum(local, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+// A22 -= v w^T + w v^T with w = p - (tau/2)(p^T v) v
+__global__ void __launch_bounds__(256)
+    rank2_kernel(double* __restrict__ a, int64_t n, int64_t k, const double* __restrict__ tau,
+                 const double* __restrict__ vref, const double* __restrict__ p,
+                 const double* __restrict__ part, int nparts) {
+  __shared__ double alpha_sh;
+  if (threadIdx.x == 0) {
+    double ptv = 0.0;
+    for (int i = 0; i < nparts; ++i) ptv += part[i];
+    alpha_sh = 0.5 * tau[k] * ptv;
+  }
+  __syncthreads();
+  const double alpha = alpha_sh;
+  const double* v = vref + k * n;
+  const int64_t m0 = k + 1;
+  const int64_t m = n - m0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < m * m;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = m0 + idx / m, j = m0 + idx % m;
+    const double wi = p[i] - alpha * v[i], wj = p[j] - alpha * v[j];
+    a[i * n + j] -= v[i] * wj + wi * v[j];
+  }
+}
+
+// Whole tridiagonalisation in one cooperative launch (one CTA per SM, two
+// grid-wide barriers per reflector instead of three kernel launches): every
+// CTA recomputes the reflector of column k redundantly from L2 (no barrier
+// needed for it), SYMV rows are spread over all warps of the grid, then the
+// rank-2 update.
+__global__ void __launch_bounds__(256)
+    tridiag_coop_kernel(double* __restrict__ a, int64_t n, double* __restrict__ d,
+                        double* __restrict__ e, double* __restrict__ tau,
+                        double* __restrict__ vref, double* __restrict__ p,
+                        double* __restrict__ part) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double smv[];
+  double* vs = smv;       // v (n)   -- reflector, from row k (A stays exactly symmetric)
+  double* ps = smv + n;   // p (n)
+  __shared__ double red[8];
+  __shared__ double sh[3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gwarps = (int64_t)gridDim.x * 8;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + warp;
+  for (int64_t k = 0; k + 2 < n; ++k) {
+    const int64_t m0 = k + 1;
+    const double* rowk = a + k * n;
+    // -- reflector (redundant per CTA; row k == column k bit for bit)
+    double s = 0.0;
+    for (int64_t i = m0 + 1 + threadIdx.x; i < n; i += blockDim.x) s = fma(rowk[i], rowk[i], s);
+    const double tail2 = block_reduce_sum(s, red);
+    if (threadIdx.x == 0) {
+      const double x0 = rowk[m0];
+      if (tail2 == 0.0) {
+        sh[0] = 0.0;
+        sh[1] = x0;
+        sh[2] = 0.0;
+      } else {
+        const double nrm = sqrt(x0 * x0 + tail2);
+        const double beta = (x0 >= 0.0) ? -nrm : nrm;
+        sh[0] = (beta - x0) / beta;
+        sh[1] = beta;
+        sh[2] = 1.0 / (x0 - beta);
+      }
+      if (blockIdx.x == 0) {
+        d[k] = rowk[k];
+        tau[k] = sh[0];
+        e[k] = sh[1];
+      }
+    }
+    __syncthreads();
+    const double t = sh[0], sc = sh[2];
+    for (int64_t i = m0 + threadIdx.x; i < n; i += blockDim.x)
+      vs[i] = (i == m0) ? 1.0 : rowk[i] * sc;
+    if (blockIdx.x == 0)
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        vref[k * n + i] = (i < m0) ? 0.0 : ((i == m0) ? 1.0 : rowk[i] * sc);
+    __syncthreads();
+    // -- SYMV: p_i = t * sum_j A[i][j] v[j]
+    double local = 0.0;
+    for (int64_t i = m0 + gw; i < n; i += gwarps) {
+      const double* row = a + i * n;
+      double acc = 0.0;
+      for (int64_t j = m0 + lane; j < n; j += 32) acc = fma(row[j], vs[j], acc);
+      acc = warp_sum(acc) * t;
+      if (lane == 0) {
+        p[i] = acc;
+        local = fma(acc, vs[i], local);
+      }
+    }
+    const double tot = block_reduce_sum(local, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = tot;
+    grid.sync();
+    // -- rank-2 update A22 -= v w^T + w v^T, w = p - (t/2)(p^T v) v
+    if (threadIdx.x == 0) {
+      double ptv = 0.0;
+      for (int i = 0; i < (int)gridDim.x; ++i) ptv += part[i];
+      sh[0] = 0.5 * t * ptv;
+    }
+    __syncthreads();
+    const double alpha = sh[0];
+    for (int64_t i = m0 + threadIdx.x; i < n; i += blockDim.x) ps[i] = p[i] - alpha * vs[i];  // w
+    __syncthreads();
+    const int64_t m = n - m0;
+    // rows of A22 spread over the grid, columns over the lanes (coalesced)
+    for (int64_t i = m0 + gw; i < n; i += gwarps) {
+      double* row = a + i * n;
+      const double vi = vs[i], wi = ps[i];
+      for (int64_t j = m0 + lane; j < n; j += 32) row[j] -= vi * ps[j] + wi * vs[j];
+    }
+    (void)m;
+    grid.sync();
+  }
+}
+
+__global__ void tail_kernel(const double* __restrict__ a, int64_t n, double* __restrict__ d,
+                            double* __restrict__ e) {
+  if (threadIdx.x == 0) {
+    d[n - 2] = a[(n - 2) * n + (n - 2)];
+    d[n - 1] = a[(n - 1) * n + (n - 1)];
+    e[n - 2] = a[(n - 1) * n + (n - 2)];
+  }
+}
+
+// number of eigenvalues of T strictly less than x (Sturm sequence, dstebz)
+__device__ int sturm_less(const double* __restrict__ d, const double* __restrict__ e2, int64_t n,
+                          double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  if (q < 0.0) ++cnt;
+  for (int64_t i = 1; i < n; ++i) {
+    q = d[i] - x - e2[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    if (q < 0.0) ++cnt;
+  }
+  return cnt;
+}
+
+// e2 = e^2, bounds (Gershgorin), pivmin
+__global__ void prep_kernel(const double* __restrict__ d, const double* __restrict__ e, int64_t n,
+                            double* __restrict__ e2, double* __restrict__ bounds) {
+  __shared__ double lo_s[256], hi_s[256], em_s[256];
+  double lo = INFINITY, hi = -INFINITY, em = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double el = (i > 0) ? fabs(e[i - 1]) : 0.0;
+    const double er = (i < n - 1) ? fabs(e[i]) : 0.0;
+    lo = fmin(lo, d[i] - el - er);
+    hi = fmax(hi, d[i] + el + er);
+    if (i < n - 1) {
+      e2[i] = e[i] * e[i];
+      em = fmax(em, e[i] * e[i]);
+    }
+  }
+  lo_s[threadIdx.x] = lo;
+  hi_s[threadIdx.x] = hi;
+  em_s[threadIdx.x] = em;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 1; t < (int)blockDim.x; ++t) {
+      lo = fmin(lo, lo_s[t]);
+      hi = fmax(hi, hi_s[t]);
+      em = fmax(em, em_s[t]);
+    }
+    const double tnorm = fmax(fabs(lo), fabs(hi));
+    bounds[0] = lo - 4.0 * 2.2e-16 * tnorm - 1e-300;
+    bounds[1] = hi + 4.0 * 2.2e-16 * tnorm + 1e-300;
+    bounds[2] = fmax(2.2e-308, 2.2e-308 * em);  // pivmin (dstebz: safmin * max e^2)
+    bounds[3] = tnorm;
+  }
+}
+
+// w[c] = (c+1)-th largest eigenvalue, c < nvec: multisection, one warp per
+// eigenvalue, 32 Sturm counts per round (the interval shrinks 33x a round)
+__global__ void __launch_bounds__(256)
+    bisect_kernel(const double* __restrict__ d, const double* __restrict__ e2, int64_t n,
+                  int64_t nvec, const double* __restrict__ bounds, double* __restrict__ w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c >= nvec) return;
+  const int target = static_cast<int>(n - 1 - c);  // eigenvalue index in ascending order
+  double lo = bounds[0], hi = bounds[1];
+  const double pivmin = bounds[2];
+  for (int round = 0; round < 40; ++round) {
+    if (hi - lo <= 2.0 * 2.2e-16 * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+    const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
+    const bool le = sturm_less(d, e2, n, x, pivmin) <= target;   // lambda_target >= x
+    const unsigned mask = __ballot_sync(0xffffffffu, le);
+    // points are increasing in lane; le is true for a prefix of lanes
+    const int cnt = __popc(mask);
+    const double nlo = (cnt > 0) ? lo + (hi - lo) * (double)cnt / 33.0 : lo;
+    const double nhi = (cnt < 32) ? lo + (hi - lo) * (double)(cnt + 1) / 33.0 : hi;
+    if (!(nlo < nhi) || (nlo == lo && nhi == hi)) break;
+    lo = nlo;
+    hi = nhi;
+  }
+  if (lane == 0) w[c] = 0.5 * (lo + hi);
+}
+
+// cluster starts: start[c] = 1 if c == 0 or w[c-1] - w[c] > 1e-3 ||T||;
+// eigenvalues at or below tau * |w0| get no vector (start = -1)
+__global__ void cluster_kernel(const double* __restrict__ w, int64_t nvec,
+                               const double* __restrict__ bounds, double tau,
+                               int* __restrict__ start) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nvec) return;
+  if (c > 0 && !(w[c] > tau * fabs(w[0]))) {
+    start[c] = -1;
+    return;
+  }
+  start[c] = (c == 0 || (w[c - 1] - w[c]) > 1e-3 * bounds[3]) ? 1 : 0;
+}
+
+// Inverse iteration: one warp per cluster (a warp whose first vector is not a
+// cluster start exits).  Y is stored vector-major: y[c * n + i].
+__global__ void __launch_bounds__(32)
+    invit_kernel(const double* __restrict__ d, const double* __restrict__ e, int64_t n,
+                 int64_t nvec, const double* __restrict__ wv, const int* __restrict__ start,
+                 const double* __restrict__ bounds, double* __restrict__ y,
+                 double* __restrict__ scratch) {
+  const int64_t c0 = blockIdx.x;
+  if (c0 >= nvec) return;
+  if (start[c0] == -1) {
+    for (int64_t i = threadIdx.x; i < n; i += 32) y[c0 * n + i] = 0.0;
+    return;
+  }
+  if (!start[c0]) return;
+  int64_t c1 = c0 + 1;
+  while (c1 < nvec && start[c1] == 0) ++c1;
+  const int lane = threadIdx.x;
+  // LU of T - lambda I with partial pivoting: rows i store (u0 diag, u1, u2 super) and
+  // multiplier l, piv flag
+  double* u0 = scratch + c0 * 5 * n;
+  double* u1 = u0 + n;
+  double* u2 = u1 + n;
+  double* lm = u2 + n;
+  double* pv = lm + n;
+  const double tnorm = bounds[3];
+  const double eps = 2.2e-16;
+  double prev_lambda = 0.0;
+  for (int64_t c = c0; c < c1; ++c) {
+    double lambda = wv[c];
+    // dstein: separate coincident eigenvalues in a cluster slightly
+    if (c > c0 && lambda >= prev_lambda - 10.0 * eps * tnorm) lambda = prev_lambda - 10.0 * eps * tnorm;
+    prev_lambda = lambda;
+    double* yc = y + c * n;
+    if (lane == 0) {
+      // factor T - lambda I = P L U (U: diagonal u0, superdiagonals u1, u2)
+      double al = d[0] - lambda, be = (n > 1) ? e[0] : 0.0;
+      for (int64_t i = 0; i < n - 1; ++i) {
+        const double sub = e[i];
+        const double dn = d[i + 1] - lambda;
+        const double en = (i + 1 < n - 1) ? e[i + 1] : 0.0;
+        if (fabs(al) >= fabs(sub)) {
+          const double piv = (al == 0.0) ? eps * tnorm + 1e-300 : al;
+          const double l = sub / piv;
+          u0[i] = piv;
+          u1[i] = be;
+          u2[i] = 0.0;
+          lm[i] = l;
+          pv[i] = 0.0;
+          al = dn - l * be;
+          be = en;
+        } else {
+          const double l = al / sub;
+          u0[i] = sub;
+          u1[i] = dn;
+          u2[i] = en;
+          lm[i] = l;
+          pv[i] = 1.0;
+          al = be - l * dn;
+          be = -l * en;
+        }
+      }
+      const double a0 = al;
+      u0[n - 1] = (a0 == 0.0) ? eps * tnorm + 1e-300 : a0;
+      u1[n - 1] = 0.0;
+      u2[n - 1] = 0.0;
+      // deterministic start vector
+      for (int64_t i = 0; i < n; ++i) {
+        uint64_t h = (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull ^ (uint64_t)(c + 7) * 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 31;
+        yc[i] = 1.0 + 0.5 * ((double)(h & 0xFFFFF) / 1048576.0 - 0.5);
+      }
+    }
+    __syncwarp();
+    for (int iter = 0; iter < 3; ++iter) {
+      if (lane == 0) {
+        // forward: apply row interchanges and multipliers
+        for (int64_t i = 0; i < n - 1; ++i) {
+          if (pv[i] != 0.0) {
+            const double t = yc[i];
+            yc[i] = yc[i + 1];
+            yc[i + 1] = t;
+          }
+          yc[i + 1] -= lm[i] * yc[i];
+        }
+        // back substitution with U (diag u0, super u1, super-super u2)
+        yc[n - 1] = yc[n - 1] / u0[n - 1];
+        if (n > 1) yc[n - 2] = (yc[n - 2] - u1[n - 2] * yc[n - 1]) / u0[n - 2];
+        for (int64_t i = n - 3; i >= 0; --i)
+          yc[i] = (yc[i] - u1[i] * yc[i + 1] - u2[i] * yc[i + 2]) / u0[i];
+      }
+      __syncwarp();
+      // MGS against earlier members of the cluster, then normalise
+      for (int64_t o = c0; o < c; ++o) {
+        const double* yo = y + o * n;
+        double s = 0.0;
+        for (int64_t i = lane; i < n; i += 32) s = fma(yo[i], yc[i], s);
+        s = warp_sum(s);
+        for (int64_t i = lane; i < n; i += 32) yc[i] -= s * yo[i];
+        __syncwarp();
+      }
+      double s = 0.0;
+      for (int64_t i = lane; i < n; i += 32) s = fma(yc[i], yc[i], s);
+      s = warp_sum(s);
+      const double inv = (s > 0.0) ? 1.0 / sqrt(s) : 0.0;
+      for (int64_t i = lane; i < n; i += 32) yc[i] *= inv;
+      __syncwarp();
+    }
+  }
+}
+
+// V = Q Y: apply reflectors k = n-3 .. 0 to each vector (warp per vector)
+__global__ void __launch_bounds__(256)
+    backtransform_kernel(const double* __restrict__ vref, const double* __restrict__ tau,
+                         int64_t n, int64_t nvec, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c >= nvec) return;
+  double* yc = y + c * n;
+  for (int64_t k = n - 3; k >= 0; --k) {
+    const double t = tau[k];
+    if (t == 0.0) continue;
+    const double* v = vref + k * n;
+    double s = 0.0;
+    for (int64_t i = k + 1 + lane; i < n; i += 32) s = fma(v[i], yc[i], s);
+    s = warp_sum(s) * t;
+    for (int64_t i = k + 1 + lane; i < n; i += 32) yc[i] -= s * v[i];
+    __syncwarp();
+  }
+}
+
+// sign rule + row-major output vout (n x nvec)
+__global__ void __launch_bounds__(256)
+    sign_out_kernel(const double* __restrict__ y, int64_t n, int64_t nvec,
+                    double* __restrict__ vout) {
+  __shared__ double bv[256];
+  __shared__ int64_t bi[256];
+  for (int64_t c = blockIdx.x; c < nvec; c += gridDim.x) {
+    const double* yc = y + c * n;
+    double best = -1.0;
+    int64_t bidx = 0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const double x = fabs(yc[i]);
+      if (x > best) {
+        best = x;
+        bidx = i;
+      }
+    }
+    bv[threadIdx.x] = best;
+    bi[threadIdx.x] = bidx;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+      if (threadIdx.x < s) {
+        const double o = bv[threadIdx.x + s];
+        const int64_t oi = bi[threadIdx.x + s];
+        if (o > bv[threadIdx.x] || (o == bv[threadIdx.x] && oi < bi[threadIdx.x])) {
+          bv[threadIdx.x] = o;
+          bi[threadIdx.x] = oi;
+        }
+      }
+      __syncthreads();
+    }
+    const double sgn = (yc[bi[0]] < 0.0) ? -1.0 : 1.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) vout[i * nvec + c] = sgn * yc[i];
+    __syncthreads();
+  }
+}
+
+struct XPlan {
+  int64_t off_a, off_v, off_d, off_e, off_e2, off_tau, off_p, off_part, off_bounds, off_start,
+      off_y, off_scr, total;
+  int parts;
+};
+
+XPlan xplan(int64_t n, int64_t nvec) {
+  XPlan p;
+  p.parts = 148 * 4;
+  int64_t o = 0;
+  auto take = [&](int64_t k) {
+    int64_t at = o;
+    o += (k + 1) / 2 * 2;
+    return at;
+  };
+  p.off_a = take(n * n);
+  p.off_v = take(n * n);
+  p.off_d = take(n);
+  p.off_e = take(n);
+  p.off_e2 = take(n);
+  p.off_tau = take(n);
+  p.off_p = take(n);
+  p.off_part = take(p.parts);
+  p.off_bounds = take(4);
+  p.off_start = take(nvec);  // ints fit in doubles
+  p.off_y = take(nvec * n);
+  p.off_scr = take(nvec * 5 * n);
+  p.total = o;
+  return p;
+}
+
+}  // namespace
+
+extern "C" int64_t bt_syevx_ws_bytes(int64_t n, int64_t nvec) { return xplan(n, nvec).total * 8; }
+
+extern "C" int bt_syevx_f64(const double* a, int64_t n, int64_t nvec, double vec_tau, double* w,
+                            double* v, void* wsv, int64_t ws_bytes, void* stream) {
+  BT_REQUIRE(n >= 3 && nvec >= 1 && nvec <= n, BT_E_SHAPE, "syevx: need n >= 3, 1 <= nvec <= n");
+  XPlan p = xplan(n, nvec);
+  BT_REQUIRE(ws_bytes >= p.total * 8, BT_E_VALUE, "syevx: workspace too small");
+  cudaStream_t st = bt_stream(stream);
+  double* ws = static_cast<double*>(wsv);
+  double* A = ws + p.off_a;
+  double* V = ws + p.off_v;
+  double* d = ws + p.off_d;
+  double* e = ws + p.off_e;
+  double* e2 = ws + p.off_e2;
+  double* tau = ws + p.off_tau;
+  double* pp = ws + p.off_p;
+  double* part = ws + p.off_part;
+  double* bounds = ws + p.off_bounds;
+  int* start = reinterpret_cast<int*>(ws + p.off_start);
+  double* y = ws + p.off_y;
+  double* scr = ws + p.off_scr;
+  BT_CUDA_CHECK(cudaMemcpyAsync(A, a, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
+  const bool dbg = getenv("BT_EIG_DEBUG") != nullptr;
+  cudaEvent_t ev[6];
+  if (dbg)
+    for (auto& x : ev) cudaEventCreate(&x);
+  if (dbg) cudaEventRecord(ev[0], st);
+  {
+    int dev = 0, per_sm = 0;
+    BT_CUDA_CHECK(cudaGetDevice(&dev));
+    BT_CUDA_CHECK(cudaFuncSetAttribute(tridiag_coop_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sizeof(double) * 2 * n)));
+    BT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tridiag_coop_kernel, 256,
+                                                                sizeof(double) * 2 * n));
+    const int grid = std::min(bt_num_sms() * std::max(per_sm, 1), std::min(p.parts, bt_num_sms()));
+    void* args[] = {&A, (void*)&n, &d, &e, &tau, &V, &pp, &part};
+    const size_t sm = sizeof(double) * 2 * n;
+    BT_CUDA_CHECK(cudaFuncSetAttribute(tridiag_coop_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(std::max<size_t>(sm, 1))));
+    BT_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)tridiag_coop_kernel, dim3(grid),
+                                              dim3(256), args, sm, st));
+    BT_LAUNCH_CHECK();
+  }
+  if (dbg) cudaEventRecord(ev[1], st);
+  tail_kernel<<<1, 32, 0, st>>>(A, n, d, e);
+  BT_LAUNCH_CHECK();
+  prep_kernel<<<1, 256, 0, st>>>(d, e, n, e2, bounds);
+  BT_LAUNCH_CHECK();
+  bisect_kernel<<<static_cast<unsigned>(bt_cdiv(nvec, 8)), 256, 0, st>>>(d, e2, n, nvec, bounds, w);
+  BT_LAUNCH_CHECK();
+  if (dbg) cudaEventRecord(ev[2], st);
+  cluster_kernel<<<static_cast<unsigned>(bt_cdiv(nvec, 256)), 256, 0, st>>>(w, nvec, bounds, vec_tau,
+                                                                          start);
+  BT_LAUNCH_CHECK();
+  invit_kernel<<<static_cast<unsigned>(nvec), 32, 0, st>>>(d, e, n, nvec, w, start, bounds, y, scr);
+  BT_LAUNCH_CHECK();
+  if (dbg) cudaEventRecord(ev[3], st);
+  backtransform_kernel<<<static_cast<unsigned>(bt_cdiv(nvec, 8)), 256, 0, st>>>(V, tau, n, nvec, y);
+  BT_LAUNCH_CHECK();
+  if (dbg) cudaEventRecord(ev[4], st);
+  sign_out_kernel<<<static_cast<unsigned>(std::min<int64_t>(nvec, 4096)), 256, 0, st>>>(y, n, nvec, v);
+  BT_LAUNCH_CHECK();
+  if (dbg) {
+    cudaEventRecord(ev[5], st);
+    cudaEventSynchronize(ev[5]);
+    float t[5];
+    for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+    fprintf(stderr, "[syevx n=%lld nvec=%lld] tridiag %.3f bisect %.3f invit %.3f back %.3f out %.3f ms\n",
+            (long long)n, (long long)nvec, t[0], t[1], t[2], t[3], t[4]);
+    for (auto& x : ev) cudaEventDestroy(x);
+  }
+  return BT_OK;
+}

@@ -106,6 +106,9 @@ struct BtTileLoader {
 };
 
 // The main loop over k-tiles [kt0, kt1) of one (m0, n0) output tile.
+// k-tile coordinates (ko, ki) advance incrementally (no divisions in the
+// loop); fragments are double-buffered in registers so the smem reads of
+// step kk+4 overlap the DMMAs of step kk.
 template <class Cfg>
 __device__ __forceinline__ void bt_gemm_mainloop(const BtGemmArgs& g, int64_t batch, int64_t m0,
                                                  int64_t n0, int64_t kt0, int64_t kt1,
@@ -120,6 +123,7 @@ __device__ __forceinline__ void bt_gemm_mainloop(const BtGemmArgs& g, int64_t ba
   const int64_t ktPerKo = (g.Kin + Cfg::BK - 1) / Cfg::BK;
   const double* Ab = g.A.ptr + batch * g.A.s_b;
   const double* Bb = g.B.ptr + batch * g.B.s_b;
+  constexpr int KSTEPS = Cfg::BK / 4;
 
   // A: K-contig -> rows m (stride s_mn), cols ki; M-contig -> rows ki (stride s_ki), cols m
   BtTileLoader<Cfg::ROWS_A, (Cfg::A_KCONTIG ? Cfg::BK : Cfg::BM), Cfg::LDA, Cfg::VEC, Cfg::THREADS>
@@ -137,30 +141,38 @@ __device__ __forceinline__ void bt_gemm_mainloop(const BtGemmArgs& g, int64_t ba
 #pragma unroll
     for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  auto load_stage = [&](int stage, int64_t kt) {
-    const int64_t ko = kt / ktPerKo;
-    const int64_t ki0 = (kt - ko * ktPerKo) * Cfg::BK;
+  // load-side k-tile cursor (runs STAGES-1 tiles ahead of the compute side)
+  int64_t l_ko = kt0 / ktPerKo;
+  int64_t l_ki = kt0 - l_ko * ktPerKo;
+  int64_t c_ko = l_ko, c_ki = l_ki;  // compute-side cursor
+  auto load_stage = [&](int stage) {
+    const int64_t ki0 = l_ki * Cfg::BK;
     const int64_t k_left = g.Kin - ki0;
     double* as = As + stage * Cfg::A_STAGE;
     double* bs = Bs + stage * Cfg::B_STAGE;
     if (Cfg::A_KCONTIG)
-      la.issue(as, a_tile + ko * g.A.s_ko + ki0, m_left, k_left, g.A.ptr);
+      la.issue(as, a_tile + l_ko * g.A.s_ko + ki0, m_left, k_left, g.A.ptr);
     else
-      la.issue(as, a_tile + ko * g.A.s_ko + ki0 * g.A.s_ki, k_left, m_left, g.A.ptr);
+      la.issue(as, a_tile + l_ko * g.A.s_ko + ki0 * g.A.s_ki, k_left, m_left, g.A.ptr);
     if (Cfg::B_KCONTIG)
-      lb.issue(bs, b_tile + ko * g.B.s_ko + ki0, n_left, k_left, g.B.ptr);
+      lb.issue(bs, b_tile + l_ko * g.B.s_ko + ki0, n_left, k_left, g.B.ptr);
     else
-      lb.issue(bs, b_tile + ko * g.B.s_ko + ki0 * g.B.s_ki, k_left, n_left, g.B.ptr);
+      lb.issue(bs, b_tile + l_ko * g.B.s_ko + ki0 * g.B.s_ki, k_left, n_left, g.B.ptr);
+    if (++l_ki == ktPerKo) {
+      l_ki = 0;
+      ++l_ko;
+    }
   };
 
 #pragma unroll
   for (int s = 0; s < Cfg::STAGES - 1; ++s) {
-    if (kt0 + s < kt1) load_stage(s, kt0 + s);
+    if (kt0 + s < kt1) load_stage(s);
     cp_async_commit();
   }
 
   int stage = 0;
   int next_stage = Cfg::STAGES - 1;
+  double afr[2][Cfg::FM], bfr[2][Cfg::FN];
   for (int64_t kt = kt0; kt < kt1; ++kt) {
     cp_async_wait<Cfg::STAGES - 2>();
     __syncthreads();
@@ -168,8 +180,7 @@ __device__ __forceinline__ void bt_gemm_mainloop(const BtGemmArgs& g, int64_t ba
     const double* bs = Bs + stage * Cfg::B_STAGE;
     double sc[Cfg::FN];
     if (g.bscale != nullptr) {
-      const int64_t ko = kt / ktPerKo;
-      const double* srow = g.bscale + batch * g.s_scale_b + ko * g.s_scale_ko;
+      const double* srow = g.bscale + batch * g.s_scale_b + c_ko * g.s_scale_ko;
 #pragma unroll
       for (int j = 0; j < Cfg::FN; ++j) {
         const int64_t n = n0 + wn0 + j * 8 + gq;
@@ -179,39 +190,45 @@ __device__ __forceinline__ void bt_gemm_mainloop(const BtGemmArgs& g, int64_t ba
     const double* arow = nullptr;
     int64_t a_kleft = 0;
     if (g.ascale != nullptr) {
-      const int64_t ko = kt / ktPerKo;
-      const int64_t ki0 = (kt - ko * ktPerKo) * Cfg::BK;
-      arow = g.ascale + batch * g.s_ascale_b + ko * g.s_ascale_ko + ki0;
+      const int64_t ki0 = c_ki * Cfg::BK;
+      arow = g.ascale + batch * g.s_ascale_b + c_ko * g.s_ascale_ko + ki0;
       a_kleft = g.Kin - ki0;
     }
-#pragma unroll
-    for (int kk = 0; kk < Cfg::BK; kk += 4) {
-      double a[Cfg::FM], b[Cfg::FN];
+    auto load_frags = [&](int buf, int kk) {
       double asc = 1.0;
       if (g.ascale != nullptr) asc = (kk + tq < a_kleft) ? __ldg(arow + kk + tq) : 0.0;
 #pragma unroll
       for (int i = 0; i < Cfg::FM; ++i) {
         const int m = wm0 + i * 8 + gq;
-        a[i] = Cfg::A_KCONTIG ? as[m * Cfg::LDA + kk + tq] : as[(kk + tq) * Cfg::LDA + m];
-        if (g.ascale != nullptr) a[i] *= asc;
+        afr[buf][i] = Cfg::A_KCONTIG ? as[m * Cfg::LDA + kk + tq] : as[(kk + tq) * Cfg::LDA + m];
+        if (g.ascale != nullptr) afr[buf][i] *= asc;
       }
 #pragma unroll
       for (int j = 0; j < Cfg::FN; ++j) {
         const int n = wn0 + j * 8 + gq;
-        b[j] = Cfg::B_KCONTIG ? bs[n * Cfg::LDB + kk + tq] : bs[(kk + tq) * Cfg::LDB + n];
-        if (g.bscale != nullptr) b[j] *= sc[j];
+        bfr[buf][j] = Cfg::B_KCONTIG ? bs[n * Cfg::LDB + kk + tq] : bs[(kk + tq) * Cfg::LDB + n];
+        if (g.bscale != nullptr) bfr[buf][j] *= sc[j];
       }
+    };
+    load_frags(0, 0);
+#pragma unroll
+    for (int ks = 0; ks < KSTEPS; ++ks) {
+      if (ks + 1 < KSTEPS) load_frags((ks + 1) & 1, (ks + 1) * 4);
 #pragma unroll
       for (int i = 0; i < Cfg::FM; ++i)
 #pragma unroll
-        for (int j = 0; j < Cfg::FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-      if (kk == 0) {
+        for (int j = 0; j < Cfg::FN; ++j)
+          dmma884(acc[i][j][0], acc[i][j][1], afr[ks & 1][i], bfr[ks & 1][j]);
+      if (ks == 0) {
         // refill the stage consumed in the previous iteration while this
         // stage's DMMAs drain
-        const int64_t nk = kt + Cfg::STAGES - 1;
-        if (nk < kt1) load_stage(next_stage, nk);
+        if (kt + Cfg::STAGES - 1 < kt1) load_stage(next_stage);
         cp_async_commit();
       }
+    }
+    if (++c_ki == ktPerKo) {
+      c_ki = 0;
+      ++c_ko;
     }
     stage = (stage + 1 == Cfg::STAGES) ? 0 : stage + 1;
     next_stage = (next_stage + 1 == Cfg::STAGES) ? 0 : next_stage + 1;

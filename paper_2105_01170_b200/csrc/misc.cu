@@ -114,6 +114,20 @@ extern "C" int bt_peak_dmma(int64_t iters, int blocks, int threads, double* sink
   return BT_OK;
 }
 
+extern "C" int bt_peak_dmma_chains(int64_t iters, int blocks, int threads, int chains,
+                                   double* sink, double* flops, void* stream) {
+  switch (chains) {
+    case 2: bt_peak_dmma_kernel<2><<<blocks, threads, 0, bt_stream(stream)>>>(iters, sink); break;
+    case 4: bt_peak_dmma_kernel<4><<<blocks, threads, 0, bt_stream(stream)>>>(iters, sink); break;
+    case 16: bt_peak_dmma_kernel<16><<<blocks, threads, 0, bt_stream(stream)>>>(iters, sink); break;
+    case 32: bt_peak_dmma_kernel<32><<<blocks, threads, 0, bt_stream(stream)>>>(iters, sink); break;
+    default: chains = 8; bt_peak_dmma_kernel<8><<<blocks, threads, 0, bt_stream(stream)>>>(iters, sink);
+  }
+  BT_LAUNCH_CHECK();
+  *flops = (double)blocks * (threads / 32) * (double)iters * chains * 512.0;
+  return BT_OK;
+}
+
 extern "C" int bt_peak_dfma(int64_t iters, int blocks, int threads, double* sink, double* flops,
                             void* stream) {
   bt_peak_dfma_kernel<8><<<blocks, threads, 0, bt_stream(stream)>>>(iters, sink);
@@ -275,6 +289,55 @@ extern "C" int bt_col_normalize_f64(double* x, int64_t rows, int64_t cols, void*
   if (rows <= 0 || cols <= 0) return BT_OK;
   const int64_t blocks = (cols + 7) / 8 < 1024 ? (cols + 7) / 8 : 1024;
   bt_col_normalize_kernel<<<static_cast<int>(blocks), 256, 0, bt_stream(stream)>>>(x, rows, cols);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// sign rule of decomp.py:176-179 on every column of a row-major matrix:
+// flip so the largest-|.| entry (first on ties) is positive
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) bt_sign_fix_kernel(double* __restrict__ x, int64_t rows,
+                                                          int64_t cols) {
+  __shared__ double bv[256];
+  __shared__ int64_t bi[256];
+  for (int64_t c = blockIdx.x; c < cols; c += gridDim.x) {
+    double best = -1.0;
+    int64_t bidx = 0;
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+      const double v = fabs(x[i * cols + c]);
+      if (v > best) {
+        best = v;
+        bidx = i;
+      }
+    }
+    bv[threadIdx.x] = best;
+    bi[threadIdx.x] = bidx;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+      if (threadIdx.x < s) {
+        const double o = bv[threadIdx.x + s];
+        const int64_t oi = bi[threadIdx.x + s];
+        if (o > bv[threadIdx.x] || (o == bv[threadIdx.x] && oi < bi[threadIdx.x])) {
+          bv[threadIdx.x] = o;
+          bi[threadIdx.x] = oi;
+        }
+      }
+      __syncthreads();
+    }
+    const bool flip = x[bi[0] * cols + c] < 0.0;
+    __syncthreads();
+    if (flip)
+      for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) x[i * cols + c] = -x[i * cols + c];
+    __syncthreads();
+  }
+}
+
+extern "C" int bt_sign_fix_f64(double* x, int64_t rows, int64_t cols, void* stream) {
+  if (rows <= 0 || cols <= 0) return BT_OK;
+  const int64_t g = cols < 4096 ? cols : 4096;
+  bt_sign_fix_kernel<<<static_cast<int>(g), 256, 0, bt_stream(stream)>>>(x, rows, cols);
   BT_LAUNCH_CHECK();
   return BT_OK;
 }

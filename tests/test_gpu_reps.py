@@ -158,7 +158,10 @@ def test_c3_small_partial_tucker_and_spsd(golden):
     rep = bt.tucker_partial(z["c3s_t"], [8, 4, 8], shared=(1, 3))
     assert rep.factors[0] is rep.factors[2]
     assert subspace_angle(rep.factors[0], z["c3s_u"]) < 1e-8
-    assert rel(rep.core, z["c3s_core"]) < 1e-9
+    # the core depends on the basis inside degenerate singular pairs (the
+    # symmetric tensor has them); the projected tensor does not
+    recon = lambda c, u: port.mode_multiply(port.mode_multiply(c, 1, u), 3, u)  # noqa: E731
+    assert rel(recon(rep.core, rep.factors[0]), recon(z["c3s_core"], z["c3s_u"])) < 1e-10
     pat = bt.build_pattern("toeplitz", 10, 10, 36, 36, block_symmetric=True)
     sp = psd.spsd_compress_blocks(pat, z["c3s_blocks"], 8)
     assert subspace_angle(sp.basis, z["c3s_spsd_u"]) < 1e-8
