@@ -5,6 +5,8 @@ sign rule, truncated SVD / mode bases built on them, thin QR."""
 from __future__ import annotations
 
 import ctypes as C
+import os
+import sys
 
 import numpy as np
 
@@ -57,6 +59,7 @@ def eigh_dev(gd, nvec: int | None = None, tau: float = -1.0):
     return w, v
 
 
+_DEBUG = bool(os.environ.get("BT_BASIS_DEBUG"))
 RESOLVE_TAU = 1e-3   # per pass: eigenvectors with lambda > tau * lambda_max are kept (cut accuracy ~eps/tau)
 
 
@@ -149,6 +152,9 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
         if top == 0.0 or wh[0] <= 1e-28 * top:
             break                                   # remainder is rounding noise
         k = int(np.sum(wh[:need] > RESOLVE_TAU * wh[0]))
+        if _DEBUG:
+            print(f"[mode_basis n={n} r={r}] pass: need {need} resolved {k} "
+                  f"lambda_top {wh[0]:.3e} ({wh[0] / top:.1e} of first)", file=sys.stderr)
         if basis is None and k >= need:
             return v[:, :need].contiguous()         # one pass resolved everything
         k = max(1, min(need, k))

@@ -130,33 +130,42 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Whole tridiagonalisation in one cooperative launch (one CTA per SM, two
-// grid-wide barriers per reflector instead of three kernel launches): every
-// CTA recomputes the reflector of column k redundantly from L2 (no barrier
-// needed for it), SYMV rows are spread over all warps of the grid, then the
-// rank-2 update.
-__global__ void __launch_bounds__(256)
+// Whole tridiagonalisation in one cooperative launch (one 1024-thread CTA
+// per SM, two grid-wide barriers per reflector): every CTA recomputes the
+// reflector of column k redundantly from row k (A is kept exactly symmetric),
+// the SYMV and the rank-2 update are split into (row, 256-column chunk) work
+// items over all warps of the grid for memory-level parallelism, with
+// per-chunk SYMV partials summed in a fixed order (deterministic).
+constexpr int TCHUNK = 256;
+
+__global__ void __launch_bounds__(1024)
     tridiag_coop_kernel(double* __restrict__ a, int64_t n, double* __restrict__ d,
                         double* __restrict__ e, double* __restrict__ tau,
-                        double* __restrict__ vref, double* __restrict__ p,
+                        double* __restrict__ vref, double* __restrict__ ppart,
                         double* __restrict__ part) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double smv[];
-  double* vs = smv;       // v (n)   -- reflector, from row k (A stays exactly symmetric)
-  double* ps = smv + n;   // p (n)
-  __shared__ double red[8];
+  double* vs = smv;       // v (n)
+  double* ws = smv + n;   // w (n)
+  __shared__ double red[32];
   __shared__ double sh[3];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t gwarps = (int64_t)gridDim.x * 8;
-  const int64_t gw = (int64_t)blockIdx.x * 8 + warp;
+  const int nw = blockDim.x >> 5;
+  const int64_t gwarps = (int64_t)gridDim.x * nw;
+  const int64_t gw = (int64_t)blockIdx.x * nw + warp;
+  const int64_t nchunk = (n + TCHUNK - 1) / TCHUNK;
   for (int64_t k = 0; k + 2 < n; ++k) {
     const int64_t m0 = k + 1;
     const double* rowk = a + k * n;
-    // -- reflector (redundant per CTA; row k == column k bit for bit)
+    // -- reflector (redundant per CTA)
     double s = 0.0;
     for (int64_t i = m0 + 1 + threadIdx.x; i < n; i += blockDim.x) s = fma(rowk[i], rowk[i], s);
-    const double tail2 = block_reduce_sum(s, red);
+    s = warp_sum(s);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
     if (threadIdx.x == 0) {
+      double tail2 = 0.0;
+      for (int w2 = 0; w2 < nw; ++w2) tail2 += red[w2];
       const double x0 = rowk[m0];
       if (tail2 == 0.0) {
         sh[0] = 0.0;
@@ -177,46 +186,145 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     const double t = sh[0], sc = sh[2];
-    for (int64_t i = m0 + threadIdx.x; i < n; i += blockDim.x)
-      vs[i] = (i == m0) ? 1.0 : rowk[i] * sc;
+    for (int64_t i = m0 + threadIdx.x; i < n; i += blockDim.x) vs[i] = (i == m0) ? 1.0 : rowk[i] * sc;
     if (blockIdx.x == 0)
       for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
         vref[k * n + i] = (i < m0) ? 0.0 : ((i == m0) ? 1.0 : rowk[i] * sc);
     __syncthreads();
-    // -- SYMV: p_i = t * sum_j A[i][j] v[j]
+    // -- SYMV partials: item (row i, chunk c) -> ppart[i * nchunk + c]
+    const int64_t c0 = m0 / TCHUNK;
+    const int64_t nc = nchunk - c0;
+    const int64_t items = (n - m0) * nc;
+    for (int64_t it = gw; it < items; it += gwarps) {
+      const int64_t i = m0 + it / nc;
+      const int64_t c = c0 + it % nc;
+      const int64_t j0 = max(m0, c * TCHUNK), j1 = min(n, (c + 1) * TCHUNK);
+      const double* row = a + i * n;
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < TCHUNK / 32; ++q) {
+        const int64_t j = j0 + lane + 32 * q;
+        if (j < j1) acc = fma(row[j], vs[j], acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) ppart[i * nchunk + c] = acc;
+    }
+    grid.sync();
+    // -- p = t * sum_c ppart (every CTA, fixed order), p^T v, w = p - (t/2)(p^T v) v
     double local = 0.0;
-    for (int64_t i = m0 + gw; i < n; i += gwarps) {
+    for (int64_t i = m0 + threadIdx.x; i < n; i += blockDim.x) {
+      double acc = 0.0;
+      for (int64_t c = c0; c < nchunk; ++c) acc += ppart[i * nchunk + c];
+      acc *= t;
+      ws[i] = acc;
+      local = fma(acc, vs[i], local);
+    }
+    local = warp_sum(local);
+    if (lane == 0) red[warp] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double ptv = 0.0;
+      for (int w2 = 0; w2 < nw; ++w2) ptv += red[w2];
+      sh[0] = 0.5 * t * ptv;
+    }
+    __syncthreads();
+    const double alpha = sh[0];
+    for (int64_t i = m0 + threadIdx.x; i < n; i += blockDim.x) ws[i] = ws[i] - alpha * vs[i];
+    __syncthreads();
+    // -- rank-2 update over the same (row, chunk) items
+    for (int64_t it = gw; it < items; it += gwarps) {
+      const int64_t i = m0 + it / nc;
+      const int64_t c = c0 + it % nc;
+      const int64_t j0 = max(m0, c * TCHUNK), j1 = min(n, (c + 1) * TCHUNK);
+      double* row = a + i * n;
+      const double vi = vs[i], wi = ws[i];
+#pragma unroll
+      for (int q = 0; q < TCHUNK / 32; ++q) {
+        const int64_t j = j0 + lane + 32 * q;
+        if (j < j1) row[j] -= vi * ws[j] + wi * vs[j];
+      }
+    }
+    grid.sync();
+  }
+}
+
+// Single-CTA tridiagonalisation for small n (<= 512): block barriers instead
+// of grid barriers (the multi-CTA version is barrier-latency bound there).
+__global__ void __launch_bounds__(1024)
+    tridiag_cta_kernel(double* __restrict__ a, int64_t n, double* __restrict__ d,
+                       double* __restrict__ e, double* __restrict__ tau,
+                       double* __restrict__ vref) {
+  extern __shared__ __align__(16) double smv[];
+  double* vs = smv;
+  double* ps = smv + n;
+  __shared__ double red[32];
+  __shared__ double sh[3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  for (int64_t k = 0; k + 2 < n; ++k) {
+    const int64_t m0 = k + 1;
+    const double* rowk = a + k * n;
+    double s = 0.0;
+    for (int64_t i = m0 + 1 + threadIdx.x; i < n; i += blockDim.x) s = fma(rowk[i], rowk[i], s);
+    s = warp_sum(s);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tail2 = 0.0;
+      for (int w = 0; w < nwarps; ++w) tail2 += red[w];
+      const double x0 = rowk[m0];
+      if (tail2 == 0.0) {
+        sh[0] = 0.0;
+        sh[1] = x0;
+        sh[2] = 0.0;
+      } else {
+        const double nrm = sqrt(x0 * x0 + tail2);
+        const double beta = (x0 >= 0.0) ? -nrm : nrm;
+        sh[0] = (beta - x0) / beta;
+        sh[1] = beta;
+        sh[2] = 1.0 / (x0 - beta);
+      }
+      d[k] = rowk[k];
+      tau[k] = sh[0];
+      e[k] = sh[1];
+    }
+    __syncthreads();
+    const double t = sh[0], sc = sh[2];
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const double v = (i < m0) ? 0.0 : ((i == m0) ? 1.0 : rowk[i] * sc);
+      vs[i] = v;
+      vref[k * n + i] = v;
+    }
+    __syncthreads();
+    // SYMV: warp per row
+    double local = 0.0;
+    for (int64_t i = m0 + warp; i < n; i += nwarps) {
       const double* row = a + i * n;
       double acc = 0.0;
       for (int64_t j = m0 + lane; j < n; j += 32) acc = fma(row[j], vs[j], acc);
       acc = warp_sum(acc) * t;
       if (lane == 0) {
-        p[i] = acc;
+        ps[i] = acc;
         local = fma(acc, vs[i], local);
       }
     }
-    const double tot = block_reduce_sum(local, red);
-    if (threadIdx.x == 0) part[blockIdx.x] = tot;
-    grid.sync();
-    // -- rank-2 update A22 -= v w^T + w v^T, w = p - (t/2)(p^T v) v
+    if (lane == 0) red[warp] = local;
+    __syncthreads();
     if (threadIdx.x == 0) {
       double ptv = 0.0;
-      for (int i = 0; i < (int)gridDim.x; ++i) ptv += part[i];
+      for (int w = 0; w < nwarps; ++w) ptv += red[w];
       sh[0] = 0.5 * t * ptv;
     }
     __syncthreads();
     const double alpha = sh[0];
-    for (int64_t i = m0 + threadIdx.x; i < n; i += blockDim.x) ps[i] = p[i] - alpha * vs[i];  // w
+    for (int64_t i = m0 + threadIdx.x; i < n; i += blockDim.x) ps[i] = ps[i] - alpha * vs[i];
     __syncthreads();
-    const int64_t m = n - m0;
-    // rows of A22 spread over the grid, columns over the lanes (coalesced)
-    for (int64_t i = m0 + gw; i < n; i += gwarps) {
+    for (int64_t i = m0 + warp; i < n; i += nwarps) {
       double* row = a + i * n;
       const double vi = vs[i], wi = ps[i];
       for (int64_t j = m0 + lane; j < n; j += 32) row[j] -= vi * ps[j] + wi * vs[j];
     }
-    (void)m;
-    grid.sync();
+    __syncthreads();
   }
 }
 
@@ -487,7 +595,7 @@ __global__ void __launch_bounds__(256)
 
 struct XPlan {
   int64_t off_a, off_v, off_d, off_e, off_e2, off_tau, off_p, off_part, off_bounds, off_start,
-      off_y, off_scr, total;
+      off_y, off_scr, off_ppart, total;
   int parts;
 };
 
@@ -512,6 +620,7 @@ XPlan xplan(int64_t n, int64_t nvec) {
   p.off_start = take(nvec);  // ints fit in doubles
   p.off_y = take(nvec * n);
   p.off_scr = take(nvec * 5 * n);
+  p.off_ppart = take(n * ((n + 255) / 256));
   p.total = o;
   return p;
 }
@@ -545,22 +654,32 @@ extern "C" int bt_syevx_f64(const double* a, int64_t n, int64_t nvec, double vec
   if (dbg)
     for (auto& x : ev) cudaEventCreate(&x);
   if (dbg) cudaEventRecord(ev[0], st);
-  {
+  if (n <= 160) {
+    const size_t sm = sizeof(double) * 2 * n;
+    BT_CUDA_CHECK(cudaFuncSetAttribute(tridiag_cta_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sm)));
+    tridiag_cta_kernel<<<1, 1024, sm, st>>>(A, n, d, e, tau, V);
+    BT_LAUNCH_CHECK();
+  } else {
     int dev = 0, per_sm = 0;
     BT_CUDA_CHECK(cudaGetDevice(&dev));
     BT_CUDA_CHECK(cudaFuncSetAttribute(tridiag_coop_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sizeof(double) * 2 * n)));
-    BT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tridiag_coop_kernel, 256,
+    BT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tridiag_coop_kernel, 1024,
                                                                 sizeof(double) * 2 * n));
-    const int grid = std::min(bt_num_sms() * std::max(per_sm, 1), std::min(p.parts, bt_num_sms()));
-    void* args[] = {&A, (void*)&n, &d, &e, &tau, &V, &pp, &part};
+    // small problems are grid-barrier bound (fewer CTAs), large ones latency
+    // bound on the L2-resident SYMV/update (more warps in flight)
+    const int grid = std::min(bt_num_sms() * std::max(per_sm, 1), bt_num_sms());
+    double* ppart = ws + p.off_ppart;
+    void* args[] = {&A, (void*)&n, &d, &e, &tau, &V, &ppart, &part};
     const size_t sm = sizeof(double) * 2 * n;
     BT_CUDA_CHECK(cudaFuncSetAttribute(tridiag_coop_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(std::max<size_t>(sm, 1))));
     BT_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)tridiag_coop_kernel, dim3(grid),
-                                              dim3(256), args, sm, st));
+                                              dim3(1024), args, sm, st));
     BT_LAUNCH_CHECK();
   }
   if (dbg) cudaEventRecord(ev[1], st);

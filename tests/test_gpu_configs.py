@@ -1,0 +1,131 @@
+"""Parity at (or near) the BASELINE config sizes: C1 full pipeline, C2 at full
+size against the numpy oracle (HOSVD of the 32x2047x32 Hankel tensor: operator
+and matvec agreement), C3 and C4 recipes at reduced sizes, and size-independent
+properties at C5-like sizes (fit monotone, replicated determinism)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2105_01170_b200 as bt  # noqa: E402
+from paper_2105_01170_b200 import configs, decomp, multilevel, psd, reconstruct  # noqa: E402
+from oracle import configs as oc  # noqa: E402
+from oracle import port  # noqa: E402
+
+from _helpers import subspace_angle  # noqa: E402
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
+
+
+def test_c1_full_pipeline(golden):
+    z = golden("cp")
+    pat, a = configs.c1_matrix()
+    t = bt.mat_to_tensor(a, pat)
+    assert np.array_equal(t.cpu().numpy(), z["c1_t"])
+    init = oc.normal_init((32, 32, 32), 8, 0)
+    saved = decomp._cp_init
+    decomp._cp_init = lambda _t, _r: [torch.from_numpy(f).cuda() for f in init]
+    try:
+        res = bt.cp_als(t, 8, 50, 0.0)
+    finally:
+        decomp._cp_init = saved
+    ks = reconstruct.kron_sum_from_kruskal(res.rep, pat)
+    err = reconstruct.error_fro(a, ks)
+    assert abs(err - float(z["c1_relerr"])) < 1e-8           # north_star: 1e-8 absolute
+    ys = reconstruct.matvec(ks, torch.from_numpy(z["c1_rhs"]).cuda())
+    assert rel(ys.cpu().numpy(), z["c1_mv"]) < 1e-10          # north_star: 1e-10 relative
+
+
+def test_c2_full_size_operator_parity():
+    params = configs.c2_markov()
+    pat, t = configs.c2_build(params)
+    _, to = oc.c2_tensor(params)
+    assert np.array_equal(t.cpu().numpy(), to)
+    rep = bt.hosvd(t, [32, 400, 32])
+    core_o, fac_o = port.hosvd(to, [32, 400, 32])
+    # leading, well-gapped block of the mode-2 basis
+    sv = np.linalg.svd(port.unfold(to, 2), compute_uv=False)
+    lead = int(np.sum(sv > 1e-4 * sv[0]))
+    assert subspace_angle(rep.factors[1][:, :lead].cpu().numpy(), fac_o[1][:, :lead]) < 1e-8
+    # the operator: M[T x2 P_V] must agree everywhere (projector, not basis)
+    blr = reconstruct.blr_from_tucker(rep, pat)
+    left, right, mids = port.blr_from_tucker(core_o, fac_o, pat.m, pat.n)
+    rhs = np.random.default_rng(1002).standard_normal((32768, 4))
+    y = reconstruct.matvec(blr, torch.from_numpy(rhs).cuda()).cpu().numpy()
+    yo = port.matvec_blr_fast(pat, left, right, mids, rhs)
+    assert rel(y, yo) < 1e-10
+    recon = port.mode_multiply(rep.core.cpu().numpy(), 2, rep.factors[1].cpu().numpy())
+    recon_o = port.mode_multiply(core_o, 2, fac_o[1])
+    assert rel(recon, recon_o) < 1e-10
+
+
+def test_c3_reduced_st_hosvd_spsd_vs_oracle():
+    pat, t = configs.c3_build(side=12, lags=40, lag_scale=40)
+    _, blocks, to = oc.c3_tensor(side=12, lags=40, lag_scale=40)
+    assert rel(t.cpu().numpy(), to) < 1e-14
+    rep = decomp.st_hosvd(t, [24, 12, 24], shared=(1, 3))
+    core_o, fac_o = port.st_hosvd_shared13(to, 24, 12)
+    sv = np.linalg.svd(port.unfold(to, 1), compute_uv=False)
+    ang = subspace_angle(rep.factors[0].cpu().numpy(), fac_o[0])
+    assert ang < 1e-8, (ang, sv[22:26] / sv[0])
+    rep2 = decomp.hooi(t, rep, 5, shared=(1, 3))
+    core2, fac2 = port.hooi_shared13(to, fac_o[0], fac_o[1], 5)
+    recon = lambda c, f: port.mode_multiply(port.mode_multiply(port.mode_multiply(c, 1, f[0]), 2, f[1]), 3, f[2])  # noqa: E731
+    got = recon(rep2.core.cpu().numpy(), [f.cpu().numpy() for f in rep2.factors])
+    assert rel(got, recon(core2, fac2)) < 1e-10
+    # PSD-preserving reconstruction (psd.py:164-187)
+    sp = psd.spsd_compress_blocks(pat, torch.from_numpy(blocks).cuda(), 24)
+    u_o, proj_o = port.spsd_blocks(pat, blocks, 24)
+    assert subspace_angle(sp.basis.cpu().numpy(), u_o) < 1e-8
+    pr = lambda u, b: np.einsum("ia,kab,jb->kij", u, b, u)  # noqa: E731
+    assert rel(pr(sp.basis.cpu().numpy(), sp.blocks.cpu().numpy()), pr(u_o, proj_o)) < 1e-10
+
+
+def test_c4_reduced_cp_and_ml_matvec():
+    k, grid, r = 31, 16, 4
+    psf = oc.c4_psf(k)
+    x, mlp = multilevel.psf_weighted_tensor(psf, grid=grid)
+    xo = port.psf_weighted(psf, grid)
+    assert np.array_equal(x[0, :, :, :, 0], xo)
+    init = oc.normal_init((k, k, k), r, 2)
+    saved = decomp._cp_init
+    decomp._cp_init = lambda _t, _r: [f.copy() for f in init]
+    try:
+        res = bt.cp_als(np.ascontiguousarray(xo), r, 12, 0.0)
+    finally:
+        decomp._cp_init = saved
+    ref = port.cp_als(xo, r, 12, 0.0, init=lambda _t, _r: [f.copy() for f in init])
+    # north_star: relative errors (1 - fit) agree within 1e-8 absolute
+    np.testing.assert_allclose(res.fit_history, ref.fit_history, rtol=0, atol=1e-8)
+    terms = multilevel.ml_kron_sum_from_kruskal(res.rep, mlp)
+    vols = np.random.default_rng(1004).standard_normal((grid**3, 3))
+    y = multilevel.ml_matvec(terms, vols)
+    levels = [port.kernel_level_pattern(k, grid * grid, grid * grid, grid),
+              port.kernel_level_pattern(k, grid, grid, grid), port.kernel_level_pattern(k, 1, 1, grid)]
+    to = port.ml_kron_from_kruskal(levels, res.rep.x, res.rep.y, res.rep.z)  # same factors
+    yo = port.ml_matvec(to, vols.T.reshape(3, grid, grid, grid)).reshape(3, -1).T
+    assert rel(y, yo) < 1e-9
+
+
+def test_c5_like_fit_monotone_and_deterministic():
+    I, J, K, r = 256, 192, 128, 16
+    x = configs.c5_build(I, J, K, r)
+    init = oc.normal_init((I, J, K), r, 1003)
+    saved = decomp._cp_init
+    decomp._cp_init = lambda _t, _r: [torch.from_numpy(f).cuda() for f in init]
+    try:
+        r1 = bt.cp_als(x, r, 15, 0.0)
+        r2 = bt.cp_als(x, r, 15, 0.0)
+    finally:
+        decomp._cp_init = saved
+    h = np.array(r1.fit_history)
+    assert np.all(np.diff(h) >= -1e-12)                        # ALS fit never decreases
+    assert np.array_equal(h, np.array(r2.fit_history))         # bit-reproducible
+    assert torch.equal(r1.rep.x, r2.rep.x)
