@@ -248,6 +248,8 @@ int bt_maxabs_f64(const double* x, int64_t n, double* out, void* ws, int64_t ws_
  * ws: p ints.  Synchronises the stream. */
 int bt_transpose_check_f64(const double* blocks, int64_t p, int64_t n, const int64_t* partner,
                            double tol, void* ws, int64_t* bad_class, void* stream);
+/* out = 1 / sqrt(x) elementwise */
+int bt_inv_sqrt_f64(const double* x, int64_t n, double* out, void* stream);
 /* sign rule (decomp.py:176-179) on every column of a row-major matrix */
 int bt_sign_fix_f64(double* x, int64_t rows, int64_t cols, void* stream);
 /* normalise every column of a row-major (rows x cols) matrix to unit 2-norm */

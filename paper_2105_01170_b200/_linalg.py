@@ -43,7 +43,7 @@ def eigh_dev(gd, nvec: int | None = None, tau: float = -1.0):
     n = int(gd.shape[0])
     if tuple(gd.shape) != (n, n):
         raise ShapeError("eigh expects a square matrix")
-    if nvec is not None and n > SMALL_EIG and int(nvec) < n:
+    if nvec is not None and SMALL_EIG < n <= 3200 and int(nvec) < n:
         nv = max(1, int(nvec))
         w = _dev.empty((nv,))
         v = _dev.empty((n, nv))
@@ -60,7 +60,8 @@ def eigh_dev(gd, nvec: int | None = None, tau: float = -1.0):
 
 
 _DEBUG = bool(os.environ.get("BT_BASIS_DEBUG"))
-RESOLVE_TAU = 1e-3   # per pass: eigenvectors with lambda > tau * lambda_max are kept (cut accuracy ~eps/tau)
+NOISE_REL = 1e-22    # remainder eigenvalue below this * lambda_1 (sigma < 1e-11 sigma_1)
+RESOLVE_TAU = 1e-6   # per pass: eigenvectors with lambda > tau * lambda_max are kept (cut accuracy ~eps/tau)
 
 
 def _gram_modes(xd, modes):
@@ -96,17 +97,41 @@ def _orth_normalize(basis, new):
     return out
 
 
+def _orthonormalize_block(y):
+    """Symmetric (Loewdin) orthonormalisation Y (Y^T Y)^{-1/2} of a thin
+    block on device -- GEMMs plus the one-CTA eigensolver; applied twice by
+    the caller (like CholeskyQR2) for orthogonality to working precision."""
+    w, v = eigh_dev(gemm_dev(y, y, ta=True))
+    if float(_dev.to_host(w).min()) <= 0.0:
+        raise RuntimeError("orthonormalisation of a rank-deficient block")
+    s = _dev.empty(tuple(w.shape))
+    N.call("bt_inv_sqrt_f64", _dev.ptr(w), int(w.numel()), _dev.ptr(s), _dev.stream())
+    # Y V diag(lambda^-1/2): the diagonal rides on the engine's B-scale
+    k = int(v.shape[0])
+    m = int(y.shape[0])
+    out = _dev.empty((m, k))
+    d = N.GemmDesc()
+    d.M, d.N, d.Kin, d.Kout, d.batch = m, k, k, 1, 1
+    d.A, d.sAm, d.sAki = _dev.ptr(y), k, 1
+    d.B, d.sBn, d.sBki = _dev.ptr(v), 1, k
+    d.bscale, d.s_scale_ko = _dev.ptr(s), 0
+    d.C, d.sCm, d.sCn = _dev.ptr(out), k, 1
+    d.alpha, d.beta = 1.0, 0.0
+    ws = _dev.workspace(N.load().bt_gemm_f64_ws_bytes(C.byref(d)))
+    N.call("bt_gemm_f64", C.byref(d), _dev.ptr(ws), int(ws.numel()) * 8, _dev.stream())
+    return out
+
+
 def _complete(basis, g, need: int, block: int = 32):
-    """``need`` orthonormal columns orthogonal to ``basis``, drawn from the
-    range of g (deterministic sketch g @ Omega), by block classical
-    Gram-Schmidt with reorthogonalisation (two projection + Householder QR
-    passes per 32-column block), sign-normalised.  Used once the remainder
-    is at rounding level, where any orthonormal completion is as good as
-    LAPACK's."""
+    """``need`` orthonormal columns orthogonal to ``basis`` from a
+    deterministic Gaussian block, block by block: project out the accepted
+    columns, orthonormalise, twice (reorthogonalisation), sign-normalised.
+    Used once the remainder is at rounding level (or exhausted), where any
+    orthonormal completion is as good as LAPACK's."""
     t = _dev.torch()
     n = int(g.shape[0])
     rng = np.random.default_rng(12345)
-    y = gemm_dev(g, _dev.to_device(rng.standard_normal((n, need))))
+    y = _dev.to_device(rng.standard_normal((n, need)))
     cur = basis
     outs = []
     for j0 in range(0, need, block):
@@ -114,7 +139,7 @@ def _complete(basis, g, need: int, block: int = 32):
         for _ in range(2):
             if cur is not None:
                 blk = _axpby(1.0, blk, -1.0, gemm_dev(cur, gemm_dev(cur, blk, ta=True)))
-            blk, _ = qr_thin_dev(blk)
+            blk = _orthonormalize_block(blk)
         outs.append(blk)
         cur = blk if cur is None else t.cat([cur, blk], dim=1).contiguous()
     out = t.cat(outs, dim=1).contiguous()
@@ -149,8 +174,8 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
         wh = _dev.to_host(w)
         if top is None:
             top = max(float(wh[0]), 0.0)
-        if top == 0.0 or wh[0] <= 1e-28 * top:
-            break                                   # remainder is rounding noise
+        if top == 0.0 or wh[0] <= NOISE_REL * top:
+            break                                   # remainder negligible: complete
         k = int(np.sum(wh[:need] > RESOLVE_TAU * wh[0]))
         if _DEBUG:
             print(f"[mode_basis n={n} r={r}] pass: need {need} resolved {k} "

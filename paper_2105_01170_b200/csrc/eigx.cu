@@ -385,14 +385,20 @@ __global__ void prep_kernel(const double* __restrict__ d, const double* __restri
   }
 }
 
-// w[c] = (c+1)-th largest eigenvalue, c < nvec: multisection, one warp per
-// eigenvalue, 32 Sturm counts per round (the interval shrinks 33x a round)
+// w[c] = (c+1)-th largest eigenvalue, c in [c_begin, nvec): multisection,
+// one warp per eigenvalue, 32 Sturm counts per round (interval shrinks 33x a
+// round).  With limit != null only c <= *limit are computed (the rest = 0).
 __global__ void __launch_bounds__(256)
     bisect_kernel(const double* __restrict__ d, const double* __restrict__ e2, int64_t n,
-                  int64_t nvec, const double* __restrict__ bounds, double* __restrict__ w) {
+                  int64_t c_begin, int64_t nvec, const double* __restrict__ bounds,
+                  const int64_t* __restrict__ limit, double* __restrict__ w) {
   const int lane = threadIdx.x & 31;
-  const int64_t c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t c = c_begin + blockIdx.x * 8 + (threadIdx.x >> 5);
   if (c >= nvec) return;
+  if (limit != nullptr && c > *limit) {
+    if (lane == 0) w[c] = 0.0;
+    return;
+  }
   const int target = static_cast<int>(n - 1 - c);  // eigenvalue index in ascending order
   double lo = bounds[0], hi = bounds[1];
   const double pivmin = bounds[2];
@@ -410,6 +416,21 @@ __global__ void __launch_bounds__(256)
     hi = nhi;
   }
   if (lane == 0) w[c] = 0.5 * (lo + hi);
+}
+
+// number of eigenvalues strictly above tau * |w0| (Sturm count), into *count
+__global__ void count_above_kernel(const double* __restrict__ d, const double* __restrict__ e2,
+                                   int64_t n, const double* __restrict__ bounds,
+                                   const double* __restrict__ w, double tau,
+                                   int64_t* __restrict__ count) {
+  if (threadIdx.x != 0) return;
+  if (tau < 0.0) {
+    *count = n;
+    return;
+  }
+  const double x = tau * fabs(w[0]);
+  // eigenvalues > x  ==  n - #(<= x) ; use #(< x) as a slight over-count (safe)
+  *count = n - sturm_less(d, e2, n, x, bounds[2]);
 }
 
 // cluster starts: start[c] = 1 if c == 0 or w[c-1] - w[c] > 1e-3 ||T||;
@@ -536,23 +557,33 @@ __global__ void __launch_bounds__(32)
   }
 }
 
-// V = Q Y: apply reflectors k = n-3 .. 0 to each vector (warp per vector)
+// V = Q Y: apply reflectors k = n-3 .. 0; a CTA stages 8 vectors in shared
+// memory (one warp each) so the reflector sweep runs out of smem, the
+// reflector rows (shared by the 8 warps) come through L1.
 __global__ void __launch_bounds__(256)
     backtransform_kernel(const double* __restrict__ vref, const double* __restrict__ tau,
-                         int64_t n, int64_t nvec, double* __restrict__ y) {
-  const int lane = threadIdx.x & 31;
-  const int64_t c = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (c >= nvec) return;
-  double* yc = y + c * n;
-  for (int64_t k = n - 3; k >= 0; --k) {
-    const double t = tau[k];
-    if (t == 0.0) continue;
-    const double* v = vref + k * n;
-    double s = 0.0;
-    for (int64_t i = k + 1 + lane; i < n; i += 32) s = fma(v[i], yc[i], s);
-    s = warp_sum(s) * t;
-    for (int64_t i = k + 1 + lane; i < n; i += 32) yc[i] -= s * v[i];
-    __syncwarp();
+                         int64_t n, int64_t nvec, const int* __restrict__ start,
+                         double* __restrict__ y) {
+  extern __shared__ __align__(16) double ysm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c = blockIdx.x * 8 + warp;
+  const bool live = c < nvec && start[c] != -1;
+  double* yc = ysm + warp * n;
+  if (live)
+    for (int64_t i = lane; i < n; i += 32) yc[i] = y[c * n + i];
+  __syncwarp();
+  if (live) {
+    for (int64_t k = n - 3; k >= 0; --k) {
+      const double t = tau[k];
+      if (t == 0.0) continue;
+      const double* v = vref + k * n;
+      double s = 0.0;
+      for (int64_t i = k + 1 + lane; i < n; i += 32) s = fma(__ldg(v + i), yc[i], s);
+      s = warp_sum(s) * t;
+      for (int64_t i = k + 1 + lane; i < n; i += 32) yc[i] -= s * __ldg(v + i);
+      __syncwarp();
+    }
+    for (int64_t i = lane; i < n; i += 32) y[c * n + i] = yc[i];
   }
 }
 
@@ -595,7 +626,7 @@ __global__ void __launch_bounds__(256)
 
 struct XPlan {
   int64_t off_a, off_v, off_d, off_e, off_e2, off_tau, off_p, off_part, off_bounds, off_start,
-      off_y, off_scr, off_ppart, total;
+      off_y, off_scr, off_ppart, off_cnt, total;
   int parts;
 };
 
@@ -621,6 +652,7 @@ XPlan xplan(int64_t n, int64_t nvec) {
   p.off_y = take(nvec * n);
   p.off_scr = take(nvec * 5 * n);
   p.off_ppart = take(n * ((n + 255) / 256));
+  p.off_cnt = take(2);
   p.total = o;
   return p;
 }
@@ -632,6 +664,8 @@ extern "C" int64_t bt_syevx_ws_bytes(int64_t n, int64_t nvec) { return xplan(n, 
 extern "C" int bt_syevx_f64(const double* a, int64_t n, int64_t nvec, double vec_tau, double* w,
                             double* v, void* wsv, int64_t ws_bytes, void* stream) {
   BT_REQUIRE(n >= 3 && nvec >= 1 && nvec <= n, BT_E_SHAPE, "syevx: need n >= 3, 1 <= nvec <= n");
+  BT_REQUIRE(n <= 3200, BT_E_SHAPE, "syevx: n = %lld above the shared-memory limit 3200",
+             (long long)n);
   XPlan p = xplan(n, nvec);
   BT_REQUIRE(ws_bytes >= p.total * 8, BT_E_VALUE, "syevx: workspace too small");
   cudaStream_t st = bt_stream(stream);
@@ -687,8 +721,17 @@ extern "C" int bt_syevx_f64(const double* a, int64_t n, int64_t nvec, double vec
   BT_LAUNCH_CHECK();
   prep_kernel<<<1, 256, 0, st>>>(d, e, n, e2, bounds);
   BT_LAUNCH_CHECK();
-  bisect_kernel<<<static_cast<unsigned>(bt_cdiv(nvec, 8)), 256, 0, st>>>(d, e2, n, nvec, bounds, w);
+  // largest eigenvalue first, then only those above vec_tau * w0 (+1 for the count)
+  int64_t* cnt = reinterpret_cast<int64_t*>(ws + p.off_cnt);
+  bisect_kernel<<<1, 32, 0, st>>>(d, e2, n, 0, 1, bounds, nullptr, w);
   BT_LAUNCH_CHECK();
+  count_above_kernel<<<1, 32, 0, st>>>(d, e2, n, bounds, w, vec_tau, cnt);
+  BT_LAUNCH_CHECK();
+  if (nvec > 1) {
+    bisect_kernel<<<static_cast<unsigned>(bt_cdiv(nvec - 1, 8)), 256, 0, st>>>(d, e2, n, 1, nvec,
+                                                                                bounds, cnt, w);
+    BT_LAUNCH_CHECK();
+  }
   if (dbg) cudaEventRecord(ev[2], st);
   cluster_kernel<<<static_cast<unsigned>(bt_cdiv(nvec, 256)), 256, 0, st>>>(w, nvec, bounds, vec_tau,
                                                                           start);
@@ -696,7 +739,14 @@ extern "C" int bt_syevx_f64(const double* a, int64_t n, int64_t nvec, double vec
   invit_kernel<<<static_cast<unsigned>(nvec), 32, 0, st>>>(d, e, n, nvec, w, start, bounds, y, scr);
   BT_LAUNCH_CHECK();
   if (dbg) cudaEventRecord(ev[3], st);
-  backtransform_kernel<<<static_cast<unsigned>(bt_cdiv(nvec, 8)), 256, 0, st>>>(V, tau, n, nvec, y);
+  {
+    const size_t sm = sizeof(double) * 8 * n;
+    BT_CUDA_CHECK(cudaFuncSetAttribute(backtransform_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sm)));
+    backtransform_kernel<<<static_cast<unsigned>(bt_cdiv(nvec, 8)), 256, sm, st>>>(V, tau, n, nvec,
+                                                                                 start, y);
+  }
   BT_LAUNCH_CHECK();
   if (dbg) cudaEventRecord(ev[4], st);
   sign_out_kernel<<<static_cast<unsigned>(std::min<int64_t>(nvec, 4096)), 256, 0, st>>>(y, n, nvec, v);

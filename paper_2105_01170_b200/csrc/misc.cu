@@ -341,3 +341,18 @@ extern "C" int bt_sign_fix_f64(double* x, int64_t rows, int64_t cols, void* stre
   BT_LAUNCH_CHECK();
   return BT_OK;
 }
+
+// out[i] = 1 / sqrt(x[i])   (x > 0)
+__global__ void bt_inv_sqrt_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = 1.0 / sqrt(x[i]);
+}
+
+extern "C" int bt_inv_sqrt_f64(const double* x, int64_t n, double* out, void* stream) {
+  if (n <= 0) return BT_OK;
+  bt_inv_sqrt_kernel<<<static_cast<int>((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024), 256, 0,
+                       bt_stream(stream)>>>(x, n, out);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
