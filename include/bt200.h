@@ -205,6 +205,16 @@ int bt_syevx_f64(const double* a, int64_t n, int64_t nvec, double tau, double* w
 int64_t bt_qr_thin_ws_bytes(int64_t m, int64_t n);
 int bt_qr_thin_f64(const double* a, int64_t m, int64_t n, double* q, double* r, void* ws,
                    int64_t ws_bytes, void* stream);
+/* Lower Cholesky factor (decomp.py:196-212 / numpy potrf; lower triangle of
+ * a read, a == l allowed): blocked, 64-wide panels, DMMA trailing updates.
+ * BT_E_NOT_PD with *bad_pivot = 1-based failing pivot.  Synchronises the
+ * stream.  bt_tri_inv_lower_f64: linv = L^-1 (blocked forward substitution;
+ * replaces the two solve_triangular calls per block of psd.py:248-257). */
+int64_t bt_cholesky_ws_bytes(int64_t n);
+int bt_cholesky_f64(const double* a, int64_t n, double* l, void* ws, int64_t* bad_pivot,
+                    void* stream);
+int64_t bt_tri_inv_lower_ws_bytes(int64_t n);
+int bt_tri_inv_lower_f64(const double* l, int64_t n, double* linv, void* ws, void* stream);
 /* Mode product y = x x_mode u (tensor.py:75-90): u is (rows, dims[mode-1])
  * row-major (transpose=0) or u^T is given as (dims[mode-1], rows) (transpose=1). */
 int64_t bt_ttm_ws_bytes(const int64_t* dims, int order, int mode, int64_t rows);

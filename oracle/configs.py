@@ -188,6 +188,26 @@ def c5_tensor(i, j, k, r, noise=1e-4, seed=3, k_slab=None):
 # ---------------------------------------------------------------------------
 
 
+def spd_toeplitz(seed, ell=4, nb=5, decay=0.3):
+    """Seeded SPD block-Toeplitz input for spd_compress (psd.py:205): an SPD
+    anchor on the diagonal, random off-diagonal classes (A_-d = A_d^T), the
+    anchor shifted until the assembled matrix has lambda_min >= 1."""
+    rng = np.random.default_rng(seed)
+    from .port import assemble, make_pattern
+
+    pat = make_pattern("toeplitz", ell, ell, nb, nb)
+    g = rng.standard_normal((nb, nb))
+    anchor = g @ g.T + nb * np.eye(nb)
+    up = [decay * rng.standard_normal((nb, nb)) for _ in range(ell - 1)]
+    blocks = [anchor] + up + [u.T for u in up]
+    a = assemble(pat, blocks)
+    lo = np.linalg.eigvalsh(a).min()
+    if lo < 1.0:
+        blocks[0] = blocks[0] + (1.0 - lo) * np.eye(nb)
+        a = assemble(pat, blocks)
+    return pat, a
+
+
 def gather_standin(nb=256, ell=128):
     x = np.linspace(0.0, 1.0, nb)
     base = np.exp(-((x[:, None] - x[None, :]) ** 2) / (2 * 0.1**2))

@@ -504,6 +504,96 @@ def spsd_blocks(pat, blocks, r):
     return u, proj
 
 
+def classify_placements(placements, ell, q):
+    """blocks.py:228-263 (descriptive tag, no arithmetic)."""
+    allc = np.vstack(placements) if placements else np.zeros((0, 2), dtype=np.int64)
+    if len(allc) and np.all(allc[:, 0] == allc[:, 1]):
+        return "diagonal"
+
+    def full_diag(cells):
+        offs = {int(j - i) for i, j in cells}
+        if ell != q:
+            return None
+        if len(offs) == 1:
+            (d,) = offs
+            return d if len(cells) == ell - abs(d) else None
+        if len(offs) == 2:
+            lo, hi = sorted(offs)
+            if lo == -hi and hi > 0 and len(cells) == 2 * (ell - hi):
+                return hi
+        return None
+
+    def full_anti(cells):
+        sums = {int(i + j) for i, j in cells}
+        if ell != q or len(sums) != 1:
+            return None
+        (s,) = sums
+        return s if len(cells) == min(s + 1, ell, 2 * ell - 1 - s) else None
+
+    if placements and all(full_diag(c) is not None for c in placements):
+        return "toeplitz"
+    if placements and all(full_anti(c) is not None for c in placements):
+        return "hankel"
+    if len(allc):
+        b = int(np.max(np.abs(allc[:, 0] - allc[:, 1])))
+        if b < max(ell, q) - 1:
+            return f"banded:{b}"
+    return "general"
+
+
+def cholesky(a):
+    """decomp.py:196-212 (numpy's LAPACK potrf; asymmetry > 1e-12 max|a|
+    is a ShapeError, a failed pivot a ValueError here)."""
+    scale = np.max(np.abs(a)) or 1.0
+    if np.max(np.abs(a - a.T)) > 1e-12 * scale:
+        raise ShapeError("cholesky expects a symmetric matrix")
+    return np.linalg.cholesky(a)
+
+
+def spd_compress(a, pat, r):
+    """psd.py:205-271 -> (chol, remainder placements, remainder basis,
+    remainder projected blocks)."""
+    from scipy.linalg import solve_triangular
+
+    blocks = [a[c[0, 0] * pat.m:(c[0, 0] + 1) * pat.m, c[0, 1] * pat.n:(c[0, 1] + 1) * pat.n]
+              for c in pat.placements]
+    k0 = next(k for k, c in enumerate(pat.placements)
+              if np.any((c[:, 0] == 0) & (c[:, 1] == 0)))
+    anchor = blocks[k0]
+    low = cholesky(anchor)
+    cells_out, rem = [], []
+    for k, cells in enumerate(pat.placements):
+        on = cells[:, 0] == cells[:, 1]
+        for mask, shift in ((on, anchor), (~on, None)):
+            if not mask.any():
+                continue
+            blk = blocks[k] - shift if shift is not None else blocks[k]
+            if not blk.any():
+                continue
+            cells_out.append(cells[mask])
+            rem.append(blk)
+    scaled = []
+    for blk in rem:
+        half = solve_triangular(low, blk, lower=True)
+        scaled.append(solve_triangular(low, half.T, lower=True).T)
+    if not cells_out:
+        return low, [], np.eye(pat.m)[:, :r], np.zeros((0, r, r))
+    rp = Pattern(pat.ell, pat.q, pat.m, pat.n, tuple(cells_out))
+    u, proj = spsd_blocks(rp, scaled, r)
+    return low, cells_out, u, proj
+
+
+def densify_spd(pat, low, cells, u, proj):
+    """psd.py:129-138: (I (x) L)(I + M)(I (x) L^T)."""
+    n = low.shape[0]
+    inner = np.eye(pat.ell * n)
+    if cells:
+        rp = Pattern(pat.ell, pat.q, n, n, tuple(cells))
+        inner = inner + assemble(rp, np.stack([u @ b @ u.T for b in proj]))
+    lf = np.kron(np.eye(pat.ell), low)
+    return lf @ inner @ lf.T
+
+
 # ---------------------------------------------------------------------------
 # multilevel (multilevel.py:197-298) + restated CP route / matvec
 # ---------------------------------------------------------------------------

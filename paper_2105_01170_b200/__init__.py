@@ -8,16 +8,17 @@ provides device memory and streams.
 
 from __future__ import annotations
 
-from .blocks import (BlockPattern, build_pattern, extract_blocks, kernel_level_pattern,
-                     mat_to_tensor, struct_assemble, struct_expand, struct_scalars,
-                     tensor_to_mat)
-from .decomp import (CpResult, KruskalRep, SketchConfig, TuckerRep, cp_als, hooi, hosvd,
-                     qr_thin, st_hosvd, svd_truncated, tucker_partial)
+from .blocks import (BlockPattern, build_pattern, classify_placements, extract_blocks,
+                     kernel_level_pattern, mat_to_tensor, struct_assemble, struct_expand,
+                     struct_scalars, tensor_to_mat)
+from .decomp import (CpResult, KruskalRep, SketchConfig, TuckerRep, cholesky, cp_als, hooi,
+                     hosvd, qr_thin, st_hosvd, svd_truncated, tucker_partial)
 from .errors import (ContainerExtentError, ContainerFormatError, ConvergenceError,
                      NotPositiveDefiniteError, PatternMismatchError, ShapeError)
 from .multilevel import (MlKronTerm, MultilevelPattern, ml_kron_sum_from_kruskal,
                          ml_kron_sum_from_tucker, ml_matvec, psf_weighted_tensor)
-from .psd import SpsdRep, check_transpose_closed, spsd_compress, spsd_compress_blocks
+from .psd import (SpdRep, SpsdRep, check_transpose_closed, spd_compress, spsd_compress,
+                  spsd_compress_blocks)
 from .reconstruct import (BlockLowRankRep, FlopCounter, KronSumRep, TuckerBlockRep,
                           blr_from_kruskal, blr_from_tucker, densify, error_fro,
                           kron_sum_from_kruskal, kron_sum_from_tucker, matvec)

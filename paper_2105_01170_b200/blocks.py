@@ -25,6 +25,7 @@ from .errors import PatternMismatchError, ShapeError
 
 __all__ = [
     "BlockPattern",
+    "classify_placements",
     "build_pattern",
     "struct_assemble",
     "struct_expand",
@@ -251,6 +252,43 @@ def kernel_level_pattern(k: int, bm: int, bn: int, grid: int | None = None) -> B
     if grid < h + 1:
         raise ShapeError("image grid smaller than the kernel radius")
     return _make(grid, grid, bm, bn, [_diag(grid, h - i) for i in range(k)], f"toeplitz:{h}")
+
+
+def classify_placements(placements, ell: int, q: int) -> str:
+    """blocks.py:228-263: descriptive structure tag of a placement family."""
+    allc = np.vstack(placements) if placements else np.zeros((0, 2), dtype=np.int64)
+    if len(allc) and np.all(allc[:, 0] == allc[:, 1]):
+        return "diagonal"
+
+    def full_diag(cells):
+        offs = set(int(j - i) for i, j in cells)
+        if ell != q:
+            return None
+        if len(offs) == 1:
+            (d,) = offs
+            return d if len(cells) == ell - abs(d) else None
+        if len(offs) == 2:
+            d1, d2 = sorted(offs)
+            if d1 == -d2 and d2 > 0 and len(cells) == 2 * (ell - d2):
+                return d2
+        return None
+
+    def full_anti(cells):
+        sums = set(int(i + j) for i, j in cells)
+        if ell != q or len(sums) != 1:
+            return None
+        (s,) = sums
+        return s if len(cells) == min(s + 1, ell, 2 * ell - 1 - s) else None
+
+    if placements and all(full_diag(c) is not None for c in placements):
+        return "toeplitz"
+    if placements and all(full_anti(c) is not None for c in placements):
+        return "hankel"
+    if len(allc):
+        b = int(np.max(np.abs(allc[:, 0] - allc[:, 1])))
+        if b < max(ell, q) - 1:
+            return f"banded:{b}"
+    return "general"
 
 
 # ---------------------------------------------------------------------------

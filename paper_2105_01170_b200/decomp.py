@@ -28,11 +28,11 @@ import numpy as np
 from . import _dev
 from . import _linalg as L
 from . import _native as N
-from .errors import ShapeError
+from .errors import NotPositiveDefiniteError, ShapeError
 from .tensor import fro_norm_dev, ttm_dev
 
 __all__ = [
-    "TuckerRep", "KruskalRep", "CpResult", "SketchConfig", "svd_truncated", "qr_thin",
+    "TuckerRep", "KruskalRep", "CpResult", "SketchConfig", "svd_truncated", "qr_thin", "cholesky",
     "hosvd", "tucker_partial", "cp_als", "st_hosvd", "hooi",
 ]
 
@@ -153,6 +153,37 @@ def qr_thin(a):
         raise ShapeError(f"qr_thin expects a tall or square matrix, got {tuple(a.shape)}")
     q, rr = L.qr_thin_dev(_dev.to_device(a))
     return _dev.like_input(a, q), _dev.like_input(a, rr)
+
+
+def cholesky(a):
+    """decomp.py:196-212: lower Cholesky factor on the GPU.  ShapeError for a
+    non-square or asymmetric (> 1e-12 * max|a|) matrix, NotPositiveDefiniteError
+    for a non-positive pivot (the package's SPD test)."""
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ShapeError("cholesky expects a square matrix")
+    ad = _dev.to_device(a)
+    n = int(ad.shape[0])
+    from .psd import _max_abs
+
+    scale = _max_abs(ad) or 1.0
+    ws = _dev.workspace(n * 8 + 16)
+    one = _dev.to_device(np.zeros(1, dtype=np.int64), dtype=_dev.torch().int64)
+    bad = C.c_int64(-1)
+    st = N.load().bt_transpose_check_f64(_dev.ptr(ad), 1, n, _dev.ptr(one), 1e-12 * scale,
+                                         _dev.ptr(ws), C.byref(bad), _dev.stream())
+    if st == N.BT_E_PATTERN:
+        raise ShapeError("cholesky expects a symmetric matrix")
+    N.check(st, "symmetry check")
+    low = _dev.empty((n, n))
+    ws = _dev.workspace(N.load().bt_cholesky_ws_bytes(n))
+    piv = C.c_int64(0)
+    st = N.load().bt_cholesky_f64(_dev.ptr(ad), n, _dev.ptr(low), _dev.ptr(ws), C.byref(piv),
+                                  _dev.stream())
+    if st == N.BT_E_NOT_PD:
+        # numpy's LinAlgError text, re-raised as in the reference
+        raise NotPositiveDefiniteError("Matrix is not positive definite")
+    N.check(st, "bt_cholesky_f64")
+    return _dev.like_input(a, low)
 
 
 def _mode_basis(mat, r: int):

@@ -320,6 +320,39 @@ def psf_cases():
     np.savez_compressed(os.path.join(OUT, "psf.npz"), **out)
 
 
+def spd_cases():
+    """psd.py:205-271 spd_compress and decomp.py:196 cholesky on seeded SPD
+    block-Toeplitz inputs (oracle/configs.spd_toeplitz) at every rank."""
+    out = {}
+    for case, (seed, ell, nb) in enumerate(((21, 4, 5), (22, 3, 8), (23, 6, 3))):
+        pat_o, a = oc.spd_toeplitz(seed, ell, nb)
+        pat = bt.build_pattern("toeplitz", ell, ell, nb, nb)
+        out[f"s{case}_a"] = a
+        for r in range(1, nb + 1):
+            rep = bt.spd_compress(a, pat, r)
+            key = f"s{case}_r{r}"
+            out[key + "_dense"] = rep.densify()
+            out[key + "_basis"] = rep.remainder.basis
+            out[key + "_blocks"] = rep.remainder.blocks
+            if r == 1:
+                out[f"s{case}_chol"] = rep.chol
+                out[f"s{case}_rem_cells"] = np.concatenate(rep.remainder.pattern.placements)
+                out[f"s{case}_rem_counts"] = np.array(rep.remainder.pattern.counts)
+                out[f"s{case}_rem_class"] = np.array(rep.remainder.pattern.structure_class)
+    # block diagonal input: empty remainder
+    g = np.random.default_rng(24).standard_normal((4, 4))
+    t0 = g @ g.T + 4 * np.eye(4)
+    cells = np.column_stack([np.arange(3), np.arange(3)])
+    pat = bt.BlockPattern(ell=3, q=3, m=4, n=4, placements=(cells,), structure_class="diagonal")
+    a = bt.struct_assemble(pat, np.stack([t0]))
+    rep = bt.spd_compress(a, pat, 2)
+    out.update(bd_a=a, bd_dense=rep.densify(), bd_chol=rep.chol)
+    g = np.random.default_rng(25).standard_normal((7, 7))
+    out["chol_in"] = g @ g.T + 7 * np.eye(7)
+    out["chol_out"] = bt.cholesky(out["chol_in"])
+    np.savez_compressed(os.path.join(OUT, "spd.npz"), **out)
+
+
 if __name__ == "__main__":
     np.seterr(all="ignore")
     patterns()
@@ -328,5 +361,6 @@ if __name__ == "__main__":
     tucker_cases()
     rep_cases()
     psf_cases()
+    spd_cases()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -116,3 +116,28 @@ def test_library_exports_every_header_symbol():
     assert names <= set(_native.exported_symbols())
     _native.load()
     assert _native.load().bt_version() == 1
+
+
+def test_classify_placements_matches_oracle():
+    """blocks.py:228-263 host tag on every builder kind and on random splits."""
+    from oracle import port as _port
+    from paper_2105_01170_b200.blocks import build_pattern, classify_placements
+
+    rng = np.random.default_rng(5)
+    for kind in ("toeplitz", "hankel", "diagonal", "banded", "circulant", "general"):
+        for ell in (1, 2, 4, 7):
+            try:
+                pat = build_pattern(kind, ell, ell, 2, 2, **({"band": 1} if kind == "banded" else {}))
+            except Exception:
+                continue
+            pl = pat.placements
+            assert classify_placements(pl, ell, ell) == _port.classify_placements(pl, ell, ell)
+            # split every class by the diagonal as spd_compress does
+            split = []
+            for c in pl:
+                on = c[:, 0] == c[:, 1]
+                split += [x for x in (c[on], c[~on]) if len(x)]
+            split = [split[i] for i in rng.permutation(len(split))]
+            assert (classify_placements(tuple(split), ell, ell)
+                    == _port.classify_placements(tuple(split), ell, ell))
+    assert classify_placements((), 3, 3) == "general"

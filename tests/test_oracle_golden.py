@@ -189,3 +189,27 @@ def test_psf_and_multilevel_golden(golden):
     np.testing.assert_allclose(y, z["c4s_mv"], rtol=0, atol=1e-13 * np.abs(z["c4s_mv"]).max())
     # generalised grid == K reduces to the reference weighting
     np.testing.assert_array_equal(port.psf_weighted(z["psf5"], 5), z["x5"][0, :, :, :, 0])
+
+
+def test_spd_compress_golden(golden):
+    """oracle spd_compress / cholesky vs the reference (psd.py:205-271)."""
+    z = golden("spd")
+    for case, (seed, ell, nb) in enumerate(((21, 4, 5), (22, 3, 8), (23, 6, 3))):
+        pat, a = oc.spd_toeplitz(seed, ell, nb)
+        assert np.array_equal(a, z[f"s{case}_a"])
+        for r in range(1, nb + 1):
+            low, cells, u, proj = port.spd_compress(a, pat, r)
+            dense = port.densify_spd(pat, low, cells, u, proj)
+            ref = z[f"s{case}_r{r}_dense"]
+            assert np.linalg.norm(dense - ref) <= 1e-12 * np.linalg.norm(ref)
+            if r == 1:
+                assert np.array_equal(low, z[f"s{case}_chol"])
+                assert np.array_equal(np.concatenate(cells), z[f"s{case}_rem_cells"])
+                assert [len(c) for c in cells] == list(z[f"s{case}_rem_counts"])
+                assert port.classify_placements(tuple(cells), ell, ell) == str(
+                    z[f"s{case}_rem_class"])
+    assert np.array_equal(port.cholesky(z["chol_in"]), z["chol_out"])
+    pat = port.Pattern(3, 3, 4, 4, (np.column_stack([np.arange(3)] * 2),))
+    low, cells, u, proj = port.spd_compress(z["bd_a"], pat, 2)
+    assert cells == []
+    assert np.abs(port.densify_spd(pat, low, cells, u, proj) - z["bd_dense"]).max() < 1e-12
