@@ -64,11 +64,13 @@ NOISE_REL = 1e-22    # remainder eigenvalue below this * lambda_1 (sigma < 1e-11
 RESOLVE_TAU = 1e-6   # per pass: eigenvectors with lambda > tau * lambda_max are kept (cut accuracy ~eps/tau)
 
 
-def _gram_modes(xd, modes):
+def _gram_modes(xd, modes, reduce=None):
     g = None
     for m in modes:
         gm = unfold_gram_dev(xd, m)
         g = gm if g is None else _axpby(1.0, g, 1.0, gm)
+    if reduce is not None:
+        reduce(g)
     return g
 
 
@@ -147,7 +149,8 @@ def _complete(basis, g, need: int, block: int = 32):
     return out
 
 
-def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_passes: int = 16):
+def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_passes: int = 16,
+                   reduce=None):
     """Leading r left singular vectors of unfold(x, mode) (decomp.py:220-234),
     sign rule included.  extra_mode: basis of the column concatenation
     [unfold(x, mode), unfold(x, extra_mode)] (tucker_partial
@@ -158,11 +161,16 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
     lambda_max of the current Gram, deflates them out of the tensor and
     re-Grams the remainder (SVD-grade accuracy for the fast-decaying spectra
     of C2/C3).  Once the remainder is at rounding level the
-    basis is completed orthonormally (full_matrices completion, too)."""
+    basis is completed orthonormally (full_matrices completion, too).
+
+    reduce: in-place cross-rank sum applied to every Gram, for a tensor
+    sharded along a mode other than ``mode`` (each rank's Gram is then a
+    partial sum; the deflation residual is slab-local).  The eigensolves are
+    replicated and deterministic, so every rank takes the same branches."""
     modes = [mode] if extra_mode is None else [mode, extra_mode]
     t = _dev.torch()
     n = int(xd.shape[mode - 1])
-    g = _gram_modes(xd, modes)
+    g = _gram_modes(xd, modes, reduce)
     basis = None
     top = None
     for _ in range(max_passes):
@@ -195,6 +203,8 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
             gm = unfold_gram_dev(xr, m)
             g = gm if g is None else _axpby(1.0, g, 1.0, gm)
         del res
+        if reduce is not None:
+            reduce(g)
     have = 0 if basis is None else int(basis.shape[1])
     if have < r:
         extra = _complete(basis, g, r - have)

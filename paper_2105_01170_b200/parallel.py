@@ -175,3 +175,119 @@ def cp_als_distributed(x_local, r: int, max_iters: int = 500, tol: float = 1e-10
     rep = KruskalRep(x=_dev.like_input(x_local, f[0]), y=_dev.like_input(x_local, f[1]),
                      z=_dev.like_input(x_local, f[2]))
     return CpResult(rep=rep, fit=hist[-1], fit_history=tuple(hist), n_iters=n_it, converged=conv)
+
+
+# ---------------------------------------------------------------------------
+# ST-HOSVD / HOOI sharded along the time (class) mode -- C3, SURVEY.md 8e
+# ---------------------------------------------------------------------------
+
+
+class NativeTuckerOps:
+    """Device kernels behind the sharded Tucker driver: mode bases (DMMA
+    Gram + eigensolver, optional cross-rank Gram sum) and mode products."""
+
+    def mode_basis(self, x, mode, r, reduce=None):
+        from . import _linalg as L
+
+        return L.mode_basis_dev(x, mode, int(r), reduce=reduce)
+
+    def ttm_t(self, x, mode, u):
+        """x x_mode u^T (u: extent x r)."""
+        from .tensor import ttm_dev
+
+        return ttm_dev(x, mode, u, int(u.shape[1]), transpose=True)
+
+    def rows(self, u, r0, r1):
+        return u[r0:r1].contiguous()
+
+
+def torch_allgather_mode2(group=None):
+    """Gather an order-3 tensor sharded along mode 2 (uneven slabs allowed)
+    into the full tensor on every rank: slabs are exchanged as contiguous
+    (P_local, a, b) blocks (padded to the largest slab) and re-interleaved."""
+    import torch.distributed as dist
+
+    t = _dev.torch()
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return lambda y: y
+
+    def gather(y):
+        world = dist.get_world_size(group)
+        a, pl, b = (int(s) for s in y.shape)
+        sizes = t.tensor([pl], dtype=t.int64, device=y.device)
+        all_sizes = [t.zeros_like(sizes) for _ in range(world)]
+        dist.all_gather(all_sizes, sizes, group=group)
+        counts = [int(s.item()) for s in all_sizes]
+        pmax = max(counts)
+        blk = t.zeros((pmax, a, b), dtype=y.dtype, device=y.device)
+        blk[:pl] = y.permute(1, 0, 2)
+        outs = [t.empty_like(blk) for _ in range(world)]
+        dist.all_gather(outs, blk, group=group)
+        full = t.cat([o[:c] for o, c in zip(outs, counts)], dim=0)
+        return full.permute(1, 0, 2).contiguous()
+
+    return gather
+
+
+def st_hosvd_sharded(ops, x_local, r13: int, r2: int, allreduce, allgather):
+    """ST-HOSVD of an (I, P, J) tensor with modes 1 and 3 sharing one basis
+    (the C3 recipe; decomp.st_hosvd with shared=(1, 3)), the tensor sharded
+    along mode 2.  Exchanges: the I x I mode-1 Gram (sum, once per deflation
+    pass) and the projected (r13, P, r13) tensor (all-gather).  Returns
+    (U, V, core), replicated on every rank."""
+    u = ops.mode_basis(x_local, 1, r13, reduce=allreduce)
+    y = allgather(ops.ttm_t(ops.ttm_t(x_local, 1, u), 3, u))
+    v = ops.mode_basis(y, 2, r2)
+    return u, v, ops.ttm_t(y, 2, v)
+
+
+def hooi_sharded(ops, x_local, u, v, sweeps: int, p0: int, p1: int, allreduce, allgather):
+    """HOOI sweeps (decomp.hooi, shared=(1, 3)) on the mode-2-sharded tensor.
+    U-step: the local partial of x x2 V^T x3 U^T over this rank's rows
+    [p0, p1) of V is summed across ranks (I x r2 x r13); V-step: the projected
+    (r13, P_local, r13) slabs are all-gathered.  Returns (U, V, core)."""
+    y = None
+    for _ in range(int(sweeps)):
+        z = ops.ttm_t(ops.ttm_t(x_local, 2, ops.rows(v, p0, p1)), 3, u)
+        allreduce(z)
+        u = ops.mode_basis(z, 1, int(u.shape[1]))
+        y = allgather(ops.ttm_t(ops.ttm_t(x_local, 1, u), 3, u))
+        v = ops.mode_basis(y, 2, int(v.shape[1]))
+    if y is None:
+        y = allgather(ops.ttm_t(ops.ttm_t(x_local, 1, u), 3, u))
+    return u, v, ops.ttm_t(y, 2, v)
+
+
+def tucker_c3_distributed(x_local, r13: int, r2: int, hooi_sweeps: int = 0, p_offset: int = 0,
+                          group=None):
+    """Public multi-GPU ST-HOSVD (+ HOOI) for the C3 shape: ``x_local`` is
+    this rank's (I, P_local, J) slab of the weighted tensor (rows
+    [p_offset, p_offset + P_local) of mode 2).  Returns a TuckerRep with
+    factors (U, V, U) and the core, replicated, as numpy for host input."""
+    from .decomp import TuckerRep
+
+    xd = _dev.to_device(x_local)
+    ops = NativeTuckerOps()
+    red = torch_allreduce(group)
+    gat = torch_allgather_mode2(group)
+    u, v, core = st_hosvd_sharded(ops, xd, r13, r2, red, gat)
+    if hooi_sweeps:
+        pl = int(xd.shape[1])
+        u, v, core = hooi_sharded(ops, xd, u, v, hooi_sweeps, p_offset, p_offset + pl, red, gat)
+    fu = _dev.like_input(x_local, u)
+    return TuckerRep(core=_dev.like_input(x_local, core),
+                     factors=(fu, _dev.like_input(x_local, v), fu))
+
+
+# ---------------------------------------------------------------------------
+# RHS-sharded matvec (independent units, no data-path collective)
+# ---------------------------------------------------------------------------
+
+
+def matvec_sharded(rep, x, world: int, rank: int):
+    """Columns [c0, c1) of rep @ x for this rank (reconstruct.matvec on a
+    shard of the right-hand sides; SURVEY.md 8e "shard RHS columns")."""
+    from .reconstruct import matvec
+
+    c0, c1 = shard_bounds(int(x.shape[1]), world, rank)
+    return matvec(rep, x[:, c0:c1])

@@ -81,3 +81,62 @@ def test_cp_als_sharded_single_rank_matches_driver():
     ref = port.cp_als(x.cpu().numpy(), r, iters, 0.0, init=port.cp_init_normal(1003))
     np.testing.assert_allclose(hist, ref.fit_history, rtol=0, atol=1e-11)
     ops.close()
+
+
+def test_tucker_sharded_native_single_rank_matches_decomp():
+    """parallel.st_hosvd_sharded / hooi_sharded on the native ops with
+    identity collectives == decomp.st_hosvd / hooi (shared=(1, 3))."""
+    import paper_2105_01170_b200 as bt
+    from paper_2105_01170_b200.parallel import NativeTuckerOps, hooi_sharded, st_hosvd_sharded
+
+    pat, t = configs.c3_build(side=6, lags=10)
+    ops = NativeTuckerOps()
+    ident = lambda b: None  # noqa: E731
+    same = lambda y: y      # noqa: E731
+    u, v, core = st_hosvd_sharded(ops, t, 8, 4, ident, same)
+    rep = bt.st_hosvd(t, [8, 4, 8], shared=(1, 3))
+    assert torch.equal(u, rep.factors[0]) and torch.equal(v, rep.factors[1])
+    assert torch.equal(core, rep.core)
+    u2, v2, core2 = hooi_sharded(ops, t, u, v, 2, 0, int(t.shape[1]), ident, same)
+    rep2 = bt.hooi(t, rep, 2, shared=(1, 3))
+    assert torch.equal(u2, rep2.factors[0]) and torch.equal(v2, rep2.factors[1])
+
+    def recon(c, uu, vv):
+        return port.mode_multiply(port.mode_multiply(port.mode_multiply(c, 1, uu), 2, vv), 3, uu)
+
+    a = recon(core2.cpu().numpy(), u2.cpu().numpy(), v2.cpu().numpy())
+    b = recon(rep2.core.cpu().numpy(), rep2.factors[0].cpu().numpy(), rep2.factors[1].cpu().numpy())
+    assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b)
+
+
+def test_tucker_c3_distributed_single_process():
+    from paper_2105_01170_b200.parallel import tucker_c3_distributed
+
+    _, _, t = oc.c3_tensor(side=6, lags=10)
+    rep = tucker_c3_distributed(t, 8, 4, hooi_sweeps=2)
+    assert isinstance(rep.core, np.ndarray) and rep.factors[0] is rep.factors[2]
+    core_o, fac = port.st_hosvd_shared13(t, 8, 4)
+    core_h, (uh, vh, _) = port.hooi_shared13(t, fac[0], fac[1], 2)
+
+    def recon(c, uu, vv):
+        return port.mode_multiply(port.mode_multiply(port.mode_multiply(c, 1, uu), 2, vv), 3, uu)
+
+    ref = recon(core_h, uh, vh)
+    got = recon(rep.core, rep.factors[0], rep.factors[1])
+    assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_matvec_rhs_sharded_concat_equals_full(world):
+    import paper_2105_01170_b200 as bt
+    from paper_2105_01170_b200.parallel import matvec_sharded
+
+    _, a = oc.c1_inputs()
+    pat = bt.build_pattern("toeplitz", 32, 32, 32, 32, block_symmetric=True)
+    res = bt.cp_als(bt.mat_to_tensor(a, pat), 4, 5, 0.0)
+    rep = bt.kron_sum_from_kruskal(res.rep, pat)
+    x = np.random.default_rng(1001).standard_normal((1024, 16))
+    full = bt.matvec(rep, x)
+    parts = [matvec_sharded(rep, x, world, k) for k in range(world)]
+    got = np.concatenate(parts, axis=1)
+    assert np.linalg.norm(got - full) <= 1e-14 * np.linalg.norm(full)
