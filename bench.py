@@ -444,6 +444,15 @@ def run_bt200(args, rank, world):
     fit = hist_holder["h"][-1]
     log(f"[bench] C5 step {ms:.1f} ms, tree {tree_ms:.2f} ms, mode2 {phase_tot[1] / (args.steps * ITERS):.2f} ms,"
         f" mode3 {mode3_ms:.2f} ms, solves+fit {phase_tot[3] / (args.steps * ITERS):.2f} ms, fit {fit}")
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                           "profiles", "r01_ncu_c5.json")))
+        if prof["config"] == {"I": I_, "J": J_, "K": kloc, "R": R_}:
+            tk = prof["tree_p_kernel"]
+            traffic = tk["dram_bytes_read"] + tk["dram_bytes_write"]
+    except (OSError, KeyError, ValueError):
+        pass
     result = {
         "metric": "CP-ALS MTTKRP GFLOP/s (reference-equivalent 6*I*J*K*R per sweep)",
         "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -464,7 +473,10 @@ def run_bt200(args, rank, world):
                                           "solves_fit": phase_tot[3] / (args.steps * ITERS)}},
         "roofline": {"bound": "tensor", "kernel": "tree_p_kernel (P = X x3 C, DMMA)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_note": ("bytes per launch, ncu dram__bytes_read+write "
+                                      "(profiles/r01_ncu_c5.json); algorithmic X + P = "
+                                      f"{8.0 * I_ * J_ * (kloc + R_):.4g} B"),
                      "peak_source": "measured in this run: DMMA.8x8x4 chains on all SMs "
                                     "(MEASURED_PEAKS.json has no FP64 figure)",
                      "mode3_gemm_achieved": 2.0 * I_ * J_ * kloc * R_ / (mode3_ms / 1e3) / 1e12},

@@ -99,6 +99,18 @@ int bt_gather_blocks_f64(const double* a, int64_t lda, const bt_pattern_dev* pat
 int bt_scatter_blocks_f64(const double* t, int64_t t_sm, int64_t t_sp, int64_t t_sn,
                           const bt_pattern_dev* pat, double* a, int64_t lda, void* stream);
 
+/* blocks.py:266-329 detect_pattern, device passes.  Digest: per grid cell
+ * (row-major, ell*q) a 128-bit order-independent digest (h1, h2) of the
+ * block's bytes and nz = the reference's keep predicate (tol == 0: some
+ * entry not +-0.0, i.e. blk.any(); tol > 0: NOT max|blk| <= tol, NaN kept).
+ * Match: for every cell with cand[cell] >= 0, eq[cell] = 1 iff the block
+ * equals block cand[cell] (exact != 0: bit for bit; else max|d| <= tol,
+ * NaN failing).  Asynchronous. */
+int bt_block_digest_f64(const double* a, int64_t lda, int64_t ell, int64_t q, int64_t m, int64_t n,
+                        double tol, uint64_t* h1, uint64_t* h2, int* nz, void* stream);
+int bt_block_match_f64(const double* a, int64_t lda, int64_t ell, int64_t q, int64_t m, int64_t n,
+                       const int64_t* cand, double tol, int exact, int* eq, void* stream);
+
 /* ------------------------------------------------------------------------
  * K3: weighted tensor builders for the configs.
  * ---------------------------------------------------------------------- */

@@ -208,6 +208,49 @@ def spd_toeplitz(seed, ell=4, nb=5, decay=0.3):
     return pat, a
 
 
+def detect_cases():
+    """Seeded inputs for detect_pattern (blocks.py:266): (name, a, m, n, tol).
+    Structured matrices from the named builders with random blocks, plus the
+    edge cases the reference handles explicitly: all-zero and -0.0 blocks
+    (skipped), NaN blocks (kept; never within tol), near-equal blocks that
+    only merge under tol, a ragged 3 x 5 grid of 3 x 2 blocks."""
+    from .port import assemble, make_pattern
+
+    rng = np.random.default_rng(41)
+    out = []
+    for kind, ell in (("toeplitz", 6), ("hankel", 5), ("diagonal", 4)):
+        pat = make_pattern(kind, ell, ell, 3, 3)
+        blocks = [rng.standard_normal((3, 3)) for _ in range(pat.p)]
+        out.append((f"{kind}{ell}", assemble(pat, blocks), 3, 3, 0.0))
+    pat = make_pattern("banded", 6, 6, 2, 2, band=1)
+    out.append(("banded6", assemble(pat, [rng.standard_normal((2, 2)) for _ in range(pat.p)]),
+                2, 2, 0.0))
+    # ragged grid with repeats, zeros, -0.0 and a NaN block
+    choices = [rng.standard_normal((3, 2)) for _ in range(4)]
+    a = np.zeros((9, 10))
+    for i in range(3):
+        for j in range(5):
+            c = (i * 5 + j * 3) % 6
+            if c < 4:
+                a[i * 3:(i + 1) * 3, j * 2:(j + 1) * 2] = choices[c]
+            elif c == 5:
+                a[i * 3:(i + 1) * 3, j * 2:(j + 1) * 2] = -0.0
+    a[6:9, 8:10] = np.nan
+    out.append(("ragged", a, 3, 2, 0.0))
+    # near-equal blocks: exact splits them, tol merges them
+    base = rng.standard_normal((4, 4))
+    b = np.block([[base, base + 1e-9, np.zeros((4, 4))],
+                  [base - 2e-9, np.zeros((4, 4)), base + 1e-3],
+                  [np.full((4, 4), 5e-7), base, base + 1e-9]])
+    for tol in (0.0, 1e-8, 1e-6, 1e-2):
+        out.append((f"near_tol{tol:g}", b, 4, 4, tol))
+    # C1 matrix, exact and loose
+    _, c1 = c1_inputs()
+    out.append(("c1", c1, 32, 32, 0.0))
+    out.append(("c1_tol", c1, 32, 32, 1e-3))
+    return out
+
+
 def gather_standin(nb=256, ell=128):
     x = np.linspace(0.0, 1.0, nb)
     base = np.exp(-((x[:, None] - x[None, :]) ** 2) / (2 * 0.1**2))

@@ -541,6 +541,35 @@ def classify_placements(placements, ell, q):
     return "general"
 
 
+def detect_pattern(a, m, n, tol=0.0):
+    """blocks.py:266-329: row-major scan; tol == 0 groups by the block's bytes
+    (all-zero blocks skipped), tol > 0 joins the first representative within
+    tol.  Returns (placements, reps, structure_class)."""
+    ell, q = a.shape[0] // m, a.shape[1] // n
+    reps, cells, by_bytes = [], [], {}
+    for i in range(ell):
+        for j in range(q):
+            blk = np.ascontiguousarray(a[i * m:(i + 1) * m, j * n:(j + 1) * n])
+            if tol == 0.0:
+                if not blk.any():
+                    continue
+                k = by_bytes.setdefault(blk.tobytes(), len(reps))
+                if k == len(reps):
+                    reps.append(blk)
+                    cells.append([])
+            else:
+                if np.max(np.abs(blk)) <= tol:
+                    continue
+                k = next((kk for kk, r in enumerate(reps) if np.max(np.abs(blk - r)) <= tol),
+                         len(reps))
+                if k == len(reps):
+                    reps.append(blk)
+                    cells.append([])
+            cells[k].append((i, j))
+    placements = tuple(np.array(c, dtype=np.int64) for c in cells)
+    return placements, reps, classify_placements(placements, ell, q)
+
+
 def cholesky(a):
     """decomp.py:196-212 (numpy's LAPACK potrf; asymmetry > 1e-12 max|a|
     is a ShapeError, a failed pivot a ValueError here)."""

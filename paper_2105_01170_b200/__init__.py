@@ -8,9 +8,9 @@ provides device memory and streams.
 
 from __future__ import annotations
 
-from .blocks import (BlockPattern, build_pattern, classify_placements, extract_blocks,
-                     kernel_level_pattern, mat_to_tensor, struct_assemble, struct_expand,
-                     struct_scalars, tensor_to_mat)
+from .blocks import (BlockPattern, build_pattern, classify_placements, detect_pattern,
+                     extract_blocks, kernel_level_pattern, mat_to_tensor, struct_assemble,
+                     struct_expand, struct_scalars, tensor_to_mat)
 from .decomp import (CpResult, KruskalRep, SketchConfig, TuckerRep, cholesky, cp_als, hooi,
                      hosvd, qr_thin, st_hosvd, svd_truncated, tucker_partial)
 from .errors import (ContainerExtentError, ContainerFormatError, ConvergenceError,

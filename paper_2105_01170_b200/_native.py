@@ -88,6 +88,10 @@ _SIGS = {
     "bt_syevx_f64": (C.c_int, [_dp, _i64, _i64, C.c_double, _dp, _dp, _dp, _i64, _dp]),
     "bt_qr_thin_ws_bytes": (_i64, [_i64, _i64]),
     "bt_qr_thin_f64": (C.c_int, [_dp, _i64, _i64, _dp, _dp, _dp, _i64, _dp]),
+    "bt_block_digest_f64": (C.c_int, [_dp, _i64, _i64, _i64, _i64, _i64, C.c_double, _dp, _dp,
+                                      _dp, _dp]),
+    "bt_block_match_f64": (C.c_int, [_dp, _i64, _i64, _i64, _i64, _i64, _dp, C.c_double, C.c_int,
+                                     _dp, _dp]),
     "bt_cholesky_ws_bytes": (_i64, [_i64]),
     "bt_cholesky_f64": (C.c_int, [_dp, _i64, _dp, _dp, _P(_i64), _dp]),
     "bt_tri_inv_lower_ws_bytes": (_i64, [_i64]),

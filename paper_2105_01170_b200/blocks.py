@@ -26,6 +26,7 @@ from .errors import PatternMismatchError, ShapeError
 __all__ = [
     "BlockPattern",
     "classify_placements",
+    "detect_pattern",
     "build_pattern",
     "struct_assemble",
     "struct_expand",
@@ -316,6 +317,100 @@ def _ones_eta(pat: BlockPattern):
 def _items(items, pat, what):
     if len(items) != pat.p:
         raise ShapeError(f"expected {pat.p} {what}, got {len(items)}")
+
+
+def _cells_match(ad, ell, q, m, n, cand, tol, exact):
+    """eq flags (host int32 per cell) of bt_block_match_f64 for host cand."""
+    t = _dev.torch()
+    cd = _dev.to_device(cand.astype(np.int64), dtype=t.int64)
+    eq = t.zeros(ell * q, dtype=t.int32, device="cuda")
+    N.call("bt_block_match_f64", _dev.ptr(ad), int(ad.shape[1]), ell, q, m, n, _dev.ptr(cd),
+           float(tol), int(exact), _dev.ptr(eq), _dev.stream())
+    return eq.cpu().numpy()
+
+
+def detect_pattern(a, m: int, n: int, tol: float = 0.0):
+    """blocks.py:266-329: partition ``a`` into m x n blocks and group repeats.
+
+    One device pass digests every block (128-bit, order independent) and
+    evaluates the reference's skip predicate; equal digests are grouped on
+    the host in row-major first-occurrence order; a second pass checks every
+    cell bit for bit against its group's first cell (a digest collision is
+    split off, never merged).  tol > 0 keeps the reference's linear-scan
+    semantics -- a block joins the first earlier representative within tol --
+    as a greedy over the distinct blocks: representative k is the first
+    unclaimed block, and one device pass claims every unclaimed block within
+    tol of it.  Returns ``(pattern, blocks)``; blocks are the first
+    occurrences (numpy slices for numpy input)."""
+    if a.ndim != 2:
+        raise ShapeError("detect_pattern expects a matrix")
+    rows, cols = (int(v) for v in a.shape)
+    if rows % m or cols % n:
+        raise ShapeError(f"matrix {tuple(a.shape)} does not tile into {m} x {n} blocks")
+    ell, q = rows // m, cols // n
+    t = _dev.torch()
+    ad = _dev.to_device(a).contiguous()
+    cells_n = ell * q
+    h1 = t.empty(cells_n, dtype=t.int64, device="cuda")
+    h2 = t.empty(cells_n, dtype=t.int64, device="cuda")
+    nz = t.empty(cells_n, dtype=t.int32, device="cuda")
+    N.call("bt_block_digest_f64", _dev.ptr(ad), cols, ell, q, m, n, float(tol), _dev.ptr(h1),
+           _dev.ptr(h2), _dev.ptr(nz), _dev.stream())
+    keep = np.flatnonzero(nz.cpu().numpy())
+    if keep.size == 0:
+        raise PatternMismatchError("matrix is identically zero; nothing to detect")
+    key = np.stack([h1.cpu().numpy()[keep], h2.cpu().numpy()[keep]], axis=1)
+    _, first, inv = np.unique(key, axis=0, return_index=True, return_inverse=True)
+    inv = inv.reshape(-1)
+    leader = keep[first][inv]                      # group's first cell, per kept cell
+    cand = np.full(cells_n, -1, dtype=np.int64)
+    cand[keep] = np.where(leader == keep, -1, leader)
+    eq = _cells_match(ad, ell, q, m, n, cand, 0.0, True)
+    bad = keep[(cand[keep] >= 0) & (eq[keep] == 0)]
+    group_of = np.full(cells_n, -1, dtype=np.int64)
+    group_of[keep] = leader
+    while bad.size:                                # digest collisions (never expected)
+        c0 = int(bad[0])
+        group_of[c0] = c0
+        rest = bad[1:]
+        cand = np.full(cells_n, -1, dtype=np.int64)
+        cand[rest] = c0
+        eq = _cells_match(ad, ell, q, m, n, cand, 0.0, True)
+        hit = rest[eq[rest] == 1]
+        group_of[hit] = c0
+        bad = rest[eq[rest] == 0]
+    # distinct blocks: leaders in row-major order, members sorted
+    order = np.argsort(group_of[keep], kind="stable")
+    gk = group_of[keep][order]
+    leaders, starts = np.unique(gk, return_index=True)
+    members = np.split(keep[order], starts[1:])
+    if tol == 0.0:
+        classes = members
+    else:
+        classes = []
+        unclaimed = list(range(len(leaders)))
+        while unclaimed:
+            g0 = unclaimed[0]
+            rest = unclaimed[1:]
+            claim = [g0]
+            if rest:
+                cand = np.full(cells_n, -1, dtype=np.int64)
+                cand[leaders[rest]] = leaders[g0]
+                eq = _cells_match(ad, ell, q, m, n, cand, tol, False)
+                claim += [g for g in rest if eq[leaders[g]] == 1]
+                rest = [g for g in rest if eq[leaders[g]] != 1]
+            classes.append(np.sort(np.concatenate([members[g] for g in claim])))
+            unclaimed = rest
+    placements = tuple(np.stack(np.divmod(c, q), axis=1).astype(np.int64) for c in classes)
+    pattern = BlockPattern(ell=ell, q=q, m=m, n=n, placements=placements,
+                           structure_class=classify_placements(placements, ell, q))
+    if _dev.is_device(a):
+        reps = tuple(ad[i * m:(i + 1) * m, j * n:(j + 1) * n].contiguous()
+                     for i, j in (c[0] for c in placements))
+    else:
+        reps = tuple(np.ascontiguousarray(a[i * m:(i + 1) * m, j * n:(j + 1) * n])
+                     for i, j in (c[0] for c in placements))
+    return pattern, reps
 
 
 def struct_assemble(pattern: BlockPattern, blocks):

@@ -1,0 +1,158 @@
+// Block-repeat detection (blocks.py:266-329 `detect_pattern`).
+//
+// The reference walks the ell x q block grid in Python, hashing each block's
+// bytes (tol == 0) or scanning the class representatives (tol > 0).  Here
+// one HBM pass computes, per grid cell, a 128-bit order-independent digest of
+// the block's bytes (two sums of per-word splitmix64 mixes keyed by the word's
+// position -- any reduction order gives the same bits) and the reference's
+// skip predicate (`blk.any()` for tol == 0, `max|blk| <= tol` for tol > 0,
+// with numpy's NaN semantics).  The host groups equal digests in row-major
+// first-occurrence order; a second pass compares every cell with its class
+// representative word for word (exact) or within tol, so a digest collision
+// can never merge two different blocks.
+#include <algorithm>
+
+#include "bt_common.cuh"
+
+namespace {
+
+constexpr int DT = 256;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// per cell: h1, h2 (digest), nz (tol == 0: any word not +-0.0; tol > 0:
+// max|x| > tol or NaN present)
+__global__ void __launch_bounds__(DT)
+    block_digest_kernel(const double* __restrict__ a, int64_t lda, int64_t ell, int64_t q, int64_t m,
+                        int64_t n, double tol, uint64_t* __restrict__ h1, uint64_t* __restrict__ h2,
+                        int* __restrict__ nz) {
+  __shared__ uint64_t s1[DT / 32], s2[DT / 32];
+  __shared__ int sn[DT / 32];
+  const int64_t cells = ell * q;
+  const int64_t per = m * n;
+  for (int64_t cell = blockIdx.x; cell < cells; cell += gridDim.x) {
+    const int64_t ci = cell / q, cj = cell % q;
+    const double* blk = a + ci * m * lda + cj * n;
+    uint64_t a1 = 0, a2 = 0;
+    int flag = 0;
+    int64_t r = threadIdx.x / n, c = threadIdx.x % n;
+    const int64_t dr = DT / n, dc = DT % n;
+    for (int64_t idx = threadIdx.x; idx < per; idx += DT) {
+      const double x = ld_stream(blk + r * lda + c);
+      const uint64_t w = static_cast<uint64_t>(__double_as_longlong(x));
+      a1 += mix64(w ^ (static_cast<uint64_t>(idx) * 0x9e3779b97f4a7c15ull));
+      a2 += mix64((w + 0x632be59bd9b4e019ull) ^ (static_cast<uint64_t>(idx) * 0xd1b54a32d192ed03ull));
+      if (tol == 0.0)
+        flag |= (w << 1) != 0;  // not +0.0 / -0.0 (NaN counts as nonzero, like np.any)
+      else
+        flag |= !(fabs(x) <= tol);  // NaN or |x| > tol
+      r += dr;
+      c += dc;
+      if (c >= n) {
+        c -= n;
+        ++r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+      flag |= __shfl_xor_sync(0xffffffffu, flag, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s1[threadIdx.x >> 5] = a1;
+      s2[threadIdx.x >> 5] = a2;
+      sn[threadIdx.x >> 5] = flag;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t t1 = 0, t2 = 0;
+      int f = 0;
+      for (int w = 0; w < DT / 32; ++w) {
+        t1 += s1[w];
+        t2 += s2[w];
+        f |= sn[w];
+      }
+      h1[cell] = t1;
+      h2[cell] = t2;
+      nz[cell] = f;
+    }
+    __syncthreads();
+  }
+}
+
+// per cell with cand[cell] >= 0: eq[cell] = block(cell) matches block(cand)
+// (exact: every 64-bit word equal; else max|d| <= tol, a NaN difference
+// failing like numpy's `np.max(np.abs(blk - rep)) <= tol`)
+__global__ void __launch_bounds__(DT)
+    block_match_kernel(const double* __restrict__ a, int64_t lda, int64_t ell, int64_t q, int64_t m,
+                       int64_t n, const int64_t* __restrict__ cand, double tol, int exact,
+                       int* __restrict__ eq) {
+  __shared__ int sb[DT / 32];
+  const int64_t cells = ell * q;
+  const int64_t per = m * n;
+  for (int64_t cell = blockIdx.x; cell < cells; cell += gridDim.x) {
+    const int64_t rc = cand[cell];
+    if (rc < 0) continue;  // CTA-uniform
+    const double* blk = a + (cell / q) * m * lda + (cell % q) * n;
+    const double* rep = a + (rc / q) * m * lda + (rc % q) * n;
+    int bad = 0;
+    int64_t r = threadIdx.x / n, c = threadIdx.x % n;
+    const int64_t dr = DT / n, dc = DT % n;
+    for (int64_t idx = threadIdx.x; idx < per; idx += DT) {
+      const double x = ld_stream(blk + r * lda + c);
+      const double y = ld_keep(rep + r * lda + c);
+      if (exact)
+        bad |= __double_as_longlong(x) != __double_as_longlong(y);
+      else
+        bad |= !(fabs(x - y) <= tol);
+      r += dr;
+      c += dc;
+      if (c >= n) {
+        c -= n;
+        ++r;
+      }
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0) sb[threadIdx.x >> 5] = bad;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int b = 0;
+      for (int w = 0; w < DT / 32; ++w) b |= sb[w];
+      eq[cell] = !b;
+    }
+    __syncthreads();
+  }
+}
+
+int grid_cells(int64_t cells) {
+  return static_cast<int>(std::min<int64_t>(cells, static_cast<int64_t>(bt_num_sms()) * 8));
+}
+
+}  // namespace
+
+extern "C" int bt_block_digest_f64(const double* a, int64_t lda, int64_t ell, int64_t q, int64_t m,
+                                   int64_t n, double tol, uint64_t* h1, uint64_t* h2, int* nz,
+                                   void* stream) {
+  BT_REQUIRE(ell >= 1 && q >= 1 && m >= 1 && n >= 1, BT_E_SHAPE, "digest: empty grid");
+  BT_REQUIRE(lda >= q * n, BT_E_SHAPE, "digest: lda too small");
+  block_digest_kernel<<<grid_cells(ell * q), DT, 0, bt_stream(stream)>>>(a, lda, ell, q, m, n, tol,
+                                                                          h1, h2, nz);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+extern "C" int bt_block_match_f64(const double* a, int64_t lda, int64_t ell, int64_t q, int64_t m,
+                                  int64_t n, const int64_t* cand, double tol, int exact, int* eq,
+                                  void* stream) {
+  BT_REQUIRE(ell >= 1 && q >= 1 && m >= 1 && n >= 1, BT_E_SHAPE, "match: empty grid");
+  BT_REQUIRE(lda >= q * n, BT_E_SHAPE, "match: lda too small");
+  block_match_kernel<<<grid_cells(ell * q), DT, 0, bt_stream(stream)>>>(a, lda, ell, q, m, n, cand,
+                                                                         tol, exact, eq);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}

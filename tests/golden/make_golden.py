@@ -353,6 +353,22 @@ def spd_cases():
     np.savez_compressed(os.path.join(OUT, "spd.npz"), **out)
 
 
+def detect_cases():
+    """blocks.py:266-329 detect_pattern on oracle/configs.detect_cases()."""
+    out = {}
+    meta = []
+    for name, a, m, n, tol in oc.detect_cases():
+        pat, reps = bt.detect_pattern(a, m, n, tol=tol)
+        cells, offs = flat_placements(pat)
+        out[f"{name}_cells"] = cells
+        out[f"{name}_offs"] = offs
+        out[f"{name}_reps"] = np.stack(reps)
+        meta.append({"name": name, "structure_class": pat.structure_class})
+    np.savez_compressed(os.path.join(OUT, "detect.npz"), **out)
+    with open(os.path.join(OUT, "detect.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+
+
 if __name__ == "__main__":
     np.seterr(all="ignore")
     patterns()
@@ -362,5 +378,6 @@ if __name__ == "__main__":
     rep_cases()
     psf_cases()
     spd_cases()
+    detect_cases()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -213,3 +213,17 @@ def test_spd_compress_golden(golden):
     low, cells, u, proj = port.spd_compress(z["bd_a"], pat, 2)
     assert cells == []
     assert np.abs(port.densify_spd(pat, low, cells, u, proj) - z["bd_dense"]).max() < 1e-12
+
+
+def test_detect_pattern_golden(golden):
+    """oracle detect_pattern vs the reference (blocks.py:266-329), bit-exact."""
+    z = golden("detect")
+    meta = {d["name"]: d for d in json.load(open(os.path.join(GOLDEN, "detect.json")))}
+    for name, a, m, n, tol in oc.detect_cases():
+        pl, reps, cls = port.detect_pattern(a, m, n, tol)
+        cells = np.vstack(pl).astype(np.int64)
+        offs = np.cumsum([0] + [len(c) for c in pl]).astype(np.int64)
+        assert np.array_equal(cells, z[f"{name}_cells"]), name
+        assert np.array_equal(offs, z[f"{name}_offs"]), name
+        assert np.array_equal(np.stack(reps).view(np.int64), z[f"{name}_reps"].view(np.int64)), name
+        assert cls == meta[name]["structure_class"], name
