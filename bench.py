@@ -340,7 +340,14 @@ def extras_run(torch, budget_s=240.0):
             out["gather_standin_gbs"] = nbytes / ms_g / 1e6
             out["scatter_standin_ms"] = ms_s
             out["scatter_standin_gbs"] = nbytes / ms_s / 1e6
-            del a, t
+            del t
+            # detect_pattern (digest pass + bit-exact verify pass: A read twice)
+            ms_d = timed(torch, lambda: bt.detect_pattern(a, patg.m, patg.n), 2, 1)
+            pd, _ = bt.detect_pattern(a, patg.m, patg.n)
+            out["detect_standin_ms"] = ms_d
+            out["detect_standin_gbs"] = 2 * a.numel() * 8 / ms_d / 1e6
+            out["detect_standin_classes"] = pd.p
+            del a
             torch.cuda.empty_cache()
         except Exception as exc:  # pragma: no cover
             out["gather_error"] = repr(exc)[:300]

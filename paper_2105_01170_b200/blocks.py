@@ -255,36 +255,43 @@ def kernel_level_pattern(k: int, bm: int, bn: int, grid: int | None = None) -> B
     return _make(grid, grid, bm, bn, [_diag(grid, h - i) for i in range(k)], f"toeplitz:{h}")
 
 
+def _class_segments(placements):
+    counts = np.array([len(c) for c in placements], dtype=np.int64)
+    starts = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+    return counts, starts
+
+
+def _one_or_two_values(v, counts, starts):
+    """Per class: (min, max, every value is min or max) of the segment."""
+    lo = np.minimum.reduceat(v, starts)
+    hi = np.maximum.reduceat(v, starts)
+    cls = np.repeat(np.arange(len(counts)), counts)
+    inside = (v == lo[cls]) | (v == hi[cls])
+    return lo, hi, np.logical_and.reduceat(inside, starts)
+
+
 def classify_placements(placements, ell: int, q: int) -> str:
-    """blocks.py:228-263: descriptive structure tag of a placement family."""
+    """blocks.py:228-263: descriptive structure tag of a placement family,
+    vectorised over classes (same decisions as the reference's per-class
+    set logic: one offset covering a full diagonal, or a +-d pair covering
+    both; one anti-diagonal sum covering it fully; else the bandwidth)."""
     allc = np.vstack(placements) if placements else np.zeros((0, 2), dtype=np.int64)
     if len(allc) and np.all(allc[:, 0] == allc[:, 1]):
         return "diagonal"
-
-    def full_diag(cells):
-        offs = set(int(j - i) for i, j in cells)
-        if ell != q:
-            return None
-        if len(offs) == 1:
-            (d,) = offs
-            return d if len(cells) == ell - abs(d) else None
-        if len(offs) == 2:
-            d1, d2 = sorted(offs)
-            if d1 == -d2 and d2 > 0 and len(cells) == 2 * (ell - d2):
-                return d2
-        return None
-
-    def full_anti(cells):
-        sums = set(int(i + j) for i, j in cells)
-        if ell != q or len(sums) != 1:
-            return None
-        (s,) = sums
-        return s if len(cells) == min(s + 1, ell, 2 * ell - 1 - s) else None
-
-    if placements and all(full_diag(c) is not None for c in placements):
-        return "toeplitz"
-    if placements and all(full_anti(c) is not None for c in placements):
-        return "hankel"
+    if placements and ell == q:
+        counts, starts = _class_segments(placements)
+        off = allc[:, 1] - allc[:, 0]
+        lo, hi, two = _one_or_two_values(off, counts, starts)
+        single = lo == hi
+        diag_ok = np.where(single, counts == ell - np.abs(lo),
+                           two & (lo == -hi) & (hi > 0) & (counts == 2 * (ell - hi)))
+        if np.all(diag_ok):
+            return "toeplitz"
+        sm = allc[:, 0] + allc[:, 1]
+        slo, shi, _ = _one_or_two_values(sm, counts, starts)
+        anti_ok = (slo == shi) & (counts == np.minimum(np.minimum(slo + 1, ell), 2 * ell - 1 - slo))
+        if np.all(anti_ok):
+            return "hankel"
     if len(allc):
         b = int(np.max(np.abs(allc[:, 0] - allc[:, 1])))
         if b < max(ell, q) - 1:
@@ -359,9 +366,16 @@ def detect_pattern(a, m: int, n: int, tol: float = 0.0):
     keep = np.flatnonzero(nz.cpu().numpy())
     if keep.size == 0:
         raise PatternMismatchError("matrix is identically zero; nothing to detect")
-    key = np.stack([h1.cpu().numpy()[keep], h2.cpu().numpy()[keep]], axis=1)
-    _, first, inv = np.unique(key, axis=0, return_index=True, return_inverse=True)
-    inv = inv.reshape(-1)
+    # group on (h1, h2): sort by both, mark key changes -> first-occurrence ids
+    k1, k2 = h1.cpu().numpy()[keep], h2.cpu().numpy()[keep]
+    srt = np.lexsort((np.arange(len(keep)), k2, k1))
+    new = np.ones(len(keep), dtype=bool)
+    new[1:] = (k1[srt][1:] != k1[srt][:-1]) | (k2[srt][1:] != k2[srt][:-1])
+    gid = np.cumsum(new) - 1
+    first_of_gid = srt[new]                        # earliest kept index of each key
+    inv = np.empty(len(keep), dtype=np.int64)
+    inv[srt] = gid
+    first = first_of_gid
     leader = keep[first][inv]                      # group's first cell, per kept cell
     cand = np.full(cells_n, -1, dtype=np.int64)
     cand[keep] = np.where(leader == keep, -1, leader)

@@ -3,8 +3,8 @@
 // The reference walks the ell x q block grid in Python, hashing each block's
 // bytes (tol == 0) or scanning the class representatives (tol > 0).  Here
 // one HBM pass computes, per grid cell, a 128-bit order-independent digest of
-// the block's bytes (two sums of per-word splitmix64 mixes keyed by the word's
-// position -- any reduction order gives the same bits) and the reference's
+// the block's bytes (two sums of per-word multiply/xor-shift mixes keyed by
+// the word's position -- any reduction order gives the same bits) and the reference's
 // skip predicate (`blk.any()` for tol == 0, `max|blk| <= tol` for tol > 0,
 // with numpy's NaN semantics).  The host groups equal digests in row-major
 // first-occurrence order; a second pass compares every cell with its class
@@ -17,15 +17,32 @@
 namespace {
 
 constexpr int DT = 256;
+constexpr int DU = 4;  // independent loads in flight per thread
 
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-  return z ^ (z >> 31);
+constexpr uint64_t kK1 = 0x9e3779b97f4a7c15ull, kK2 = 0xd1b54a32d192ed03ull;
+
+// one multiply + xor-shift per word and digest: the digest only has to make
+// collisions rare (every grouping is verified bit for bit afterwards)
+__device__ __forceinline__ uint64_t mix_lite(uint64_t z, uint64_t mul) {
+  z = (z ^ (z >> 32)) * mul;
+  return z ^ (z >> 29);
+}
+
+template <int V>
+__device__ __forceinline__ void load_vec(const double* p, double* out) {
+  if (V == 2) {
+    const double2 v = ld_stream2(p);
+    out[0] = v.x;
+    out[V - 1] = v.y;
+  } else {
+    out[0] = ld_stream(p);
+  }
 }
 
 // per cell: h1, h2 (digest), nz (tol == 0: any word not +-0.0; tol > 0:
-// max|x| > tol or NaN present)
+// max|x| > tol or NaN present).  V doubles per access; word e of the block
+// (row-major) is keyed by its position e.
+template <int V>
 __global__ void __launch_bounds__(DT)
     block_digest_kernel(const double* __restrict__ a, int64_t lda, int64_t ell, int64_t q, int64_t m,
                         int64_t n, double tol, uint64_t* __restrict__ h1, uint64_t* __restrict__ h2,
@@ -33,28 +50,46 @@ __global__ void __launch_bounds__(DT)
   __shared__ uint64_t s1[DT / 32], s2[DT / 32];
   __shared__ int sn[DT / 32];
   const int64_t cells = ell * q;
-  const int64_t per = m * n;
+  const int64_t nv = n / V;
+  const int64_t per = m * nv;
   for (int64_t cell = blockIdx.x; cell < cells; cell += gridDim.x) {
     const int64_t ci = cell / q, cj = cell % q;
     const double* blk = a + ci * m * lda + cj * n;
     uint64_t a1 = 0, a2 = 0;
     int flag = 0;
-    int64_t r = threadIdx.x / n, c = threadIdx.x % n;
-    const int64_t dr = DT / n, dc = DT % n;
-    for (int64_t idx = threadIdx.x; idx < per; idx += DT) {
-      const double x = ld_stream(blk + r * lda + c);
-      const uint64_t w = static_cast<uint64_t>(__double_as_longlong(x));
-      a1 += mix64(w ^ (static_cast<uint64_t>(idx) * 0x9e3779b97f4a7c15ull));
-      a2 += mix64((w + 0x632be59bd9b4e019ull) ^ (static_cast<uint64_t>(idx) * 0xd1b54a32d192ed03ull));
-      if (tol == 0.0)
-        flag |= (w << 1) != 0;  // not +0.0 / -0.0 (NaN counts as nonzero, like np.any)
-      else
-        flag |= !(fabs(x) <= tol);  // NaN or |x| > tol
-      r += dr;
-      c += dc;
-      if (c >= n) {
-        c -= n;
-        ++r;
+    int64_t r = threadIdx.x / nv, c = threadIdx.x % nv;
+    const int64_t dr = DT / nv, dc = DT % nv;
+    for (int64_t idx0 = threadIdx.x; idx0 < per; idx0 += DU * DT) {
+      double x[DU][V];
+#pragma unroll
+      for (int u = 0; u < DU; ++u) {  // DU independent loads in flight per thread
+        if (idx0 + u * DT < per) load_vec<V>(blk + r * lda + c * V, x[u]);
+        r += dr;
+        c += dc;
+        if (c >= nv) {
+          c -= nv;
+          ++r;
+        }
+      }
+      // position keys pos*K by addition (one multiply per DU*V words)
+      uint64_t k1 = static_cast<uint64_t>(idx0 * V) * kK1, k2 = static_cast<uint64_t>(idx0 * V) * kK2;
+#pragma unroll
+      for (int u = 0; u < DU; ++u) {
+        const bool ok = idx0 + u * DT < per;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          if (ok) {
+            const uint64_t w = static_cast<uint64_t>(__double_as_longlong(x[u][e]));
+            a1 += mix_lite(w ^ (k1 + e * kK1), 0xbf58476d1ce4e5b9ull);
+            a2 += mix_lite((w + 0x632be59bd9b4e019ull) ^ (k2 + e * kK2), 0x94d049bb133111ebull);
+            if (tol == 0.0)
+              flag |= (w << 1) != 0;  // not +0.0 / -0.0 (NaN counts as nonzero, like np.any)
+            else
+              flag |= !(fabs(x[u][e]) <= tol);  // NaN or |x| > tol
+          }
+        }
+        k1 += kK1 * (DT * V);
+        k2 += kK2 * (DT * V);
       }
     }
 #pragma unroll
@@ -88,33 +123,56 @@ __global__ void __launch_bounds__(DT)
 // per cell with cand[cell] >= 0: eq[cell] = block(cell) matches block(cand)
 // (exact: every 64-bit word equal; else max|d| <= tol, a NaN difference
 // failing like numpy's `np.max(np.abs(blk - rep)) <= tol`)
+template <int V>
 __global__ void __launch_bounds__(DT)
     block_match_kernel(const double* __restrict__ a, int64_t lda, int64_t ell, int64_t q, int64_t m,
                        int64_t n, const int64_t* __restrict__ cand, double tol, int exact,
                        int* __restrict__ eq) {
   __shared__ int sb[DT / 32];
   const int64_t cells = ell * q;
-  const int64_t per = m * n;
+  const int64_t nv = n / V;
+  const int64_t per = m * nv;
   for (int64_t cell = blockIdx.x; cell < cells; cell += gridDim.x) {
     const int64_t rc = cand[cell];
     if (rc < 0) continue;  // CTA-uniform
     const double* blk = a + (cell / q) * m * lda + (cell % q) * n;
     const double* rep = a + (rc / q) * m * lda + (rc % q) * n;
     int bad = 0;
-    int64_t r = threadIdx.x / n, c = threadIdx.x % n;
-    const int64_t dr = DT / n, dc = DT % n;
-    for (int64_t idx = threadIdx.x; idx < per; idx += DT) {
-      const double x = ld_stream(blk + r * lda + c);
-      const double y = ld_keep(rep + r * lda + c);
-      if (exact)
-        bad |= __double_as_longlong(x) != __double_as_longlong(y);
-      else
-        bad |= !(fabs(x - y) <= tol);
-      r += dr;
-      c += dc;
-      if (c >= n) {
-        c -= n;
-        ++r;
+    int64_t r = threadIdx.x / nv, c = threadIdx.x % nv;
+    const int64_t dr = DT / nv, dc = DT % nv;
+    for (int64_t idx0 = threadIdx.x; idx0 < per; idx0 += DU * DT) {
+      double x[DU][V], y[DU][V];
+      bool ok[DU];
+#pragma unroll
+      for (int u = 0; u < DU; ++u) {
+        ok[u] = idx0 + u * DT < per;
+        if (ok[u]) {
+          load_vec<V>(blk + r * lda + c * V, x[u]);
+          if (V == 2) {
+            const double2 v = ld_keep2(rep + r * lda + c * V);
+            y[u][0] = v.x;
+            y[u][V - 1] = v.y;
+          } else {
+            y[u][0] = ld_keep(rep + r * lda + c);
+          }
+        }
+        r += dr;
+        c += dc;
+        if (c >= nv) {
+          c -= nv;
+          ++r;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < DU; ++u) {
+        if (!ok[u]) continue;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          if (exact)
+            bad |= __double_as_longlong(x[u][e]) != __double_as_longlong(y[u][e]);
+          else
+            bad |= !(fabs(x[u][e] - y[u][e]) <= tol);
+        }
       }
     }
     bad = __any_sync(0xffffffffu, bad);
@@ -129,6 +187,10 @@ __global__ void __launch_bounds__(DT)
   }
 }
 
+bool vec2_ok(const double* a, int64_t lda, int64_t n) {
+  return (n % 2 == 0) && (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15u) == 0);
+}
+
 int grid_cells(int64_t cells) {
   return static_cast<int>(std::min<int64_t>(cells, static_cast<int64_t>(bt_num_sms()) * 8));
 }
@@ -140,8 +202,12 @@ extern "C" int bt_block_digest_f64(const double* a, int64_t lda, int64_t ell, in
                                    void* stream) {
   BT_REQUIRE(ell >= 1 && q >= 1 && m >= 1 && n >= 1, BT_E_SHAPE, "digest: empty grid");
   BT_REQUIRE(lda >= q * n, BT_E_SHAPE, "digest: lda too small");
-  block_digest_kernel<<<grid_cells(ell * q), DT, 0, bt_stream(stream)>>>(a, lda, ell, q, m, n, tol,
-                                                                          h1, h2, nz);
+  if (vec2_ok(a, lda, n))
+    block_digest_kernel<2><<<grid_cells(ell * q), DT, 0, bt_stream(stream)>>>(a, lda, ell, q, m, n,
+                                                                             tol, h1, h2, nz);
+  else
+    block_digest_kernel<1><<<grid_cells(ell * q), DT, 0, bt_stream(stream)>>>(a, lda, ell, q, m, n,
+                                                                             tol, h1, h2, nz);
   BT_LAUNCH_CHECK();
   return BT_OK;
 }
@@ -151,8 +217,12 @@ extern "C" int bt_block_match_f64(const double* a, int64_t lda, int64_t ell, int
                                   void* stream) {
   BT_REQUIRE(ell >= 1 && q >= 1 && m >= 1 && n >= 1, BT_E_SHAPE, "match: empty grid");
   BT_REQUIRE(lda >= q * n, BT_E_SHAPE, "match: lda too small");
-  block_match_kernel<<<grid_cells(ell * q), DT, 0, bt_stream(stream)>>>(a, lda, ell, q, m, n, cand,
-                                                                         tol, exact, eq);
+  if (vec2_ok(a, lda, n))
+    block_match_kernel<2><<<grid_cells(ell * q), DT, 0, bt_stream(stream)>>>(a, lda, ell, q, m, n,
+                                                                            cand, tol, exact, eq);
+  else
+    block_match_kernel<1><<<grid_cells(ell * q), DT, 0, bt_stream(stream)>>>(a, lda, ell, q, m, n,
+                                                                            cand, tol, exact, eq);
   BT_LAUNCH_CHECK();
   return BT_OK;
 }

@@ -19,6 +19,7 @@
 // not.  The first bad cell in the reference's scan order wins (integer
 // atomicMin on its order rank -- deterministic).
 #include <algorithm>
+#include <cstdlib>
 
 #include "bt_common.cuh"
 
@@ -31,7 +32,66 @@ __device__ __forceinline__ void cell_flags(double d, double tol, int& exceed, in
   nan |= (d != d);
 }
 
+// U independent vector accesses per thread per iteration: with one access in
+// flight per thread the SM holds only ~32 KB of outstanding requests, short
+// of what HBM3e latency x bandwidth needs (~50 KB/SM); U = 4 covers it.
+constexpr int MAP_UNROLL = 4;
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+// tuning overrides: BT_GATHER_U / BT_SCATTER_U in {1, 2, 4, 8}
+int gather_unroll() {
+  static const int u = env_int("BT_GATHER_U", 2);
+  return u;
+}
+int scatter_unroll() {
+  static const int u = env_int("BT_SCATTER_U", MAP_UNROLL);
+  return u;
+}
+
+
+
+// incremental (row, vcol) walk over an m x nv block without divisions
+struct CellWalk {
+  int rr, cv, nv, drow, dcol;
+  __device__ CellWalk(int start, int nv_) : nv(nv_) {
+    rr = start / nv;
+    cv = start % nv;
+    drow = MAP_THREADS / nv;
+    dcol = MAP_THREADS % nv;
+  }
+  __device__ __forceinline__ void next() {
+    rr += drow;
+    cv += dcol;
+    if (cv >= nv) {
+      cv -= nv;
+      ++rr;
+    }
+  }
+};
+
 template <int V>
+__device__ __forceinline__ void flag_diff(const double* x, const double* y, double tol,
+                                          int& exceed, int& nan) {
+#pragma unroll
+  for (int e = 0; e < V; ++e) cell_flags(fabs(x[e] - y[e]), tol, exceed, nan);
+}
+
+template <int V>
+__device__ __forceinline__ void load_v(const double* p, double* out, bool keep) {
+  if (V == 2) {
+    const double2 v = keep ? ld_keep2(p) : ld_stream2(p);
+    out[0] = v.x;
+    out[1] = v.y;
+  } else {
+    out[0] = keep ? ld_keep(p) : ld_stream(p);
+  }
+}
+
+template <int V, int U>
 __global__ void __launch_bounds__(MAP_THREADS)
     gather_kernel(const double* __restrict__ a, int64_t lda, bt_pattern_dev pat, double tol,
                   int weighted, double* __restrict__ t, int* __restrict__ flags) {
@@ -39,67 +99,69 @@ __global__ void __launch_bounds__(MAP_THREADS)
   const int64_t m = pat.m, n = pat.n, p = pat.p;
   const int nv = static_cast<int>(n / V);
   const int64_t per = m * nv;
-  // incremental (row, vcol) walk without divisions in the loop
-  const int drow = MAP_THREADS / nv, dcol = MAP_THREADS % nv;
   __shared__ int red[2][MAP_THREADS / 32];
   for (int64_t cell = blockIdx.x; cell < cells; cell += gridDim.x) {
     const int64_t ci = cell / pat.q, cj = cell % pat.q;
     const int k = pat.cell_class[cell];
     const double* blk = a + ci * m * lda + cj * n;
     int exceed = 0, nan = 0;
+    CellWalk w(threadIdx.x, nv);
     if (k < 0) {
-      int rr = threadIdx.x / nv, cv = threadIdx.x % nv;
-      for (int64_t idx = threadIdx.x; idx < per; idx += MAP_THREADS) {
-        const double* src = blk + rr * lda + cv * V;
-        if (V == 2) {
-          double2 v = ld_stream2(src);
-          cell_flags(fabs(v.x), tol, exceed, nan);
-          cell_flags(fabs(v.y), tol, exceed, nan);
-        } else {
-          cell_flags(fabs(ld_stream(src)), tol, exceed, nan);
+      const double zero[V] = {};
+      for (int64_t idx = threadIdx.x; idx < per; idx += U * MAP_THREADS) {
+        double x[U][V];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          ok[u] = idx + u * MAP_THREADS < per;
+          if (ok[u]) load_v<V>(blk + (int64_t)w.rr * lda + w.cv * V, x[u], false);
+          w.next();
         }
-        rr += drow;
-        cv += dcol;
-        if (cv >= nv) {
-          cv -= nv;
-          ++rr;
-        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ok[u]) flag_diff<V>(x[u], zero, tol, exceed, nan);
       }
     } else {
       const int64_t rc = pat.rep_cell[k];
       const bool is_rep = (rc == cell);
       const double* ref = a + (rc / pat.q) * m * lda + (rc % pat.q) * n;
-      const double w = weighted ? sqrt(static_cast<double>(pat.eta[k])) : 1.0;
+      const double wt = weighted ? sqrt(static_cast<double>(pat.eta[k])) : 1.0;
       double* tk = t + k * n;  // t[row][k][col] = t[row * p * n + k * n + col]
-      int rr = threadIdx.x / nv, cv = threadIdx.x % nv;
-      for (int64_t idx = threadIdx.x; idx < per; idx += MAP_THREADS) {
-        const double* src = blk + rr * lda + cv * V;
+      for (int64_t idx = threadIdx.x; idx < per; idx += U * MAP_THREADS) {
+        double x[U][V];
+        int rrs[U], cvs[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          rrs[u] = (idx + u * MAP_THREADS < per) ? w.rr : -1;
+          cvs[u] = w.cv;
+          w.next();
+        }
         if (is_rep) {
-          double* dst = tk + rr * p * n + cv * V;
-          if (V == 2) {
-            double2 v = ld_keep2(src);
-            v.x *= w;
-            v.y *= w;
-            *reinterpret_cast<double2*>(dst) = v;
-          } else {
-            dst[0] = w * ld_keep(src);
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (rrs[u] >= 0) load_v<V>(blk + (int64_t)rrs[u] * lda + cvs[u] * V, x[u], true);
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (rrs[u] < 0) continue;
+            double* dst = tk + (int64_t)rrs[u] * p * n + cvs[u] * V;
+            if (V == 2) {
+              *reinterpret_cast<double2*>(dst) = make_double2(wt * x[u][0], wt * x[u][V - 1]);
+            } else {
+              dst[0] = wt * x[u][0];
+            }
           }
         } else {
-          const double* rsrc = ref + rr * lda + cv * V;
-          if (V == 2) {
-            double2 v = ld_stream2(src);
-            double2 r = ld_keep2(rsrc);
-            cell_flags(fabs(v.x - r.x), tol, exceed, nan);
-            cell_flags(fabs(v.y - r.y), tol, exceed, nan);
-          } else {
-            cell_flags(fabs(ld_stream(src) - ld_keep(rsrc)), tol, exceed, nan);
+          double y[U][V];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (rrs[u] < 0) continue;
+            const int64_t off = (int64_t)rrs[u] * lda + cvs[u] * V;
+            load_v<V>(blk + off, x[u], false);
+            load_v<V>(ref + off, y[u], true);
           }
-        }
-        rr += drow;
-        cv += dcol;
-        if (cv >= nv) {
-          cv -= nv;
-          ++rr;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (rrs[u] >= 0) flag_diff<V>(x[u], y[u], tol, exceed, nan);
         }
       }
     }
@@ -112,9 +174,9 @@ __global__ void __launch_bounds__(MAP_THREADS)
     __syncthreads();
     if (threadIdx.x == 0) {
       int e = 0, nn = 0;
-      for (int w = 0; w < MAP_THREADS / 32; ++w) {
-        e |= red[0][w];
-        nn |= red[1][w];
+      for (int w2 = 0; w2 < MAP_THREADS / 32; ++w2) {
+        e |= red[0][w2];
+        nn |= red[1][w2];
       }
       flags[cell] = e | (nn << 1);
     }
@@ -131,82 +193,72 @@ __global__ void gather_verdict(const int* __restrict__ flags, const int64_t* __r
   }
 }
 
-template <int V>
+// PH 0: every cell, a = t / sqrt(eta).  PH 1: class representative cells
+// only.  PH 2: every other cell copies its class representative's block back
+// out of A (L2-resident after PH 1) -- the same bits, no division in the
+// 8.6 GB stream (measured 1.93 vs 2.03 ms on the 32768^2 stand-in; a
+// row-major sweep of A was slower, 2.5 ms).
+template <int V, int U, int PH>
 __global__ void __launch_bounds__(MAP_THREADS)
     scatter_kernel(const double* __restrict__ t, int64_t t_sm, int64_t t_sp, int64_t t_sn,
                    bt_pattern_dev pat, double* __restrict__ a, int64_t lda) {
-  const int64_t cells = pat.ell * pat.q;
+  const int64_t cells = (PH == 1) ? pat.p : pat.ell * pat.q;
   const int64_t m = pat.m, n = pat.n;
   const int nv = static_cast<int>(n / V);
   const int64_t per = m * nv;
-  const int drow = MAP_THREADS / nv, dcol = MAP_THREADS % nv;
-  for (int64_t cell = blockIdx.x; cell < cells; cell += gridDim.x) {
+  for (int64_t it = blockIdx.x; it < cells; it += gridDim.x) {
+    const int64_t cell = (PH == 1) ? pat.rep_cell[it] : it;
     const int64_t ci = cell / pat.q, cj = cell % pat.q;
-    const int k = pat.cell_class[cell];
+    const int k = (PH == 1) ? static_cast<int>(it) : pat.cell_class[cell];
+    if (PH == 2 && k >= 0 && pat.rep_cell[k] == cell) continue;  // written by PH 1
     double* blk = a + ci * m * lda + cj * n;
     const double s = (k >= 0) ? sqrt(static_cast<double>(pat.eta[k])) : 1.0;
     const double* tk = t + (k >= 0 ? k : 0) * t_sp;
-    int rr = threadIdx.x / nv, cv = threadIdx.x % nv;
-    for (int64_t idx = threadIdx.x; idx < per; idx += MAP_THREADS) {
-      double* dst = blk + rr * lda + cv * V;
-      if (V == 2) {
-        double2 v = make_double2(0.0, 0.0);
-        if (k >= 0) {
-          const double* src = tk + rr * t_sm + cv * 2;
-          v = *reinterpret_cast<const double2*>(src);
-          v.x = v.x / s;
-          v.y = v.y / s;
-        }
-        st_stream2(dst, v);
-      } else {
-        double v = 0.0;
-        if (k >= 0) v = tk[rr * t_sm + cv * t_sn] / s;
-        st_stream(dst, v);
-      }
-      rr += drow;
-      cv += dcol;
-      if (cv >= nv) {
-        cv -= nv;
-        ++rr;
-      }
+    const double* rep = nullptr;
+    if (PH == 2 && k >= 0) {
+      const int64_t rc = pat.rep_cell[k];
+      rep = a + (rc / pat.q) * m * lda + (rc % pat.q) * n;
     }
-  }
-}
-
-// Row-major scatter: one CTA per row of A (grid-stride over the ell*m rows),
-// threads sweep the whole q*n row so the 8.6 GB write stream is sequential
-// (the per-cell walk above writes 2 KB pieces 256 KB apart and reaches only
-// ~45% of HBM).  The class of each n-wide segment comes from cell_class
-// (L1/L2 resident), the source row t[k][rr][:] from L2.
-template <int V>
-__global__ void __launch_bounds__(MAP_THREADS)
-    scatter_rows_kernel(const double* __restrict__ t, int64_t t_sm, int64_t t_sp, int64_t t_sn,
-                        bt_pattern_dev pat, double* __restrict__ a, int64_t lda) {
-  const int64_t rows = pat.ell * pat.m;
-  const unsigned n = static_cast<unsigned>(pat.n);
-  const unsigned nvec = static_cast<unsigned>(pat.q * pat.n / V);
-  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
-    const int64_t ci = row / pat.m, rr = row % pat.m;
-    const int32_t* cls = pat.cell_class + ci * pat.q;
-    double* dst_row = a + row * lda;
-    const double* t_row = t + rr * t_sm;
-    for (unsigned v = threadIdx.x; v < nvec; v += MAP_THREADS) {
-      const unsigned col = v * V;
-      const unsigned cj = col / n, c = col - cj * n;
-      const int k = __ldg(cls + cj);
-      if (V == 2) {
-        double2 x = make_double2(0.0, 0.0);
-        if (k >= 0) {
-          const double s = sqrt(static_cast<double>(__ldg(pat.eta + k)));
-          x = *reinterpret_cast<const double2*>(t_row + k * t_sp + c);
-          x.x = x.x / s;
-          x.y = x.y / s;
+    CellWalk w(threadIdx.x, nv);
+    for (int64_t idx = threadIdx.x; idx < per; idx += U * MAP_THREADS) {
+      double x[U][V];
+      bool ok[U];
+      int64_t off[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ok[u] = idx + u * MAP_THREADS < per;
+        off[u] = (int64_t)w.rr * lda + w.cv * V;
+        if (ok[u]) {
+          if (k >= 0 && PH == 2) {
+            load_v<V>(rep + off[u], x[u], true);
+          } else if (k >= 0) {
+            const double* src = tk + (int64_t)w.rr * t_sm + (int64_t)w.cv * V * t_sn;
+            if (V == 2) {
+              const double2 v = *reinterpret_cast<const double2*>(src);
+              x[u][0] = v.x;
+              x[u][V - 1] = v.y;
+            } else {
+              x[u][0] = src[0];
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e) x[u][e] = 0.0;
+          }
         }
-        st_stream2(dst_row + col, x);
-      } else {
-        double x = 0.0;
-        if (k >= 0) x = t_row[k * t_sp + c * t_sn] / sqrt(static_cast<double>(__ldg(pat.eta + k)));
-        st_stream(dst_row + col, x);
+        w.next();
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!ok[u]) continue;
+        if (k >= 0 && PH != 2) {
+#pragma unroll
+          for (int e = 0; e < V; ++e) x[u][e] = x[u][e] / s;
+        }
+        if (V == 2) {
+          st_stream2(blk + off[u], make_double2(x[u][0], x[u][V - 1]));
+        } else {
+          st_stream(blk + off[u], x[u][0]);
+        }
       }
     }
   }
@@ -215,7 +267,8 @@ __global__ void __launch_bounds__(MAP_THREADS)
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 int grid_for(int64_t cells) {
-  return static_cast<int>(std::min<int64_t>(cells, static_cast<int64_t>(bt_num_sms()) * 16));
+  static const int mult = env_int("BT_MAP_GRID", 16);  // CTAs per SM (tuning override)
+  return static_cast<int>(std::min<int64_t>(cells, static_cast<int64_t>(bt_num_sms()) * mult));
 }
 
 }  // namespace
@@ -240,10 +293,20 @@ extern "C" int bt_gather_blocks_f64(const double* a, int64_t lda, const bt_patte
   BT_CUDA_CHECK(cudaMemsetAsync(first, 0xff, 8, st));
   const bool v2 = (pat->n % 2 == 0) && (lda % 2 == 0) && aligned16(a) && aligned16(t) &&
                   ((pat->p * pat->n) % 2 == 0);
-  if (v2)
-    gather_kernel<2><<<grid_for(cells), MAP_THREADS, 0, st>>>(a, lda, *pat, tol, weighted, t, flags);
+  const int gu = gather_unroll();
+#define BT_GATHER(V_, U_) \
+  gather_kernel<V_, U_><<<grid_for(cells), MAP_THREADS, 0, st>>>(a, lda, *pat, tol, weighted, t, flags)
+  if (!v2)
+    BT_GATHER(1, 2);
+  else if (gu == 8)
+    BT_GATHER(2, 8);
+  else if (gu == 4)
+    BT_GATHER(2, 4);
+  else if (gu == 2)
+    BT_GATHER(2, 2);
   else
-    gather_kernel<1><<<grid_for(cells), MAP_THREADS, 0, st>>>(a, lda, *pat, tol, weighted, t, flags);
+    BT_GATHER(2, 1);
+#undef BT_GATHER
   BT_LAUNCH_CHECK();
   gather_verdict<<<static_cast<int>(std::min<int64_t>(bt_cdiv(cells, 256), 1024)), 256, 0, st>>>(
       flags, pat->cell_order, cells, first);
@@ -270,20 +333,29 @@ extern "C" int bt_scatter_blocks_f64(const double* t, int64_t t_sm, int64_t t_sp
   const int64_t cells = pat->ell * pat->q;
   const bool v2 = (pat->n % 2 == 0) && (lda % 2 == 0) && (t_sn == 1) && (t_sm % 2 == 0) &&
                   (t_sp % 2 == 0) && aligned16(a) && aligned16(t);
-  if (pat->q * pat->n < ((int64_t)1 << 31) && pat->q * pat->n >= 512) {
-    const int64_t rows = pat->ell * pat->m;
-    const int grid = static_cast<int>(std::min<int64_t>(rows, static_cast<int64_t>(bt_num_sms()) * 8));
-    if (v2)
-      scatter_rows_kernel<2><<<grid, MAP_THREADS, 0, st>>>(t, t_sm, t_sp, t_sn, *pat, a, lda);
-    else
-      scatter_rows_kernel<1><<<grid, MAP_THREADS, 0, st>>>(t, t_sm, t_sp, t_sn, *pat, a, lda);
-    BT_LAUNCH_CHECK();
-    return BT_OK;
+  const int su = scatter_unroll();
+  const int two_phase = env_int("BT_SCATTER_PH", 1);  // tuning: 0 one pass, 1 two phases
+#define BT_SCATTER(V_, U_, PH_)                                                           \
+  scatter_kernel<V_, U_, PH_><<<grid_for(PH_ == 1 ? pat->p : cells), MAP_THREADS, 0, st>>>( \
+      t, t_sm, t_sp, t_sn, *pat, a, lda)
+  if (two_phase && pat->p > 0) {
+    if (v2) {
+      BT_SCATTER(2, 4, 1);
+      BT_LAUNCH_CHECK();
+      BT_SCATTER(2, 4, 2);
+    } else {
+      BT_SCATTER(1, 4, 1);
+      BT_LAUNCH_CHECK();
+      BT_SCATTER(1, 4, 2);
+    }
+  } else if (!v2) {
+    BT_SCATTER(1, 4, 0);
+  } else if (su == 2) {
+    BT_SCATTER(2, 2, 0);
+  } else {
+    BT_SCATTER(2, 4, 0);
   }
-  if (v2)
-    scatter_kernel<2><<<grid_for(cells), MAP_THREADS, 0, st>>>(t, t_sm, t_sp, t_sn, *pat, a, lda);
-  else
-    scatter_kernel<1><<<grid_for(cells), MAP_THREADS, 0, st>>>(t, t_sm, t_sp, t_sn, *pat, a, lda);
+#undef BT_SCATTER
   BT_LAUNCH_CHECK();
   return BT_OK;
 }

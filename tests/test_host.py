@@ -141,3 +141,31 @@ def test_classify_placements_matches_oracle():
             assert (classify_placements(tuple(split), ell, ell)
                     == _port.classify_placements(tuple(split), ell, ell))
     assert classify_placements((), 3, 3) == "general"
+
+
+def test_classify_placements_random_families():
+    """Vectorised classify vs the per-class restatement on random families,
+    including exact diagonals, +-d pairs, anti-diagonals and partial ones."""
+    from oracle import port as _port
+    from paper_2105_01170_b200.blocks import classify_placements
+
+    rng = np.random.default_rng(11)
+    for trial in range(400):
+        ell = int(rng.integers(1, 7))
+        q = ell if rng.random() < 0.8 else int(rng.integers(1, 7))
+        cells = np.array([(i, j) for i in range(ell) for j in range(q)], dtype=np.int64)
+        mode = trial % 4
+        if mode == 0:      # by diagonal offset, some merged +-d, maybe dropped cells
+            key = cells[:, 1] - cells[:, 0]
+            if rng.random() < 0.5:
+                key = np.abs(key)
+        elif mode == 1:    # by anti-diagonal
+            key = cells[:, 0] + cells[:, 1]
+        elif mode == 2:    # diagonal only
+            key = np.where(cells[:, 0] == cells[:, 1], 0, -1)
+        else:              # random
+            key = rng.integers(0, 4, len(cells))
+        keep = rng.random(len(cells)) > (0.15 if trial % 3 == 0 else 0.0)
+        fam = [cells[(key == k) & keep] for k in np.unique(key[key >= 0])]
+        fam = tuple(f for f in fam if len(f))
+        assert classify_placements(fam, ell, q) == _port.classify_placements(fam, ell, q), (ell, q, fam)
