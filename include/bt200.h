@@ -276,6 +276,10 @@ int bt_inv_sqrt_f64(const double* x, int64_t n, double* out, void* stream);
 int bt_sign_fix_f64(double* x, int64_t rows, int64_t cols, void* stream);
 /* normalise every column of a row-major (rows x cols) matrix to unit 2-norm */
 int bt_col_normalize_f64(double* x, int64_t rows, int64_t cols, void* stream);
+/* Ritz residual norms out[c] = ||gv[:, c] - theta[c] v[:, c]|| over the first
+ * cols columns of row-major (rows x ld) gv and v. */
+int bt_ritz_resid_f64(const double* gv, const double* v, const double* theta, int64_t rows,
+                      int64_t cols, int64_t ld, double* out, void* stream);
 /* z = alpha * x + beta * y elementwise (n doubles) */
 int bt_axpby_f64(int64_t n, double alpha, const double* x, double beta, const double* y, double* z,
                  void* stream);

@@ -60,6 +60,115 @@ def eigh_dev(gd, nvec: int | None = None, tau: float = -1.0):
 
 
 _DEBUG = bool(os.environ.get("BT_BASIS_DEBUG"))
+SUBSPACE = os.environ.get("BT_SUBSPACE", "1") != "0"
+SUB_OVERSAMPLE = 16
+SUB_MAX_BLOCK = 96     # Rayleigh-Ritz matrices stay on the one-CTA Jacobi path
+SUB_MAX_ITERS = 10
+SUB_RESID = 32.0      # accept a Ritz pair at ||G v - theta v|| <= SUB_RESID eps theta_1
+
+
+def _orth_svqb(y, passes: int = 1, drop: float = 1e3 * np.finfo(np.float64).eps):
+    """Orthonormal basis of the numerically significant part of span(y)
+    (n x b, n >> b) by SVQB: Y^T Y = V diag(mu) V^T (one-CTA Jacobi),
+    Q = Y V_k diag(mu_k)^-1/2 over the mu_k > drop * mu_max.  The dropped
+    directions have singular values below ~sqrt(drop) of the largest (far
+    below what the subspace iteration accepts).  One Newton-Schulz step
+    Q (3I - Q^T Q) / 2 then squares the remaining orthogonality error (GEMMs
+    only).  Returns (q, dropped)."""
+    dropped = 0
+    for _ in range(passes):
+        m = gemm_dev(y, y, ta=True)
+        m = _axpby(0.5, m, 0.5, m.t().contiguous())
+        w, v = eigh_dev(m)                       # descending
+        wh = _dev.to_host(w)
+        if not wh[0] > 0.0:
+            return None, 0
+        keep = int(np.sum(wh > drop * wh[0]))
+        dropped += int(y.shape[1]) - keep
+        s = _dev.empty((keep,))
+        N.call("bt_inv_sqrt_f64", _dev.ptr(w), keep, _dev.ptr(s), _dev.stream())
+        b, rows = int(v.shape[0]), int(y.shape[0])
+        out = _dev.empty((rows, keep))
+        d = N.GemmDesc()
+        d.M, d.N, d.Kin, d.Kout, d.batch = rows, keep, b, 1, 1
+        d.A, d.sAm, d.sAki = _dev.ptr(y), b, 1
+        d.B, d.sBn, d.sBki = _dev.ptr(v), 1, b      # V[:, :keep] addressed in place
+        d.bscale, d.s_scale_ko = _dev.ptr(s), 0
+        d.C, d.sCm, d.sCn = _dev.ptr(out), keep, 1
+        d.alpha, d.beta = 1.0, 0.0
+        ws = _dev.workspace(N.load().bt_gemm_f64_ws_bytes(C.byref(d)))
+        N.call("bt_gemm_f64", C.byref(d), _dev.ptr(ws), int(ws.numel()) * 8, _dev.stream())
+        y = out
+    t = _dev.torch()
+    kq = int(y.shape[1])
+    m = gemm_dev(y, y, ta=True)
+    corr = _axpby(1.5, t.eye(kq, dtype=t.float64, device=m.device), -0.5, m)
+    return gemm_dev(y, corr), dropped
+
+
+def _leading_subspace(gd, need: int, tau: float):
+    """Leading eigenpairs of a symmetric n x n Gram by block subspace
+    iteration with Rayleigh-Ritz (GEMMs + thin QR + the one-CTA Jacobi on
+    the b x b projection), b = min(need, 80) + 16 columns.
+
+    Returns (w, v, k): the b Ritz values (descending, device), Ritz vectors
+    (n x b, sign-normalised) and the count k of leading pairs that are
+    (i) above tau * w[0] and (ii) converged to a residual
+    ||G v - theta v|| <= 32 eps theta_1 -- at most b - 16, so every
+    eigenvalue above the cut is known to be captured.  None when the
+    iteration did not converge (the caller falls back to bt_syevx_f64).
+    Accuracy per accepted pair is the Gram eigensolver's (residual / gap);
+    the deflation passes of mode_basis_dev handle the rest."""
+    n = int(gd.shape[0])
+    b = min(n, min(need, SUB_MAX_BLOCK - SUB_OVERSAMPLE) + SUB_OVERSAMPLE)
+    if b < 2 or b > SUB_MAX_BLOCK or 2 * b > n:
+        return None
+    rng = np.random.default_rng(20210501 + n)
+    q, _ = _orth_svqb(_dev.to_device(rng.standard_normal((n, b))))
+    eps = np.finfo(np.float64).eps
+    prev = None
+    for it in range(SUB_MAX_ITERS):
+        if q is None:
+            return None
+        q, dropped = _orth_svqb(gemm_dev(gd, q))
+        if q is None:
+            return None
+        bq = int(q.shape[1])
+        gq = gemm_dev(gd, q)
+        h = gemm_dev(q, gq, ta=True)
+        h = _axpby(0.5, h, 0.5, h.t().contiguous())   # exact symmetry for Jacobi
+        w, s = eigh_dev(h)                      # b x b, full spectrum, descending
+        v = gemm_dev(q, s)
+        gv = gemm_dev(gq, s)                    # G v = (G q) s
+        res = _dev.empty((bq,))
+        N.call("bt_ritz_resid_f64", _dev.ptr(gv), _dev.ptr(v), _dev.ptr(w), n, bq, bq,
+               _dev.ptr(res), _dev.stream())
+        wh = _dev.to_host(w)
+        rh = _dev.to_host(res)
+        top = float(wh[0])
+        if top <= 0.0:
+            return None
+        # accept at most b - 16 pairs, and never the whole retained block
+        # unless SVQB dropped directions (those sit below ~sqrt(1e3 eps) of
+        # the top, i.e. under the cut, which certifies nothing was missed)
+        k = int(np.sum(wh[:min(need, b - SUB_OVERSAMPLE, bq if dropped else bq - 1)]
+                       > tau * top))
+        worst = float(rh[:max(k, 1)].max())
+        target = SUB_RESID * eps * top
+        if _DEBUG:
+            print(f"[subspace n={n} b={b}] it {it}: k {k} max resid/theta1 "
+                  f"{worst / top:.2e}", file=sys.stderr)
+        if worst <= target:
+            N.call("bt_sign_fix_f64", _dev.ptr(v), n, bq, _dev.stream())
+            return w, v, k
+        if prev is not None and worst > 0.0:
+            rate = worst / prev                    # linear convergence factor
+            left = SUB_MAX_ITERS - 1 - it
+            if rate >= 1.0 or np.log(target / worst) / np.log(max(rate, 1e-300)) > left:
+                return None                        # too slow: the tridiagonal path wins
+        prev = worst
+        q = v
+    return None
 NOISE_REL = 1e-22    # remainder eigenvalue below this * lambda_1 (sigma < 1e-11 sigma_1)
 RESOLVE_TAU = 1e-6   # per pass: eigenvectors with lambda > tau * lambda_max are kept (cut accuracy ~eps/tau)
 
@@ -178,13 +287,18 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
         need = r - have
         if need <= 0:
             break
-        w, v = eigh_dev(g, nvec=need, tau=RESOLVE_TAU)
+        sub = _leading_subspace(g, need, RESOLVE_TAU) if SUBSPACE and n > SMALL_EIG else None
+        if sub is not None:
+            w, v, k_sub = sub
+        else:
+            w, v = eigh_dev(g, nvec=need, tau=RESOLVE_TAU)
+            k_sub = None
         wh = _dev.to_host(w)
         if top is None:
             top = max(float(wh[0]), 0.0)
         if top == 0.0 or wh[0] <= NOISE_REL * top:
             break                                   # remainder negligible: complete
-        k = int(np.sum(wh[:need] > RESOLVE_TAU * wh[0]))
+        k = int(np.sum(wh[:need] > RESOLVE_TAU * wh[0])) if k_sub is None else k_sub
         if _DEBUG:
             print(f"[mode_basis n={n} r={r}] pass: need {need} resolved {k} "
                   f"lambda_top {wh[0]:.3e} ({wh[0] / top:.1e} of first)", file=sys.stderr)

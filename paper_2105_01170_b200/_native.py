@@ -92,6 +92,7 @@ _SIGS = {
                                       _dp, _dp]),
     "bt_block_match_f64": (C.c_int, [_dp, _i64, _i64, _i64, _i64, _i64, _dp, C.c_double, C.c_int,
                                      _dp, _dp]),
+    "bt_ritz_resid_f64": (C.c_int, [_dp, _dp, _dp, _i64, _i64, _i64, _dp, _dp]),
     "bt_cholesky_ws_bytes": (_i64, [_i64]),
     "bt_cholesky_f64": (C.c_int, [_dp, _i64, _dp, _dp, _P(_i64), _dp]),
     "bt_tri_inv_lower_ws_bytes": (_i64, [_i64]),

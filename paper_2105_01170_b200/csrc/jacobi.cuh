@@ -43,9 +43,11 @@ static __device__ __noinline__ int jacobi_smem(double* a, double* qv, int n, int
         const double apq = a[p * ld + q];
         const double app = a[p * ld + p], aqq = a[q * ld + q];
         double c = 1.0, s = 0.0;
-        // rotate unless a_pq is negligible relative to the diagonal pair
+        // rotate unless a_pq is negligible relative to the diagonal pair (the
+        // Demmel-Veselic relative test at working precision; a threshold
+        // below eps is never met by rounding noise and only burns sweeps)
         if (apq != 0.0 && fabs(apq) > abs_tol &&
-            fabs(apq) > 1e-18 * sqrt(fabs(app) * fabs(aqq))) {
+            fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq))) {
           const double theta = (aqq - app) / (2.0 * apq);
           const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
           c = 1.0 / sqrt(t * t + 1.0);
@@ -76,8 +78,9 @@ static __device__ __noinline__ int jacobi_smem(double* a, double* qv, int n, int
         if (s == 0.0) continue;
         const int p = pp[k], q = qq[k];
         double x = a[i * ld + p], y = a[i * ld + q];
-        a[i * ld + p] = c * x - s * y;
-        a[i * ld + q] = s * x + c * y;
+        // the rotated pair's own off-diagonal is zero by construction
+        a[i * ld + p] = (i == q) ? 0.0 : c * x - s * y;
+        a[i * ld + q] = (i == p) ? 0.0 : s * x + c * y;
         x = qv[i * ld + p];
         y = qv[i * ld + q];
         qv[i * ld + p] = c * x - s * y;
@@ -93,3 +96,81 @@ static __device__ __noinline__ int jacobi_smem(double* a, double* qv, int n, int
   return any;
 }
 
+
+// Same cyclic round-robin Jacobi, restructured for latency: one parameter
+// phase and ONE update phase per round.  The update applies both rotations
+// of a round to disjoint 2x2 blocks (pair k1 rows x pair k2 columns: new
+// block = L1 B L2^T), so rows and columns need no separate passes, and the
+// eigenvector accumulator's column pairs are updated in the same phase.
+// Rotate iff |a_pq| > abs_tol and |a_pq| > rel_tol sqrt(|a_pp a_qq|).
+// Works for any blockDim (multiple of 32); callers use 1024 threads.
+static __device__ __noinline__ int jacobi_fast(double* a, double* qv, int n, int ld, double* cs,
+                                               double* sn, int* pp, int* qq, int max_sweeps,
+                                               double abs_tol, double rel_tol) {
+  __shared__ int rotated;
+  const int nt = blockDim.x;
+  const int half = n / 2;
+  int any = 0;
+  for (int idx = threadIdx.x; idx < n * n; idx += nt) {
+    const int r = idx / n, c = idx - r * n;
+    qv[r * ld + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    for (int rnd = 0; rnd < n - 1; ++rnd) {
+      for (int k = threadIdx.x; k < half; k += nt) {
+        int p, q;
+        rr_pair(n, rnd, k, p, q);
+        const double apq = a[p * ld + q];
+        const double app = a[p * ld + p], aqq = a[q * ld + q];
+        double c = 1.0, s = 0.0;
+        if (apq != 0.0 && fabs(apq) > abs_tol && fabs(apq) > rel_tol * sqrt(fabs(app) * fabs(aqq))) {
+          const double theta = (aqq - app) / (2.0 * apq);
+          const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+          c = 1.0 / sqrt(t * t + 1.0);
+          s = t * c;
+          rotated = 1;
+        }
+        cs[k] = c;
+        sn[k] = s;
+        pp[k] = p;
+        qq[k] = q;
+      }
+      __syncthreads();
+      // 2-D thread map (lane -> k2 / row, warp -> k1 / pair): no divisions
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = nt >> 5;
+      for (int k1 = wid; k1 < half; k1 += nw) {
+        const double s1 = sn[k1], c1 = cs[k1];
+        const int p1 = pp[k1], q1 = qq[k1];
+        for (int k2 = lane; k2 < half; k2 += 32) {
+          const double s2 = sn[k2];
+          if (s1 == 0.0 && s2 == 0.0) continue;
+          const double c2 = cs[k2];
+          const int p2 = pp[k2], q2 = qq[k2];
+          const double x11 = a[p1 * ld + p2], x12 = a[p1 * ld + q2];
+          const double x21 = a[q1 * ld + p2], x22 = a[q1 * ld + q2];
+          const double y11 = c1 * x11 - s1 * x21, y12 = c1 * x12 - s1 * x22;
+          const double y21 = s1 * x11 + c1 * x21, y22 = s1 * x12 + c1 * x22;
+          a[p1 * ld + p2] = c2 * y11 - s2 * y12;
+          a[q1 * ld + q2] = s2 * y21 + c2 * y22;
+          a[p1 * ld + q2] = (k1 == k2) ? 0.0 : s2 * y11 + c2 * y12;
+          a[q1 * ld + p2] = (k1 == k2) ? 0.0 : c2 * y21 - s2 * y22;
+        }
+        if (s1 == 0.0) continue;
+        for (int i = lane; i < n; i += 32) {
+          const double x = qv[i * ld + p1], y = qv[i * ld + q1];
+          qv[i * ld + p1] = c1 * x - s1 * y;
+          qv[i * ld + q1] = s1 * x + c1 * y;
+        }
+      }
+      __syncthreads();
+    }
+    const int r = rotated;
+    __syncthreads();
+    if (!r) break;
+    any = 1;
+  }
+  return any;
+}

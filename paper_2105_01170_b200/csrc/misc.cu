@@ -285,6 +285,35 @@ __global__ void bt_col_normalize_kernel(double* __restrict__ x, int64_t rows, in
   }
 }
 
+// out[c] = || gv[:, c] - theta[c] * v[:, c] ||  (Ritz residual norms; one warp per column)
+__global__ void bt_ritz_resid_kernel(const double* __restrict__ gv, const double* __restrict__ v,
+                                     const double* __restrict__ theta, int64_t rows, int64_t cols,
+                                     int64_t ld, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); c < cols;
+       c += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    const double th = theta[c];
+    double s = 0.0;
+    for (int64_t r = lane; r < rows; r += 32) {
+      const double d = fma(-th, v[r * ld + c], gv[r * ld + c]);
+      s = fma(d, d, s);
+    }
+    s = warp_sum(s);
+    if (lane == 0) out[c] = sqrt(s);
+  }
+}
+
+extern "C" int bt_ritz_resid_f64(const double* gv, const double* v, const double* theta,
+                                 int64_t rows, int64_t cols, int64_t ld, double* out, void* stream) {
+  if (rows <= 0 || cols <= 0) return BT_OK;
+  BT_REQUIRE(ld >= cols, BT_E_SHAPE, "ritz_resid: ld < cols");
+  const int64_t blocks = (cols + 7) / 8 < 1024 ? (cols + 7) / 8 : 1024;
+  bt_ritz_resid_kernel<<<static_cast<int>(blocks), 256, 0, bt_stream(stream)>>>(gv, v, theta, rows,
+                                                                                 cols, ld, out);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
 extern "C" int bt_col_normalize_f64(double* x, int64_t rows, int64_t cols, void* stream) {
   if (rows <= 0 || cols <= 0) return BT_OK;
   const int64_t blocks = (cols + 7) / 8 < 1024 ? (cols + 7) / 8 : 1024;
