@@ -69,14 +69,28 @@ __global__ void bt_gemm_reduce_kernel(BtGemmArgs g, int64_t bm, int64_t bn) {
 // launch
 // ---------------------------------------------------------------------------
 
+// Split-K count for grids smaller than one wave (2 CTAs per SM for every
+// config): the smallest split whose CTA count fills its last wave best --
+// e.g. the C3 mode-1 SYRK (36 lower tiles) takes 8 splits = 288 CTAs (97% of
+// the 296 slots), where "ceil(296 / 36) = 9" would spill 28 CTAs into a
+// second, nearly empty wave.
 static int bt_pick_splits(int64_t tiles, int64_t batch, int64_t KT) {
-  const int64_t target = 2 * bt_num_sms();
+  const int64_t slots = 2 * bt_num_sms();
   const int64_t have = tiles * batch;
-  if (have >= target || KT < 8) return 1;
-  int64_t s = (target + have - 1) / have;
-  s = std::min<int64_t>(s, KT / 4);
-  s = std::min<int64_t>(s, 64);
-  return static_cast<int>(std::max<int64_t>(s, 1));
+  if (have >= slots || KT < 8) return 1;
+  int best = 1;
+  double best_eff = static_cast<double>(have) / static_cast<double>(slots);
+  const int64_t smax = std::min<int64_t>(64, KT / 4);
+  for (int64_t s = 2; s <= smax; ++s) {
+    const int64_t n = have * s;
+    const int64_t waves = (n + slots - 1) / slots;
+    const double eff = static_cast<double>(n) / static_cast<double>(waves * slots);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = static_cast<int>(s);
+    }
+  }
+  return best;
 }
 
 template <class Cfg>

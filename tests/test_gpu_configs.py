@@ -114,6 +114,43 @@ def test_c4_reduced_cp_and_ml_matvec():
     assert rel(y, yo) < 1e-9
 
 
+def test_c4_full_size_first_sweep_and_conditioning(golden):
+    """C4 at full size (255^3, R=16): the first two factor updates agree with
+    the oracle to ~1e-13, and the mode-3 normal matrix V3 = (A^T A) o (B^T B)
+    is singular to working precision (cond ~1e18: the smooth PSF has low
+    numerical rank), so from the first mode-3 pinv on the ALS trajectory is
+    decided by rounding -- the reference's own fit history oscillates
+    (tests/golden/c4_oracle_hist.json, tools/c4_oracle_fit.py).  Parity for
+    C4's CP is therefore asserted at the reduced size above."""
+    import json
+    import os
+
+    from scipy.linalg import khatri_rao
+
+    from conftest import GOLDEN
+
+    xo = oc.c4_tensor().reshape(255, 255, 255)
+    x, _ = multilevel.psf_weighted_tensor(torch.from_numpy(oc.c4_psf()).cuda(), grid=128)
+    assert torch.equal(x.reshape(255, 255, 255).cpu(), torch.from_numpy(xo))
+    init = oc.normal_init((255, 255, 255), 16, 2)
+    a, b, c = (f.copy() for f in init)
+    a = port.unfold(xo, 1) @ khatri_rao(c, b) @ np.linalg.pinv((c.T @ c) * (b.T @ b))
+    a /= np.linalg.norm(a, axis=0)
+    b = port.unfold(xo, 2) @ khatri_rao(c, a) @ np.linalg.pinv((c.T @ c) * (a.T @ a))
+    b /= np.linalg.norm(b, axis=0)
+    sv = np.linalg.svd((a.T @ a) * (b.T @ b), compute_uv=False)
+    assert sv[0] / sv[-1] > 1e15
+    saved = decomp._cp_init
+    decomp._cp_init = lambda _t, _r: [f.copy() for f in init]
+    try:
+        res = bt.cp_als(xo, 16, 1, 0.0)
+    finally:
+        decomp._cp_init = saved
+    assert rel(res.rep.y, b) < 1e-12
+    hist = json.load(open(os.path.join(GOLDEN, "c4_oracle_hist.json")))["fit_history"]
+    assert min(hist) < 0.995 and max(hist) > 0.9999   # the reference oscillates
+
+
 def test_c5_like_fit_monotone_and_deterministic():
     I, J, K, r = 256, 192, 128, 16
     x = configs.c5_build(I, J, K, r)
