@@ -354,6 +354,94 @@ def extras_run(torch, budget_s=240.0):
     return out
 
 
+def extras_cpu(budget_s=120.0):
+    """The reference path timed on the host beside each secondary config:
+    the oracle port (numpy restatement of the reference, oracle/port.py) with
+    all host threads, on bounded samples scaled to the full config where the
+    full run would take minutes (stated per entry)."""
+    import numpy as np
+
+    from oracle import configs as oc
+    from oracle import port
+
+    out = {}
+    t_start = time.time()
+
+    def left():
+        return budget_s - (time.time() - t_start)
+
+    def clock(fn):
+        t0 = time.perf_counter()
+        r = fn()
+        return (time.perf_counter() - t0) * 1e3, r
+
+    try:   # C1 full pipeline, full size
+        pat, a = oc.c1_inputs()
+        init = oc.normal_init((32, 32, 32), 8, 0)
+        rhs = np.random.default_rng(1001).standard_normal((1024, 16))
+
+        def c1():
+            t = port.gather(a, pat)
+            res = port.cp_als(t, 8, 50, 0.0, init=lambda _t, _r: [f.copy() for f in init])
+            coeffs, terms = port.kron_from_kruskal(res.x, res.y, res.z)
+            err = np.linalg.norm(a - port.densify_kron(pat, coeffs, terms)) / np.linalg.norm(a)
+            y = np.stack([port.matvec_kron(pat, coeffs, terms, rhs[:, j]) for j in range(16)], 1)
+            return err, y
+
+        out["c1_pipeline_ms"], _ = clock(c1)
+        out["c1_sample"] = "full C1 pipeline (gather, 50 sweeps, Kron sum, error, 16 matvecs)"
+    except Exception as exc:  # pragma: no cover
+        out["c1_error"] = repr(exc)[:200]
+    if left() > 0:
+        try:   # C2 HOSVD full size; BLR matvec: 1 RHS x 64
+            params = oc.c2_markov()
+            pat2, t2 = oc.c2_tensor(params)
+            ms, (core, fac) = clock(lambda: port.hosvd(t2, [32, 400, 32]))
+            out["c2_hosvd_ms"] = ms
+            left_, right_, mids = port.blr_from_tucker(core, fac, pat2.m, pat2.n)
+            x = np.random.default_rng(1002).standard_normal(32768)
+            ms1, _ = clock(lambda: port.matvec_blr(pat2, left_, right_, mids, x))
+            out["c2_matvec64_ms"] = 64 * ms1
+            out["c2_sample"] = "HOSVD full size; BLR matvec timed on 1 RHS, x64"
+        except Exception as exc:  # pragma: no cover
+            out["c2_error"] = repr(exc)[:200]
+    if left() > 0:
+        try:   # C3 ST-HOSVD on the first 64 lags (same u_k), x8
+            _, _, t3 = oc.c3_tensor(side=32, lags=64, lag_scale=512)
+            ms, _ = clock(lambda: port.st_hosvd_shared13(t3, 64, 32))
+            out["c3_st_hosvd_ms"] = 8 * ms
+            out["c3_sample"] = "ST-HOSVD on a (1024, 64, 1024) lag prefix, x8 (extrapolated)"
+            del t3
+        except Exception as exc:  # pragma: no cover
+            out["c3_error"] = repr(exc)[:200]
+    if left() > 0:
+        try:   # C4 one sweep x30
+            x4 = oc.c4_tensor().reshape(255, 255, 255)
+            init4 = oc.normal_init((255, 255, 255), 16, 2)
+            ms, _ = clock(lambda: port.cp_als(x4, 16, 1, 0.0, init=lambda _t, _r: init4))
+            out["c4_cp_ms"] = 30 * ms
+            out["c4_sample"] = "1 ALS sweep x30 (extrapolated)"
+            del x4
+        except Exception as exc:  # pragma: no cover
+            out["c4_error"] = repr(exc)[:200]
+    if left() > 0:
+        try:   # gather stand-in: 8 of 128 block rows (2048 x 32768), x16
+            nb, ell = 256, 128
+            pat, blocks = oc.gather_standin(nb, ell)
+            rows = 8
+            sub = port.Pattern(rows, ell, nb, nb, tuple(c[c[:, 0] < rows] for c in pat.placements))
+            sub = port.Pattern(rows, ell, nb, nb, tuple(c for c in sub.placements if len(c)))
+            a = port.assemble(sub, [blocks[k] for k, c in enumerate(pat.placements)
+                                    if np.any(c[:, 0] < rows)])
+            ms, _ = clock(lambda: port.gather(a, sub))
+            out["gather_standin_ms"] = (ell // rows) * ms
+            out["gather_sample"] = "8 of 128 block rows (2048 x 32768), x16 (extrapolated)"
+        except Exception as exc:  # pragma: no cover
+            out["gather_error"] = repr(exc)[:200]
+    out["cores"] = os.cpu_count()
+    return out
+
+
 def run_bt200(args, rank, world):
     import numpy as np
     import torch
@@ -521,7 +609,15 @@ def run_bt200(args, rank, world):
         except Exception as exc:  # pragma: no cover
             result["cpu_baseline"] = {"value": None, "error": repr(exc)[:300]}
     if not args.no_extras and rank == 0:
-        result["extras"] = extras_run(torch)
+        ex = extras_run(torch)
+        result["extras"] = ex
+        if not args.no_cpu and world == 1:
+            cpu = extras_cpu()
+            result["extras_cpu_reference"] = cpu
+            result["extras_speedup_vs_cpu"] = {
+                k: cpu[k] / ex[k] for k in ("c1_pipeline_ms", "c2_hosvd_ms", "c2_matvec64_ms",
+                                            "c3_st_hosvd_ms", "c4_cp_ms", "gather_standin_ms")
+                if isinstance(cpu.get(k), float) and isinstance(ex.get(k), float) and ex[k] > 0}
     if rank == 0:
         print(json.dumps(result), flush=True)
 
