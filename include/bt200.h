@@ -83,6 +83,11 @@ typedef struct bt_pattern_dev {
   const int64_t* cell_order;
   const int64_t* rep_cell;
   const int64_t* eta;
+  /* optional (may be NULL): the cells of class k are class_cells[class_ptr[k]
+   * .. class_ptr[k+1]) (i*q+j, placement order) -- lets the scatter write a
+   * class's block from one read of its representative */
+  const int64_t* class_ptr;
+  const int64_t* class_cells;
 } bt_pattern_dev;
 
 /* workspace: 2 * ell * q int32 flags + 2 int64 */
@@ -274,6 +279,12 @@ int bt_transpose_check_f64(const double* blocks, int64_t p, int64_t n, const int
 int bt_inv_sqrt_f64(const double* x, int64_t n, double* out, void* stream);
 /* sign rule (decomp.py:176-179) on every column of a row-major matrix */
 int bt_sign_fix_f64(double* x, int64_t rows, int64_t cols, void* stream);
+/* Same rule on x, with every flipped column also flipped in y (yrows x cols):
+ * the u / v pair of svd_truncated (decomp.py:176-179). */
+int bt_sign_fix_pair_f64(double* x, int64_t rows, int64_t cols, double* y, int64_t yrows,
+                         void* stream);
+/* s = sqrt(max(w, 0)) and sinv = 1 / s (1 where s == 0), elementwise. */
+int bt_svals_f64(const double* w, int64_t n, double* s, double* sinv, void* stream);
 /* normalise every column of a row-major (rows x cols) matrix to unit 2-norm */
 int bt_col_normalize_f64(double* x, int64_t rows, int64_t cols, void* stream);
 /* Ritz residual norms out[c] = ||gv[:, c] - theta[c] v[:, c]|| over the first

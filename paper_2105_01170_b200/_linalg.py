@@ -326,26 +326,48 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
     return basis[:, :r].contiguous()
 
 
+def _scaled_gemm(a, b, scale, ta=False):
+    """op(a) @ b @ diag(scale) on the engine (the diagonal rides on B's
+    per-column scale)."""
+    a = a.contiguous()
+    b = b.contiguous()
+    M = int(a.shape[1] if ta else a.shape[0])
+    K = int(a.shape[0] if ta else a.shape[1])
+    Nn = int(b.shape[1])
+    out = _dev.empty((M, Nn))
+    d = N.GemmDesc()
+    d.M, d.N, d.Kin, d.Kout, d.batch = M, Nn, K, 1, 1
+    d.A = _dev.ptr(a)
+    d.sAm, d.sAki = (1, int(a.shape[1])) if ta else (int(a.shape[1]), 1)
+    d.B, d.sBn, d.sBki = _dev.ptr(b), 1, Nn
+    d.bscale, d.s_scale_ko = _dev.ptr(scale), 0
+    d.C, d.sCm, d.sCn = _dev.ptr(out), Nn, 1
+    d.alpha, d.beta = 1.0, 0.0
+    ws = _dev.workspace(N.load().bt_gemm_f64_ws_bytes(C.byref(d)))
+    N.call("bt_gemm_f64", C.byref(d), _dev.ptr(ws), int(ws.numel()) * 8, _dev.stream())
+    return out
+
+
 def svd_truncated_dev(ad, r: int):
-    """(u, s, v) of a matrix on device via the Gram of its short side."""
+    """(u, s, v) of a matrix on device via the Gram of its short side
+    (decomp.py:149-179): eigenpairs of the Gram (sign-normalised), s =
+    sqrt(lambda), the long-side vectors by one engine GEMM scaled by 1/s,
+    and the sign rule on u compensated in v."""
     m, n = int(ad.shape[0]), int(ad.shape[1])
-    t = _dev.torch()
     if m <= n:
         w, uu = eigh_dev(unfold_gram_dev(ad, 1))
         u = uu[:, :r].contiguous()
-        s = t.sqrt(t.clamp(w[:r], min=0.0))
-        v = _gemm_tn(ad, u)                       # a^T u   (n x r)
-        v = v / t.where(s > 0, s, t.ones_like(s))
+        s, sinv = _dev.empty((r,)), _dev.empty((r,))
+        N.call("bt_svals_f64", _dev.ptr(w), r, _dev.ptr(s), _dev.ptr(sinv), _dev.stream())
+        v = _scaled_gemm(ad, u, sinv, ta=True)          # a^T u / s   (n x r)
         return u, s, v
     w, vv = eigh_dev(unfold_gram_dev(ad, 2))
     v = vv[:, :r].contiguous()
-    s = t.sqrt(t.clamp(w[:r], min=0.0))
-    u = _gemm_nn(ad, v) / t.where(s > 0, s, t.ones_like(s))
-    # sign rule on u, compensated in v (decomp.py:176-179)
-    lead = t.argmax(t.abs(u), dim=0)
-    sg = t.sign(u[lead, t.arange(r, device=u.device)])
-    sg = t.where(sg == 0, t.ones_like(sg), sg)
-    return (u * sg).contiguous(), s, (v * sg).contiguous()
+    s, sinv = _dev.empty((r,)), _dev.empty((r,))
+    N.call("bt_svals_f64", _dev.ptr(w), r, _dev.ptr(s), _dev.ptr(sinv), _dev.stream())
+    u = _scaled_gemm(ad, v, sinv)                        # a v / s   (m x r)
+    N.call("bt_sign_fix_pair_f64", _dev.ptr(u), m, r, _dev.ptr(v), n, _dev.stream())
+    return u, s, v
 
 
 def _gemm(a_ptr, M, N_, K, sAm, sAk, b_ptr, sBk, sBn, out):

@@ -36,7 +36,8 @@ class GemmDesc(C.Structure):
 
 class PatternDev(C.Structure):
     _fields_ = [("ell", _i64), ("q", _i64), ("m", _i64), ("n", _i64), ("p", _i64), ("nnz", _i64),
-                ("cell_class", _dp), ("cell_order", _dp), ("rep_cell", _dp), ("eta", _dp)]
+                ("cell_class", _dp), ("cell_order", _dp), ("rep_cell", _dp), ("eta", _dp),
+                ("class_ptr", _dp), ("class_cells", _dp)]
 
 
 class CpProblem(C.Structure):
@@ -92,6 +93,8 @@ _SIGS = {
                                       _dp, _dp]),
     "bt_block_match_f64": (C.c_int, [_dp, _i64, _i64, _i64, _i64, _i64, _dp, C.c_double, C.c_int,
                                      _dp, _dp]),
+    "bt_sign_fix_pair_f64": (C.c_int, [_dp, _i64, _i64, _dp, _i64, _dp]),
+    "bt_svals_f64": (C.c_int, [_dp, _i64, _dp, _dp, _dp]),
     "bt_ritz_resid_f64": (C.c_int, [_dp, _dp, _dp, _i64, _i64, _i64, _dp, _dp]),
     "bt_cholesky_ws_bytes": (_i64, [_i64]),
     "bt_cholesky_f64": (C.c_int, [_dp, _i64, _dp, _dp, _P(_i64), _dp]),

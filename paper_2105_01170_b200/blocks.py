@@ -141,8 +141,10 @@ class BlockPattern:
         np.add.at(row_ptr, rows + 1, 1)
         row_ptr = np.cumsum(row_ptr)
         row_cells = (allc[srt, 1] * max(self.p, 1) + cls[srt]) if nnz else np.zeros(0, np.int64)
+        class_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
         return dict(cell_class=cell_class, cell_order=order, rep_cell=rep, eta=counts,
-                    row_ptr=row_ptr, row_cells=row_cells.astype(np.int64), nnz=nnz)
+                    row_ptr=row_ptr, row_cells=row_cells.astype(np.int64), nnz=nnz,
+                    class_ptr=class_ptr, class_cells=ids.astype(np.int64))
 
     def device(self):
         """Device copies of :meth:`host_maps` (cached) + the ctypes struct."""
@@ -155,7 +157,8 @@ class BlockPattern:
                  for k, v in h.items() if k != "nnz"}
             s = N.PatternDev(self.ell, self.q, self.m, self.n, self.p, h["nnz"],
                              _dev.ptr(d["cell_class"]), _dev.ptr(d["cell_order"]),
-                             _dev.ptr(d["rep_cell"]), _dev.ptr(d["eta"]))
+                             _dev.ptr(d["rep_cell"]), _dev.ptr(d["eta"]),
+                             _dev.ptr(d["class_ptr"]), _dev.ptr(d["class_cells"]))
             cache = (d, s, h)
             object.__setattr__(self, "_dev_cache", cache)
         return cache
@@ -309,7 +312,7 @@ def _scatter_dev(t_dev, sm, sp, sn, pat: BlockPattern, eta_override=None):
     d, s, _ = pat.device()
     if eta_override is not None:
         s = N.PatternDev(s.ell, s.q, s.m, s.n, s.p, s.nnz, s.cell_class, s.cell_order,
-                         s.rep_cell, _dev.ptr(eta_override))
+                         s.rep_cell, _dev.ptr(eta_override), s.class_ptr, s.class_cells)
     out = _dev.empty((pat.ell * pat.m, pat.q * pat.n))
     N.call("bt_scatter_blocks_f64", _dev.ptr(t_dev), sm, sp, sn, C.byref(s), _dev.ptr(out),
            pat.q * pat.n, _dev.stream())

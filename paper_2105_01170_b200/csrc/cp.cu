@@ -17,6 +17,7 @@
 // (DMMA reconstruction tile - X tile) when the identity would lose digits.
 // Every reduction is a fixed-order tree: results are bit-reproducible.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 #include <cmath>
@@ -26,6 +27,7 @@
 #include "jacobi.cuh"
 
 int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, int64_t ws_elems);
+extern "C" const char* bt_last_error(void);
 int64_t bt_gemm_ws_elems(BtGemmArgs g, int64_t batch);
 
 namespace {
@@ -183,6 +185,26 @@ __global__ void __launch_bounds__(256) pinv_kernel(const double* __restrict__ g0
 // parameters by the first NP/2 threads, row and column phases as flat loops
 // with constant-size index math; full sweeps until no rotation happens.
 template <int NP>
+__device__ __forceinline__ void load_v(const double* __restrict__ g0, const double* __restrict__ g1,
+                                       int R, double* a, double& ss) {
+  constexpr int LD = NP + 1;
+  ss = 0.0;
+  for (int idx = threadIdx.x; idx < NP * NP; idx += blockDim.x) {
+    const int r = idx / NP, c = idx % NP;
+    double v = 0.0;
+    if (r < R && c < R) v = g1 ? g0[r * R + c] * g1[r * R + c] : g0[r * R + c];
+    a[r * LD + c] = v;
+    ss = fma(v, v, ss);
+  }
+}
+
+// Vp = pinv(V), V = G0 o G1 (SPD Gram-Hadamard product, R <= NP).
+// Fast path: V^-1 = L^-T L^-1 from a Cholesky factorisation in shared memory
+// (R steps), accepted when the exact 1-norm condition number
+// ||V||_1 ||V^-1||_1 <= 1e12 -- there numpy's pinv (decomp.py:387, cutoff
+// 1e-15 sigma_max) is the inverse and both agree to ~cond * eps.  Otherwise
+// (or on a non-positive pivot) the eigen path: cyclic Jacobi + the pinv cutoff.
+template <int NP>
 __global__ void __launch_bounds__(1024) pinv_fast_kernel(const double* __restrict__ g0,
                                                          const double* __restrict__ g1, int R,
                                                          double* __restrict__ vp) {
@@ -191,22 +213,111 @@ __global__ void __launch_bounds__(1024) pinv_fast_kernel(const double* __restric
   extern __shared__ __align__(16) double smf[];
   double* a = smf;
   double* q = a + NP * LD;
+  double* x = q + NP * LD;
   __shared__ double cs[HALF], sn[HALF];
   __shared__ int pp[HALF], qq[HALF];
   __shared__ double fro_red[32];
-  double ss = 0.0;
-  for (int idx = threadIdx.x; idx < NP * NP; idx += blockDim.x) {
-    const int r = idx / NP, c = idx % NP;
-    double v = 0.0;
-    if (r < R && c < R) v = g1 ? g0[r * R + c] * g1[r * R + c] : g0[r * R + c];
-    a[r * LD + c] = v;
-    ss = fma(v, v, ss);
+  __shared__ int chol_ok;
+  __shared__ double vnorm1, inorm1;
+  const int tid = threadIdx.x;
+  double ss;
+  load_v<NP>(g0, g1, R, a, ss);
+  if (tid == 0) chol_ok = 1;
+  __syncthreads();
+  // ||V||_1 (column sums in parallel) and the working copy of the lower triangle
+  if (tid < 32) {
+    double m = 0.0;
+    for (int c = tid; c < R; c += 32) {
+      double c1 = 0.0;
+      for (int r = 0; r < R; ++r) c1 += fabs(a[r * LD + c]);
+      m = fmax(m, c1);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (tid == 0) vnorm1 = m;
   }
-  // absolute floor 1e-15 ||V||_F: off-diagonals below it are rounding noise
-  // (the reference's SVD-based pinv resolves V only to ~eps ||V|| as well);
-  // without it the relative test chases noise for all 40 sweeps
+  for (int idx = tid; idx < R * R; idx += blockDim.x) {
+    const int r = idx / R, c = idx % R;
+    q[r * LD + c] = a[r * LD + c];
+  }
+  __syncthreads();
+  // Cholesky, one barrier per step: the trailing update uses the unscaled
+  // pivot column (q[i][k] q[j][k] / d) and L's column k goes to x, so no
+  // value read in the phase is written in it
+  const int tx = tid & 31, ty = tid >> 5, ny = blockDim.x >> 5;
+  for (int k = 0; k < R; ++k) {
+    const double d = q[k * LD + k];
+    if (!(d > 0.0)) {
+      chol_ok = 0;  // every thread sees the same d: uniform exit
+      break;
+    }
+    const double rs = 1.0 / sqrt(d), rd = rs * rs;
+    for (int i = k + ty; i < R; i += ny) {
+      const double qik = q[i * LD + k];
+      if (tx == 0) x[i * LD + k] = qik * rs;
+      for (int j = k + 1 + tx; j <= i; j += 32) q[i * LD + j] -= qik * q[j * LD + k] * rd;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (chol_ok) {
+    // Y = L^-1 by right-looking substitution on the identity, one barrier
+    // per step (row k's division is applied one step late, when no thread
+    // reads it any more); Y overwrites q
+    for (int idx = tid; idx < R * R; idx += blockDim.x) {
+      const int r = idx / R, c = idx % R;
+      q[r * LD + c] = (r == c) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int k = 0; k < R; ++k) {
+      const double rk = 1.0 / x[k * LD + k];
+      if (k > 0 && ty == 0) {
+        const double rp = 1.0 / x[(k - 1) * LD + (k - 1)];
+        for (int j = tx; j < R; j += 32) q[(k - 1) * LD + j] *= rp;
+      }
+      for (int i = k + 1 + ty; i < R; i += ny) {
+        const double f = x[i * LD + k] * rk;
+        for (int j = tx; j < R; j += 32) q[i * LD + j] -= f * q[k * LD + j];
+      }
+      __syncthreads();
+    }
+    {
+      const double rl = 1.0 / x[(R - 1) * LD + (R - 1)];
+      for (int j = tid; j < R; j += blockDim.x) q[(R - 1) * LD + j] *= rl;
+    }
+    __syncthreads();
+    // V^-1 = Y^T Y into a (V is reloaded if the eigen path is needed)
+    for (int idx = tid; idx < R * R; idx += blockDim.x) {
+      const int r = idx / R, c = idx % R;
+      const int k0 = r > c ? r : c;
+      double v = 0.0;
+      for (int k = k0; k < R; ++k) v = fma(q[k * LD + r], q[k * LD + c], v);
+      a[r * LD + c] = v;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      double m = 0.0;
+      for (int c = tid; c < R; c += 32) {
+        double c1 = 0.0;
+        for (int r = 0; r < R; ++r) c1 += fabs(a[r * LD + c]);
+        m = fmax(m, c1);
+      }
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (tid == 0) inorm1 = m;
+    }
+    __syncthreads();
+    if (vnorm1 * inorm1 <= 1e12) {
+      for (int idx = tid; idx < R * R; idx += blockDim.x)
+        vp[idx] = a[(idx / R) * LD + idx % R];
+      return;
+    }
+    load_v<NP>(g0, g1, R, a, ss);
+    __syncthreads();
+  }
+  // eigen path.  Absolute floor 1e-15 ||V||_F: off-diagonals below it are
+  // rounding noise (the reference's SVD-based pinv resolves V only to
+  // ~eps ||V|| as well)
   ss = warp_sum(ss);
-  if ((threadIdx.x & 31) == 0) fro_red[threadIdx.x >> 5] = ss;
+  if ((tid & 31) == 0) fro_red[tid >> 5] = ss;
   __syncthreads();
   double fro2 = 0.0;
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) fro2 += fro_red[w];
@@ -285,11 +396,25 @@ struct CpState {
   double* lam;         // R
   double* scal;        // [0] ||X||^2, [1] <X,Xhat>, [2] explicit residual^2, [3] use_explicit
   double* fit_hist;    // max_iters
+  int* iter;           // device sweep index, read by kernels launched with it < 0 (graph replay)
 };
+
+__global__ void set_iter_kernel(int* iter, int v) {
+  if (threadIdx.x == 0) *iter = v;
+}
+__global__ void advance_iter_kernel(int* iter) {
+  if (threadIdx.x == 0) *iter += 1;
+}
 
 // Sum the per-CTA Gram partials (and <F_un, M> partials) of one solve into
 // gbuf = [G_un (R*R), inner, 0] -- the buffer a mode-3-sharded caller sums
 // across ranks before the finish.
+__device__ __forceinline__ double warp_ordered_sum(const double* __restrict__ p, int64_t n) {
+  double s = 0.0;
+  for (int64_t k = threadIdx.x & 31; k < n; k += 32) s += p[k];
+  return warp_sum(s);
+}
+
 __global__ void __launch_bounds__(256)
     gram_reduce_kernel(const double* __restrict__ gram_part, int64_t nparts, int R,
                        const double* __restrict__ inner_part, double* __restrict__ gbuf) {
@@ -298,12 +423,12 @@ __global__ void __launch_bounds__(256)
     for (int64_t p = 0; p < nparts; ++p) s += gram_part[p * R * R + idx];
     gbuf[idx] = s;
   }
-  if (threadIdx.x == 0) {
-    double inner = 0.0;
-    if (inner_part)
-      for (int64_t p = 0; p < nparts; ++p) inner += inner_part[p];
-    gbuf[R * R] = inner;
-    gbuf[R * R + 1] = 0.0;
+  if (threadIdx.x < 32) {
+    const double inner = inner_part ? warp_ordered_sum(inner_part, nparts) : 0.0;
+    if (threadIdx.x == 0) {
+      gbuf[R * R] = inner;
+      gbuf[R * R + 1] = 0.0;
+    }
   }
 }
 
@@ -313,6 +438,7 @@ __global__ void __launch_bounds__(256)
     solve_finish_kernel(const double* __restrict__ gbuf, int R, double* __restrict__ norms,
                         double* __restrict__ gram_out, double* __restrict__ lam, CpState st,
                         int it, int fit_mode) {
+  if (it < 0) it = *st.iter;
   __shared__ double nrm[PINV_MAX_R];
   __shared__ double red[8];
   for (int r = threadIdx.x; r < R; r += blockDim.x) {
@@ -441,15 +567,16 @@ __global__ void __launch_bounds__(Cfg::THREADS)
   }
 }
 
+// Fixed-order warp sum of n partials (lane-strided runs, then a fixed
+// shuffle tree): deterministic, and no 1-thread chain of dependent loads.
 __global__ void residual_reduce_kernel(const double* __restrict__ part, int n,
                                        double* __restrict__ out) {
-  if (threadIdx.x != 0) return;
-  double s = 0.0;
-  for (int k = 0; k < n; ++k) s += part[k];
-  out[0] = s;
+  const double s = warp_ordered_sum(part, n);
+  if (threadIdx.x == 0) out[0] = s;
 }
 
 __global__ void residual_finish_kernel(const double* __restrict__ res2, CpState st, int it) {
+  if (it < 0) it = *st.iter;
   if (threadIdx.x != 0) return;
   if (st.scal[3] == 0.0) return;
   st.scal[2] = res2[0];
@@ -681,14 +808,16 @@ int run_mode3(const Plan& pl, const double* X, const double* A, const double* B,
 
 template <int NP>
 int launch_pinv_fast(const double* g0, const double* g1, int R, double* vp, cudaStream_t st) {
-  constexpr int SM = 2 * NP * (NP + 1) * 8;
+  constexpr int SM = 3 * NP * (NP + 1) * 8;
   static bool attr = false;
   if (!attr) {
     BT_CUDA_CHECK(cudaFuncSetAttribute(pinv_fast_kernel<NP>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
     attr = true;
   }
-  pinv_fast_kernel<NP><<<1, 1024, SM, st>>>(g0, g1, R, vp);
+  // barrier cost grows with the CTA: small systems take small CTAs
+  constexpr int THREADS = NP <= 16 ? 64 : 256;
+  pinv_fast_kernel<NP><<<1, THREADS, SM, st>>>(g0, g1, R, vp);
   BT_LAUNCH_CHECK();
   return BT_OK;
 }
@@ -907,6 +1036,7 @@ extern "C" int bt_cp_state_create(const bt_cp_problem* pb, double* a, double* b,
   S->s.norms = sb + 4 * RR;
   S->s.lam = lam;
   S->s.scal = sb + 4 * RR + S->pl.R;
+  S->s.iter = reinterpret_cast<int*>(S->s.scal + 6);
   cudaError_t e = cudaMallocAsync(&S->dhist, sizeof(double) * max_iters, S->st);
   if (e != cudaSuccess) {
     delete S;
@@ -1008,7 +1138,8 @@ extern "C" int bt_cp_solve(void* state, int mode, const double* m, double* gbuf)
 
 extern "C" int bt_cp_solve_finish(void* state, int mode, int it, const double* gbuf) {
   auto* S = static_cast<bt_cp_state*>(state);
-  BT_REQUIRE(it >= 0 && it < S->max_iters, BT_E_VALUE, "sweep index out of range");
+  // it == -1: take the index from the state's device counter (graph replay)
+  BT_REQUIRE(it >= -1 && it < S->max_iters, BT_E_VALUE, "sweep index out of range");
   const Plan& pl = S->pl;
   const int k = mode - 1;
   const int64_t rows[3] = {pl.I, pl.J, pl.K};
@@ -1096,29 +1227,87 @@ extern "C" int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, doub
   };
   double prev = -INFINITY;
   int it = 0, conv = 0;
+  // one ALS sweep; ix < 0: the kernels take the sweep index from the device
+  // counter (graph replay), which the sweep then advances
+  auto sweep = [&](int ix) -> int {
+    BT_TRY(mark());
+    BT_TRY(bt_cp_mttkrp(h, 1, m1));
+    BT_TRY(mark());
+    BT_TRY(bt_cp_solve(h, 1, m1, gbuf));
+    BT_TRY(bt_cp_solve_finish(h, 1, ix, gbuf));
+    BT_TRY(mark());
+    BT_TRY(bt_cp_mttkrp(h, 2, m2));
+    BT_TRY(mark());
+    BT_TRY(bt_cp_solve(h, 2, m2, gbuf));
+    BT_TRY(bt_cp_solve_finish(h, 2, ix, gbuf));
+    BT_TRY(mark());
+    BT_TRY(bt_cp_mttkrp(h, 3, m3));
+    BT_TRY(mark());
+    BT_TRY(bt_cp_solve(h, 3, m3, gbuf));
+    BT_TRY(bt_cp_solve_finish(h, 3, ix, gbuf));
+    BT_TRY(bt_cp_residual(h, res2));
+    BT_TRY(bt_cp_residual_finish(h, ix, res2));
+    BT_TRY(mark());
+    if (ix < 0) {
+      advance_iter_kernel<<<1, 32, 0, S->st>>>(S->s.iter);
+      BT_LAUNCH_CHECK();
+    }
+    return BT_OK;
+  };
+  // Small problems are launch-latency bound (C1: ~25 launches per sweep of a
+  // few us each): after one eager sweep the sweep is captured once as a CUDA
+  // graph and replayed.  Not used when per-phase events are requested.
+  const bool use_graph = (phase_ms == nullptr) && max_iters >= 3 &&
+                         (double)pl.I * pl.J * pl.K * pl.R <= 1e10 && [] {
+                           const char* e = getenv("BT_CP_GRAPH");
+                           return !(e && e[0] == '0');
+                         }();
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
   do {
     if ((rc = bt_cp_init_local(h, pb->norm_x, ws + pl.off_init)) != BT_OK) break;
     if ((rc = bt_cp_init_finish(h, ws + pl.off_init)) != BT_OK) break;
     for (it = 1; it <= max_iters; ++it) {
       const int ix = it - 1;
-      if ((rc = mark()) != BT_OK) break;
-      if ((rc = bt_cp_mttkrp(h, 1, m1)) != BT_OK) break;
-      if ((rc = mark()) != BT_OK) break;
-      if ((rc = bt_cp_solve(h, 1, m1, gbuf)) != BT_OK) break;
-      if ((rc = bt_cp_solve_finish(h, 1, ix, gbuf)) != BT_OK) break;
-      if ((rc = mark()) != BT_OK) break;
-      if ((rc = bt_cp_mttkrp(h, 2, m2)) != BT_OK) break;
-      if ((rc = mark()) != BT_OK) break;
-      if ((rc = bt_cp_solve(h, 2, m2, gbuf)) != BT_OK) break;
-      if ((rc = bt_cp_solve_finish(h, 2, ix, gbuf)) != BT_OK) break;
-      if ((rc = mark()) != BT_OK) break;
-      if ((rc = bt_cp_mttkrp(h, 3, m3)) != BT_OK) break;
-      if ((rc = mark()) != BT_OK) break;
-      if ((rc = bt_cp_solve(h, 3, m3, gbuf)) != BT_OK) break;
-      if ((rc = bt_cp_solve_finish(h, 3, ix, gbuf)) != BT_OK) break;
-      if ((rc = bt_cp_residual(h, res2)) != BT_OK) break;
-      if ((rc = bt_cp_residual_finish(h, ix, res2)) != BT_OK) break;
-      if ((rc = mark()) != BT_OK) break;
+      if (use_graph && it >= 2) {
+        if (!gexec) {
+          set_iter_kernel<<<1, 32, 0, st>>>(S->s.iter, ix);
+          BT_LAUNCH_CHECK();
+          // capture on a private stream (the caller's may be the legacy
+          // default stream, which cannot be captured); replay on the caller's
+          cudaStream_t cs = nullptr;
+          if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess ||
+              cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            if (cs) cudaStreamDestroy(cs);
+            bt_set_error("cp_als: cannot start the sweep graph capture");
+            rc = BT_E_CUDA;
+            break;
+          }
+          S->st = cs;
+          const int cap_rc = sweep(-1);
+          const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+          S->st = st;
+          cudaStreamDestroy(cs);
+          cudaError_t ei = cudaSuccess;
+          if (cap_rc == BT_OK && ec == cudaSuccess) ei = cudaGraphInstantiate(&gexec, graph, 0);
+          if (cap_rc != BT_OK || ec != cudaSuccess || ei != cudaSuccess) {
+            char inner[512];
+            snprintf(inner, sizeof(inner), "%s", bt_last_error());
+            bt_set_error("cp_als: sweep graph capture failed (rc %d: %s; end %s; instantiate %s)",
+                         cap_rc, inner, cudaGetErrorString(ec), cudaGetErrorString(ei));
+            cudaGetLastError();
+            rc = BT_E_CUDA;
+            break;
+          }
+        }
+        if (cudaGraphLaunch(gexec, st) != cudaSuccess) {
+          bt_set_error("cp_als: graph launch failed");
+          rc = BT_E_CUDA;
+          break;
+        }
+      } else {
+        if ((rc = sweep(ix)) != BT_OK) break;
+      }
       if (tol > 0.0) {
         double fit = 0.0;
         if ((rc = bt_cp_read_fit(h, ix, &fit)) != BT_OK) break;
@@ -1152,6 +1341,8 @@ extern "C" int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, doub
       }
     }
   }
+  if (gexec) cudaGraphExecDestroy(gexec);
+  if (graph) cudaGraphDestroy(graph);
   for (auto e : ev) cudaEventDestroy(e);
   bt_cp_state_destroy(h);
   return rc;

@@ -3,8 +3,9 @@
 // The reference walks the ell x q block grid in Python, hashing each block's
 // bytes (tol == 0) or scanning the class representatives (tol > 0).  Here
 // one HBM pass computes, per grid cell, a 128-bit order-independent digest of
-// the block's bytes (two sums of per-word multiply/xor-shift mixes keyed by
-// the word's position -- any reduction order gives the same bits) and the reference's
+// the block's bytes (a sum of per-word multiply/xor-shift mixes and a sum of
+// position-rotated words, both keyed by the word's position -- any reduction
+// order gives the same bits) and the reference's
 // skip predicate (`blk.any()` for tol == 0, `max|blk| <= tol` for tol > 0,
 // with numpy's NaN semantics).  The host groups equal digests in row-major
 // first-occurrence order; a second pass compares every cell with its class
@@ -81,7 +82,9 @@ __global__ void __launch_bounds__(DT)
           if (ok) {
             const uint64_t w = static_cast<uint64_t>(__double_as_longlong(x[u][e]));
             a1 += mix_lite(w ^ (k1 + e * kK1), 0xbf58476d1ce4e5b9ull);
-            a2 += mix_lite((w + 0x632be59bd9b4e019ull) ^ (k2 + e * kK2), 0x94d049bb133111ebull);
+            // second digest without a multiply: position-rotated word plus key
+            const unsigned rot = (static_cast<unsigned>((idx0 + u * DT) * V + e) & 63u) | 1u;
+            a2 += ((w << rot) | (w >> (64u - rot))) ^ (k2 + e * kK2);
             if (tol == 0.0)
               flag |= (w << 1) != 0;  // not +0.0 / -0.0 (NaN counts as nonzero, like np.any)
             else

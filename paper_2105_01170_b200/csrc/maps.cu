@@ -264,6 +264,75 @@ __global__ void __launch_bounds__(MAP_THREADS)
   }
 }
 
+// Class-major second phase (needs class_ptr/class_cells): work item (k, c)
+// holds chunk c of class k's representative block -- CHUNK vectors, VPT per
+// thread -- in registers, read once from A (written by PH 1), and writes it
+// into every other cell of the class.  The representative is read once per
+// class instead of once per cell, so the write stream no longer evicts the
+// 67 MB of representatives from L2 (ncu: 2.1 GB of DRAM re-reads in the
+// cell-major pass on the 32768^2 stand-in).
+template <int V, int VPT>
+__global__ void __launch_bounds__(MAP_THREADS)
+    scatter_class_kernel(bt_pattern_dev pat, double* __restrict__ a, int64_t lda, int64_t chunks) {
+  constexpr int64_t CHUNK = (int64_t)MAP_THREADS * VPT;
+  const int64_t n = pat.n;
+  const int64_t nv = n / V;
+  const int64_t per = pat.m * nv;
+  for (int64_t item = blockIdx.x; item < pat.p * chunks; item += gridDim.x) {
+    const int64_t k = item / chunks, c = item - k * chunks;
+    const int64_t c0 = pat.class_ptr[k], c1 = pat.class_ptr[k + 1];
+    if (c1 - c0 < 2) continue;  // only the representative itself
+    const int64_t rc = pat.rep_cell[k];
+    const double* rep = a + (rc / pat.q) * pat.m * lda + (rc % pat.q) * n;
+    double x[VPT][V];
+    int64_t off[VPT];
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int64_t v = c * CHUNK + u * MAP_THREADS + threadIdx.x;
+      off[u] = -1;
+      if (v < per) {
+        const int64_t r = v / nv, cv = v - r * nv;
+        off[u] = r * lda + cv * V;
+        load_v<V>(rep + off[u], x[u], false);
+      }
+    }
+    for (int64_t e = c0; e < c1; ++e) {
+      const int64_t cell = pat.class_cells[e];
+      if (cell == rc) continue;
+      double* blk = a + (cell / pat.q) * pat.m * lda + (cell % pat.q) * n;
+#pragma unroll
+      for (int u = 0; u < VPT; ++u) {
+        if (off[u] < 0) continue;
+        if (V == 2)
+          st_stream2(blk + off[u], make_double2(x[u][0], x[u][V - 1]));
+        else
+          st_stream(blk + off[u], x[u][0]);
+      }
+    }
+  }
+}
+
+// zero the uncovered cells (class -1) only
+template <int V>
+__global__ void __launch_bounds__(MAP_THREADS)
+    zero_uncovered_kernel(bt_pattern_dev pat, double* __restrict__ a, int64_t lda) {
+  const int64_t cells = pat.ell * pat.q;
+  const int nv = static_cast<int>(pat.n / V);
+  const int64_t per = pat.m * nv;
+  for (int64_t cell = blockIdx.x; cell < cells; cell += gridDim.x) {
+    if (pat.cell_class[cell] >= 0) continue;
+    double* blk = a + (cell / pat.q) * pat.m * lda + (cell % pat.q) * pat.n;
+    CellWalk w(threadIdx.x, nv);
+    for (int64_t idx = threadIdx.x; idx < per; idx += MAP_THREADS) {
+      if (V == 2)
+        st_stream2(blk + (int64_t)w.rr * lda + w.cv * V, make_double2(0.0, 0.0));
+      else
+        st_stream(blk + (int64_t)w.rr * lda + w.cv, 0.0);
+      w.next();
+    }
+  }
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 int grid_for(int64_t cells) {
@@ -334,10 +403,37 @@ extern "C" int bt_scatter_blocks_f64(const double* t, int64_t t_sm, int64_t t_sp
   const bool v2 = (pat->n % 2 == 0) && (lda % 2 == 0) && (t_sn == 1) && (t_sm % 2 == 0) &&
                   (t_sp % 2 == 0) && aligned16(a) && aligned16(t);
   const int su = scatter_unroll();
-  const int two_phase = env_int("BT_SCATTER_PH", 1);  // tuning: 0 one pass, 1 two phases
+  // tuning: 0 one pass, 1 representatives + class-major copies, 2 cell-major copies
+  const int two_phase = env_int("BT_SCATTER_PH", 1);
 #define BT_SCATTER(V_, U_, PH_)                                                           \
   scatter_kernel<V_, U_, PH_><<<grid_for(PH_ == 1 ? pat->p : cells), MAP_THREADS, 0, st>>>( \
       t, t_sm, t_sp, t_sn, *pat, a, lda)
+  if (two_phase == 1 && pat->p > 0 && pat->class_ptr && pat->class_cells) {
+    // PH 1 (representatives, with the division), class-major copies, zeros
+    constexpr int VPT = 8;
+    const int64_t nvec = pat->m * (pat->n / (v2 ? 2 : 1));
+    const int64_t chunks = bt_cdiv(nvec, (int64_t)MAP_THREADS * VPT);
+    const int grid = static_cast<int>(
+        std::min<int64_t>(pat->p * chunks, static_cast<int64_t>(bt_num_sms()) * 16));
+    if (v2) {
+      BT_SCATTER(2, 4, 1);
+      BT_LAUNCH_CHECK();
+      scatter_class_kernel<2, VPT><<<grid, MAP_THREADS, 0, st>>>(*pat, a, lda, chunks);
+    } else {
+      BT_SCATTER(1, 4, 1);
+      BT_LAUNCH_CHECK();
+      scatter_class_kernel<1, VPT><<<grid, MAP_THREADS, 0, st>>>(*pat, a, lda, chunks);
+    }
+    BT_LAUNCH_CHECK();
+    if (pat->nnz < cells) {
+      if (v2)
+        zero_uncovered_kernel<2><<<grid_for(cells), MAP_THREADS, 0, st>>>(*pat, a, lda);
+      else
+        zero_uncovered_kernel<1><<<grid_for(cells), MAP_THREADS, 0, st>>>(*pat, a, lda);
+      BT_LAUNCH_CHECK();
+    }
+    return BT_OK;
+  }
   if (two_phase && pat->p > 0) {
     if (v2) {
       BT_SCATTER(2, 4, 1);

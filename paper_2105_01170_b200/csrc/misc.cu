@@ -328,7 +328,8 @@ extern "C" int bt_col_normalize_f64(double* x, int64_t rows, int64_t cols, void*
 // ---------------------------------------------------------------------------
 
 __global__ void __launch_bounds__(256) bt_sign_fix_kernel(double* __restrict__ x, int64_t rows,
-                                                          int64_t cols) {
+                                                          int64_t cols, double* __restrict__ y,
+                                                          int64_t yrows) {
   __shared__ double bv[256];
   __shared__ int64_t bi[256];
   for (int64_t c = blockIdx.x; c < cols; c += gridDim.x) {
@@ -357,8 +358,11 @@ __global__ void __launch_bounds__(256) bt_sign_fix_kernel(double* __restrict__ x
     }
     const bool flip = x[bi[0] * cols + c] < 0.0;
     __syncthreads();
-    if (flip)
+    if (flip) {
       for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) x[i * cols + c] = -x[i * cols + c];
+      if (y)  // companion factor flipped with it (v of an SVD, decomp.py:176-179)
+        for (int64_t i = threadIdx.x; i < yrows; i += blockDim.x) y[i * cols + c] = -y[i * cols + c];
+    }
     __syncthreads();
   }
 }
@@ -366,7 +370,35 @@ __global__ void __launch_bounds__(256) bt_sign_fix_kernel(double* __restrict__ x
 extern "C" int bt_sign_fix_f64(double* x, int64_t rows, int64_t cols, void* stream) {
   if (rows <= 0 || cols <= 0) return BT_OK;
   const int64_t g = cols < 4096 ? cols : 4096;
-  bt_sign_fix_kernel<<<static_cast<int>(g), 256, 0, bt_stream(stream)>>>(x, rows, cols);
+  bt_sign_fix_kernel<<<static_cast<int>(g), 256, 0, bt_stream(stream)>>>(x, rows, cols, nullptr, 0);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+extern "C" int bt_sign_fix_pair_f64(double* x, int64_t rows, int64_t cols, double* y,
+                                    int64_t yrows, void* stream) {
+  if (rows <= 0 || cols <= 0) return BT_OK;
+  const int64_t g = cols < 4096 ? cols : 4096;
+  bt_sign_fix_kernel<<<static_cast<int>(g), 256, 0, bt_stream(stream)>>>(x, rows, cols, y, yrows);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+// singular values from Gram eigenvalues: s = sqrt(max(w, 0)), sinv = 1/s (1 where s == 0)
+__global__ void bt_svals_kernel(const double* __restrict__ w, int64_t n, double* __restrict__ s,
+                                double* __restrict__ sinv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = sqrt(fmax(w[i], 0.0));
+    s[i] = v;
+    sinv[i] = v > 0.0 ? 1.0 / v : 1.0;
+  }
+}
+
+extern "C" int bt_svals_f64(const double* w, int64_t n, double* s, double* sinv, void* stream) {
+  if (n <= 0) return BT_OK;
+  bt_svals_kernel<<<static_cast<int>((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024), 256, 0,
+                    bt_stream(stream)>>>(w, n, s, sinv);
   BT_LAUNCH_CHECK();
   return BT_OK;
 }

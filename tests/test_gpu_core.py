@@ -205,6 +205,21 @@ def test_svd_truncated_sign_rule(golden):
     np.testing.assert_allclose(v, z["svd_v"], atol=1e-12)
 
 
+@pytest.mark.parametrize("shape", [(40, 300), (300, 40), (64, 64)])
+def test_svd_truncated_both_sides_vs_oracle(shape):
+    """Gram of the short side either way; the sign rule lands on u and is
+    compensated in v (decomp.py:176-179), as in the oracle's LAPACK SVD."""
+    rng = np.random.default_rng(sum(shape))
+    m, n = shape
+    a = rng.standard_normal((m, 6)) @ np.diag(10.0 ** -np.arange(6)) @ rng.standard_normal((6, n))
+    a += 1e-7 * rng.standard_normal((m, n))
+    u, s, v = bt.svd_truncated(a, 4)
+    uo, so, vo = port.svd_trunc(a, 4)
+    np.testing.assert_allclose(s, so, rtol=1e-10)
+    np.testing.assert_allclose(u, uo, atol=1e-9)
+    np.testing.assert_allclose(v, vo, atol=1e-9)
+
+
 def test_hosvd_golden(golden):
     z = golden("tucker")
     for n in range(int(z["n_hosvd"])):
