@@ -184,6 +184,97 @@ __global__ void __launch_bounds__(MAP_THREADS)
   }
 }
 
+// Split gather, check half: every non-representative cell against its class
+// representative (uncovered cells against zero), U independent 16-byte loads
+// in flight per operand per thread; representative cells are skipped (their
+// flags are zero).  Same flag semantics as gather_kernel.
+template <int V, int U>
+__global__ void __launch_bounds__(MAP_THREADS)
+    gather_check_kernel(const double* __restrict__ a, int64_t lda, bt_pattern_dev pat, double tol,
+                        int* __restrict__ flags) {
+  const int64_t cells = pat.ell * pat.q;
+  const int64_t m = pat.m, n = pat.n;
+  const int nv = static_cast<int>(n / V);
+  const int64_t per = m * nv;
+  __shared__ int red[2][MAP_THREADS / 32];
+  for (int64_t cell = blockIdx.x; cell < cells; cell += gridDim.x) {
+    const int k = pat.cell_class[cell];
+    const int64_t rc = k >= 0 ? pat.rep_cell[k] : -1;
+    if (rc == cell) {  // CTA-uniform
+      if (threadIdx.x == 0) flags[cell] = 0;
+      continue;
+    }
+    const double* blk = a + (cell / pat.q) * m * lda + (cell % pat.q) * n;
+    const double* ref = k >= 0 ? a + (rc / pat.q) * m * lda + (rc % pat.q) * n : nullptr;
+    int exceed = 0, nan = 0;
+    CellWalk w(threadIdx.x, nv);
+    for (int64_t idx = threadIdx.x; idx < per; idx += U * MAP_THREADS) {
+      double x[U][V], y[U][V];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ok[u] = idx + u * MAP_THREADS < per;
+        if (ok[u]) {
+          const int64_t off = (int64_t)w.rr * lda + w.cv * V;
+          load_v<V>(blk + off, x[u], false);
+          if (ref) {
+            load_v<V>(ref + off, y[u], true);
+          } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e) y[u][e] = 0.0;
+          }
+        }
+        w.next();
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (ok[u]) flag_diff<V>(x[u], y[u], tol, exceed, nan);
+    }
+    exceed = __any_sync(0xffffffffu, exceed);
+    nan = __any_sync(0xffffffffu, nan);
+    if ((threadIdx.x & 31) == 0) {
+      red[0][threadIdx.x >> 5] = exceed;
+      red[1][threadIdx.x >> 5] = nan;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int e = 0, nn = 0;
+      for (int w2 = 0; w2 < MAP_THREADS / 32; ++w2) {
+        e |= red[0][w2];
+        nn |= red[1][w2];
+      }
+      flags[cell] = e | (nn << 1);
+    }
+    __syncthreads();
+  }
+}
+
+// Split gather, tensor half: t[:, k, :] = w_k * (representative block of k).
+template <int V>
+__global__ void __launch_bounds__(MAP_THREADS)
+    gather_rep_kernel(const double* __restrict__ a, int64_t lda, bt_pattern_dev pat, int weighted,
+                      double* __restrict__ t) {
+  const int64_t m = pat.m, n = pat.n, p = pat.p;
+  const int64_t nv = n / V;
+  const int64_t per = m * nv;
+  const int64_t total = p * per;
+  for (int64_t g = blockIdx.x * (int64_t)MAP_THREADS + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * MAP_THREADS) {
+    const int64_t k = g / per, v = g - k * per;
+    const int64_t r = v / nv, cv = v - r * nv;
+    const int64_t rc = pat.rep_cell[k];
+    const double wt = weighted ? sqrt(static_cast<double>(pat.eta[k])) : 1.0;
+    const double* src = a + ((rc / pat.q) * m + r) * lda + (rc % pat.q) * n + cv * V;
+    double* dst = t + r * p * n + k * n + cv * V;
+    if (V == 2) {
+      const double2 x = ld_stream2(src);
+      *reinterpret_cast<double2*>(dst) = make_double2(wt * x.x, wt * x.y);
+    } else {
+      dst[0] = wt * ld_stream(src);
+    }
+  }
+}
+
 __global__ void gather_verdict(const int* __restrict__ flags, const int64_t* __restrict__ order,
                                int64_t cells, unsigned long long* __restrict__ first) {
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cells;
@@ -363,6 +454,24 @@ extern "C" int bt_gather_blocks_f64(const double* a, int64_t lda, const bt_patte
   const bool v2 = (pat->n % 2 == 0) && (lda % 2 == 0) && aligned16(a) && aligned16(t) &&
                   ((pat->p * pat->n) % 2 == 0);
   const int gu = gather_unroll();
+  if (env_int("BT_GATHER_SPLIT", 1)) {
+    // check pass (all cells but the representatives) + representative pass
+    if (v2) {
+      gather_check_kernel<2, 4><<<grid_for(cells), MAP_THREADS, 0, st>>>(a, lda, *pat, tol, flags);
+      BT_LAUNCH_CHECK();
+      if (pat->p > 0) {
+        gather_rep_kernel<2><<<bt_num_sms() * 8, MAP_THREADS, 0, st>>>(a, lda, *pat, weighted, t);
+        BT_LAUNCH_CHECK();
+      }
+    } else {
+      gather_check_kernel<1, 4><<<grid_for(cells), MAP_THREADS, 0, st>>>(a, lda, *pat, tol, flags);
+      BT_LAUNCH_CHECK();
+      if (pat->p > 0) {
+        gather_rep_kernel<1><<<bt_num_sms() * 8, MAP_THREADS, 0, st>>>(a, lda, *pat, weighted, t);
+        BT_LAUNCH_CHECK();
+      }
+    }
+  } else {
 #define BT_GATHER(V_, U_) \
   gather_kernel<V_, U_><<<grid_for(cells), MAP_THREADS, 0, st>>>(a, lda, *pat, tol, weighted, t, flags)
   if (!v2)
@@ -377,6 +486,7 @@ extern "C" int bt_gather_blocks_f64(const double* a, int64_t lda, const bt_patte
     BT_GATHER(2, 1);
 #undef BT_GATHER
   BT_LAUNCH_CHECK();
+  }
   gather_verdict<<<static_cast<int>(std::min<int64_t>(bt_cdiv(cells, 256), 1024)), 256, 0, st>>>(
       flags, pat->cell_order, cells, first);
   BT_LAUNCH_CHECK();

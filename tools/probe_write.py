@@ -53,8 +53,8 @@ def main():
     print(json.dumps(res))
     del x, y
     torch.cuda.empty_cache()
-    for ph, plain in (("0", "0"), ("1", "0"), ("2", "0")):
-        env = dict(os.environ, BT_SCATTER_PH=ph, BT_SCATTER_PLAIN=plain)
+    for ph, plain in (("1", "0"), ("1", "1")):
+        env = dict(os.environ, BT_SCATTER_PH=ph, BT_GATHER_SPLIT=plain)
         print(subprocess.run([sys.executable, __file__, "scatter"], env=env, capture_output=True,
                              text=True).stdout.strip())
 
