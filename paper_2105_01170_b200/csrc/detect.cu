@@ -40,10 +40,15 @@ __device__ __forceinline__ void load_vec(const double* p, double* out) {
   }
 }
 
-// per cell: h1, h2 (digest), nz (tol == 0: any word not +-0.0; tol > 0:
-// max|x| > tol or NaN present).  V doubles per access; word e of the block
-// (row-major) is keyed by its position e.
-template <int V>
+__device__ __forceinline__ uint64_t rotl64(uint64_t w, unsigned r) {
+  return (w << r) | (w >> (64u - r));
+}
+
+// per cell: h1, h2 (digest), nz (EXACT, i.e. tol == 0: any word not +-0.0;
+// else max|x| > tol or NaN present).  V doubles per access, keyed by the
+// access's position in the block (row-major); the V words of an access share
+// one multiply in h1.  32-bit walk indices (a block has < 2^31 accesses).
+template <int V, bool EXACT>
 __global__ void __launch_bounds__(DT)
     block_digest_kernel(const double* __restrict__ a, int64_t lda, int64_t ell, int64_t q, int64_t m,
                         int64_t n, double tol, uint64_t* __restrict__ h1, uint64_t* __restrict__ h2,
@@ -51,20 +56,20 @@ __global__ void __launch_bounds__(DT)
   __shared__ uint64_t s1[DT / 32], s2[DT / 32];
   __shared__ int sn[DT / 32];
   const int64_t cells = ell * q;
-  const int64_t nv = n / V;
-  const int64_t per = m * nv;
+  const int nv = static_cast<int>(n / V);
+  const int per = static_cast<int>(m) * nv;
+  const int dr = DT / nv, dc = DT % nv;
   for (int64_t cell = blockIdx.x; cell < cells; cell += gridDim.x) {
     const int64_t ci = cell / q, cj = cell % q;
     const double* blk = a + ci * m * lda + cj * n;
     uint64_t a1 = 0, a2 = 0;
     int flag = 0;
-    int64_t r = threadIdx.x / nv, c = threadIdx.x % nv;
-    const int64_t dr = DT / nv, dc = DT % nv;
-    for (int64_t idx0 = threadIdx.x; idx0 < per; idx0 += DU * DT) {
+    int r = threadIdx.x / nv, c = threadIdx.x % nv;
+    for (int idx0 = threadIdx.x; idx0 < per; idx0 += DU * DT) {
       double x[DU][V];
 #pragma unroll
       for (int u = 0; u < DU; ++u) {  // DU independent loads in flight per thread
-        if (idx0 + u * DT < per) load_vec<V>(blk + r * lda + c * V, x[u]);
+        if (idx0 + u * DT < per) load_vec<V>(blk + (int64_t)r * lda + c * V, x[u]);
         r += dr;
         c += dc;
         if (c >= nv) {
@@ -72,27 +77,26 @@ __global__ void __launch_bounds__(DT)
           ++r;
         }
       }
-      // position keys pos*K by addition (one multiply per DU*V words)
-      uint64_t k1 = static_cast<uint64_t>(idx0 * V) * kK1, k2 = static_cast<uint64_t>(idx0 * V) * kK2;
+      const uint64_t kbase = static_cast<uint64_t>(idx0) * kK1;  // one multiply per DU accesses
 #pragma unroll
       for (int u = 0; u < DU; ++u) {
-        const bool ok = idx0 + u * DT < per;
-#pragma unroll
-        for (int e = 0; e < V; ++e) {
-          if (ok) {
-            const uint64_t w = static_cast<uint64_t>(__double_as_longlong(x[u][e]));
-            a1 += mix_lite(w ^ (k1 + e * kK1), 0xbf58476d1ce4e5b9ull);
-            // second digest without a multiply: position-rotated word plus key
-            const unsigned rot = (static_cast<unsigned>((idx0 + u * DT) * V + e) & 63u) | 1u;
-            a2 += ((w << rot) | (w >> (64u - rot))) ^ (k2 + e * kK2);
-            if (tol == 0.0)
-              flag |= (w << 1) != 0;  // not +0.0 / -0.0 (NaN counts as nonzero, like np.any)
-            else
-              flag |= !(fabs(x[u][e]) <= tol);  // NaN or |x| > tol
-          }
+        const int pos = idx0 + u * DT;
+        if (pos >= per) continue;
+        const uint64_t k1 = kbase + static_cast<uint64_t>(u) * (static_cast<uint64_t>(DT) * kK1);
+        const uint64_t w0 = static_cast<uint64_t>(__double_as_longlong(x[u][0]));
+        const uint64_t w1 = static_cast<uint64_t>(__double_as_longlong(x[u][V - 1]));
+        const uint64_t z = (V == 2) ? (w0 ^ k1) + rotl64(w1 ^ kK2, 29) : (w0 ^ k1);
+        a1 += mix_lite(z, 0xbf58476d1ce4e5b9ull);
+        const unsigned rot = (static_cast<unsigned>(pos) & 63u) | 1u;
+        a2 += rotl64(w0, rot) ^ k1;
+        if (V == 2) a2 += rotl64(w1, rot ^ 62u) + k1;
+        if (EXACT) {
+          flag |= (w0 << 1) != 0;  // not +0.0 / -0.0 (NaN counts as nonzero, like np.any)
+          if (V == 2) flag |= (w1 << 1) != 0;
+        } else {
+          flag |= !(fabs(x[u][0]) <= tol);  // NaN or |x| > tol
+          if (V == 2) flag |= !(fabs(x[u][V - 1]) <= tol);
         }
-        k1 += kK1 * (DT * V);
-        k2 += kK2 * (DT * V);
       }
     }
 #pragma unroll
@@ -205,12 +209,21 @@ extern "C" int bt_block_digest_f64(const double* a, int64_t lda, int64_t ell, in
                                    void* stream) {
   BT_REQUIRE(ell >= 1 && q >= 1 && m >= 1 && n >= 1, BT_E_SHAPE, "digest: empty grid");
   BT_REQUIRE(lda >= q * n, BT_E_SHAPE, "digest: lda too small");
-  if (vec2_ok(a, lda, n))
-    block_digest_kernel<2><<<grid_cells(ell * q), DT, 0, bt_stream(stream)>>>(a, lda, ell, q, m, n,
-                                                                             tol, h1, h2, nz);
-  else
-    block_digest_kernel<1><<<grid_cells(ell * q), DT, 0, bt_stream(stream)>>>(a, lda, ell, q, m, n,
-                                                                             tol, h1, h2, nz);
+  BT_REQUIRE(m * (n / (vec2_ok(a, lda, n) ? 2 : 1)) < ((int64_t)1 << 31), BT_E_SHAPE,
+             "digest: block too large");
+  const int grid = grid_cells(ell * q);
+  cudaStream_t st = bt_stream(stream);
+  if (vec2_ok(a, lda, n)) {
+    if (tol == 0.0)
+      block_digest_kernel<2, true><<<grid, DT, 0, st>>>(a, lda, ell, q, m, n, tol, h1, h2, nz);
+    else
+      block_digest_kernel<2, false><<<grid, DT, 0, st>>>(a, lda, ell, q, m, n, tol, h1, h2, nz);
+  } else {
+    if (tol == 0.0)
+      block_digest_kernel<1, true><<<grid, DT, 0, st>>>(a, lda, ell, q, m, n, tol, h1, h2, nz);
+    else
+      block_digest_kernel<1, false><<<grid, DT, 0, st>>>(a, lda, ell, q, m, n, tol, h1, h2, nz);
+  }
   BT_LAUNCH_CHECK();
   return BT_OK;
 }
