@@ -454,7 +454,8 @@ extern "C" int bt_gather_blocks_f64(const double* a, int64_t lda, const bt_patte
   const bool v2 = (pat->n % 2 == 0) && (lda % 2 == 0) && aligned16(a) && aligned16(t) &&
                   ((pat->p * pat->n) % 2 == 0);
   const int gu = gather_unroll();
-  if (env_int("BT_GATHER_SPLIT", 1)) {
+  const int split = env_int("BT_GATHER_SPLIT", 1);
+  if (split) {
     // check pass (all cells but the representatives) + representative pass
     if (v2) {
       gather_check_kernel<2, 4><<<grid_for(cells), MAP_THREADS, 0, st>>>(a, lda, *pat, tol, flags);

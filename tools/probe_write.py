@@ -38,7 +38,7 @@ def main():
                           "gather_u": os.environ.get("BT_GATHER_U"),
                           "scatter_u": os.environ.get("BT_SCATTER_U"),
                           "ph": os.environ.get("BT_SCATTER_PH"),
-                          "plain": os.environ.get("BT_SCATTER_PLAIN"),
+                          "gather_split": os.environ.get("BT_GATHER_SPLIT"),
                           "scatter_ms": ms, "scatter_gbs": nb / ms / 1e6,
                           "gather_ms": mg, "gather_gbs": nb / mg / 1e6}))
         return
@@ -53,7 +53,7 @@ def main():
     print(json.dumps(res))
     del x, y
     torch.cuda.empty_cache()
-    for ph, plain in (("1", "0"), ("1", "1")):
+    for ph, plain in (("1", "1"), ("1", "2")):
         env = dict(os.environ, BT_SCATTER_PH=ph, BT_GATHER_SPLIT=plain)
         print(subprocess.run([sys.executable, __file__, "scatter"], env=env, capture_output=True,
                              text=True).stdout.strip())
