@@ -283,6 +283,10 @@ int bt_sign_fix_f64(double* x, int64_t rows, int64_t cols, void* stream);
  * the u / v pair of svd_truncated (decomp.py:176-179). */
 int bt_sign_fix_pair_f64(double* x, int64_t rows, int64_t cols, double* y, int64_t yrows,
                          void* stream);
+/* Container payload layout (container.py:111-159): out = x's elements in
+ * first-index-fastest order (the C-order array of the axis-reversed tensor),
+ * rank 1..6; the same call with the reversed extents inverts it. */
+int bt_reverse_axes_f64(const double* x, const int64_t* dims, int ndim, double* out, void* stream);
 /* s = sqrt(max(w, 0)) and sinv = 1 / s (1 where s == 0), elementwise. */
 int bt_svals_f64(const double* w, int64_t n, double* s, double* sinv, void* stream);
 /* normalise every column of a row-major (rows x cols) matrix to unit 2-norm */

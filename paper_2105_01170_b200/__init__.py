@@ -15,14 +15,16 @@ from .decomp import (CpResult, KruskalRep, SketchConfig, TuckerRep, cholesky, cp
                      hosvd, qr_thin, st_hosvd, svd_truncated, tucker_partial)
 from .errors import (ContainerExtentError, ContainerFormatError, ConvergenceError,
                      NotPositiveDefiniteError, PatternMismatchError, ShapeError)
-from .multilevel import (MlKronTerm, MultilevelPattern, ml_kron_sum_from_kruskal,
-                         ml_kron_sum_from_tucker, ml_matvec, psf_weighted_tensor)
+from .multilevel import (MlKronTerm, MultilevelPattern, MultilevelTuckerRep,
+                         ml_kron_sum_from_kruskal, ml_kron_sum_from_tucker, ml_matvec,
+                         psf_weighted_tensor)
 from .psd import (SpdRep, SpsdRep, check_transpose_closed, spd_compress, spsd_compress,
                   spsd_compress_blocks)
 from .reconstruct import (BlockLowRankRep, FlopCounter, KronSumRep, TuckerBlockRep,
                           blr_from_kruskal, blr_from_tucker, densify, error_fro,
                           kron_sum_from_kruskal, kron_sum_from_tucker, matvec)
 from .tensor import fold, fro_norm, mode_multiply, squeeze, twist, unfold
-from . import decomp, multilevel, parallel, psd, reconstruct  # noqa: F401  (module access)
+from .container import container_kind, container_read, container_write
+from . import container, decomp, multilevel, parallel, psd, reconstruct  # noqa: F401
 
 __version__ = "0.1.0"

@@ -417,3 +417,50 @@ extern "C" int bt_inv_sqrt_f64(const double* x, int64_t n, double* out, void* st
   BT_LAUNCH_CHECK();
   return BT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// axis reversal (container payloads, container.py:111-159): out is the
+// C-order array of the axis-reversed tensor, i.e. x's elements in
+// first-index-fastest order.  Applying it to that result with the reversed
+// extents gives x back.  One thread per output element, coalesced writes.
+// ---------------------------------------------------------------------------
+
+struct RevDims {
+  int64_t d[6];
+  int64_t stride[6];  // input strides (C order) of axis k
+  int nd;
+};
+
+__global__ void bt_reverse_axes_kernel(const double* __restrict__ x, RevDims rd, int64_t total,
+                                       double* __restrict__ out) {
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    // output index is F-order over the input axes: axis 0 fastest
+    int64_t rem = o, off = 0;
+    for (int k = 0; k < rd.nd; ++k) {
+      const int64_t i = rem % rd.d[k];
+      rem /= rd.d[k];
+      off += i * rd.stride[k];
+    }
+    out[o] = x[off];
+  }
+}
+
+extern "C" int bt_reverse_axes_f64(const double* x, const int64_t* dims, int ndim, double* out,
+                                   void* stream) {
+  BT_REQUIRE(ndim >= 1 && ndim <= 6, BT_E_SHAPE, "reverse_axes: rank %d outside 1..6", ndim);
+  RevDims rd;
+  rd.nd = ndim;
+  int64_t total = 1;
+  for (int k = ndim - 1; k >= 0; --k) {
+    BT_REQUIRE(dims[k] >= 0, BT_E_SHAPE, "reverse_axes: negative extent");
+    rd.d[k] = dims[k];
+    rd.stride[k] = total;
+    total *= dims[k];
+  }
+  if (total == 0) return BT_OK;
+  const int64_t blocks = (total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096;
+  bt_reverse_axes_kernel<<<static_cast<int>(blocks), 256, 0, bt_stream(stream)>>>(x, rd, total, out);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}

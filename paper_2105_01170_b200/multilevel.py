@@ -27,7 +27,8 @@ from .errors import ShapeError
 from .tensor import ttm_dev
 
 __all__ = ["MultilevelPattern", "MlKronTerm", "ml_kron_sum_from_tucker",
-           "ml_kron_sum_from_kruskal", "ml_matvec", "psf_weighted_tensor", "MAX_LEVELS"]
+           "ml_kron_sum_from_kruskal", "ml_matvec", "psf_weighted_tensor", "MAX_LEVELS",
+           "MultilevelTuckerRep"]
 
 MAX_LEVELS = 3  # multilevel.py:40
 
@@ -70,6 +71,59 @@ class MultilevelPattern:
     @property
     def shape(self) -> tuple:
         return self.levels[0].shape
+
+
+@dataclass(frozen=True)
+class MultilevelTuckerRep:
+    """multilevel.py:156-183: a level chain with the Tucker factorization of
+    its weighted order-(L+2) tensor."""
+
+    pattern: MultilevelPattern
+    tucker: object
+
+    def __post_init__(self) -> None:
+        if self.tucker.dims != self.pattern.dims:
+            raise ShapeError(f"tucker dims {self.tucker.dims} != pattern dims {self.pattern.dims}")
+
+    @property
+    def shape(self) -> tuple:
+        return self.pattern.shape
+
+    def terms(self):
+        return ml_kron_sum_from_tucker(self.tucker, self.pattern)
+
+    def densify(self):
+        """multilevel.py:177-183: ml_tensor_to_mat of the reconstructed
+        tensor, as K2 scatters from the innermost level outwards (each level's
+        assembled matrices are the next level's class items)."""
+        from .blocks import _scatter_dev
+        from .reconstruct import DENSIFY_LIMIT
+
+        rows, cols = self.pattern.shape
+        if rows * cols > DENSIFY_LIMIT:
+            raise ShapeError(f"dense result would hold {rows * cols} entries (limit {DENSIFY_LIMIT})")
+        t = _dev.torch()
+        x = _dev.to_device(self.tucker.reconstruct())          # (m, p1, ..., pL, n)
+        levels = self.pattern.levels
+        depth = len(levels)
+        # items[prefix] = (M, p_t, N) tensor of level t, prefix over outer classes
+        outer = [range(lv.p) for lv in levels[:-1]]
+        mats = {}
+        for prefix in product(*outer):
+            idx = (slice(None),) + tuple(prefix) + (slice(None), slice(None))
+            items = x[idx]                                       # (m, pL, n) view
+            sm, sp, sn = (int(v) for v in items.stride())
+            pat = levels[-1]
+            mats[prefix] = _scatter_dev(items, sm, sp, sn, pat)
+        for lvl in range(depth - 2, -1, -1):
+            pat = levels[lvl]
+            nxt = {}
+            for prefix in product(*outer[:lvl]):
+                items = t.stack([mats[prefix + (k,)] for k in range(pat.p)], dim=1).contiguous()
+                sm, sp, sn = (int(v) for v in items.stride())
+                nxt[prefix] = _scatter_dev(items, sm, sp, sn, pat)
+            mats = nxt
+        return _dev.like_input(self.tucker.core, mats[()])
 
 
 @dataclass(frozen=True)

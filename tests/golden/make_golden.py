@@ -369,6 +369,40 @@ def detect_cases():
         json.dump(meta, fh, indent=1)
 
 
+def container_cases():
+    """container.py writer output for every representation kind, from seeded
+    inputs; the device reader/writer must reproduce these bytes."""
+    from blockten.decomp import tucker_partial
+    from blockten.multilevel import MultilevelTuckerRep, ml_mat_to_tensor, ml_tensor_to_mat
+    from blockten.psd import spd_compress, spsd_compress
+    from blockten.reconstruct import TuckerBlockRep, blr_from_tucker, kron_sum_from_tucker
+
+    root = os.path.join(OUT, "containers")
+    os.makedirs(root, exist_ok=True)
+    rng = np.random.default_rng(61)
+    pat = bt.build_pattern("toeplitz", 4, 4, 3, 5)
+    a = bt.struct_assemble(pat, rng.standard_normal((pat.p, 3, 5)))
+    tk = bt.hosvd(bt.mat_to_tensor(a, pat), [3, 5, 4])
+    bt.container_write(os.path.join(root, "kron_sum.btc"), kron_sum_from_tucker(tk, pat),
+                       seed=7, ranks=(3, 5, 4))
+    bt.container_write(os.path.join(root, "blr.btc"), blr_from_tucker(tk, pat))
+    patb = bt.build_pattern("banded", 5, 5, 2, 3, band=1)
+    ab = bt.struct_assemble(patb, rng.standard_normal((patb.p, 2, 3)))
+    tkp = tucker_partial(bt.mat_to_tensor(ab, patb), [None, 3, None])
+    bt.container_write(os.path.join(root, "tucker_raw.btc"), TuckerBlockRep(pattern=patb, tucker=tkp))
+    pat_s, a_s = oc.spd_toeplitz(62, 3, 4)
+    pat_s = bt.build_pattern("toeplitz", 3, 3, 4, 4)
+    bt.container_write(os.path.join(root, "spsd.btc"), spsd_compress(a_s, pat_s, 3))
+    bt.container_write(os.path.join(root, "spd.btc"), spd_compress(a_s, pat_s, 2))
+    inner = bt.build_pattern("banded", 3, 3, 2, 2, band=1)
+    outer = bt.build_pattern("hankel", 2, 2, inner.shape[0], inner.shape[1])
+    mlp = bt.MultilevelPattern(levels=(outer, inner))
+    tm = rng.standard_normal(mlp.dims)
+    am = ml_tensor_to_mat(tm, mlp)
+    tkm = bt.hosvd(ml_mat_to_tensor(am, mlp), [2, 3, 3, 2])
+    bt.container_write(os.path.join(root, "multilevel.btc"), MultilevelTuckerRep(pattern=mlp, tucker=tkm))
+
+
 if __name__ == "__main__":
     np.seterr(all="ignore")
     patterns()
@@ -379,5 +413,6 @@ if __name__ == "__main__":
     psf_cases()
     spd_cases()
     detect_cases()
+    container_cases()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
