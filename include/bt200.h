@@ -287,6 +287,11 @@ int bt_sign_fix_pair_f64(double* x, int64_t rows, int64_t cols, double* y, int64
  * first-index-fastest order (the C-order array of the axis-reversed tensor),
  * rank 1..6; the same call with the reversed extents inverts it. */
 int bt_reverse_axes_f64(const double* x, const int64_t* dims, int ndim, double* out, void* stream);
+/* out[i][j] = left[i] x[i][j] right[j] (left / right may be NULL). */
+int bt_diag_scale_f64(const double* x, int64_t rows, int64_t cols, const double* left,
+                      const double* right, double* out, void* stream);
+/* out[c] = ||x[:, c]||_2 of a row-major rows x cols matrix. */
+int bt_col_norms_f64(const double* x, int64_t rows, int64_t cols, double* out, void* stream);
 /* s = sqrt(max(w, 0)) and sinv = 1 / s (1 where s == 0), elementwise. */
 int bt_svals_f64(const double* w, int64_t n, double* s, double* sinv, void* stream);
 /* normalise every column of a row-major (rows x cols) matrix to unit 2-norm */

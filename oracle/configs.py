@@ -251,6 +251,14 @@ def detect_cases():
     return out
 
 
+def era_system(seed, d=6, n_out=2, n_in=2, rho=0.9):
+    """Seeded stable LTI system for the ERA cases (spectral radius rho)."""
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((d, d))
+    a *= rho / np.max(np.abs(np.linalg.eigvals(a)))
+    return a, rng.standard_normal((d, n_in)), rng.standard_normal((n_out, d))
+
+
 def gather_standin(nb=256, ell=128):
     x = np.linspace(0.0, 1.0, nb)
     base = np.exp(-((x[:, None] - x[None, :]) ** 2) / (2 * 0.1**2))

@@ -541,6 +541,40 @@ def classify_placements(placements, ell, q):
     return "general"
 
 
+def markov_from_lti(a, b, c, count):
+    """apps.py:105-114."""
+    out = np.empty((count, c.shape[0], b.shape[1]))
+    x = b.copy()
+    for k in range(count):
+        out[k] = c @ x
+        x = a @ x
+    return out
+
+
+def era_identify(params, ranks, order, tera=False):
+    """apps.py:153-237 -> (a, b, c, sing_vals, reduced, u, w)."""
+    s = (params.shape[0] + 1) // 2
+    pat = make_pattern("hankel", s, s, params.shape[1], params.shape[2])
+    r1, r2, r3 = ranks
+    t = np.transpose(params, (1, 0, 2)).copy()
+    rp = Pattern(pat.ell, pat.q, r1, r3, pat.placements)
+    if tera:
+        u = mode_basis(unfold(t, 1), r1)
+        w = mode_basis(unfold(t, 3), r3)
+        reduced = assemble(rp, [u.T @ h @ w for h in params])
+    else:
+        t *= np.sqrt(np.asarray(pat.counts, dtype=np.float64))[None, :, None]
+        core, (u, v, w) = hosvd(t, [r1, r2, r3])
+        items = np.einsum("kj,ajb->kab", v, core)
+        reduced = expand(rp, items)
+    su, sv, svt = np.linalg.svd(reduced, full_matrices=False)
+    root = np.sqrt(sv[:order])
+    theta = su[:, :order] * root
+    gamma_t = root[:, None] * svt[:order]
+    a_til = np.linalg.lstsq(theta[: r1 * (s - 1)], theta[r1:], rcond=None)[0]
+    return a_til, gamma_t[:, :r3] @ w.T, u @ theta[:r1], sv, reduced, u, w
+
+
 def detect_pattern(a, m, n, tol=0.0):
     """blocks.py:266-329: row-major scan; tol == 0 groups by the block's bytes
     (all-zero blocks skipped), tol > 0 joins the first representative within

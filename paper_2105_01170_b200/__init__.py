@@ -25,6 +25,8 @@ from .reconstruct import (BlockLowRankRep, FlopCounter, KronSumRep, TuckerBlockR
                           kron_sum_from_kruskal, kron_sum_from_tucker, matvec)
 from .tensor import fold, fro_norm, mode_multiply, squeeze, twist, unfold
 from .container import container_kind, container_read, container_write
-from . import container, decomp, multilevel, parallel, psd, reconstruct  # noqa: F401
+from .apps import (EraResult, LtiSystem, MarkovSequence, era_identify_compressed,
+                   hankel_pattern_from_markov, markov_from_lti)
+from . import apps, container, decomp, multilevel, parallel, psd, reconstruct  # noqa: F401
 
 __version__ = "0.1.0"

@@ -464,3 +464,50 @@ extern "C" int bt_reverse_axes_f64(const double* x, const int64_t* dims, int ndi
   BT_LAUNCH_CHECK();
   return BT_OK;
 }
+
+// out[i][j] = left[i] * x[i][j] * right[j] (either scale may be null) -- the
+// diagonal similarity of the ERA shift solve (apps.py:216-218)
+__global__ void bt_diag_scale_kernel(const double* __restrict__ x, int64_t rows, int64_t cols,
+                                     const double* __restrict__ left,
+                                     const double* __restrict__ right, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * cols;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / cols, j = e % cols;
+    double v = x[e];
+    if (left) v = left[i] * v;
+    if (right) v = v * right[j];
+    out[e] = v;
+  }
+}
+
+extern "C" int bt_diag_scale_f64(const double* x, int64_t rows, int64_t cols, const double* left,
+                                 const double* right, double* out, void* stream) {
+  if (rows <= 0 || cols <= 0) return BT_OK;
+  const int64_t n = rows * cols;
+  bt_diag_scale_kernel<<<static_cast<int>((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0,
+                         bt_stream(stream)>>>(x, rows, cols, left, right, out);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+// out[c] = || x[:, c] || for a row-major rows x cols matrix (one warp per column)
+__global__ void bt_col_norms_kernel(const double* __restrict__ x, int64_t rows, int64_t cols,
+                                    double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); c < cols;
+       c += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    double s = 0.0;
+    for (int64_t r = lane; r < rows; r += 32) s = fma(x[r * cols + c], x[r * cols + c], s);
+    s = warp_sum(s);
+    if (lane == 0) out[c] = sqrt(s);
+  }
+}
+
+extern "C" int bt_col_norms_f64(const double* x, int64_t rows, int64_t cols, double* out,
+                                void* stream) {
+  if (rows <= 0 || cols <= 0) return BT_OK;
+  const int64_t blocks = (cols + 7) / 8 < 1024 ? (cols + 7) / 8 : 1024;
+  bt_col_norms_kernel<<<static_cast<int>(blocks), 256, 0, bt_stream(stream)>>>(x, rows, cols, out);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}

@@ -403,6 +403,34 @@ def container_cases():
     bt.container_write(os.path.join(root, "multilevel.btc"), MultilevelTuckerRep(pattern=mlp, tucker=tkm))
 
 
+ERA_CASES = (  # (name, system seed, d, n_out, n_in, s, ranks, order, tera)
+    ("full", 71, 6, 2, 2, 20, (2, 39, 2), 6, False),
+    ("cut", 72, 5, 3, 2, 16, (3, 12, 2), 5, False),
+    ("tera", 73, 4, 3, 3, 12, (2, 0, 2), 4, True),
+    ("siso", 74, 2, 1, 1, 10, (1, 19, 1), 2, False),
+)
+
+
+def era_cases():
+    """apps.py:153-237 era_identify_compressed on seeded stable systems."""
+    from blockten.apps import LtiSystem, era_identify_compressed, markov_from_lti
+
+    out = {}
+    for name, seed, d, no, ni, s, ranks, order, tera in ERA_CASES:
+        a, b, c = oc.era_system(seed, d, no, ni)
+        seq = markov_from_lti(LtiSystem(a=a, b=b, c=c), 2 * s - 1)
+        res = era_identify_compressed(seq, ranks, order, tera=tera)
+        out[f"{name}_params"] = seq.params
+        out[f"{name}_sv"] = res.sing_vals
+        out[f"{name}_eig"] = np.linalg.eigvals(res.system.a)
+        out[f"{name}_markov"] = markov_from_lti(res.system, 2 * s - 1).params
+        out[f"{name}_reduced"] = res.reduced_hankel
+        out[f"{name}_u"] = res.basis_left
+        out[f"{name}_w"] = res.basis_right
+        out[f"{name}_approx"] = res.hankel_approx()
+    np.savez_compressed(os.path.join(OUT, "era.npz"), **out)
+
+
 if __name__ == "__main__":
     np.seterr(all="ignore")
     patterns()
@@ -414,5 +442,6 @@ if __name__ == "__main__":
     spd_cases()
     detect_cases()
     container_cases()
+    era_cases()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -227,3 +227,24 @@ def test_detect_pattern_golden(golden):
         assert np.array_equal(offs, z[f"{name}_offs"]), name
         assert np.array_equal(np.stack(reps).view(np.int64), z[f"{name}_reps"].view(np.int64)), name
         assert cls == meta[name]["structure_class"], name
+
+
+def test_era_golden(golden):
+    """oracle ERA vs the reference (apps.py:153-237): invariant quantities."""
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    z = golden("era")
+    cases = (("full", 71, 6, 2, 2, 20, (2, 39, 2), 6, False),
+             ("cut", 72, 5, 3, 2, 16, (3, 12, 2), 5, False),
+             ("tera", 73, 4, 3, 3, 12, (2, 0, 2), 4, True),
+             ("siso", 74, 2, 1, 1, 10, (1, 19, 1), 2, False))
+    for name, seed, d, no, ni, s, ranks, order, tera in cases:
+        a, b, c = oc.era_system(seed, d, no, ni)
+        params = port.markov_from_lti(a, b, c, 2 * s - 1)
+        assert np.allclose(params, z[f"{name}_params"], rtol=0, atol=1e-14)
+        at, bt_, ct, sv, red, u, w = port.era_identify(params, ranks, order, tera)
+        assert np.abs(sv - z[f"{name}_sv"]).max() <= 1e-12 * sv[0], name
+        assert np.abs(red - z[f"{name}_reduced"]).max() <= 1e-12 * np.abs(red).max(), name
+        mk = port.markov_from_lti(at, bt_, ct, 2 * s - 1)
+        assert np.abs(mk - z[f"{name}_markov"]).max() <= 1e-10 * np.abs(mk).max(), name
