@@ -156,34 +156,6 @@ __device__ void pinv_from_eig(const double* a, const double* qv, int R, int ld, 
   }
 }
 
-// V = G0 o G1 (Hadamard) if g1 != null else V = G0; Vp = pinv(V)
-__global__ void __launch_bounds__(256) pinv_kernel(const double* __restrict__ g0,
-                                                   const double* __restrict__ g1, int R,
-                                                   double* __restrict__ vp) {
-  extern __shared__ __align__(16) double sm[];
-  const int n = R + (R & 1);
-  const int ld = n + 1;
-  double* a = sm;
-  double* qv = a + n * ld;
-  double* cs = qv + n * ld;
-  double* sn = cs + n / 2;
-  int* pp = reinterpret_cast<int*>(sn + n / 2);
-  int* qq = pp + n / 2;
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-    const int r = idx / n, c = idx % n;
-    double v = 0.0;
-    if (r < R && c < R) v = g1 ? g0[r * R + c] * g1[r * R + c] : g0[r * R + c];
-    a[r * ld + c] = v;
-  }
-  __syncthreads();
-  jacobi_smem(a, qv, n, ld, cs, sn, pp, qq, 40, 0.0);
-  __syncthreads();
-  pinv_from_eig(a, qv, R, ld, vp);
-}
-
-// Fast variant for a compile-time padded size NP (even, <= 96): rotation
-// parameters by the first NP/2 threads, row and column phases as flat loops
-// with constant-size index math; full sweeps until no rotation happens.
 template <int NP>
 __device__ __forceinline__ void load_v(const double* __restrict__ g0, const double* __restrict__ g1,
                                        int R, double* a, double& ss) {
@@ -326,10 +298,6 @@ __global__ void __launch_bounds__(1024) pinv_fast_kernel(const double* __restric
   pinv_from_eig(a, q, R, LD, vp);
 }
 
-size_t pinv_smem_bytes(int R) {
-  const int n = R + (R & 1);
-  return (size_t)(2 * n * (n + 1) + n) * 8 + (size_t)n * 4;
-}
 
 // ---------------------------------------------------------------------------
 // solve: F_un = (sum_s Mpart[s]) @ Vp ; per-CTA Gram + <F_un, M> partials
@@ -827,17 +795,7 @@ int run_pinv(const double* g0, const double* g1, int R, double* vp, cudaStream_t
   if (R <= 16) return launch_pinv_fast<16>(g0, g1, R, vp, st);
   if (R <= 32) return launch_pinv_fast<32>(g0, g1, R, vp, st);
   if (R <= 64) return launch_pinv_fast<64>(g0, g1, R, vp, st);
-  if (R <= 96) return launch_pinv_fast<96>(g0, g1, R, vp, st);
-  const size_t sm = pinv_smem_bytes(R);
-  static bool attr = false;
-  if (!attr) {
-    BT_CUDA_CHECK(cudaFuncSetAttribute(pinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(pinv_smem_bytes(PINV_MAX_R))));
-    attr = true;
-  }
-  pinv_kernel<<<1, 256, sm, st>>>(g0, g1, R, vp);
-  BT_LAUNCH_CHECK();
-  return BT_OK;
+  return launch_pinv_fast<96>(g0, g1, R, vp, st);  // R <= PINV_MAX_R is enforced upstream
 }
 
 // Factor update, local half: Vp = pinv(G_o0 o G_o1), F_un = M Vp (M summed

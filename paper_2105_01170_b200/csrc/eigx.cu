@@ -39,97 +39,6 @@ __device__ double block_reduce_sum(double v, double* red) {
   return t;
 }
 
-// reflector for column k: x = A[k+1:, k];  H = I - tau v v^T, v[k+1] = 1
-// (LAPACK dlarfg convention).  Writes d[k], e[k], tau[k], V row k.
-__global__ void __launch_bounds__(256)
-    house_kernel(double* __restrict__ a, int64_t n, int64_t k, double* __restrict__ d,
-                 double* __restrict__ e, double* __restrict__ tau, double* __restrict__ vref) {
-  __shared__ double red[8];
-  __shared__ double sh[3];
-  const int64_t m0 = k + 1;
-  double s = 0.0;
-  for (int64_t i = m0 + 1 + threadIdx.x; i < n; i += blockDim.x) {
-    const double x = a[i * n + k];
-    s = fma(x, x, s);
-  }
-  const double tail2 = block_reduce_sum(s, red);
-  if (threadIdx.x == 0) {
-    const double x0 = a[m0 * n + k];
-    d[k] = a[k * n + k];
-    if (tail2 == 0.0) {
-      sh[0] = 0.0;       // tau
-      sh[1] = x0;        // beta
-      sh[2] = 0.0;       // scale
-    } else {
-      const double nrm = sqrt(x0 * x0 + tail2);
-      const double beta = (x0 >= 0.0) ? -nrm : nrm;
-      sh[0] = (beta - x0) / beta;
-      sh[1] = beta;
-      sh[2] = 1.0 / (x0 - beta);
-    }
-    tau[k] = sh[0];
-    e[k] = sh[1];
-  }
-  __syncthreads();
-  const double sc = sh[2];
-  double* v = vref + k * n;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    double val = 0.0;
-    if (i == m0) val = 1.0;
-    else if (i > m0) val = a[i * n + k] * sc;
-    v[i] = val;
-  }
-}
-
-// p[i] = tau * sum_{j > k} A[i][j] v[j] for i > k; part[cta] = sum_i p_i v_i
-__global__ void __launch_bounds__(256)
-    symv_kernel(const double* __restrict__ a, int64_t n, int64_t k,
-                const double* __restrict__ tau, const double* __restrict__ vref,
-                double* __restrict__ p, double* __restrict__ part) {
-  __shared__ double red[8];
-  const double t = tau[k];
-  const double* v = vref + k * n;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t m0 = k + 1;
-  double local = 0.0;
-  for (int64_t i = m0 + blockIdx.x * 8 + warp; i < n; i += (int64_t)gridDim.x * 8) {
-    const double* row = a + i * n;
-    double s = 0.0;
-    for (int64_t j = m0 + lane; j < n; j += 32) s = fma(row[j], v[j], s);
-    s = warp_sum(s) * t;
-    if (lane == 0) {
-      p[i] = s;
-      local = fma(s, v[i], local);
-    }
-  }
-  const double tot = block_reduce_sum(local, red);
-  if (threadIdx.x == 0) part[blockIdx.x] = tot;
-}
-
-// A22 -= v w^T + w v^T with w = p - (tau/2)(p^T v) v
-__global__ void __launch_bounds__(256)
-    rank2_kernel(double* __restrict__ a, int64_t n, int64_t k, const double* __restrict__ tau,
-                 const double* __restrict__ vref, const double* __restrict__ p,
-                 const double* __restrict__ part, int nparts) {
-  __shared__ double alpha_sh;
-  if (threadIdx.x == 0) {
-    double ptv = 0.0;
-    for (int i = 0; i < nparts; ++i) ptv += part[i];
-    alpha_sh = 0.5 * tau[k] * ptv;
-  }
-  __syncthreads();
-  const double alpha = alpha_sh;
-  const double* v = vref + k * n;
-  const int64_t m0 = k + 1;
-  const int64_t m = n - m0;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < m * m;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = m0 + idx / m, j = m0 + idx % m;
-    const double wi = p[i] - alpha * v[i], wj = p[j] - alpha * v[j];
-    a[i * n + j] -= v[i] * wj + wi * v[j];
-  }
-}
-
 // Whole tridiagonalisation in one cooperative launch (one 1024-thread CTA
 // per SM, two grid-wide barriers per reflector): every CTA recomputes the
 // reflector of column k redundantly from row k (A is kept exactly symmetric),

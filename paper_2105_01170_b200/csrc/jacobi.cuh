@@ -22,83 +22,9 @@ static __device__ __forceinline__ void rr_pair(int n, int rnd, int k, int& p, in
   }
 }
 
-// In-place cyclic Jacobi on a (n x n, ld) smem matrix a, accumulating q (n x n).
-// Threads of the CTA cooperate; returns with a diagonalised.
-static __device__ __noinline__ int jacobi_smem(double* a, double* qv, int n, int ld, double* cs,
-                                        double* sn, int* pp, int* qq, int max_sweeps,
-                                        double abs_tol) {
-  __shared__ int rotated;
-  int any = 0;
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x)
-    qv[(idx / n) * ld + idx % n] = (idx / n == idx % n) ? 1.0 : 0.0;
-  __syncthreads();
-  const int half = n / 2;
-  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-    if (threadIdx.x == 0) rotated = 0;
-    __syncthreads();
-    for (int rnd = 0; rnd < n - 1; ++rnd) {
-      for (int k = threadIdx.x; k < half; k += blockDim.x) {
-        int p, q;
-        rr_pair(n, rnd, k, p, q);
-        const double apq = a[p * ld + q];
-        const double app = a[p * ld + p], aqq = a[q * ld + q];
-        double c = 1.0, s = 0.0;
-        // rotate unless a_pq is negligible relative to the diagonal pair (the
-        // Demmel-Veselic relative test at working precision; a threshold
-        // below eps is never met by rounding noise and only burns sweeps)
-        if (apq != 0.0 && fabs(apq) > abs_tol &&
-            fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq))) {
-          const double theta = (aqq - app) / (2.0 * apq);
-          const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-          c = 1.0 / sqrt(t * t + 1.0);
-          s = t * c;
-          rotated = 1;
-        }
-        cs[k] = c;
-        sn[k] = s;
-        pp[k] = p;
-        qq[k] = q;
-      }
-      __syncthreads();
-      // rows p, q
-      for (int idx = threadIdx.x; idx < half * n; idx += blockDim.x) {
-        const int k = idx / n, j = idx % n;
-        const double c = cs[k], s = sn[k];
-        if (s == 0.0) continue;
-        const int p = pp[k], q = qq[k];
-        const double x = a[p * ld + j], y = a[q * ld + j];
-        a[p * ld + j] = c * x - s * y;
-        a[q * ld + j] = s * x + c * y;
-      }
-      __syncthreads();
-      // columns p, q of a and of the eigenvector accumulator
-      for (int idx = threadIdx.x; idx < half * n; idx += blockDim.x) {
-        const int k = idx / n, i = idx % n;
-        const double c = cs[k], s = sn[k];
-        if (s == 0.0) continue;
-        const int p = pp[k], q = qq[k];
-        double x = a[i * ld + p], y = a[i * ld + q];
-        // the rotated pair's own off-diagonal is zero by construction
-        a[i * ld + p] = (i == q) ? 0.0 : c * x - s * y;
-        a[i * ld + q] = (i == p) ? 0.0 : s * x + c * y;
-        x = qv[i * ld + p];
-        y = qv[i * ld + q];
-        qv[i * ld + p] = c * x - s * y;
-        qv[i * ld + q] = s * x + c * y;
-      }
-      __syncthreads();
-    }
-    const int r = rotated;
-    __syncthreads();
-    if (!r) break;
-    any = 1;
-  }
-  return any;
-}
-
-
-// Same cyclic round-robin Jacobi, restructured for latency: one parameter
-// phase and ONE update phase per round.  The update applies both rotations
+// Cyclic round-robin Jacobi on a symmetric (n x n, ld) smem matrix,
+// accumulating the eigenvectors in qv; one parameter phase and ONE update
+// phase per round.  The update applies both rotations
 // of a round to disjoint 2x2 blocks (pair k1 rows x pair k2 columns: new
 // block = L1 B L2^T), so rows and columns need no separate passes, and the
 // eigenvector accumulator's column pairs are updated in the same phase.

@@ -227,3 +227,25 @@ def test_hosvd_golden(golden):
         np.testing.assert_allclose(rep.core, z[f"h{n}_core"], atol=1e-12)
         for k in range(3):
             np.testing.assert_allclose(rep.factors[k], z[f"h{n}_u{k}"], atol=1e-12)
+
+
+@pytest.mark.parametrize("R", [3, 8, 16, 33, 64, 96])
+def test_pinv_sym_vs_numpy(R):
+    """bt_pinv_sym_f64 (decomp.py:387 np.linalg.pinv of the Hadamard Gram):
+    well-conditioned SPD (Cholesky path), rank-deficient PSD (eigen path with
+    numpy's 1e-15 cutoff) across the NP size classes."""
+    from paper_2105_01170_b200 import _dev
+    from paper_2105_01170_b200 import _native as N
+
+    rng = np.random.default_rng(R)
+    g = rng.standard_normal((R, 2 * R))
+    cases = [g @ g.T]
+    h = rng.standard_normal((R, max(1, R // 2)))
+    cases.append(h @ h.T)                       # rank R/2: pinv != inverse
+    for v in cases:
+        vd = torch.from_numpy(v).cuda()
+        out = torch.empty_like(vd)
+        N.call("bt_pinv_sym_f64", _dev.ptr(vd), R, _dev.ptr(out), _dev.stream())
+        ref = np.linalg.pinv(v)
+        err = np.abs(out.cpu().numpy() - ref).max() / np.abs(ref).max()
+        assert err < 1e-9, (R, err)
