@@ -176,13 +176,13 @@ __device__ __forceinline__ void load_v(const double* __restrict__ g0, const doub
 // ||V||_1 ||V^-1||_1 <= 1e12 -- there numpy's pinv (decomp.py:387, cutoff
 // 1e-15 sigma_max) is the inverse and both agree to ~cond * eps.  Otherwise
 // (or on a non-positive pivot) the eigen path: cyclic Jacobi + the pinv cutoff.
+// The whole CTA computes vp (global or shared); smf: 3 NP (NP+1) doubles of
+// shared scratch.  Used by pinv_fast_kernel and by the fused small CP-ALS.
 template <int NP>
-__global__ void __launch_bounds__(1024) pinv_fast_kernel(const double* __restrict__ g0,
-                                                         const double* __restrict__ g1, int R,
-                                                         double* __restrict__ vp) {
+__device__ void pinv_block(const double* __restrict__ g0, const double* __restrict__ g1, int R,
+                           double* __restrict__ vp, double* smf) {
   constexpr int LD = NP + 1;
   constexpr int HALF = NP / 2;
-  extern __shared__ __align__(16) double smf[];
   double* a = smf;
   double* q = a + NP * LD;
   double* x = q + NP * LD;
@@ -296,6 +296,14 @@ __global__ void __launch_bounds__(1024) pinv_fast_kernel(const double* __restric
   jacobi_fast(a, q, NP, LD, cs, sn, pp, qq, 40, 1e-15 * sqrt(fro2), 1e-15);
   __syncthreads();
   pinv_from_eig(a, q, R, LD, vp);
+}
+
+template <int NP>
+__global__ void __launch_bounds__(1024) pinv_fast_kernel(const double* __restrict__ g0,
+                                                         const double* __restrict__ g1, int R,
+                                                         double* __restrict__ vp) {
+  extern __shared__ __align__(16) double smf[];
+  pinv_block<NP>(g0, g1, R, vp, smf);
 }
 
 
