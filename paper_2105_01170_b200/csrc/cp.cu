@@ -293,7 +293,10 @@ __device__ void pinv_block(const double* __restrict__ g0, const double* __restri
   __syncthreads();
   double fro2 = 0.0;
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) fro2 += fro_red[w];
-  jacobi_fast(a, q, NP, LD, cs, sn, pp, qq, 40, 1e-15 * sqrt(fro2), 1e-15);
+  if (NP <= 32)
+    jacobi_warp(a, q, NP, LD, cs, sn, pp, qq, 40, 1e-15 * sqrt(fro2), 1e-15);
+  else
+    jacobi_fast(a, q, NP, LD, cs, sn, pp, qq, 40, 1e-15 * sqrt(fro2), 1e-15);
   __syncthreads();
   pinv_from_eig(a, q, R, LD, vp);
 }
@@ -539,6 +542,59 @@ __global__ void __launch_bounds__(Cfg::THREADS)
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int w = 0; w < Cfg::THREADS / 32; ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+// Explicit residual for small ranks (R <= RS, e.g. C4's R = 16), where the
+// DMMA tile version is latency bound (a K = R reduction per X tile): a warp
+// owns a 32-wide k chunk -- C[k, :] in registers -- and streams (i, j) rows
+// of X with coalesced loads; Xhat[i][j][k] = sum_r (W[i][r] B[j][r]) C[k][r].
+// Fixed-order sums (deterministic); X read once.
+template <int RS>
+__global__ void __launch_bounds__(256)
+    residual_small_kernel(const double* __restrict__ X, const double* __restrict__ W,
+                          const double* __restrict__ Bf, const double* __restrict__ Cf, int64_t I,
+                          int64_t J, int64_t K, int R, const double* __restrict__ flag,
+                          double* __restrict__ part) {
+  __shared__ double red[8];
+  if (flag != nullptr && *flag == 0.0) {
+    if (threadIdx.x == 0) part[blockIdx.x] = 0.0;
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t kchunks = (K + 31) / 32;
+  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  double local = 0.0;
+  // warp work item: (k chunk, row group of 64 (i, j) rows)
+  const int64_t rows = I * J;
+  const int64_t groups = (rows + 63) / 64;
+  for (int64_t item = gw; item < kchunks * groups; item += nwarps) {
+    const int64_t kc = item % kchunks, g = item / kchunks;
+    const int64_t k = kc * 32 + lane;
+    double c[RS];
+#pragma unroll
+    for (int r = 0; r < RS; ++r) c[r] = (k < K && r < R) ? __ldg(Cf + k * R + r) : 0.0;
+    const int64_t r0 = g * 64, r1 = r0 + 64 < rows ? r0 + 64 : rows;
+    for (int64_t row = r0; row < r1; ++row) {
+      const int64_t i = row / J, j = row - i * J;
+      double xh = 0.0;
+#pragma unroll
+      for (int r = 0; r < RS; ++r)
+        if (r < R) xh = fma(__ldg(W + i * R + r) * __ldg(Bf + j * R + r), c[r], xh);
+      if (k < K) {
+        const double d = ld_stream(X + row * K + k) - xh;
+        local = fma(d, d, local);
+      }
+    }
+  }
+  local = warp_sum(local);
+  if (lane == 0) red[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
     part[blockIdx.x] = s;
   }
 }
@@ -1126,10 +1182,20 @@ extern "C" int bt_cp_residual(void* state, double* res2) {
   lam_scale_kernel<<<grid_n(pl.I * pl.R), 256, 0, S->st>>>(S->F[0], S->lam, pl.I,
                                                            static_cast<int>(pl.R), W);
   BT_LAUNCH_CHECK();
-  if (pl.R % 2 == 0)
+  if (pl.R <= 16) {
+    // res_grid CTAs of 256 threads; every CTA writes its partial
+    if (pl.R <= 8)
+      residual_small_kernel<8><<<pl.res_grid, 256, 0, S->st>>>(
+          S->X, W, S->F[1], S->F[2], pl.I, pl.J, pl.K, static_cast<int>(pl.R), S->s.scal + 3, rpart);
+    else
+      residual_small_kernel<16><<<pl.res_grid, 256, 0, S->st>>>(
+          S->X, W, S->F[1], S->F[2], pl.I, pl.J, pl.K, static_cast<int>(pl.R), S->s.scal + 3, rpart);
+    BT_LAUNCH_CHECK();
+  } else if (pl.R % 2 == 0) {
     BT_TRY(residual_pass<2>(pl, S->X, W, S->F[1], S->F[2], S->s.scal + 3, rpart, S->st));
-  else
+  } else {
     BT_TRY(residual_pass<1>(pl, S->X, W, S->F[1], S->F[2], S->s.scal + 3, rpart, S->st));
+  }
   residual_reduce_kernel<<<1, 32, 0, S->st>>>(rpart, pl.res_grid, res2);
   BT_LAUNCH_CHECK();
   return BT_OK;

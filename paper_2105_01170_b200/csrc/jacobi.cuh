@@ -5,21 +5,60 @@
 
 #include "bt_common.cuh"
 
-// Circle-method round-robin pair k of round rnd for n (even) players.
+// Circle-method round-robin pair k of round rnd for n (even) players
+// (0 <= rnd, k < n - 1: conditional subtractions instead of integer modulo).
 static __device__ __forceinline__ void rr_pair(int n, int rnd, int k, int& p, int& q) {
   const int m = n - 1;
   if (k == 0) {
-    p = rnd % m;
+    p = rnd;
     q = m;
   } else {
-    p = (rnd + k) % m;
-    q = (rnd - k + m) % m;
+    p = rnd + k;
+    if (p >= m) p -= m;
+    q = rnd - k + m;
+    if (q >= m) q -= m;
   }
   if (p > q) {
     int t = p;
     p = q;
     q = t;
   }
+}
+
+// Rotation (c, s) annihilating a_pq, from approximate reciprocal / rsqrt
+// refined by two Newton steps each (~1 ulp; c^2 + s^2 = 1 to working
+// precision) -- a shorter dependent chain than IEEE div + sqrt, which sets
+// the latency of every Jacobi round.
+static __device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+static __device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  return y * fma(-h * y, y, 1.5);
+}
+static __device__ __forceinline__ void jacobi_rotation(double app, double aqq, double apq,
+                                                       double& c, double& s) {
+  const double theta = (aqq - app) * rcp_nr(2.0 * apq);
+  const double at = fabs(theta);
+  double t;
+  if (at > 1e150) {
+    t = 0.5 * rcp_nr(theta);
+  } else {
+    const double q2 = fma(theta, theta, 1.0);
+    const double root = q2 * rsqrt_nr(q2);
+    t = rcp_nr(at + root);
+    if (theta < 0.0) t = -t;
+  }
+  c = rsqrt_nr(fma(t, t, 1.0));
+  s = t * c;
 }
 
 // Cyclic round-robin Jacobi on a symmetric (n x n, ld) smem matrix,
@@ -53,10 +92,7 @@ static __device__ __noinline__ int jacobi_fast(double* a, double* qv, int n, int
         const double app = a[p * ld + p], aqq = a[q * ld + q];
         double c = 1.0, s = 0.0;
         if (apq != 0.0 && fabs(apq) > abs_tol && fabs(apq) > rel_tol * sqrt(fabs(app) * fabs(aqq))) {
-          const double theta = (aqq - app) / (2.0 * apq);
-          const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-          c = 1.0 / sqrt(t * t + 1.0);
-          s = t * c;
+          jacobi_rotation(app, aqq, apq, c, s);
           rotated = 1;
         }
         cs[k] = c;
@@ -96,6 +132,75 @@ static __device__ __noinline__ int jacobi_fast(double* a, double* qv, int n, int
     const int r = rotated;
     __syncthreads();
     if (!r) break;
+    any = 1;
+  }
+  return any;
+}
+
+// Warp-synchronous variant for n <= 32 (the CP pinv at R <= 32): executed by
+// warp 0 alone, __syncwarp instead of CTA barriers (a round costs a few
+// hundred cycles instead of two CTA-wide barriers).  Same rotation rule and
+// update as jacobi_fast.  Other warps must not touch a / qv until the caller's
+// next __syncthreads.
+static __device__ __noinline__ int jacobi_warp(double* a, double* qv, int n, int ld, double* cs,
+                                               double* sn, int* pp, int* qq, int max_sweeps,
+                                               double abs_tol, double rel_tol) {
+  if (threadIdx.x >= 32) return 0;
+  const int lane = threadIdx.x;
+  const int half = n / 2;
+  int any = 0;
+  for (int idx = lane; idx < n * n; idx += 32) {
+    const int r = idx / n, c = idx - r * n;
+    qv[r * ld + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    int rotated = 0;
+    for (int rnd = 0; rnd < n - 1; ++rnd) {
+      if (lane < half) {
+        int p, q;
+        rr_pair(n, rnd, lane, p, q);
+        const double apq = a[p * ld + q];
+        const double app = a[p * ld + p], aqq = a[q * ld + q];
+        double c = 1.0, s = 0.0;
+        if (apq != 0.0 && fabs(apq) > abs_tol && fabs(apq) > rel_tol * sqrt(fabs(app) * fabs(aqq))) {
+          jacobi_rotation(app, aqq, apq, c, s);
+          rotated = 1;
+        }
+        cs[lane] = c;
+        sn[lane] = s;
+        pp[lane] = p;
+        qq[lane] = q;
+      }
+      __syncwarp();
+      for (int e = lane; e < half * half; e += 32) {
+        const int k1 = e / half, k2 = e - k1 * half;
+        const double s1 = sn[k1], s2 = sn[k2];
+        if (s1 == 0.0 && s2 == 0.0) continue;
+        const double c1 = cs[k1], c2 = cs[k2];
+        const int p1 = pp[k1], q1 = qq[k1], p2 = pp[k2], q2 = qq[k2];
+        const double x11 = a[p1 * ld + p2], x12 = a[p1 * ld + q2];
+        const double x21 = a[q1 * ld + p2], x22 = a[q1 * ld + q2];
+        const double y11 = c1 * x11 - s1 * x21, y12 = c1 * x12 - s1 * x22;
+        const double y21 = s1 * x11 + c1 * x21, y22 = s1 * x12 + c1 * x22;
+        a[p1 * ld + p2] = c2 * y11 - s2 * y12;
+        a[q1 * ld + q2] = s2 * y21 + c2 * y22;
+        a[p1 * ld + q2] = (k1 == k2) ? 0.0 : s2 * y11 + c2 * y12;
+        a[q1 * ld + p2] = (k1 == k2) ? 0.0 : c2 * y21 - s2 * y22;
+      }
+      for (int e = lane; e < half * n; e += 32) {
+        const int k = e / n, i = e - k * n;
+        const double s = sn[k];
+        if (s == 0.0) continue;
+        const double c = cs[k];
+        const int p = pp[k], q = qq[k];
+        const double x = qv[i * ld + p], y = qv[i * ld + q];
+        qv[i * ld + p] = c * x - s * y;
+        qv[i * ld + q] = s * x + c * y;
+      }
+      __syncwarp();
+    }
+    if (!__any_sync(0xffffffffu, rotated)) break;
     any = 1;
   }
   return any;
