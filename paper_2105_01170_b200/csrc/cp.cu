@@ -577,15 +577,24 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int r = 0; r < RS; ++r) c[r] = (k < K && r < R) ? __ldg(Cf + k * R + r) : 0.0;
     const int64_t r0 = g * 64, r1 = r0 + 64 < rows ? r0 + 64 : rows;
-    for (int64_t row = r0; row < r1; ++row) {
-      const int64_t i = row / J, j = row - i * J;
-      double xh = 0.0;
+    constexpr int UR = 4;  // independent X loads in flight per lane
+    for (int64_t row = r0; row < r1; row += UR) {
+      double xv[UR];
 #pragma unroll
-      for (int r = 0; r < RS; ++r)
-        if (r < R) xh = fma(__ldg(W + i * R + r) * __ldg(Bf + j * R + r), c[r], xh);
-      if (k < K) {
-        const double d = ld_stream(X + row * K + k) - xh;
-        local = fma(d, d, local);
+      for (int u = 0; u < UR; ++u)
+        xv[u] = (row + u < r1 && k < K) ? ld_stream(X + (row + u) * K + k) : 0.0;
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        if (row + u >= r1) break;
+        const int64_t i = (row + u) / J, j = (row + u) - i * J;
+        double xh = 0.0;
+#pragma unroll
+        for (int r = 0; r < RS; ++r)
+          if (r < R) xh = fma(__ldg(W + i * R + r) * __ldg(Bf + j * R + r), c[r], xh);
+        if (k < K) {
+          const double d = xv[u] - xh;
+          local = fma(d, d, local);
+        }
       }
     }
   }
