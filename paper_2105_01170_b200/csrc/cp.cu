@@ -106,6 +106,160 @@ __global__ void __launch_bounds__(Cfg::THREADS)
   }
 }
 
+// Warp-specialised variant of the tree kernel: Cfg::THREADS consumer threads
+// (the DMMA warps) plus one producer warp that streams the X / C tiles with
+// cp.async into the STAGES ring; full / empty mbarriers replace the per-stage
+// CTA barrier, and the consumers carry no copy-address state (fewer
+// registers, no cp.async issue between their DMMAs).  Same math, same
+// epilogue, same summation order as tree_p_kernel.
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS + 32, 2)
+    tree_p_ws_kernel(BtGemmArgs g, const double* __restrict__ Bf, int64_t R,
+                     double* __restrict__ m1part, int64_t jtiles, int store_p) {
+  static_assert(Cfg::A_KCONTIG && !Cfg::B_KCONTIG, "tree layout: X rows K-contiguous, C N-contiguous");
+  extern __shared__ __align__(16) double smem_dyn[];
+  __shared__ double red[Cfg::WM][Cfg::BN];
+  __shared__ __align__(8) uint64_t full[Cfg::STAGES], empty[Cfg::STAGES];
+  const int64_t tm = blockIdx.x, tn = blockIdx.y, i = blockIdx.z;
+  const int64_t m0 = tm * Cfg::BM, n0 = tn * Cfg::BN;
+  const int64_t KT = (g.Kin + Cfg::BK - 1) / Cfg::BK;
+  double* As = smem_dyn;
+  double* Bs = smem_dyn + Cfg::STAGES * Cfg::A_STAGE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int CW = Cfg::THREADS / 32;  // consumer warps
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 32);
+      mbar_init(&empty[s], CW);
+    }
+  }
+  __syncthreads();
+  if (warp == CW) {
+    // ---------------- producer warp ----------------
+    const double* a_tile = g.A.ptr + i * g.A.s_b + m0 * g.A.s_mn;
+    const double* b_tile = g.B.ptr + n0;
+    const int64_t m_left = g.M - m0, n_left = g.N - n0;
+    constexpr int V = Cfg::VEC;
+    constexpr int ACH = Cfg::BK / V;            // chunks per A row
+    constexpr int ATOT = Cfg::BM * ACH;
+    constexpr int BCH = Cfg::BN / V;            // chunks per B row (k)
+    constexpr int BTOT = Cfg::BK * BCH;
+    for (int64_t kt = 0; kt < KT; ++kt) {
+      const int s = static_cast<int>(kt % Cfg::STAGES);
+      if (kt >= Cfg::STAGES) mbar_wait(&empty[s], static_cast<unsigned>(((kt / Cfg::STAGES) - 1) & 1));
+      const int64_t k0 = kt * Cfg::BK;
+      const int64_t k_left = g.Kin - k0;
+      double* as = As + s * Cfg::A_STAGE;
+      double* bs = Bs + s * Cfg::B_STAGE;
+      for (int c = lane; c < ATOT; c += 32) {
+        const int r = c / ACH, cc = (c % ACH) * V;
+        int64_t valid = (r < m_left) ? (k_left - cc) : 0;
+        valid = valid < 0 ? 0 : (valid > V ? V : valid);
+        const double* src = valid > 0 ? a_tile + r * g.A.s_mn + k0 + cc : g.A.ptr;
+        if (V == 2)
+          cp_async16(as + r * Cfg::LDA + cc, src, static_cast<int>(valid * 8));
+        else
+          cp_async8(as + r * Cfg::LDA + cc, src, static_cast<int>(valid * 8));
+      }
+      for (int c = lane; c < BTOT; c += 32) {
+        const int r = c / BCH, cc = (c % BCH) * V;
+        int64_t valid = (r < k_left) ? (n_left - cc) : 0;
+        valid = valid < 0 ? 0 : (valid > V ? V : valid);
+        const double* src = valid > 0 ? b_tile + (k0 + r) * g.B.s_ki + cc : g.B.ptr;
+        if (V == 2)
+          cp_async16(bs + r * Cfg::LDB + cc, src, static_cast<int>(valid * 8));
+        else
+          cp_async8(bs + r * Cfg::LDB + cc, src, static_cast<int>(valid * 8));
+      }
+      mbar_cp_async_arrive(&full[s]);
+    }
+    return;
+  }
+  // ---------------- consumer warps ----------------
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wmi = warp % Cfg::WM;
+  const int wm0 = wmi * Cfg::TM;
+  const int wn0 = (warp / Cfg::WM) * Cfg::TN;
+  double acc[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+  for (int a = 0; a < Cfg::FM; ++a)
+#pragma unroll
+    for (int b = 0; b < Cfg::FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  constexpr int KSTEPS = Cfg::BK / 4;
+  double afr[2][Cfg::FM], bfr[2][Cfg::FN];
+  for (int64_t kt = 0; kt < KT; ++kt) {
+    const int s = static_cast<int>(kt % Cfg::STAGES);
+    mbar_wait(&full[s], static_cast<unsigned>((kt / Cfg::STAGES) & 1));
+    const double* as = As + s * Cfg::A_STAGE;
+    const double* bs = Bs + s * Cfg::B_STAGE;
+    auto load_frags = [&](int buf, int kk) {
+#pragma unroll
+      for (int a = 0; a < Cfg::FM; ++a) afr[buf][a] = as[(wm0 + a * 8 + gq) * Cfg::LDA + kk + tq];
+#pragma unroll
+      for (int b = 0; b < Cfg::FN; ++b) bfr[buf][b] = bs[(kk + tq) * Cfg::LDB + wn0 + b * 8 + gq];
+    };
+    load_frags(0, 0);
+#pragma unroll
+    for (int ks = 0; ks < KSTEPS; ++ks) {
+      if (ks + 1 < KSTEPS) load_frags((ks + 1) & 1, (ks + 1) * 4);
+#pragma unroll
+      for (int a = 0; a < Cfg::FM; ++a)
+#pragma unroll
+        for (int b = 0; b < Cfg::FN; ++b)
+          dmma884(acc[a][b][0], acc[a][b][1], afr[ks & 1][a], bfr[ks & 1][b]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  // epilogue (as tree_p_kernel; consumer-only named barrier)
+  double* Pb = g.C + i * g.sCb;
+  double colsum[Cfg::FN][2];
+#pragma unroll
+  for (int j = 0; j < Cfg::FN; ++j) colsum[j][0] = colsum[j][1] = 0.0;
+#pragma unroll
+  for (int fi = 0; fi < Cfg::FM; ++fi) {
+    const int64_t jrow = m0 + wm0 + fi * 8 + gq;
+    const bool rv = jrow < g.M;
+#pragma unroll
+    for (int fj = 0; fj < Cfg::FN; ++fj) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t r = n0 + wn0 + fj * 8 + 2 * tq + h;
+        if (rv && r < g.N) {
+          const double v = acc[fi][fj][h];
+          if (store_p) Pb[jrow * g.sCm + r] = v;
+          colsum[fj][h] = fma(v, __ldg(Bf + jrow * R + r), colsum[fj][h]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int fj = 0; fj < Cfg::FN; ++fj)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double v = colsum[fj][h];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      colsum[fj][h] = v;
+    }
+  if (gq == 0) {
+#pragma unroll
+    for (int fj = 0; fj < Cfg::FN; ++fj)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) red[wmi][wn0 + fj * 8 + 2 * tq + h] = colsum[fj][h];
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(Cfg::THREADS));
+  for (int c = threadIdx.x; c < Cfg::BN; c += Cfg::THREADS) {
+    const int64_t r = n0 + c;
+    if (r >= g.N) continue;
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < Cfg::WM; ++w) sum += red[w][c];
+    m1part[(i * jtiles + tm) * R + r] = sum;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // M2 partials from P: m2part[s][j][r] = sum_{i in chunk s} P[i][j][r] A[i][r]
 // ---------------------------------------------------------------------------
@@ -673,7 +827,9 @@ int tree_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("BT_TREE_CFG");
-    v = e ? atoi(e) : 6;  // variant 6 (128x64, 4 warps of 64x32, 3 stages) tuned best
+    // 9: warp-specialised (4 DMMA warps of 64x32 + 1 cp.async producer warp,
+    // mbarrier ring, 3 stages) -- 72.5 vs 73.5 ms for variant 6 on C5
+    v = e ? atoi(e) : 9;
   }
   return v;
 }
@@ -769,6 +925,40 @@ Plan make_plan(const bt_cp_problem* pb) {
   return pl;
 }
 
+// warp-specialised tree kernel (BT_TREE_CFG=9): 128x64 tile, 2x2 consumer
+// warps + 1 producer warp, 3 stages, 2 CTAs per SM
+template <int V>
+int launch_tree_ws(const Plan& pl, const double* X, const double* C, const double* B, double* P,
+                   double* m1part, int store_p, cudaStream_t st) {
+  using Cfg = GemmCfg<128, 64, 16, 2, 2, 3, true, false, V>;
+  BtGemmArgs g{};
+  g.M = pl.J;
+  g.N = pl.R;
+  g.Kin = pl.K;
+  g.Kout = 1;
+  g.A = BtOperand{X, pl.K, 0, 1, pl.J * pl.K};
+  g.B = BtOperand{C, 1, 0, pl.R, 0};
+  g.C = P;
+  g.sCm = pl.R;
+  g.sCn = 1;
+  g.sCb = pl.J * pl.R;
+  g.alpha = 1.0;
+  static bool attr = false;
+  if (!attr) {
+    BT_CUDA_CHECK(cudaFuncSetAttribute(tree_p_ws_kernel<Cfg>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Cfg::SMEM_BYTES));
+    attr = true;
+  }
+  BT_REQUIRE(pl.I <= 65535, BT_E_SHAPE, "cp: mode-1 extent %lld exceeds 65535", (long long)pl.I);
+  dim3 grid(static_cast<unsigned>(bt_cdiv(pl.J, Cfg::BM)), static_cast<unsigned>(bt_cdiv(pl.R, 64)),
+            static_cast<unsigned>(pl.I));
+  tree_p_ws_kernel<Cfg><<<grid, Cfg::THREADS + 32, Cfg::SMEM_BYTES, st>>>(g, B, pl.R, m1part,
+                                                                          pl.jtiles, store_p);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
 template <int BN, int V, int VAR = 0>
 int launch_tree(const Plan& pl, const double* X, const double* C, const double* B, double* P,
                 double* m1part, int store_p, cudaStream_t st) {
@@ -824,6 +1014,7 @@ int run_tree(const Plan& pl, const double* X, const double* C, const double* B, 
           case 6: return launch_tree<64, 2, 6>(pl, X, C, B, P, m1part, store_p, st);
           case 7: return launch_tree<64, 2, 7>(pl, X, C, B, P, m1part, store_p, st);
           case 8: return launch_tree<64, 2, 8>(pl, X, C, B, P, m1part, store_p, st);
+          case 9: return launch_tree_ws<2>(pl, X, C, B, P, m1part, store_p, st);
           default: return launch_tree<64, 2>(pl, X, C, B, P, m1part, store_p, st);
         }
       }
