@@ -235,14 +235,23 @@ def _orthonormalize_block(y):
 
 def _complete(basis, g, need: int, block: int = 32):
     """``need`` orthonormal columns orthogonal to ``basis`` from a
-    deterministic Gaussian block, block by block: project out the accepted
-    columns, orthonormalise, twice (reorthogonalisation), sign-normalised.
-    Used once the remainder is at rounding level (or exhausted), where any
-    orthonormal completion is as good as LAPACK's."""
+    deterministic Gaussian block: project out the accepted columns, then
+    thin QR (CholeskyQR2 on the engine), twice for reorthogonalisation, and
+    sign-normalise.  Used once the remainder is at rounding level (or
+    exhausted), where any orthonormal completion is as good as LAPACK's.
+    Falls back to blockwise Loewdin orthonormalisation for thin blocks."""
     t = _dev.torch()
     n = int(g.shape[0])
     rng = np.random.default_rng(12345)
     y = _dev.to_device(rng.standard_normal((n, need)))
+    if need >= 8:
+        for _ in range(2):
+            if basis is not None:
+                y = _axpby(1.0, y, -1.0, gemm_dev(basis, gemm_dev(basis, y, ta=True)))
+            y, _ = qr_thin_dev(y)
+        out = y.contiguous()
+        N.call("bt_sign_fix_f64", _dev.ptr(out), n, int(need), _dev.stream())
+        return out
     cur = basis
     outs = []
     for j0 in range(0, need, block):
@@ -404,12 +413,53 @@ def _gemm_nn(a, b):
     return gemm_dev(a, b)
 
 
-def qr_thin_dev(ad):
-    """Thin QR with nonnegative diag(R) on device (single-CTA Householder)."""
+def _householder_qr(ad):
     m, n = int(ad.shape[0]), int(ad.shape[1])
     q = _dev.empty((m, n))
     r = _dev.empty((n, n))
     ws = _dev.workspace(N.load().bt_qr_thin_ws_bytes(m, n))
     N.call("bt_qr_thin_f64", _dev.ptr(ad.contiguous()), m, n, _dev.ptr(q), _dev.ptr(r),
            _dev.ptr(ws), int(ws.numel()) * 8, _dev.stream())
+    return q, r
+
+
+QR_CHOL_MAX_COND = 1e6   # CholeskyQR2 is used when the R-diagonal ratio stays below this
+
+
+def qr_thin_dev(ad):
+    """Thin QR with nonnegative diag(R) on device (decomp.py:182-193).
+
+    CholeskyQR2 on the engine: R1 = chol(A^T A)^T, Q1 = A R1^-1, then once
+    more on Q1 (orthogonality to working precision for cond(A) up to ~1e7;
+    the factorisation is unique for full column rank, so it equals LAPACK's
+    Householder result with the sign normalisation).  Falls back to the
+    single-CTA Householder kernel when A^T A is not numerically positive
+    definite or the diagonal of R spans more than QR_CHOL_MAX_COND."""
+    from .decomp import cholesky
+    from .errors import NotPositiveDefiniteError
+
+    m, n = int(ad.shape[0]), int(ad.shape[1])
+    if n < 8:
+        return _householder_qr(ad)
+    t = _dev.torch()
+    a = ad.contiguous()
+    rs = []
+    q = a
+    for _ in range(2):
+        g = gemm_dev(q, q, ta=True)
+        g = _axpby(0.5, g, 0.5, g.t().contiguous())
+        try:
+            low = _dev.to_device(cholesky(g))
+        except (NotPositiveDefiniteError, ShapeError):
+            return _householder_qr(ad)
+        d = _dev.to_host(t.diagonal(low).contiguous())
+        if not (d.min() > 0.0) or d.max() / d.min() > QR_CHOL_MAX_COND:
+            return _householder_qr(ad)
+        linv = _dev.empty((n, n))
+        ws = _dev.workspace(N.load().bt_tri_inv_lower_ws_bytes(n))
+        N.call("bt_tri_inv_lower_f64", _dev.ptr(low), n, _dev.ptr(linv), _dev.ptr(ws),
+               _dev.stream())
+        q = gemm_dev(q, linv, tb=True)                   # Q R^-1 = Q L^-T
+        rs.append(low.t().contiguous())                   # R = L^T (upper)
+    r = gemm_dev(rs[1], rs[0])                            # R = R2 R1 (upper, positive diagonal)
     return q, r

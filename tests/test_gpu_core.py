@@ -249,3 +249,24 @@ def test_pinv_sym_vs_numpy(R):
         ref = np.linalg.pinv(v)
         err = np.abs(out.cpu().numpy() - ref).max() / np.abs(ref).max()
         assert err < 1e-9, (R, err)
+
+
+@pytest.mark.parametrize("shape,cond", [((4096, 64), 1e2), ((2047, 96), 1e4), ((300, 40), 1e9),
+                                        ((50, 5), 1e1)])
+def test_qr_thin_vs_numpy(shape, cond):
+    """decomp.py:182-193 thin QR (diag R >= 0): CholeskyQR2 for moderate
+    conditioning, Householder fallback beyond (cond 1e9 case)."""
+    rng = np.random.default_rng(int(cond))
+    m, n = shape
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    a = (u * np.logspace(0, -np.log10(cond), n)) @ v.T
+    q, r = bt.qr_thin(a)
+    qo, ro = np.linalg.qr(a)
+    sg = np.sign(np.diag(ro))
+    sg[sg == 0] = 1
+    qo, ro = qo * sg, ro * sg[:, None]
+    assert np.all(np.diag(r) >= 0)
+    assert np.abs(q.T @ q - np.eye(n)).max() < 1e-12
+    assert np.linalg.norm(q @ r - a) <= 1e-13 * np.linalg.norm(a)
+    assert np.abs(r - ro).max() <= 1e-12 * cond * np.abs(ro).max()
