@@ -287,6 +287,8 @@ int bt_sign_fix_pair_f64(double* x, int64_t rows, int64_t cols, double* y, int64
  * first-index-fastest order (the C-order array of the axis-reversed tensor),
  * rank 1..6; the same call with the reversed extents inverts it. */
 int bt_reverse_axes_f64(const double* x, const int64_t* dims, int ndim, double* out, void* stream);
+/* out[i] = Philox4x32-10 Box-Muller normal of index i under key. */
+int bt_fill_normal_f64(double* out, int64_t n, uint64_t key, void* stream);
 /* out[i][j] = left[i] x[i][j] right[j] (left / right may be NULL). */
 int bt_diag_scale_f64(const double* x, int64_t rows, int64_t cols, const double* left,
                       const double* right, double* out, void* stream);

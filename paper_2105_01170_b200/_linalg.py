@@ -106,7 +106,7 @@ def _orth_svqb(y, passes: int = 1, drop: float = 1e3 * np.finfo(np.float64).eps)
     return gemm_dev(y, corr), dropped
 
 
-def _leading_subspace(gd, need: int, tau: float):
+def _leading_subspace(gd, need: int, tau: float, start=None):
     """Leading eigenpairs of a symmetric n x n Gram by block subspace
     iteration with Rayleigh-Ritz (GEMMs + thin QR + the one-CTA Jacobi on
     the b x b projection), b = min(need, 80) + 16 columns.
@@ -123,8 +123,13 @@ def _leading_subspace(gd, need: int, tau: float):
     b = min(n, min(need, SUB_MAX_BLOCK - SUB_OVERSAMPLE) + SUB_OVERSAMPLE)
     if b < 2 or b > SUB_MAX_BLOCK or 2 * b > n:
         return None
-    rng = np.random.default_rng(20210501 + n)
-    q, _ = _orth_svqb(_dev.to_device(rng.standard_normal((n, b))))
+    q0 = gaussian_dev(n, b, 20210501 + n)
+    if start is not None:
+        # warm start (HOOI: the previous sweep's basis spans the answer to
+        # within the sweep's change): its leading columns replace the Gaussian ones
+        ks = min(int(start.shape[1]), b - SUB_OVERSAMPLE)
+        q0[:, :ks] = start[:, :ks]
+    q, _ = _orth_svqb(q0)
     eps = np.finfo(np.float64).eps
     prev = None
     for it in range(SUB_MAX_ITERS):
@@ -233,6 +238,13 @@ def _orthonormalize_block(y):
     return out
 
 
+def gaussian_dev(rows: int, cols: int, key: int):
+    """Deterministic N(0,1) block on the device (Philox, index-addressable)."""
+    out = _dev.empty((rows, cols))
+    N.call("bt_fill_normal_f64", _dev.ptr(out), rows * cols, int(key), _dev.stream())
+    return out
+
+
 def _complete(basis, g, need: int, block: int = 32):
     """``need`` orthonormal columns orthogonal to ``basis`` from a
     deterministic Gaussian block: project out the accepted columns, then
@@ -242,8 +254,7 @@ def _complete(basis, g, need: int, block: int = 32):
     Falls back to blockwise Loewdin orthonormalisation for thin blocks."""
     t = _dev.torch()
     n = int(g.shape[0])
-    rng = np.random.default_rng(12345)
-    y = _dev.to_device(rng.standard_normal((n, need)))
+    y = gaussian_dev(n, need, 12345)
     if need >= 8:
         for _ in range(2):
             if basis is not None:
@@ -268,7 +279,7 @@ def _complete(basis, g, need: int, block: int = 32):
 
 
 def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_passes: int = 16,
-                   reduce=None):
+                   reduce=None, start=None):
     """Leading r left singular vectors of unfold(x, mode) (decomp.py:220-234),
     sign rule included.  extra_mode: basis of the column concatenation
     [unfold(x, mode), unfold(x, extra_mode)] (tucker_partial
@@ -280,6 +291,9 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
     re-Grams the remainder (SVD-grade accuracy for the fast-decaying spectra
     of C2/C3).  Once the remainder is at rounding level the
     basis is completed orthonormally (full_matrices completion, too).
+
+    start: optional (n x k) basis close to the answer (HOOI's previous sweep);
+    it seeds the first pass's subspace iteration.
 
     reduce: in-place cross-rank sum applied to every Gram, for a tensor
     sharded along a mode other than ``mode`` (each rank's Gram is then a
@@ -296,7 +310,8 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
         need = r - have
         if need <= 0:
             break
-        sub = _leading_subspace(g, need, RESOLVE_TAU) if SUBSPACE and n > SMALL_EIG else None
+        sub = (_leading_subspace(g, need, RESOLVE_TAU, start if basis is None else None)
+               if SUBSPACE and n > SMALL_EIG else None)
         if sub is not None:
             w, v, k_sub = sub
         else:

@@ -206,3 +206,20 @@ extern "C" int bt_build_cp_model_f64(const double* a0, const double* b0, const d
   if (R % 2 == 0) return run_model<2>(a0, b0, c0, I, J, K, R, k0, k1, noise, key, x, st);
   return run_model<1>(a0, b0, c0, I, J, K, R, k0, k1, noise, key, x, st);
 }
+
+// out[i] = Philox4x32-10 / Box-Muller normal of index i under `key`: the
+// deterministic Gaussian blocks of the eigensolver (subspace starts,
+// orthonormal completion), generated on the device.
+__global__ void bt_fill_normal_kernel(double* __restrict__ out, int64_t n, uint64_t key) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = philox_normal(static_cast<uint64_t>(i), key);
+}
+
+extern "C" int bt_fill_normal_f64(double* out, int64_t n, uint64_t key, void* stream) {
+  if (n <= 0) return BT_OK;
+  const int64_t blocks = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;
+  bt_fill_normal_kernel<<<static_cast<int>(blocks), 256, 0, bt_stream(stream)>>>(out, n, key);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}

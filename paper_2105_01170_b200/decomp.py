@@ -311,7 +311,7 @@ def hooi(t, init: TuckerRep, sweeps: int, shared=None) -> TuckerRep:
             for j in range(order):
                 if j != k and factors[j] is not None:
                     y = ttm_dev(y, j + 1, factors[j], int(factors[j].shape[1]), transpose=True)
-            u = L.mode_basis_dev(y, k + 1, int(factors[k].shape[1]))
+            u = L.mode_basis_dev(y, k + 1, int(factors[k].shape[1]), start=factors[k])
             factors[k] = u
             if shared is not None and k + 1 == shared[0]:
                 factors[shared[1] - 1] = u

@@ -186,10 +186,10 @@ class NativeTuckerOps:
     """Device kernels behind the sharded Tucker driver: mode bases (DMMA
     Gram + eigensolver, optional cross-rank Gram sum) and mode products."""
 
-    def mode_basis(self, x, mode, r, reduce=None):
+    def mode_basis(self, x, mode, r, reduce=None, start=None):
         from . import _linalg as L
 
-        return L.mode_basis_dev(x, mode, int(r), reduce=reduce)
+        return L.mode_basis_dev(x, mode, int(r), reduce=reduce, start=start)
 
     def ttm_t(self, x, mode, u):
         """x x_mode u^T (u: extent x r)."""
@@ -250,9 +250,9 @@ def hooi_sharded(ops, x_local, u, v, sweeps: int, p0: int, p1: int, allreduce, a
     for _ in range(int(sweeps)):
         z = ops.ttm_t(ops.ttm_t(x_local, 2, ops.rows(v, p0, p1)), 3, u)
         allreduce(z)
-        u = ops.mode_basis(z, 1, int(u.shape[1]))
+        u = ops.mode_basis(z, 1, int(u.shape[1]), start=u)
         y = allgather(ops.ttm_t(ops.ttm_t(x_local, 1, u), 3, u))
-        v = ops.mode_basis(y, 2, int(v.shape[1]))
+        v = ops.mode_basis(y, 2, int(v.shape[1]), start=v)
     if y is None:
         y = allgather(ops.ttm_t(ops.ttm_t(x_local, 1, u), 3, u))
     return u, v, ops.ttm_t(y, 2, v)

@@ -12,7 +12,7 @@ def _unfold(x, mode):
 
 
 class TorchCpuTuckerOps:
-    def mode_basis(self, x, mode, r, reduce=None):
+    def mode_basis(self, x, mode, r, reduce=None, start=None):
         m = _unfold(x, mode)
         g = (m @ m.T).contiguous()
         if reduce is not None:
