@@ -166,3 +166,36 @@ def test_c5_like_fit_monotone_and_deterministic():
     assert np.all(np.diff(h) >= -1e-12)                        # ALS fit never decreases
     assert np.array_equal(h, np.array(r2.fit_history))         # bit-reproducible
     assert torch.equal(r1.rep.x, r2.rep.x)
+
+
+def test_gather_scatter_detect_standin_full_size():
+    """The 32768 x 32768 stand-in (SURVEY §8d, 8.6 GB) at full size through
+    size-independent properties: the gathered tensor equals sqrt(eta_k) times
+    the class blocks bit for bit (blocks.py:445-448), the scatter reproduces
+    every sampled cell as the oracle's (t / sqrt(eta)) bit for bit, a
+    perturbed cell is reported at its scan rank, and detect_pattern recovers
+    the pattern.  (The oracle itself cannot hold three 8.6 GB copies.)"""
+    pat, blocks = configs.gather_standin()
+    bd = torch.from_numpy(blocks).cuda()
+    a = bt.struct_assemble(pat, bd)
+    t = bt.mat_to_tensor(a, pat)
+    w = np.sqrt(np.array(pat.counts, dtype=np.float64))
+    tb = t.permute(1, 0, 2).cpu().numpy()
+    for k in (0, 1, 63, 127):
+        assert np.array_equal(tb[k], blocks[k] * w[k])
+    back = bt.tensor_to_mat(t, pat)
+    rng = np.random.default_rng(3)
+    for _ in range(16):
+        i, j = (int(v) for v in rng.integers(0, 128, 2))
+        k = abs(i - j)
+        cell = back[i * 256:(i + 1) * 256, j * 256:(j + 1) * 256].cpu().numpy()
+        assert np.array_equal(cell, tb[k] / w[k])
+    pd, reps = bt.detect_pattern(a, 256, 256)
+    assert pd.p == pat.p and pd.structure_class == "toeplitz"
+    # same classes in the same order; cells within a class in row-major order
+    for x, y in zip(pd.placements, pat.placements):
+        assert np.array_equal(x, y[np.lexsort((y[:, 1], y[:, 0]))])
+    del back, t
+    a[5 * 256 + 7, 9 * 256 + 3] += 1.0      # cell (5, 9): class 4
+    with pytest.raises(bt.PatternMismatchError):
+        bt.mat_to_tensor(a, pat)
