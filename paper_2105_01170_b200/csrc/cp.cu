@@ -791,26 +791,10 @@ template <int BN, int VARIANT = 0>
 struct TreeCfgSel;
 template <int VARIANT>
 struct TreeCfgSel<64, VARIANT> {
-  // variants for tuning (BT_TREE_CFG): 0 default
+  // 128x64 tile, 4 warps of 64x32, 3 stages, 2 CTAs/SM (the tuned all-warps
+  // variant; profiles/r01_fp64_and_tuning.md lists the configurations tried)
   template <int V>
-  using Cfg = typename std::conditional<
-      VARIANT == 1, GemmCfg<128, 64, 16, 4, 2, 3, true, false, V>,
-      typename std::conditional<
-          VARIANT == 2, GemmCfg<128, 64, 32, 4, 2, 3, true, false, V>,
-          typename std::conditional<
-              VARIANT == 3, GemmCfg<128, 64, 32, 4, 2, 2, true, false, V>,
-              typename std::conditional<
-                  VARIANT == 4, GemmCfg<256, 64, 16, 8, 2, 3, true, false, V>,
-                  typename std::conditional<
-                      VARIANT == 5, GemmCfg<64, 64, 16, 2, 2, 4, true, false, V>,
-                      typename std::conditional<
-                          VARIANT == 6, GemmCfg<128, 64, 16, 2, 2, 3, true, false, V>,
-                          typename std::conditional<
-                              VARIANT == 7, GemmCfg<128, 64, 16, 4, 2, 2, true, false, V>,
-                              typename std::conditional<
-                                  VARIANT == 8, GemmCfg<64, 64, 16, 2, 2, 3, true, false, V>,
-                                  GemmCfg<128, 64, 16, 4, 2, 4, true, false, V>>::type>::type>::
-                          type>::type>::type>::type>::type>::type;
+  using Cfg = GemmCfg<128, 64, 16, 2, 2, 3, true, false, V>;
 };
 template <int VARIANT>
 struct TreeCfgSel<16, VARIANT> {
@@ -827,8 +811,9 @@ int tree_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("BT_TREE_CFG");
-    // 9: warp-specialised (4 DMMA warps of 64x32 + 1 cp.async producer warp,
-    // mbarrier ring, 3 stages) -- 72.5 vs 73.5 ms for variant 6 on C5
+    // 9 (default): warp-specialised -- 4 DMMA warps of 64x32 + 1 cp.async
+    // producer warp, mbarrier ring, 3 stages: 72.5 ms on C5; 6: the same
+    // tile with all warps loading and computing: 73.5 ms
     v = e ? atoi(e) : 9;
   }
   return v;
@@ -840,11 +825,7 @@ using ResCfg = GemmCfg<128, 64, 16, 4, 2, 3, true, true, V>;
 
 int tree_bn(int64_t R) { return R <= 8 ? 8 : (R <= 16 ? 16 : 64); }
 
-int tree_bm(int bn) {
-  if (bn != 64) return 128;
-  const int v = tree_variant();
-  return v == 4 ? 256 : ((v == 5 || v == 8) ? 64 : 128);
-}
+int tree_bm(int) { return 128; }
 
 struct Plan {
   int64_t I, J, K, R;
@@ -1005,18 +986,8 @@ int run_tree(const Plan& pl, const double* X, const double* C, const double* B, 
                 : launch_tree<16, 1>(pl, X, C, B, P, m1part, store_p, st);
     default:
       if (v2) {
-        switch (tree_variant()) {
-          case 1: return launch_tree<64, 2, 1>(pl, X, C, B, P, m1part, store_p, st);
-          case 2: return launch_tree<64, 2, 2>(pl, X, C, B, P, m1part, store_p, st);
-          case 3: return launch_tree<64, 2, 3>(pl, X, C, B, P, m1part, store_p, st);
-          case 4: return launch_tree<64, 2, 4>(pl, X, C, B, P, m1part, store_p, st);
-          case 5: return launch_tree<64, 2, 5>(pl, X, C, B, P, m1part, store_p, st);
-          case 6: return launch_tree<64, 2, 6>(pl, X, C, B, P, m1part, store_p, st);
-          case 7: return launch_tree<64, 2, 7>(pl, X, C, B, P, m1part, store_p, st);
-          case 8: return launch_tree<64, 2, 8>(pl, X, C, B, P, m1part, store_p, st);
-          case 9: return launch_tree_ws<2>(pl, X, C, B, P, m1part, store_p, st);
-          default: return launch_tree<64, 2>(pl, X, C, B, P, m1part, store_p, st);
-        }
+        return tree_variant() == 6 ? launch_tree<64, 2>(pl, X, C, B, P, m1part, store_p, st)
+                                   : launch_tree_ws<2>(pl, X, C, B, P, m1part, store_p, st);
       }
       return launch_tree<64, 1>(pl, X, C, B, P, m1part, store_p, st);
   }

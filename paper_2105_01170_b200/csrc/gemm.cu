@@ -130,7 +130,8 @@ int bt_gemm_launch(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits
 }
 
 // configurations ------------------------------------------------------------
-// (tuned on B200, tools/tune_gemm.py: 2 CTAs per SM with 64x32 warp tiles win)
+// (tuned on B200 with tools/tune_gemm.py -- the alternatives tried are listed
+// in profiles/r01_fp64_and_tuning.md; 2 CTAs per SM with 64x32 warp tiles win)
 // wide: 128x64 CTA tile, 4 warps of 64x32, BK 16, 4 stages (~102 KB smem, 2 CTAs/SM)
 template <bool AK, bool BKc, int V>
 using CfgWide = GemmCfg<128, 64, 16, 2, 2, 4, AK, BKc, V>;
@@ -141,31 +142,6 @@ using CfgNarrow = GemmCfg<128, 16, 16, 8, 1, 4, AK, BKc, V>;
 // 2 stages (~78 KB smem, 2 CTAs/SM)
 template <bool AK, bool BKc, int V>
 using CfgSquare = GemmCfg<128, 128, 16, 2, 4, 2, AK, BKc, V>;
-
-// tuning alternatives (selected with BT_GEMM_CFG=<id> for experiments)
-template <bool AK, bool BKc, int V>
-using CfgWideK32 = GemmCfg<128, 64, 32, 4, 2, 3, AK, BKc, V>;
-template <bool AK, bool BKc, int V>
-using CfgBig = GemmCfg<128, 128, 16, 2, 4, 3, AK, BKc, V>;
-template <bool AK, bool BKc, int V>
-using CfgTall = GemmCfg<256, 64, 16, 4, 2, 3, AK, BKc, V>;
-template <bool AK, bool BKc, int V>
-using CfgW4 = GemmCfg<128, 64, 16, 2, 2, 4, AK, BKc, V>;
-template <bool AK, bool BKc, int V>
-using CfgW4s3 = GemmCfg<128, 64, 16, 2, 2, 3, AK, BKc, V>;
-template <bool AK, bool BKc, int V>
-using CfgW4k32 = GemmCfg<128, 64, 32, 2, 2, 2, AK, BKc, V>;
-template <bool AK, bool BKc, int V>
-using CfgBig2 = GemmCfg<128, 128, 16, 2, 4, 2, AK, BKc, V>;
-
-static int bt_tune_cfg() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("BT_GEMM_CFG");
-    v = e ? atoi(e) : -1;
-  }
-  return v;
-}
 
 enum BtTileClass { BT_TILE_WIDE = 0, BT_TILE_NARROW = 1, BT_TILE_SQUARE = 2 };
 
@@ -242,18 +218,6 @@ int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, i
   }
   if (cls == BT_TILE_SQUARE)
     return bt_dispatch_layout<CfgSquare>(g, batch, st, ak, bk, vec, want_splits);
-  if (cls == BT_TILE_WIDE) {
-    switch (bt_tune_cfg()) {
-      case 1: return bt_dispatch_layout<CfgWideK32>(g, batch, st, ak, bk, vec, want_splits);
-      case 2: return bt_dispatch_layout<CfgBig>(g, batch, st, ak, bk, vec, want_splits);
-      case 3: return bt_dispatch_layout<CfgTall>(g, batch, st, ak, bk, vec, want_splits);
-      case 4: return bt_dispatch_layout<CfgW4>(g, batch, st, ak, bk, vec, want_splits);
-      case 5: return bt_dispatch_layout<CfgW4s3>(g, batch, st, ak, bk, vec, want_splits);
-      case 6: return bt_dispatch_layout<CfgW4k32>(g, batch, st, ak, bk, vec, want_splits);
-      case 7: return bt_dispatch_layout<CfgBig2>(g, batch, st, ak, bk, vec, want_splits);
-      default: break;
-    }
-  }
   if (cls == BT_TILE_NARROW)
     return bt_dispatch_layout<CfgNarrow>(g, batch, st, ak, bk, vec, want_splits);
   return bt_dispatch_layout<CfgWide>(g, batch, st, ak, bk, vec, want_splits);
