@@ -249,6 +249,22 @@ def extras_run(torch, budget_s=240.0):
         from paper_2105_01170_b200.tensor import fro_norm_dev
 
         out["c3_core_norm_ratio"] = fro_norm_dev(rep.core) / fro_norm_dev(t3)
+        # K7 / K9 kernel rooflines at C3: the mode-1 unfolding Gram (SYRK over
+        # the 1024 x 524288 unfolding, unique-half work n(n+1)N/n flops, SURVEY
+        # 8d) and the first TTM t x1 U^T (2 r N flops)
+        from paper_2105_01170_b200 import _linalg
+        from paper_2105_01170_b200.tensor import ttm_dev
+
+        n1 = int(t3.shape[0])
+        big_n = t3.numel() // n1
+        ms_g = timed(torch, lambda: _linalg.unfold_gram_dev(t3, 1), 3, 1)
+        u = rep.factors[0] if torch.is_tensor(rep.factors[0]) else torch.from_numpy(
+            np.ascontiguousarray(rep.factors[0])).cuda()
+        ms_t = timed(torch, lambda: ttm_dev(t3, 1, u, int(u.shape[1]), transpose=True), 3, 1)
+        out["c3_gram_mode1_ms"] = ms_g
+        out["c3_gram_mode1_tflops"] = n1 * (n1 + 1) * big_n / ms_g / 1e9
+        out["c3_ttm_mode1_ms"] = ms_t
+        out["c3_ttm_mode1_tflops"] = 2.0 * int(u.shape[1]) * t3.numel() / ms_t / 1e9
         del t3, rep
         torch.cuda.empty_cache()
     except Exception as exc:  # pragma: no cover - reported, not fatal
@@ -610,6 +626,9 @@ def run_bt200(args, rank, world):
             result["cpu_baseline"] = {"value": None, "error": repr(exc)[:300]}
     if not args.no_extras and rank == 0:
         ex = extras_run(torch)
+        for key in ("c3_gram_mode1", "c3_ttm_mode1"):
+            if isinstance(ex.get(key + "_tflops"), float):
+                ex[key + "_frac_dmma"] = ex[key + "_tflops"] / peak
         result["extras"] = ex
         if not args.no_cpu and world == 1:
             cpu = extras_cpu()
