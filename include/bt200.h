@@ -277,6 +277,10 @@ int bt_transpose_check_f64(const double* blocks, int64_t p, int64_t n, const int
                            double tol, void* ws, int64_t* bad_class, void* stream);
 /* out = 1 / sqrt(x) elementwise */
 int bt_inv_sqrt_f64(const double* x, int64_t n, double* out, void* stream);
+/* out[0] = trace(m), m n x n row-major (device double out) */
+int bt_trace_f64(const double* m, int64_t n, double* out, void* stream);
+/* SVQB column scaling: dinv = diag(m)^-1/2 (0 for a zero diagonal), out = D (m + m^T)/2 D */
+int bt_sym_scale_f64(const double* m, int64_t b, double* dinv, double* out, void* stream);
 /* sign rule (decomp.py:176-179) on every column of a row-major matrix */
 int bt_sign_fix_f64(double* x, int64_t rows, int64_t cols, void* stream);
 /* Same rule on x, with every flipped column also flipped in y (yrows x cols):

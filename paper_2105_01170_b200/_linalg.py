@@ -69,29 +69,34 @@ SUB_RESID = 32.0      # accept a Ritz pair at ||G v - theta v|| <= SUB_RESID eps
 
 def _orth_svqb(y, passes: int = 1, drop: float = 1e3 * np.finfo(np.float64).eps):
     """Orthonormal basis of the numerically significant part of span(y)
-    (n x b, n >> b) by SVQB: Y^T Y = V diag(mu) V^T (one-CTA Jacobi),
-    Q = Y V_k diag(mu_k)^-1/2 over the mu_k > drop * mu_max.  The dropped
-    directions have singular values below ~sqrt(drop) of the largest (far
-    below what the subspace iteration accepts).  One Newton-Schulz step
-    Q (3I - Q^T Q) / 2 then squares the remaining orthogonality error (GEMMs
-    only).  Returns (q, dropped)."""
+    (n x b, n >> b) by column-scaled SVQB: D = diag(Y^T Y)^-1/2,
+    D Y^T Y D = V diag(mu) V^T (one-CTA Jacobi), Q = Y D V_k diag(mu_k)^-1/2
+    over the mu_k > drop * mu_max.  The scaling keeps graded blocks intact
+    (G Q for a spectrum that falls below eps * lambda_1 inside the block:
+    those columns are rounding-level but still independent directions), so
+    only near-dependent columns -- angle below ~sqrt(drop) -- or zero columns
+    are dropped.  One Newton-Schulz step Q (3I - Q^T Q) / 2 then squares the
+    remaining orthogonality error (GEMMs only).  Returns (q, dropped)."""
     dropped = 0
     for _ in range(passes):
+        b, rows = int(y.shape[1]), int(y.shape[0])
         m = gemm_dev(y, y, ta=True)
-        m = _axpby(0.5, m, 0.5, m.t().contiguous())
-        w, v = eigh_dev(m)                       # descending
+        dinv = _dev.empty((b,))
+        ms = _dev.empty((b, b))
+        N.call("bt_sym_scale_f64", _dev.ptr(m), b, _dev.ptr(dinv), _dev.ptr(ms), _dev.stream())
+        w, v = eigh_dev(ms)                      # descending
         wh = _dev.to_host(w)
         if not wh[0] > 0.0:
             return None, 0
         keep = int(np.sum(wh > drop * wh[0]))
-        dropped += int(y.shape[1]) - keep
+        dropped += b - keep
         s = _dev.empty((keep,))
         N.call("bt_inv_sqrt_f64", _dev.ptr(w), keep, _dev.ptr(s), _dev.stream())
-        b, rows = int(v.shape[0]), int(y.shape[0])
         out = _dev.empty((rows, keep))
         d = N.GemmDesc()
         d.M, d.N, d.Kin, d.Kout, d.batch = rows, keep, b, 1, 1
         d.A, d.sAm, d.sAki = _dev.ptr(y), b, 1
+        d.ascale, d.s_ascale_ko = _dev.ptr(dinv), 0    # Y D: D rides on A's reduction index
         d.B, d.sBn, d.sBki = _dev.ptr(v), 1, b      # V[:, :keep] addressed in place
         d.bscale, d.s_scale_ko = _dev.ptr(s), 0
         d.C, d.sCm, d.sCn = _dev.ptr(out), keep, 1
@@ -106,7 +111,7 @@ def _orth_svqb(y, passes: int = 1, drop: float = 1e3 * np.finfo(np.float64).eps)
     return gemm_dev(y, corr), dropped
 
 
-def _leading_subspace(gd, need: int, tau: float, start=None):
+def _leading_subspace(gd, need: int, tau: float, start=None, hint=None):
     """Leading eigenpairs of a symmetric n x n Gram by block subspace
     iteration with Rayleigh-Ritz (GEMMs + thin QR + the one-CTA Jacobi on
     the b x b projection), b = min(need, 80) + 16 columns.
@@ -120,7 +125,8 @@ def _leading_subspace(gd, need: int, tau: float, start=None):
     Accuracy per accepted pair is the Gram eigensolver's (residual / gap);
     the deflation passes of mode_basis_dev handle the rest."""
     n = int(gd.shape[0])
-    b = min(n, min(need, SUB_MAX_BLOCK - SUB_OVERSAMPLE) + SUB_OVERSAMPLE)
+    want = need if hint is None else max(1, min(need, int(hint)))
+    b = min(n, min(want, SUB_MAX_BLOCK - SUB_OVERSAMPLE) + SUB_OVERSAMPLE)
     if b < 2 or b > SUB_MAX_BLOCK or 2 * b > n:
         return None
     q0 = gaussian_dev(n, b, 20210501 + n)
@@ -166,6 +172,18 @@ def _leading_subspace(gd, need: int, tau: float, start=None):
         if worst <= target:
             N.call("bt_sign_fix_f64", _dev.ptr(v), n, bq, _dev.stream())
             return w, v, k
+        if (prev is None and start is None and not dropped and k >= 1 and worst > 0.0
+                and wh[-1] > 0.0):
+            # cold start: the residual of pair k falls roughly like
+            # (lambda_{b+1} / lambda_k)^it; the last Ritz value stands in for
+            # lambda_{b+1}.  A slowly decaying block edge (C3 mode 1) goes
+            # straight to the tridiagonal solver instead of spending
+            # iterations to measure the rate.  Only for an intact block: when
+            # SVQB dropped columns the last Ritz value is not near lambda_b.
+            rate0 = float(wh[-1]) / float(wh[k - 1])
+            if rate0 >= 1.0 or np.log(target / worst) / np.log(max(rate0, 1e-300)) > \
+                    1.5 * (SUB_MAX_ITERS - 1):
+                return None
         if prev is not None and worst > 0.0:
             rate = worst / prev                    # linear convergence factor
             left = SUB_MAX_ITERS - 1 - it
@@ -278,6 +296,22 @@ def _complete(basis, g, need: int, block: int = 32):
     return out
 
 
+def _next_pass_hint(wh, k: int):
+    """Predicted number of directions the next deflation pass resolves: the
+    eigen/Ritz values below this pass's cut approximate the remainder's
+    spectrum, so the next pass keeps about those above RESOLVE_TAU times the
+    first of them.  Sizes the next subspace block only (acceptance is always
+    by residual)."""
+    tail = np.asarray(wh[k:], dtype=np.float64)
+    if tail.size >= 6 and tail[0] > 0.0:
+        cnt = int(np.sum(tail > RESOLVE_TAU * tail[0]))
+        if cnt < tail.size - 4:
+            return cnt + 2
+    # unconverged Ritz values above the cut (or too short a tail): passes of
+    # a steadily decaying spectrum resolve about as many as this one did
+    return k + 4
+
+
 def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_passes: int = 16,
                    reduce=None, start=None):
     """Leading r left singular vectors of unfold(x, mode) (decomp.py:220-234),
@@ -305,13 +339,20 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
     g = _gram_modes(xd, modes, reduce)
     basis = None
     top = None
+    hint = None
     for _ in range(max_passes):
         have = 0 if basis is None else int(basis.shape[1])
         need = r - have
         if need <= 0:
             break
-        sub = (_leading_subspace(g, need, RESOLVE_TAU, start if basis is None else None)
-               if SUBSPACE and n > SMALL_EIG else None)
+        cold = start is None or basis is not None
+        # a cold block of >= 48 wanted pairs oversamples by 1/3 at most, so it
+        # converges at the spectrum's own rate near the block edge (C3 mode 1:
+        # lambda_81 / lambda_64 = 0.6); up to n ~ 1.5k the tridiagonal solver
+        # is cheaper than the iteration needed to measure that
+        direct = cold and hint is None and need >= 48 and n <= 1536
+        sub = (_leading_subspace(g, need, RESOLVE_TAU, start if basis is None else None, hint)
+               if SUBSPACE and n > SMALL_EIG and not direct else None)
         if sub is not None:
             w, v, k_sub = sub
         else:
@@ -329,6 +370,7 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
         if basis is None and k >= need:
             return v[:, :need].contiguous()         # one pass resolved everything
         k = max(1, min(need, k))
+        hint = _next_pass_hint(wh, k)
         new = v[:, :k].contiguous()
         if basis is not None:
             new = _orth_normalize(basis, new)
@@ -343,6 +385,12 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
         del res
         if reduce is not None:
             reduce(g)
+        # trace >= lambda_max: a remainder already at rounding level goes
+        # straight to the completion without an eigensolve
+        tr = _dev.empty((1,))
+        N.call("bt_trace_f64", _dev.ptr(g), n, _dev.ptr(tr), _dev.stream())
+        if float(_dev.to_host(tr)[0]) <= NOISE_REL * top:
+            break
     have = 0 if basis is None else int(basis.shape[1])
     if have < r:
         extra = _complete(basis, g, r - have)

@@ -119,6 +119,8 @@ _SIGS = {
     "bt_maxabs_f64": (C.c_int, [_dp, _i64, _dp, _dp, _i64, _dp]),
     "bt_transpose_check_f64": (C.c_int, [_dp, _i64, _i64, _dp, C.c_double, _dp, _P(_i64), _dp]),
     "bt_inv_sqrt_f64": (C.c_int, [_dp, _i64, _dp, _dp]),
+    "bt_sym_scale_f64": (C.c_int, [_dp, _i64, _dp, _dp, _dp]),
+    "bt_trace_f64": (C.c_int, [_dp, _i64, _dp, _dp]),
     "bt_sign_fix_f64": (C.c_int, [_dp, _i64, _i64, _dp]),
     "bt_col_normalize_f64": (C.c_int, [_dp, _i64, _i64, _dp]),
     "bt_axpby_f64": (C.c_int, [_i64, C.c_double, _dp, C.c_double, _dp, _dp, _dp]),

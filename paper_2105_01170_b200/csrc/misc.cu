@@ -418,6 +418,55 @@ extern "C" int bt_inv_sqrt_f64(const double* x, int64_t n, double* out, void* st
   return BT_OK;
 }
 
+// out[0] = trace(m) for an n x n row-major matrix (one CTA, fixed-order
+// reduction): an upper bound on lambda_max of a PSD Gram.
+__global__ void bt_trace_kernel(const double* __restrict__ m, int64_t n, double* __restrict__ out) {
+  __shared__ double part[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += m[i * n + i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = (threadIdx.x < (blockDim.x >> 5)) ? part[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) out[0] = s;
+  }
+}
+
+extern "C" int bt_trace_f64(const double* m, int64_t n, double* out, void* stream) {
+  bt_trace_kernel<<<1, 256, 0, bt_stream(stream)>>>(m, n, out);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+// Column-scaled symmetric Gram for SVQB: dinv[j] = m_jj > 0 ? m_jj^-1/2 : 0,
+// out = D sym(m) D with sym(m) = (m + m^T) / 2 (b x b, row-major).  Graded
+// blocks (G Q with a fast-decaying spectrum) then keep every column instead
+// of losing the small ones to the relative drop threshold.
+__global__ void bt_sym_scale_kernel(const double* __restrict__ m, int64_t b,
+                                    double* __restrict__ dinv, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < b * b;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / b, j = e - i * b;
+    const double di = m[i * b + i], dj = m[j * b + j];
+    const double si = di > 0.0 ? 1.0 / sqrt(di) : 0.0;
+    const double sj = dj > 0.0 ? 1.0 / sqrt(dj) : 0.0;
+    out[e] = (0.5 * (m[i * b + j] + m[j * b + i])) * si * sj;
+    if (i == j) dinv[i] = si;
+  }
+}
+
+extern "C" int bt_sym_scale_f64(const double* m, int64_t b, double* dinv, double* out,
+                                void* stream) {
+  if (b <= 0) return BT_OK;
+  const int64_t n = b * b;
+  bt_sym_scale_kernel<<<static_cast<int>((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024), 256, 0,
+                        bt_stream(stream)>>>(m, b, dinv, out);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
 // ---------------------------------------------------------------------------
 // axis reversal (container payloads, container.py:111-159): out is the
 // C-order array of the axis-reversed tensor, i.e. x's elements in
