@@ -342,8 +342,18 @@ __global__ void count_above_kernel(const double* __restrict__ d, const double* _
   *count = n - sturm_less(d, e2, n, x, bounds[2]);
 }
 
-// cluster starts: start[c] = 1 if c == 0 or w[c-1] - w[c] > 1e-3 ||T||;
-// eigenvalues at or below tau * |w0| get no vector (start = -1)
+// Cluster codes: start[c] = 1 opens a cluster (c == 0 or gap w[c-1] - w[c]
+// > 1e-3 ||T||, dstein's rule); 2 opens a tight sub-cluster inside one
+// (gap > TIGHT_GAP ||T||); 0 continues the current sub-cluster; -1 = no
+// vector (eigenvalue at or below tau * |w0|).  Inverse iteration runs one
+// warp per tight sub-cluster (MGS inside it, as dstein does for the whole
+// cluster): a vector of a sub-cluster separated by more than TIGHT_GAP ||T||
+// is accurate to ~eps / TIGHT_GAP on its own, so only the orthogonality
+// across sub-clusters is left, restored by cluster_orth_kernel.  This keeps
+// the sequential MGS chains short on smoothly decaying spectra (C3 mode 1:
+// one 1e-3 cluster of ~50 eigenvalues).
+constexpr double TIGHT_GAP = 1e-6;
+
 __global__ void cluster_kernel(const double* __restrict__ w, int64_t nvec,
                                const double* __restrict__ bounds, double tau,
                                int* __restrict__ start) {
@@ -353,11 +363,67 @@ __global__ void cluster_kernel(const double* __restrict__ w, int64_t nvec,
     start[c] = -1;
     return;
   }
-  start[c] = (c == 0 || (w[c - 1] - w[c]) > 1e-3 * bounds[3]) ? 1 : 0;
+  if (c == 0) {
+    start[c] = 1;
+    return;
+  }
+  const double gap = w[c - 1] - w[c];
+  start[c] = gap > 1e-3 * bounds[3] ? 1 : (gap > TIGHT_GAP * bounds[3] ? 2 : 0);
 }
 
-// Inverse iteration: one warp per cluster (a warp whose first vector is not a
-// cluster start exits).  Y is stored vector-major: y[c * n + i].
+// Orthonormalise each 1e-3 cluster that holds more than one tight
+// sub-cluster: classical Gram-Schmidt with one reorthogonalisation (CGS2)
+// over its vectors in order, one CTA per cluster.  The vectors are already
+// orthogonal to ~eps / TIGHT_GAP, so this only polishes them.
+__global__ void __launch_bounds__(1024)
+    cluster_orth_kernel(int64_t n, int64_t nvec, const int* __restrict__ start,
+                        double* __restrict__ y) {
+  extern __shared__ __align__(16) double dots[];
+  __shared__ double red[32];
+  const int64_t c0 = blockIdx.x;
+  if (c0 >= nvec || start[c0] != 1) return;
+  int64_t c1 = c0 + 1;
+  bool multi = false;
+  while (c1 < nvec && (start[c1] == 0 || start[c1] == 2)) {
+    multi |= start[c1] == 2;
+    ++c1;
+  }
+  if (!multi) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t c = c0 + 1; c < c1; ++c) {
+    double* yc = y + c * n;
+    const int64_t k = c - c0;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int64_t o = warp; o < k; o += nw) {
+        const double* yo = y + (c0 + o) * n;
+        double s = 0.0;
+        for (int64_t i = lane; i < n; i += 32) s = fma(yo[i], yc[i], s);
+        s = warp_sum(s);
+        if (lane == 0) dots[o] = s;
+      }
+      __syncthreads();
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        double acc = yc[i];
+        for (int64_t o = 0; o < k; ++o) acc = fma(-dots[o], y[(c0 + o) * n + i], acc);
+        yc[i] = acc;
+      }
+      __syncthreads();
+    }
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(yc[i], yc[i], s);
+    s = warp_sum(s);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += red[w];
+    const double inv = (t > 0.0) ? 1.0 / sqrt(t) : 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) yc[i] *= inv;
+    __syncthreads();
+  }
+}
+
+// Inverse iteration: one warp per tight sub-cluster (a warp whose first
+// vector does not open one exits).  Y is stored vector-major: y[c * n + i].
 __global__ void __launch_bounds__(32)
     invit_kernel(const double* __restrict__ d, const double* __restrict__ e, int64_t n,
                  int64_t nvec, const double* __restrict__ wv, const int* __restrict__ start,
@@ -647,6 +713,15 @@ extern "C" int bt_syevx_f64(const double* a, int64_t n, int64_t nvec, double vec
   BT_LAUNCH_CHECK();
   invit_kernel<<<static_cast<unsigned>(nvec), 32, 0, st>>>(d, e, n, nvec, w, start, bounds, y, scr);
   BT_LAUNCH_CHECK();
+  {
+    const size_t sm = sizeof(double) * static_cast<size_t>(nvec);
+    if (sm > 48 * 1024)
+      BT_CUDA_CHECK(cudaFuncSetAttribute(cluster_orth_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sm)));
+    cluster_orth_kernel<<<static_cast<unsigned>(nvec), 1024, sm, st>>>(n, nvec, start, y);
+    BT_LAUNCH_CHECK();
+  }
   if (dbg) cudaEventRecord(ev[3], st);
   {
     const size_t sm = sizeof(double) * 8 * n;

@@ -138,12 +138,16 @@ using CfgWide = GemmCfg<128, 64, 16, 2, 2, 4, AK, BKc, V>;
 // narrow: 128x16 CTA tile for N <= 16 (Grams of R <= 16 factors, TTM r <= 16)
 template <bool AK, bool BKc, int V>
 using CfgNarrow = GemmCfg<128, 16, 16, 8, 1, 4, AK, BKc, V>;
+// mid: 128x32 CTA tile for 16 < N <= 32 (TTM to r <= 32, e.g. C3's mode-2
+// projection), 4 warps of 32x32
+template <bool AK, bool BKc, int V>
+using CfgMid = GemmCfg<128, 32, 16, 4, 1, 4, AK, BKc, V>;
 // square: 128x128 for N > 64 and symmetric (SYRK) outputs, 8 warps of 64x32,
 // 2 stages (~78 KB smem, 2 CTAs/SM)
 template <bool AK, bool BKc, int V>
 using CfgSquare = GemmCfg<128, 128, 16, 2, 4, 2, AK, BKc, V>;
 
-enum BtTileClass { BT_TILE_WIDE = 0, BT_TILE_NARROW = 1, BT_TILE_SQUARE = 2 };
+enum BtTileClass { BT_TILE_WIDE = 0, BT_TILE_NARROW = 1, BT_TILE_SQUARE = 2, BT_TILE_MID = 3 };
 
 template <template <bool, bool, int> class C>
 static int bt_dispatch_layout(const BtGemmArgs& g, int64_t batch, cudaStream_t st, bool ak,
@@ -158,6 +162,14 @@ static int bt_dispatch_layout(const BtGemmArgs& g, int64_t batch, cudaStream_t s
   if (ak && !bk) return bt_gemm_launch<C<true, false, 1>>(g, batch, st, want_splits);
   if (!ak && bk) return bt_gemm_launch<C<false, true, 1>>(g, batch, st, want_splits);
   return bt_gemm_launch<C<false, false, 1>>(g, batch, st, want_splits);
+}
+
+static int bt_tile_class(const BtGemmArgs& g) {
+  if (g.symmetric) return BT_TILE_SQUARE;
+  if (g.N <= 16) return BT_TILE_NARROW;
+  static const bool no_mid = getenv("BT_GEMM_NO_MID") != nullptr;  // A/B switch (tools)
+  if (g.N <= 32 && !no_mid) return BT_TILE_MID;
+  return g.N <= 64 ? BT_TILE_WIDE : BT_TILE_SQUARE;
 }
 
 static bool even_aligned(const double* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -197,14 +209,15 @@ int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, i
                   (b_row % 2 == 0) && (g.A.s_ko % 2 == 0) && (g.B.s_ko % 2 == 0) &&
                   (g.A.s_b % 2 == 0) && (g.B.s_b % 2 == 0);
   const int vec = v2 ? 2 : 1;
-  int cls = g.symmetric ? BT_TILE_SQUARE
-                        : (g.N <= 16 ? BT_TILE_NARROW : (g.N <= 64 ? BT_TILE_WIDE : BT_TILE_SQUARE));
+  int cls = bt_tile_class(g);
   // workspace check (computed with the same geometry the launcher will use)
   BtGemmArgs probe = g;
   if (cls == BT_TILE_SQUARE)
     bt_gemm_geometry<CfgSquare<true, true, 1>>(probe, batch, want_splits);
   else if (cls == BT_TILE_NARROW)
     bt_gemm_geometry<CfgNarrow<true, true, 1>>(probe, batch, want_splits);
+  else if (cls == BT_TILE_MID)
+    bt_gemm_geometry<CfgMid<true, true, 1>>(probe, batch, want_splits);
   else
     bt_gemm_geometry<CfgWide<true, true, 1>>(probe, batch, want_splits);
   const int64_t need = (probe.splits > 1 || g.symmetric) ? batch * probe.splits * g.M * g.N : 0;
@@ -220,18 +233,21 @@ int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, i
     return bt_dispatch_layout<CfgSquare>(g, batch, st, ak, bk, vec, want_splits);
   if (cls == BT_TILE_NARROW)
     return bt_dispatch_layout<CfgNarrow>(g, batch, st, ak, bk, vec, want_splits);
+  if (cls == BT_TILE_MID)
+    return bt_dispatch_layout<CfgMid>(g, batch, st, ak, bk, vec, want_splits);
   return bt_dispatch_layout<CfgWide>(g, batch, st, ak, bk, vec, want_splits);
 }
 
 int64_t bt_gemm_ws_elems(BtGemmArgs g, int64_t batch) {
   if (!g.symmetric && g.bscale == nullptr && g.ascale == nullptr && g.N > g.M && g.N > 64)
     std::swap(g.M, g.N);
-  int cls = g.symmetric ? BT_TILE_SQUARE
-                        : (g.N <= 16 ? BT_TILE_NARROW : (g.N <= 64 ? BT_TILE_WIDE : BT_TILE_SQUARE));
+  int cls = bt_tile_class(g);
   if (cls == BT_TILE_SQUARE)
     bt_gemm_geometry<CfgSquare<true, true, 1>>(g, batch, 0);
   else if (cls == BT_TILE_NARROW)
     bt_gemm_geometry<CfgNarrow<true, true, 1>>(g, batch, 0);
+  else if (cls == BT_TILE_MID)
+    bt_gemm_geometry<CfgMid<true, true, 1>>(g, batch, 0);
   else
     bt_gemm_geometry<CfgWide<true, true, 1>>(g, batch, 0);
   return (g.splits > 1 || g.symmetric) ? batch * g.splits * g.M * g.N : 0;
