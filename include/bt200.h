@@ -277,6 +277,18 @@ int bt_transpose_check_f64(const double* blocks, int64_t p, int64_t n, const int
                            double tol, void* ws, int64_t* bad_class, void* stream);
 /* out = 1 / sqrt(x) elementwise */
 int bt_inv_sqrt_f64(const double* x, int64_t n, double* out, void* stream);
+/* Leading eigenpairs of a symmetric n x n Gram by block subspace iteration
+ * with Rayleigh-Ritz (block b = min(min(need, hint>0 ? hint : need), 80) + 16;
+ * optional warm-start columns start (n x start_cols)).  On *status == 0:
+ * w[0..bq) Ritz values descending, v (n x bq, row-major) sign-normalised
+ * Ritz vectors, *k_out leading pairs above tau*w[0] with residual
+ * <= 32 eps w[0].  *status 1: no convergence (use bt_syevx_f64), 2: block
+ * shape not applicable.  Synchronises the stream (host-side decisions). */
+int64_t bt_leading_subspace_ws_bytes(int64_t n, int64_t need, int64_t hint);
+int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need, double tau,
+                            const double* start, int64_t start_cols, int64_t hint, double* w,
+                            double* v, int64_t* bq_out, int64_t* k_out, int* status, void* ws,
+                            int64_t ws_bytes, void* stream);
 /* out[0] = trace(m), m n x n row-major (device double out) */
 int bt_trace_f64(const double* m, int64_t n, double* out, void* stream);
 /* SVQB column scaling: dinv = diag(m)^-1/2 (0 for a zero diagonal), out = D (m + m^T)/2 D */

@@ -63,135 +63,44 @@ _DEBUG = bool(os.environ.get("BT_BASIS_DEBUG"))
 SUBSPACE = os.environ.get("BT_SUBSPACE", "1") != "0"
 SUB_OVERSAMPLE = 16
 SUB_MAX_BLOCK = 96     # Rayleigh-Ritz matrices stay on the one-CTA Jacobi path
-SUB_MAX_ITERS = 10
-SUB_RESID = 32.0      # accept a Ritz pair at ||G v - theta v|| <= SUB_RESID eps theta_1
-
-
-def _orth_svqb(y, passes: int = 1, drop: float = 1e3 * np.finfo(np.float64).eps):
-    """Orthonormal basis of the numerically significant part of span(y)
-    (n x b, n >> b) by column-scaled SVQB: D = diag(Y^T Y)^-1/2,
-    D Y^T Y D = V diag(mu) V^T (one-CTA Jacobi), Q = Y D V_k diag(mu_k)^-1/2
-    over the mu_k > drop * mu_max.  The scaling keeps graded blocks intact
-    (G Q for a spectrum that falls below eps * lambda_1 inside the block:
-    those columns are rounding-level but still independent directions), so
-    only near-dependent columns -- angle below ~sqrt(drop) -- or zero columns
-    are dropped.  One Newton-Schulz step Q (3I - Q^T Q) / 2 then squares the
-    remaining orthogonality error (GEMMs only).  Returns (q, dropped)."""
-    dropped = 0
-    for _ in range(passes):
-        b, rows = int(y.shape[1]), int(y.shape[0])
-        m = gemm_dev(y, y, ta=True)
-        dinv = _dev.empty((b,))
-        ms = _dev.empty((b, b))
-        N.call("bt_sym_scale_f64", _dev.ptr(m), b, _dev.ptr(dinv), _dev.ptr(ms), _dev.stream())
-        w, v = eigh_dev(ms)                      # descending
-        wh = _dev.to_host(w)
-        if not wh[0] > 0.0:
-            return None, 0
-        keep = int(np.sum(wh > drop * wh[0]))
-        dropped += b - keep
-        s = _dev.empty((keep,))
-        N.call("bt_inv_sqrt_f64", _dev.ptr(w), keep, _dev.ptr(s), _dev.stream())
-        out = _dev.empty((rows, keep))
-        d = N.GemmDesc()
-        d.M, d.N, d.Kin, d.Kout, d.batch = rows, keep, b, 1, 1
-        d.A, d.sAm, d.sAki = _dev.ptr(y), b, 1
-        d.ascale, d.s_ascale_ko = _dev.ptr(dinv), 0    # Y D: D rides on A's reduction index
-        d.B, d.sBn, d.sBki = _dev.ptr(v), 1, b      # V[:, :keep] addressed in place
-        d.bscale, d.s_scale_ko = _dev.ptr(s), 0
-        d.C, d.sCm, d.sCn = _dev.ptr(out), keep, 1
-        d.alpha, d.beta = 1.0, 0.0
-        ws = _dev.workspace(N.load().bt_gemm_f64_ws_bytes(C.byref(d)))
-        N.call("bt_gemm_f64", C.byref(d), _dev.ptr(ws), int(ws.numel()) * 8, _dev.stream())
-        y = out
-    t = _dev.torch()
-    kq = int(y.shape[1])
-    m = gemm_dev(y, y, ta=True)
-    corr = _axpby(1.5, t.eye(kq, dtype=t.float64, device=m.device), -0.5, m)
-    return gemm_dev(y, corr), dropped
 
 
 def _leading_subspace(gd, need: int, tau: float, start=None, hint=None):
     """Leading eigenpairs of a symmetric n x n Gram by block subspace
-    iteration with Rayleigh-Ritz (GEMMs + thin QR + the one-CTA Jacobi on
-    the b x b projection), b = min(need, 80) + 16 columns.
+    iteration with Rayleigh-Ritz (bt_leading_subspace_f64: GEMMs, column-
+    scaled SVQB and the one-CTA Jacobi on the b x b projection, driven from
+    the library's host side), b = min(need, hint, 80) + 16 columns.
 
     Returns (w, v, k): the b Ritz values (descending, device), Ritz vectors
     (n x b, sign-normalised) and the count k of leading pairs that are
     (i) above tau * w[0] and (ii) converged to a residual
     ||G v - theta v|| <= 32 eps theta_1 -- at most b - 16, so every
     eigenvalue above the cut is known to be captured.  None when the
-    iteration did not converge (the caller falls back to bt_syevx_f64).
-    Accuracy per accepted pair is the Gram eigensolver's (residual / gap);
-    the deflation passes of mode_basis_dev handle the rest."""
+    iteration did not converge or was predicted too slow (the caller falls
+    back to bt_syevx_f64).  Accuracy per accepted pair is the Gram
+    eigensolver's (residual / gap); the deflation passes of mode_basis_dev
+    handle the rest."""
     n = int(gd.shape[0])
-    want = need if hint is None else max(1, min(need, int(hint)))
-    b = min(n, min(want, SUB_MAX_BLOCK - SUB_OVERSAMPLE) + SUB_OVERSAMPLE)
-    if b < 2 or b > SUB_MAX_BLOCK or 2 * b > n:
+    h = 0 if hint is None else int(hint)
+    wsb = N.load().bt_leading_subspace_ws_bytes(n, int(need), h)
+    if wsb <= 0:
         return None
-    q0 = gaussian_dev(n, b, 20210501 + n)
-    if start is not None:
-        # warm start (HOOI: the previous sweep's basis spans the answer to
-        # within the sweep's change): its leading columns replace the Gaussian ones
-        ks = min(int(start.shape[1]), b - SUB_OVERSAMPLE)
-        q0[:, :ks] = start[:, :ks]
-    q, _ = _orth_svqb(q0)
-    eps = np.finfo(np.float64).eps
-    prev = None
-    for it in range(SUB_MAX_ITERS):
-        if q is None:
-            return None
-        q, dropped = _orth_svqb(gemm_dev(gd, q))
-        if q is None:
-            return None
-        bq = int(q.shape[1])
-        gq = gemm_dev(gd, q)
-        h = gemm_dev(q, gq, ta=True)
-        h = _axpby(0.5, h, 0.5, h.t().contiguous())   # exact symmetry for Jacobi
-        w, s = eigh_dev(h)                      # b x b, full spectrum, descending
-        v = gemm_dev(q, s)
-        gv = gemm_dev(gq, s)                    # G v = (G q) s
-        res = _dev.empty((bq,))
-        N.call("bt_ritz_resid_f64", _dev.ptr(gv), _dev.ptr(v), _dev.ptr(w), n, bq, bq,
-               _dev.ptr(res), _dev.stream())
-        wh = _dev.to_host(w)
-        rh = _dev.to_host(res)
-        top = float(wh[0])
-        if top <= 0.0:
-            return None
-        # accept at most b - 16 pairs, and never the whole retained block
-        # unless SVQB dropped directions (those sit below ~sqrt(1e3 eps) of
-        # the top, i.e. under the cut, which certifies nothing was missed)
-        k = int(np.sum(wh[:min(need, b - SUB_OVERSAMPLE, bq if dropped else bq - 1)]
-                       > tau * top))
-        worst = float(rh[:max(k, 1)].max())
-        target = SUB_RESID * eps * top
-        if _DEBUG:
-            print(f"[subspace n={n} b={b}] it {it}: k {k} max resid/theta1 "
-                  f"{worst / top:.2e}", file=sys.stderr)
-        if worst <= target:
-            N.call("bt_sign_fix_f64", _dev.ptr(v), n, bq, _dev.stream())
-            return w, v, k
-        if (prev is None and start is None and not dropped and k >= 1 and worst > 0.0
-                and wh[-1] > 0.0):
-            # cold start: the residual of pair k falls roughly like
-            # (lambda_{b+1} / lambda_k)^it; the last Ritz value stands in for
-            # lambda_{b+1}.  A slowly decaying block edge (C3 mode 1) goes
-            # straight to the tridiagonal solver instead of spending
-            # iterations to measure the rate.  Only for an intact block: when
-            # SVQB dropped columns the last Ritz value is not near lambda_b.
-            rate0 = float(wh[-1]) / float(wh[k - 1])
-            if rate0 >= 1.0 or np.log(target / worst) / np.log(max(rate0, 1e-300)) > \
-                    1.5 * (SUB_MAX_ITERS - 1):
-                return None
-        if prev is not None and worst > 0.0:
-            rate = worst / prev                    # linear convergence factor
-            left = SUB_MAX_ITERS - 1 - it
-            if rate >= 1.0 or np.log(target / worst) / np.log(max(rate, 1e-300)) > left:
-                return None                        # too slow: the tridiagonal path wins
-        prev = worst
-        q = v
-    return None
+    b = min(n, min(max(1, min(int(need), h)) if h > 0 else int(need), SUB_MAX_BLOCK - SUB_OVERSAMPLE)
+            + SUB_OVERSAMPLE)
+    ws = _dev.workspace(wsb)
+    w = _dev.empty((b,))
+    vbuf = _dev.empty((n * b,))
+    bq, k, st = C.c_int64(0), C.c_int64(0), C.c_int(0)
+    sp, sc = (0, 0) if start is None else (_dev.ptr(start), int(start.shape[1]))
+    N.call("bt_leading_subspace_f64", _dev.ptr(gd), n, int(need), float(tau), sp or None, sc, h,
+           _dev.ptr(w), _dev.ptr(vbuf), C.byref(bq), C.byref(k), C.byref(st), _dev.ptr(ws),
+           int(ws.numel()) * 8, _dev.stream())
+    if st.value != 0:
+        return None
+    nb = int(bq.value)
+    return w[:nb], vbuf[:n * nb].view(n, nb), int(k.value)
+
+
 NOISE_REL = 1e-22    # remainder eigenvalue below this * lambda_1 (sigma < 1e-11 sigma_1)
 RESOLVE_TAU = 1e-6   # per pass: eigenvectors with lambda > tau * lambda_max are kept (cut accuracy ~eps/tau)
 

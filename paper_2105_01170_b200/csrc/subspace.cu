@@ -1,0 +1,305 @@
+// K8 (leading eigenpairs of a deflation pass): block subspace iteration with
+// Rayleigh-Ritz on a symmetric n x n Gram, driven from the host side of the
+// library so that one iteration costs its kernels plus two small D2H reads
+// (the Python loop it replaces spent more time in launch overhead than the
+// GPU spent computing).  Same algorithm and acceptance rule as the reference
+// restatement in _linalg.py: the leading left singular vectors that
+// decomp.py:220-234 takes from LAPACK's SVD, per deflation pass.
+//
+//   Q0 = SVQB(Gaussian [ , warm start columns])
+//   repeat:  Q = SVQB(G Q);  H = Q^T G Q;  H = S diag(theta) S^T (one-CTA
+//            Jacobi);  V = Q S;  accept the leading k pairs once every
+//            ||G v - theta v|| <= 32 eps theta_1
+//
+// SVQB is the column-scaled variant (D = diag(Y^T Y)^-1/2; eigen-decomposition
+// of D Y^T Y D; drop directions below 1e3 eps of the largest; one
+// Newton-Schulz step).  Status: 0 converged, 1 not converged / too slow (the
+// caller falls back to bt_syevx_f64), 2 not applicable (block shape).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "gemm.cuh"
+
+int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, int64_t ws_elems);
+int64_t bt_gemm_ws_elems(BtGemmArgs g, int64_t batch);
+
+extern "C" {
+int64_t bt_syevd_ws_bytes(int64_t n);
+int bt_syevd_f64(const double* a, int64_t n, double* w, double* v, void* ws, int64_t ws_bytes,
+                 void* stream);
+int bt_inv_sqrt_f64(const double* x, int64_t n, double* out, void* stream);
+int bt_sym_scale_f64(const double* m, int64_t b, double* dinv, double* out, void* stream);
+int bt_sign_fix_f64(double* x, int64_t rows, int64_t cols, void* stream);
+int bt_fill_normal_f64(double* out, int64_t n, uint64_t key, void* stream);
+int bt_ritz_resid_f64(const double* gv, const double* v, const double* theta, int64_t rows,
+                      int64_t cols, int64_t ld, double* out, void* stream);
+}
+
+namespace {
+
+constexpr int SUB_OVERSAMPLE = 16;
+constexpr int SUB_MAX_BLOCK = 96;
+constexpr int SUB_MAX_ITERS = 10;
+constexpr double SUB_RESID = 32.0;
+constexpr double EPS = 2.220446049250313e-16;
+constexpr double SVQB_DROP = 1e3 * EPS;
+
+// out = (h + h^T) / 2  (b x b)
+__global__ void sym_kernel(const double* __restrict__ h, int64_t b, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < b * b;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / b, j = e - i * b;
+    out[e] = 0.5 * h[i * b + j] + 0.5 * h[j * b + i];
+  }
+}
+
+// out = 1.5 I - 0.5 m  (Newton-Schulz correction, b x b)
+__global__ void ns_kernel(const double* __restrict__ m, int64_t b, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < b * b;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / b, j = e - i * b;
+    out[e] = 1.5 * (i == j ? 1.0 : 0.0) - 0.5 * m[e];
+  }
+}
+
+// dst[r][c] = src[r][c] for c < cols  (row strides ld_dst / ld_src)
+__global__ void copy_cols_kernel(const double* __restrict__ src, int64_t ld_src, int64_t rows,
+                                 int64_t cols, double* __restrict__ dst, int64_t ld_dst) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * cols;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols, c = e - r * cols;
+    dst[r * ld_dst + c] = src[r * ld_src + c];
+  }
+}
+
+unsigned grid_for(int64_t n) { return static_cast<unsigned>(std::min<int64_t>(bt_cdiv(n, 256), 4096)); }
+
+// C (M x N, row-major, ld N) = op(A) op(B) with explicit strides, as
+// _linalg._gemm builds it
+BtGemmArgs gemm_args(int64_t M, int64_t N, int64_t K, const double* A, int64_t sAm, int64_t sAk,
+                     const double* B, int64_t sBk, int64_t sBn, double* C) {
+  BtGemmArgs g{};
+  g.M = M;
+  g.N = N;
+  g.Kin = K;
+  g.Kout = 1;
+  g.A = BtOperand{A, sAm, 0, sAk, 0};
+  g.B = BtOperand{B, sBn, 0, sBk, 0};
+  g.C = C;
+  g.sCm = N;
+  g.sCn = 1;
+  g.alpha = 1.0;
+  g.beta = 0.0;
+  return g;
+}
+
+struct Plan {
+  int64_t b, n;
+  int64_t off_q, off_y, off_gq, off_gv, off_m, off_ms, off_s, off_w2, off_v2, off_dinv,
+      off_sv, off_h, off_hs, off_w, off_res, off_gws, off_ews, total;
+  int64_t gemm_ws, eig_ws;
+};
+
+Plan plan(int64_t n, int64_t b) {
+  Plan p{};
+  p.n = n;
+  p.b = b;
+  int64_t o = 0;
+  auto take = [&](int64_t k) {
+    const int64_t at = o;
+    o += (k + 1) / 2 * 2;
+    return at;
+  };
+  p.off_q = take(n * b);
+  p.off_y = take(n * b);
+  p.off_gq = take(n * b);
+  p.off_gv = take(n * b);
+  p.off_m = take(b * b);
+  p.off_ms = take(b * b);
+  p.off_s = take(b * b);
+  p.off_w2 = take(b);
+  p.off_v2 = take(b * b);
+  p.off_dinv = take(b);
+  p.off_sv = take(b);
+  p.off_h = take(b * b);
+  p.off_hs = take(b * b);
+  p.off_w = take(b);
+  p.off_res = take(b);
+  // GEMM split-K partials: the largest of the shapes used below
+  int64_t gw = 0;
+  gw = std::max(gw, bt_gemm_ws_elems(gemm_args(n, b, n, nullptr, n, 1, nullptr, b, 1, nullptr), 1));
+  gw = std::max(gw, bt_gemm_ws_elems(gemm_args(b, b, n, nullptr, 1, b, nullptr, b, 1, nullptr), 1));
+  gw = std::max(gw, bt_gemm_ws_elems(gemm_args(n, b, b, nullptr, b, 1, nullptr, b, 1, nullptr), 1));
+  p.gemm_ws = gw;
+  p.off_gws = take(gw);
+  p.eig_ws = (bt_syevd_ws_bytes(b) + 7) / 8;
+  p.off_ews = take(p.eig_ws);
+  p.total = o;
+  return p;
+}
+
+struct Ctx {
+  const Plan& p;
+  double* ws;
+  cudaStream_t st;
+  double* at(int64_t off) const { return ws + off; }
+  int gemm(BtGemmArgs g) const {
+    g.ws = ws + p.off_gws;
+    return bt_gemm_run(g, 1, st, 0, p.gemm_ws);
+  }
+  int eig(const double* a, int64_t b, double* w, double* v) const {
+    return bt_syevd_f64(a, b, w, v, ws + p.off_ews, p.eig_ws * 8, st);
+  }
+};
+
+// Column-scaled SVQB of y (n x b, row-major) into q (n x keep); returns keep
+// (0 when y is numerically zero) through *keep and the dropped count.
+int svqb(const Ctx& c, const double* y, int64_t n, int64_t b, double* q, int64_t* keep_out,
+         int64_t* dropped) {
+  const Plan& p = c.p;
+  double* m = c.at(p.off_m);
+  double* ms = c.at(p.off_ms);
+  double* dinv = c.at(p.off_dinv);
+  double* w2 = c.at(p.off_w2);
+  double* v2 = c.at(p.off_v2);
+  double* sv = c.at(p.off_sv);
+  BT_TRY(c.gemm(gemm_args(b, b, n, y, 1, b, y, b, 1, m)));          // Y^T Y
+  BT_TRY(bt_sym_scale_f64(m, b, dinv, ms, c.st));
+  BT_TRY(c.eig(ms, b, w2, v2));
+  std::vector<double> wh(b);
+  BT_CUDA_CHECK(cudaMemcpyAsync(wh.data(), w2, sizeof(double) * b, cudaMemcpyDeviceToHost, c.st));
+  BT_CUDA_CHECK(cudaStreamSynchronize(c.st));
+  if (!(wh[0] > 0.0)) {
+    *keep_out = 0;
+    return BT_OK;
+  }
+  int64_t keep = 0;
+  for (int64_t i = 0; i < b; ++i) keep += wh[i] > SVQB_DROP * wh[0];
+  *dropped += b - keep;
+  BT_TRY(bt_inv_sqrt_f64(w2, keep, sv, c.st));
+  // Y D V[:, :keep] diag(s): D on A's reduction index, s on B's columns
+  double* out = c.at(p.off_gv);  // scratch n x keep (gv is free here)
+  BtGemmArgs g = gemm_args(n, keep, b, y, b, 1, v2, b, 1, out);
+  g.ascale = dinv;
+  g.bscale = sv;
+  BT_TRY(c.gemm(g));
+  // one Newton-Schulz step: Q = out (1.5 I - 0.5 out^T out)
+  BT_TRY(c.gemm(gemm_args(keep, keep, n, out, 1, keep, out, keep, 1, m)));
+  ns_kernel<<<grid_for(keep * keep), 256, 0, c.st>>>(m, keep, ms);
+  BT_LAUNCH_CHECK();
+  BT_TRY(c.gemm(gemm_args(n, keep, keep, out, keep, 1, ms, keep, 1, q)));
+  *keep_out = keep;
+  return BT_OK;
+}
+
+}  // namespace
+
+extern "C" int64_t bt_leading_subspace_ws_bytes(int64_t n, int64_t need, int64_t hint) {
+  const int64_t want = hint > 0 ? std::max<int64_t>(1, std::min(need, hint)) : need;
+  const int64_t b = std::min(n, std::min<int64_t>(want, SUB_MAX_BLOCK - SUB_OVERSAMPLE) + SUB_OVERSAMPLE);
+  if (b < 2 || b > SUB_MAX_BLOCK || 2 * b > n) return 0;
+  return plan(n, b).total * 8;
+}
+
+extern "C" int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need, double tau,
+                                       const double* start, int64_t start_cols, int64_t hint,
+                                       double* w, double* v, int64_t* bq_out, int64_t* k_out,
+                                       int* status, void* wsv, int64_t ws_bytes, void* stream) {
+  *status = 2;
+  *bq_out = 0;
+  *k_out = 0;
+  const int64_t want = hint > 0 ? std::max<int64_t>(1, std::min(need, hint)) : need;
+  const int64_t b = std::min(n, std::min<int64_t>(want, SUB_MAX_BLOCK - SUB_OVERSAMPLE) + SUB_OVERSAMPLE);
+  if (b < 2 || b > SUB_MAX_BLOCK || 2 * b > n) return BT_OK;
+  const Plan p = plan(n, b);
+  BT_REQUIRE(ws_bytes >= p.total * 8, BT_E_VALUE, "leading_subspace: workspace too small");
+  const Ctx c{p, static_cast<double*>(wsv), bt_stream(stream)};
+  const bool dbg = getenv("BT_BASIS_DEBUG") != nullptr;
+  double* q = c.at(p.off_q);
+  double* y = c.at(p.off_y);
+  double* gq = c.at(p.off_gq);
+  double* h = c.at(p.off_h);
+  double* hs = c.at(p.off_hs);
+  double* sm = c.at(p.off_s);
+  double* res = c.at(p.off_res);
+  *status = 1;
+  // Gaussian start block (Philox key as _linalg.gaussian_dev), warm columns in front
+  BT_TRY(bt_fill_normal_f64(y, n * b, static_cast<uint64_t>(20210501 + n), c.st));
+  if (start != nullptr && start_cols > 0) {
+    const int64_t ks = std::min<int64_t>(start_cols, b - SUB_OVERSAMPLE);
+    if (ks > 0) {
+      copy_cols_kernel<<<grid_for(n * ks), 256, 0, c.st>>>(start, start_cols, n, ks, y, b);
+      BT_LAUNCH_CHECK();
+    }
+  }
+  int64_t bq = 0, dropped = 0;
+  BT_TRY(svqb(c, y, n, b, q, &bq, &dropped));
+  if (bq == 0) return BT_OK;
+  double prev = -1.0;
+  std::vector<double> wh(b), rh(b);
+  for (int it = 0; it < SUB_MAX_ITERS; ++it) {
+    BT_TRY(c.gemm(gemm_args(n, bq, n, g, n, 1, q, bq, 1, y)));       // G Q
+    dropped = 0;
+    int64_t nq = 0;
+    BT_TRY(svqb(c, y, n, bq, q, &nq, &dropped));
+    if (nq == 0) return BT_OK;
+    bq = nq;
+    BT_TRY(c.gemm(gemm_args(n, bq, n, g, n, 1, q, bq, 1, gq)));      // G Q
+    BT_TRY(c.gemm(gemm_args(bq, bq, n, q, 1, bq, gq, bq, 1, h)));    // Q^T G Q
+    sym_kernel<<<grid_for(bq * bq), 256, 0, c.st>>>(h, bq, hs);
+    BT_LAUNCH_CHECK();
+    BT_TRY(c.eig(hs, bq, w, sm));                                    // descending
+    BT_TRY(c.gemm(gemm_args(n, bq, bq, q, bq, 1, sm, bq, 1, v)));    // V = Q S
+    double* gv = c.at(p.off_gv);
+    BT_TRY(c.gemm(gemm_args(n, bq, bq, gq, bq, 1, sm, bq, 1, gv)));  // G V = (G Q) S
+    BT_TRY(bt_ritz_resid_f64(gv, v, w, n, bq, bq, res, c.st));
+    BT_CUDA_CHECK(cudaMemcpyAsync(wh.data(), w, sizeof(double) * bq, cudaMemcpyDeviceToHost, c.st));
+    BT_CUDA_CHECK(cudaMemcpyAsync(rh.data(), res, sizeof(double) * bq, cudaMemcpyDeviceToHost, c.st));
+    BT_CUDA_CHECK(cudaStreamSynchronize(c.st));
+    const double top = wh[0];
+    if (!(top > 0.0)) return BT_OK;
+    // accept at most b - 16 pairs, and never the whole retained block unless
+    // SVQB dropped directions (those sit below ~sqrt(1e3 eps) of the top)
+    const int64_t lim = std::min<int64_t>(std::min<int64_t>(need, b - SUB_OVERSAMPLE),
+                                          dropped ? bq : bq - 1);
+    int64_t k = 0;
+    for (int64_t i = 0; i < lim; ++i) k += wh[i] > tau * top;
+    double worst = 0.0;
+    for (int64_t i = 0; i < std::max<int64_t>(k, 1); ++i) worst = std::max(worst, rh[i]);
+    const double target = SUB_RESID * EPS * top;
+    if (dbg)
+      fprintf(stderr, "[subspace n=%lld b=%lld] it %d: k %lld max resid/theta1 %.2e\n",
+              (long long)n, (long long)b, it, (long long)k, worst / top);
+    if (worst <= target) {
+      BT_TRY(bt_sign_fix_f64(v, n, bq, c.st));
+      *bq_out = bq;
+      *k_out = k;
+      *status = 0;
+      return BT_OK;
+    }
+    if (prev < 0.0 && start == nullptr && dropped == 0 && k >= 1 && worst > 0.0 &&
+        wh[bq - 1] > 0.0) {
+      // cold start: the residual of pair k falls roughly like
+      // (lambda_{b+1} / lambda_k)^it with the last Ritz value standing in for
+      // lambda_{b+1}; a slowly decaying block edge goes straight to the
+      // tridiagonal solver
+      const double rate0 = wh[bq - 1] / wh[k - 1];
+      if (rate0 >= 1.0 ||
+          std::log(target / worst) / std::log(std::max(rate0, 1e-300)) > 1.5 * (SUB_MAX_ITERS - 1))
+        return BT_OK;
+    }
+    if (prev > 0.0 && worst > 0.0) {
+      const double rate = worst / prev;  // linear convergence factor
+      const int left = SUB_MAX_ITERS - 1 - it;
+      if (rate >= 1.0 || std::log(target / worst) / std::log(std::max(rate, 1e-300)) > left)
+        return BT_OK;  // too slow: the tridiagonal path wins
+    }
+    prev = worst;
+    // next block = the Ritz vectors (v stays the caller's output buffer)
+    BT_CUDA_CHECK(cudaMemcpyAsync(q, v, sizeof(double) * n * bq, cudaMemcpyDeviceToDevice, c.st));
+  }
+  return BT_OK;
+}

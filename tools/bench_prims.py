@@ -37,7 +37,7 @@ for n, k in ((512, 32), (1024, 64), (1024, 80), (2047, 400), (2047, 96)):
 for m, k in ((1024, 80), (2047, 96), (512, 48)):
     y = torch.randn(m, k, dtype=torch.float64, device="cuda")
     g = spd(m)
-    print(f"m={m} k={k}: qr_thin {tm(lambda: L.qr_thin_dev(y)):7.3f}  svqb {tm(lambda: L._orth_svqb(y)):7.3f}  "
+    print(f"m={m} k={k}: qr_thin {tm(lambda: L.qr_thin_dev(y)):7.3f}  "
           f"gemm GQ {tm(lambda: L.gemm_dev(g, y)):7.3f}  gemm YtY {tm(lambda: L.gemm_dev(y, y, ta=True)):7.3f} ms")
 for n in (48, 80, 96):
     a = spd(n, False)

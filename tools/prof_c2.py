@@ -7,7 +7,7 @@ from paper_2105_01170_b200 import configs, _linalg as L, decomp
 params = configs.c2_markov()
 pat, t = configs.c2_build(params)
 torch.cuda.synchronize()
-orig = {name: getattr(L, name) for name in ("unfold_gram_dev", "eigh_dev", "_residual", "_complete", "_orth_normalize", "qr_thin_dev", "_leading_subspace", "gemm_dev", "_orth_svqb")}
+orig = {name: getattr(L, name) for name in ("unfold_gram_dev", "eigh_dev", "_residual", "_complete", "_orth_normalize", "qr_thin_dev", "_leading_subspace", "gemm_dev")}
 stats = {}
 def wrap(name, fn):
     def g(*a, **k):

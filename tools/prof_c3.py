@@ -22,7 +22,7 @@ def wrap(mod, name):
     setattr(mod, name, g)
 
 
-for name in ("unfold_gram_dev", "eigh_dev", "_residual", "_complete", "_orth_normalize", "_axpby", "_leading_subspace", "gemm_dev", "_orth_svqb"):
+for name in ("unfold_gram_dev", "eigh_dev", "_residual", "_complete", "_orth_normalize", "_axpby", "_leading_subspace", "gemm_dev"):
     wrap(L, name)
 wrap(decomp, "ttm_dev")
 rep = decomp.st_hosvd(t, [64, 32, 64], shared=(1, 3))
