@@ -13,6 +13,8 @@
 //              products over the volume batch, the last one reducing over r.
 // Flop counts per RHS equal the reference's FlopCounter formulas.
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 
 #include "gemm.cuh"
 
@@ -170,6 +172,220 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Row-group variant of the middle products for dense-map patterns (every
+// cell's class read from cell_class): a CTA owns BM / RLP consecutive block
+// rows and 64 right-hand sides and walks the block columns j, so each Z_j
+// tile is loaded once for all its block rows and every stage feeds 32 DMMAs
+// per warp (4 warps of 64x32 -- the engine's tuned tile).  The A tile stacks
+// the rows' middles S_{class(i, j)} (zero for uncovered cells); BK = 16 over
+// the rr columns.  The block columns are split over gridDim.z with partials
+// reduced in a fixed order (deterministic).
+namespace blrrows {
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, THREADS = 128;
+constexpr int LDA = bt_ld(BK), LDB = bt_ld(BK);
+constexpr int A_STAGE = BM * LDA, B_STAGE = BN * LDB;
+constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * 8;
+constexpr int TM = 64, TN = 32, FM = TM / 8, FN = TN / 8;
+}  // namespace blrrows
+
+template <int RLP>
+__global__ void __launch_bounds__(blrrows::THREADS)
+    blr_rows_kernel(const double* __restrict__ shat, const double* __restrict__ z,
+                    const int32_t* __restrict__ cell_class, int64_t rl, int64_t rr, int64_t q,
+                    int64_t nrhs, int64_t ell, int64_t jchunk, double* __restrict__ out,
+                    int64_t out_split_stride) {
+  using namespace blrrows;
+  constexpr int R = BM / RLP;  // block rows per CTA
+  extern __shared__ __align__(16) double sm[];
+  double* As = sm;
+  double* Bs = sm + STAGES * A_STAGE;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm0 = (warp & 1) * TM, wn0 = (warp >> 1) * TN;
+  const int64_t i0 = blockIdx.x * (int64_t)R;
+  const int64_t s0 = blockIdx.y * (int64_t)BN;
+  const int64_t j0 = blockIdx.z * jchunk;
+  const int64_t j1 = std::min<int64_t>(q, j0 + jchunk);
+  const int ktc = static_cast<int>((rr + BK - 1) / BK);
+  const int64_t T = (j1 > j0 ? (j1 - j0) : 0) * ktc;
+  const int64_t zrow = q * rr;  // stride between right-hand sides in Z
+
+  // per-thread chunk coordinates (16-byte chunks: 8 per 16-wide row)
+  // A: 128 rows x 8 chunks = 1024 -> 8 per thread; B: 64 x 8 = 512 -> 4 per thread
+  int a_r[8], a_c[8];
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int idx = threadIdx.x + it * THREADS;
+    a_r[it] = idx >> 3;
+    a_c[it] = (idx & 7) * 2;
+  }
+  int b_r[4], b_c[4];
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int idx = threadIdx.x + it * THREADS;
+    b_r[it] = idx >> 3;
+    b_c[it] = (idx & 7) * 2;
+  }
+  int64_t l_j = j0;
+  int l_kt = 0;
+  int cls[R];
+  auto load_stage = [&](int stage) {
+    if (l_kt == 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        cls[r] = (i0 + r < ell) ? __ldg(cell_class + (i0 + r) * q + l_j) : -1;
+    }
+    const int k0 = l_kt * BK;
+    double* as = As + stage * A_STAGE;
+    double* bs = Bs + stage * B_STAGE;
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int m = a_r[it];
+      const int r = m / RLP, rho = m - r * RLP;
+      const int k = cls[r];
+      const int64_t cl = rr - k0 - a_c[it];
+      const int valid = (k >= 0 && rho < rl && cl > 0) ? static_cast<int>(cl >= 2 ? 16 : cl * 8) : 0;
+      const double* src = valid ? shat + (static_cast<int64_t>(k) * rl + rho) * rr + k0 + a_c[it]
+                                : shat;
+      cp_async16(as + m * LDA + a_c[it], src, valid);
+    }
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int n = b_r[it];
+      const int64_t s = s0 + n;
+      const int64_t cl = rr - k0 - b_c[it];
+      const int valid = (s < nrhs && cl > 0) ? static_cast<int>(cl >= 2 ? 16 : cl * 8) : 0;
+      const double* src = valid ? z + s * zrow + l_j * rr + k0 + b_c[it] : z;
+      cp_async16(bs + n * LDB + b_c[it], src, valid);
+    }
+    if (++l_kt == ktc) {
+      l_kt = 0;
+      ++l_j;
+    }
+  };
+
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int a = 0; a < FM; ++a)
+#pragma unroll
+    for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < T) load_stage(st);
+    cp_async_commit();
+  }
+  int stage = 0, next_stage = STAGES - 1;
+  double afr[2][FM], bfr[2][FN];
+  for (int64_t t = 0; t < T; ++t) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const double* as = As + stage * A_STAGE;
+    const double* bs = Bs + stage * B_STAGE;
+    auto frags = [&](int buf, int kk) {
+#pragma unroll
+      for (int a = 0; a < FM; ++a) afr[buf][a] = as[(wm0 + a * 8 + gq) * LDA + kk + tq];
+#pragma unroll
+      for (int b = 0; b < FN; ++b) bfr[buf][b] = bs[(wn0 + b * 8 + gq) * LDB + kk + tq];
+    };
+    frags(0, 0);
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      if (ks + 1 < BK / 4) frags((ks + 1) & 1, (ks + 1) * 4);
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma884(acc[a][b][0], acc[a][b][1], afr[ks & 1][a], bfr[ks & 1][b]);
+      if (ks == 0) {
+        if (t + STAGES - 1 < T) load_stage(next_stage);
+        cp_async_commit();
+      }
+    }
+    stage = (stage + 1 == STAGES) ? 0 : stage + 1;
+    next_stage = (next_stage + 1 == STAGES) ? 0 : next_stage + 1;
+  }
+  cp_async_wait<0>();
+  // out[(s * ell + i) * rl + rho] (+ split offset)
+  double* o = out + blockIdx.z * out_split_stride;
+#pragma unroll
+  for (int a = 0; a < FM; ++a) {
+    const int m = wm0 + a * 8 + gq;
+    const int r = m / RLP, rho = m - r * RLP;
+    const int64_t i = i0 + r;
+    if (rho >= rl || i >= ell) continue;
+#pragma unroll
+    for (int b = 0; b < FN; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t s = s0 + wn0 + b * 8 + 2 * tq + h;
+        if (s < nrhs) o[(s * ell + i) * rl + rho] = acc[a][b][h];
+      }
+  }
+}
+
+// yb = sum over splits of part (fixed order)
+__global__ void split_sum_kernel(const double* __restrict__ part, int64_t n, int splits,
+                                 double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double acc = part[e];
+    for (int sidx = 1; sidx < splits; ++sidx) acc += part[sidx * n + e];
+    out[e] = acc;
+  }
+}
+
+// splits of the block-column range that fill whole waves of resident CTAs
+int blr_rows_splits(int64_t ctas, int64_t q, int resident) {
+  const int64_t slots = static_cast<int64_t>(bt_num_sms()) * std::max(resident, 1);
+  int best = 1;
+  double best_eff = 0.0;
+  for (int sp = 1; sp <= 16 && sp <= q; ++sp) {
+    const double waves = static_cast<double>(ctas * sp) / static_cast<double>(slots);
+    const double eff = waves / std::ceil(waves);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = sp;
+    }
+  }
+  return best;
+}
+
+template <int RLP>
+int launch_blr_rows(const double* shat, const double* z, const int32_t* cell_class, int64_t rl,
+                    int64_t rr, int64_t q, int64_t nrhs, int64_t ell, double* yb, double* part,
+                    int splits, cudaStream_t st) {
+  using namespace blrrows;
+  static bool attr = false;
+  if (!attr) {
+    BT_CUDA_CHECK(cudaFuncSetAttribute(blr_rows_kernel<RLP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    attr = true;
+  }
+  constexpr int R = BM / RLP;
+  const int64_t jchunk = bt_cdiv(q, splits);
+  dim3 grid(static_cast<unsigned>(bt_cdiv(ell, R)), static_cast<unsigned>(bt_cdiv(nrhs, BN)),
+            static_cast<unsigned>(splits));
+  const int64_t nout = nrhs * ell * rl;
+  blr_rows_kernel<RLP><<<grid, THREADS, SMEM, st>>>(shat, z, cell_class, rl, rr, q, nrhs, ell,
+                                                    jchunk, splits > 1 ? part : yb, nout);
+  BT_LAUNCH_CHECK();
+  if (splits > 1) {
+    split_sum_kernel<<<grid1d(nout), 256, 0, st>>>(part, nout, splits, yb);
+    BT_LAUNCH_CHECK();
+  }
+  return BT_OK;
+}
+
+template <int RLP>
+int blr_rows_resident() {
+  int per_sm = 0;
+  cudaFuncSetAttribute(blr_rows_kernel<RLP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)blrrows::SMEM);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blr_rows_kernel<RLP>,
+                                                    blrrows::THREADS, blrrows::SMEM) != cudaSuccess)
+    per_sm = 1;
+  return per_sm;
+}
+
 template <int RLP, int RRP, int NB>
 int launch_blr_middle(const double* shat, const double* z, const int64_t* row_ptr,
                       const int64_t* row_cells, int64_t p, int64_t rl, int64_t rr, int64_t q,
@@ -214,11 +430,22 @@ KronPlan kron_plan(const bt_pattern_dev* pat, int64_t r, int64_t nrhs) {
 }
 
 struct BlrPlan {
-  int64_t off_shat, off_z, off_yb, off_gws, total;
+  int64_t off_shat, off_z, off_yb, off_part, off_gws, total;
+  int rows;    // 1: row-group kernel (blr_rows_kernel), 0: per-row kernel
+  int splits;  // block-column splits of the row-group kernel
 };
 
 BlrPlan blr_plan(const bt_pattern_dev* pat, int64_t rl, int64_t rr, int64_t nrhs) {
   BlrPlan b;
+  static const bool no_rows = getenv("BT_BLR_ROWS") && getenv("BT_BLR_ROWS")[0] == '0';
+  b.rows = (!no_rows && pat->cell_class != nullptr && rl <= 64 && rr % 2 == 0) ? 1 : 0;
+  b.splits = 1;
+  if (b.rows) {
+    const int rlp = rl <= 32 ? 32 : 64;
+    const int resident = rlp == 32 ? blr_rows_resident<32>() : blr_rows_resident<64>();
+    const int64_t ctas = bt_cdiv(pat->ell, blrrows::BM / rlp) * bt_cdiv(nrhs, blrrows::BN);
+    b.splits = blr_rows_splits(ctas, pat->q, resident);
+  }
   int64_t o = 0;
   auto take = [&](int64_t n) {
     int64_t at = o;
@@ -228,6 +455,7 @@ BlrPlan blr_plan(const bt_pattern_dev* pat, int64_t rl, int64_t rr, int64_t nrhs
   b.off_shat = take(pat->p * rl * rr);
   b.off_z = take(pat->q * nrhs * rr);
   b.off_yb = take(nrhs * pat->ell * rl);
+  b.off_part = take(b.splits > 1 ? b.splits * nrhs * pat->ell * rl : 0);
   BtGemmArgs g1{};
   g1.M = pat->q * nrhs;
   g1.N = rr;
@@ -327,7 +555,15 @@ extern "C" int bt_matvec_blr_f64(const bt_pattern_dev* pat, const int64_t* row_p
   g1.ws = gws;
   BT_TRY(bt_gemm_run(g1, 1, st, 0, gws_n));
   // middle products
-  if (rl <= 32 && rr <= 32) {
+  if (bp.rows) {
+    double* part = ws + bp.off_part;
+    if (rl <= 32)
+      BT_TRY(launch_blr_rows<32>(shat, z, pat->cell_class, rl, rr, q, nrhs, ell, yb, part,
+                                 bp.splits, st));
+    else
+      BT_TRY(launch_blr_rows<64>(shat, z, pat->cell_class, rl, rr, q, nrhs, ell, yb, part,
+                                 bp.splits, st));
+  } else if (rl <= 32 && rr <= 32) {
     int rc = launch_blr_middle<32, 32, 64>(shat, z, row_ptr, row_cells, p, rl, rr, q, nrhs, ell,
                                            yb, st);
     BT_TRY(rc);
