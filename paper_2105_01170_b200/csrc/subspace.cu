@@ -75,6 +75,70 @@ __global__ void copy_cols_kernel(const double* __restrict__ src, int64_t ld_src,
   }
 }
 
+// One-CTA Cholesky of a (column-scaled, unit-diagonal) Gram m (b <= 96) and
+// the inverse of its transposed factor: rinv = L^-T, so Y D rinv has
+// orthonormal columns (CholeskyQR).  status = 0 ok, 1 when a pivot falls
+// below CHOL_MIN_PIVOT (cond(m) too large for one CholeskyQR + Newton-Schulz
+// step: the caller takes the eigenvalue-based SVQB instead).
+constexpr double CHOL_MIN_PIVOT = 1e-6;
+constexpr int CHOL_MAXB = 96;
+
+__global__ void __launch_bounds__(256)
+    chol_rinv_kernel(const double* __restrict__ m, int b, double* __restrict__ rinv,
+                     int* __restrict__ status) {
+  extern __shared__ __align__(16) double chol_sm[];
+  const int ld = b + 1;
+  double* a = chol_sm;       // b x ld, lower triangle -> L
+  double* x = a + b * ld;    // b x ld, L^-1
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int i = e / b, j = e - i * b;
+    a[(i) * ld + (j)] = m[e];
+  }
+  __syncthreads();
+  for (int k = 0; k < b; ++k) {
+    const double piv = a[(k) * ld + (k)];
+    if (!(piv > CHOL_MIN_PIVOT)) {
+      if (threadIdx.x == 0) bad = 1;
+      break;  // uniform: every thread read the same pivot
+    }
+    const double lkk = sqrt(piv);
+    for (int i = k + 1 + threadIdx.x; i < b; i += blockDim.x) a[(i) * ld + (k)] /= lkk;
+    __syncthreads();
+    if (threadIdx.x == 0) a[(k) * ld + (k)] = lkk;
+    // trailing update of the lower triangle: a_ij -= l_ik l_jk, k < j <= i
+    const int t = b - k - 1;
+    for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
+      const int ii = e / t, jj = e - ii * t;
+      if (jj <= ii)
+        a[(k + 1 + ii) * ld + k + 1 + jj] -= a[(k + 1 + ii) * ld + k] * a[(k + 1 + jj) * ld + k];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (bad) {
+    if (threadIdx.x == 0) *status = 1;
+    return;
+  }
+  // X = L^-1 by columns (one thread per column, forward substitution)
+  for (int c = threadIdx.x; c < b; c += blockDim.x) {
+    for (int i = 0; i < c; ++i) x[(i) * ld + (c)] = 0.0;
+    x[(c) * ld + (c)] = 1.0 / a[(c) * ld + (c)];
+    for (int i = c + 1; i < b; ++i) {
+      double s = 0.0;
+      for (int k = c; k < i; ++k) s = fma(a[(i) * ld + (k)], x[(k) * ld + (c)], s);
+      x[(i) * ld + (c)] = -s / a[(i) * ld + (i)];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int i = e / b, j = e - i * b;
+    rinv[e] = x[(j) * ld + (i)];  // L^-T
+  }
+  if (threadIdx.x == 0) *status = 0;
+}
+
 unsigned grid_for(int64_t n) { return static_cast<unsigned>(std::min<int64_t>(bt_cdiv(n, 256), 4096)); }
 
 // C (M x N, row-major, ld N) = op(A) op(B) with explicit strides, as
@@ -99,7 +163,7 @@ BtGemmArgs gemm_args(int64_t M, int64_t N, int64_t K, const double* A, int64_t s
 struct Plan {
   int64_t b, n;
   int64_t off_q, off_y, off_gq, off_gv, off_m, off_ms, off_s, off_w2, off_v2, off_dinv,
-      off_sv, off_h, off_hs, off_w, off_res, off_gws, off_ews, total;
+      off_sv, off_h, off_hs, off_w, off_res, off_flag, off_gws, off_ews, total;
   int64_t gemm_ws, eig_ws;
 };
 
@@ -128,6 +192,7 @@ Plan plan(int64_t n, int64_t b) {
   p.off_hs = take(b * b);
   p.off_w = take(b);
   p.off_res = take(b);
+  p.off_flag = take(2);
   // GEMM split-K partials: the largest of the shapes used below
   int64_t gw = 0;
   gw = std::max(gw, bt_gemm_ws_elems(gemm_args(n, b, n, nullptr, n, 1, nullptr, b, 1, nullptr), 1));
@@ -145,6 +210,7 @@ struct Ctx {
   const Plan& p;
   double* ws;
   cudaStream_t st;
+  bool cholqr;
   double* at(int64_t off) const { return ws + off; }
   int gemm(BtGemmArgs g) const {
     g.ws = ws + p.off_gws;
@@ -168,6 +234,36 @@ int svqb(const Ctx& c, const double* y, int64_t n, int64_t b, double* q, int64_t
   double* sv = c.at(p.off_sv);
   BT_TRY(c.gemm(gemm_args(b, b, n, y, 1, b, y, b, 1, m)));          // Y^T Y
   BT_TRY(bt_sym_scale_f64(m, b, dinv, ms, c.st));
+  double* out = c.at(p.off_gv);  // scratch n x keep (gv is free here)
+  if (b <= CHOL_MAXB && c.cholqr) {
+    // well-conditioned block (the usual case once Q holds Ritz vectors):
+    // CholeskyQR  Q = Y D L^-T  + the Newton-Schulz polish
+    int* flag = reinterpret_cast<int*>(c.at(p.off_flag));
+    const size_t smb = sizeof(double) * 2 * b * (b + 1);
+    static bool attr = false;
+    if (!attr) {
+      BT_CUDA_CHECK(cudaFuncSetAttribute(chol_rinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sizeof(double) * 2 * CHOL_MAXB *
+                                                          (CHOL_MAXB + 1))));
+      attr = true;
+    }
+    chol_rinv_kernel<<<1, 256, smb, c.st>>>(ms, static_cast<int>(b), v2, flag);
+    BT_LAUNCH_CHECK();
+    int hflag = 1;
+    BT_CUDA_CHECK(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+    BT_CUDA_CHECK(cudaStreamSynchronize(c.st));
+    if (hflag == 0) {
+      BtGemmArgs g = gemm_args(n, b, b, y, b, 1, v2, b, 1, out);
+      g.ascale = dinv;
+      BT_TRY(c.gemm(g));
+      BT_TRY(c.gemm(gemm_args(b, b, n, out, 1, b, out, b, 1, m)));
+      ns_kernel<<<grid_for(b * b), 256, 0, c.st>>>(m, b, ms);
+      BT_LAUNCH_CHECK();
+      BT_TRY(c.gemm(gemm_args(n, b, b, out, b, 1, ms, b, 1, q)));
+      *keep_out = b;
+      return BT_OK;
+    }
+  }
   BT_TRY(c.eig(ms, b, w2, v2));
   std::vector<double> wh(b);
   BT_CUDA_CHECK(cudaMemcpyAsync(wh.data(), w2, sizeof(double) * b, cudaMemcpyDeviceToHost, c.st));
@@ -181,7 +277,6 @@ int svqb(const Ctx& c, const double* y, int64_t n, int64_t b, double* q, int64_t
   *dropped += b - keep;
   BT_TRY(bt_inv_sqrt_f64(w2, keep, sv, c.st));
   // Y D V[:, :keep] diag(s): D on A's reduction index, s on B's columns
-  double* out = c.at(p.off_gv);  // scratch n x keep (gv is free here)
   BtGemmArgs g = gemm_args(n, keep, b, y, b, 1, v2, b, 1, out);
   g.ascale = dinv;
   g.bscale = sv;
@@ -216,7 +311,8 @@ extern "C" int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need,
   if (b < 2 || b > SUB_MAX_BLOCK || 2 * b > n) return BT_OK;
   const Plan p = plan(n, b);
   BT_REQUIRE(ws_bytes >= p.total * 8, BT_E_VALUE, "leading_subspace: workspace too small");
-  const Ctx c{p, static_cast<double*>(wsv), bt_stream(stream)};
+  static const bool no_chol = getenv("BT_SUB_CHOLQR") && getenv("BT_SUB_CHOLQR")[0] == '0';
+  const Ctx c{p, static_cast<double*>(wsv), bt_stream(stream), !no_chol};
   const bool dbg = getenv("BT_BASIS_DEBUG") != nullptr;
   double* q = c.at(p.off_q);
   double* y = c.at(p.off_y);

@@ -93,6 +93,26 @@ def test_matvec_block_of_rhs_equals_columns():
         assert cnt.flops == one.flops
 
 
+def test_blr_matvec_wide_ranks_and_partial_patterns():
+    """The row-group BLR kernel (rl <= 32 -> 4 block rows per CTA, 33..64 ->
+    2; column splits; > 64 RHS) and the per-row fallback (odd rr) against
+    densify @ x, on full (Hankel) and partial (banded: uncovered cells)
+    patterns.  Reference semantics: reconstruct.py:300-315."""
+    rng = np.random.default_rng(17)
+    cases = [("hankel", dict(), 48, 40), ("banded", dict(band=3), 24, 32),
+             ("toeplitz", dict(), 64, 64), ("hankel", dict(), 30, 33)]
+    for kind, kw, rl, rr in cases:
+        pat = bt.build_pattern(kind, 13, 13, 70, 66, **kw)
+        left = rng.standard_normal((pat.m, rl))
+        right = rng.standard_normal((pat.n, rr))
+        mids = rng.standard_normal((pat.p, rl, rr))
+        rep = reconstruct.BlockLowRankRep(pattern=pat, left=left, right=right, middles=mids)
+        xs = rng.standard_normal((pat.shape[1], 70))
+        ref = port.expand(pat, np.einsum("ma,kab,nb->kmn", left, mids, right)) @ xs
+        got = reconstruct.matvec(rep, xs)
+        assert rel(got, ref) < 1e-12, (kind, rl, rr)
+
+
 def test_flop_count_linear_in_terms():
     """test_reconstruct.py:152-165 / acceptance 9: r * (2mnq + 2m nnz)."""
     rng = np.random.default_rng(8)
