@@ -103,10 +103,39 @@ static void bt_gemm_geometry(BtGemmArgs& g, int64_t batch, int want_splits) {
   if (g.splits > KT) g.splits = static_cast<int>(std::max<int64_t>(KT, 1));
 }
 
+// resident CTAs per SM of the persistent kernel (cached per config)
+template <class Cfg>
+static int bt_persist_resident() {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    cudaFuncSetAttribute(bt_gemm_persist_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg::SMEM_BYTES);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bt_gemm_persist_kernel<Cfg>,
+                                                      Cfg::THREADS, Cfg::SMEM_BYTES) != cudaSuccess)
+      per_sm = 0;
+  }
+  return per_sm;
+}
+
 template <class Cfg>
 int bt_gemm_launch(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits) {
   bt_gemm_geometry<Cfg>(g, batch, want_splits);
   const int64_t tiles = g.symmetric ? g.tiles_m * (g.tiles_m + 1) / 2 : g.tiles_m * g.tiles_n;
+  {
+    // short reductions over many tiles: persistent CTAs with the stage
+    // pipeline running across tile boundaries
+    static const bool no_persist = getenv("BT_GEMM_PERSIST") && getenv("BT_GEMM_PERSIST")[0] == '0';
+    const int64_t KT = bt_cdiv(g.Kin, Cfg::BK) * g.Kout;
+    const int resident = (!no_persist && !g.symmetric && g.splits == 1 && KT <= 16)
+                             ? bt_persist_resident<Cfg>() : 0;
+    const int64_t slots = static_cast<int64_t>(resident) * bt_num_sms();
+    if (resident > 0 && tiles * batch >= 3 * slots) {
+      bt_gemm_persist_kernel<Cfg><<<static_cast<unsigned>(slots), Cfg::THREADS, Cfg::SMEM_BYTES,
+                                    st>>>(g, batch);
+      BT_LAUNCH_CHECK();
+      return BT_OK;
+    }
+  }
   static bool attr_done = false;
   if (!attr_done) {
     BT_CUDA_CHECK(cudaFuncSetAttribute(bt_gemm_kernel<Cfg>,
@@ -166,6 +195,8 @@ static int bt_dispatch_layout(const BtGemmArgs& g, int64_t batch, cudaStream_t s
 
 static int bt_tile_class(const BtGemmArgs& g) {
   if (g.symmetric) return BT_TILE_SQUARE;
+  static const char* force = getenv("BT_GEMM_FORCE");  // tuning switch (tools)
+  if (force && force[0] == 'w' && g.N > 64) return BT_TILE_WIDE;
   if (g.N <= 16) return BT_TILE_NARROW;
   static const bool no_mid = getenv("BT_GEMM_NO_MID") != nullptr;  // A/B switch (tools)
   if (g.N <= 32 && !no_mid) return BT_TILE_MID;

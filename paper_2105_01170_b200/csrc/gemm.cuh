@@ -295,6 +295,178 @@ __global__ void __launch_bounds__(Cfg::THREADS) bt_gemm_kernel(BtGemmArgs g) {
   }
 }
 
+// Persistent variant for short reductions (few k-tiles per output tile, many
+// tiles -- the 128-long mode products of the multilevel matvec, batched small
+// GEMMs): each CTA walks its tiles t = blockIdx.x, += gridDim.x as ONE stream
+// of (tile, k-tile) steps, so the cp.async stages of the next tile are in
+// flight while the current tile finishes and stores its accumulators (the
+// one-tile-per-CTA kernel drains and refills its pipeline at every tile).
+// Non-symmetric, no split-K; alpha/beta and the operand scales as above.
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS) bt_gemm_persist_kernel(BtGemmArgs g,
+                                                                       int64_t batches) {
+  extern __shared__ __align__(16) double smem_dyn[];
+  double* As = smem_dyn;
+  double* Bs = smem_dyn + Cfg::STAGES * Cfg::A_STAGE;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm0 = (warp % Cfg::WM) * Cfg::TM;
+  const int wn0 = (warp / Cfg::WM) * Cfg::TN;
+  const int64_t ktPerKo = (g.Kin + Cfg::BK - 1) / Cfg::BK;
+  const int64_t KT = ktPerKo * g.Kout;
+  const int64_t per_batch = g.tiles_m * g.tiles_n;
+  const int64_t total_tiles = per_batch * batches;
+  const int64_t my_tiles =
+      blockIdx.x < total_tiles ? (total_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t steps = my_tiles * KT;
+  constexpr int KSTEPS = Cfg::BK / 4;
+
+  BtTileLoader<Cfg::ROWS_A, (Cfg::A_KCONTIG ? Cfg::BK : Cfg::BM), Cfg::LDA, Cfg::VEC, Cfg::THREADS>
+      la;
+  BtTileLoader<Cfg::ROWS_B, (Cfg::B_KCONTIG ? Cfg::BK : Cfg::BN), Cfg::LDB, Cfg::VEC, Cfg::THREADS>
+      lb;
+  la.init(Cfg::A_KCONTIG ? g.A.s_mn : g.A.s_ki);
+  lb.init(Cfg::B_KCONTIG ? g.B.s_mn : g.B.s_ki);
+
+  auto tile_of = [&](int64_t local, int64_t& b, int64_t& m0, int64_t& n0) {
+    const int64_t t = blockIdx.x + local * gridDim.x;
+    b = t / per_batch;
+    const int64_t rem = t - b * per_batch;
+    const int64_t tn = rem / g.tiles_m;
+    m0 = (rem - tn * g.tiles_m) * Cfg::BM;
+    n0 = tn * Cfg::BN;
+  };
+
+  // load-side cursor
+  int64_t l_tile = 0, l_ko = 0, l_ki = 0;
+  int64_t l_b = 0, l_m0 = 0, l_n0 = 0;
+  if (my_tiles > 0) tile_of(0, l_b, l_m0, l_n0);
+  auto load_stage = [&](int stage) {
+    const double* Ab = g.A.ptr + l_b * g.A.s_b;
+    const double* Bb = g.B.ptr + l_b * g.B.s_b;
+    const double* a_tile = Ab + (Cfg::A_KCONTIG ? l_m0 * g.A.s_mn : l_m0);
+    const double* b_tile = Bb + (Cfg::B_KCONTIG ? l_n0 * g.B.s_mn : l_n0);
+    const int64_t ki0 = l_ki * Cfg::BK;
+    const int64_t k_left = g.Kin - ki0;
+    double* as = As + stage * Cfg::A_STAGE;
+    double* bs = Bs + stage * Cfg::B_STAGE;
+    if (Cfg::A_KCONTIG)
+      la.issue(as, a_tile + l_ko * g.A.s_ko + ki0, g.M - l_m0, k_left, g.A.ptr);
+    else
+      la.issue(as, a_tile + l_ko * g.A.s_ko + ki0 * g.A.s_ki, k_left, g.M - l_m0, g.A.ptr);
+    if (Cfg::B_KCONTIG)
+      lb.issue(bs, b_tile + l_ko * g.B.s_ko + ki0, g.N - l_n0, k_left, g.B.ptr);
+    else
+      lb.issue(bs, b_tile + l_ko * g.B.s_ko + ki0 * g.B.s_ki, k_left, g.N - l_n0, g.B.ptr);
+    if (++l_ki == ktPerKo) {
+      l_ki = 0;
+      if (++l_ko == g.Kout) {
+        l_ko = 0;
+        if (++l_tile < my_tiles) tile_of(l_tile, l_b, l_m0, l_n0);
+      }
+    }
+  };
+
+  double acc[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < Cfg::STAGES - 1; ++s) {
+    if (s < steps) load_stage(s);
+    cp_async_commit();
+  }
+  // compute-side cursor
+  int64_t c_tile = 0, c_ko = 0, c_ki = 0;
+  int64_t c_b = 0, c_m0 = 0, c_n0 = 0;
+  if (my_tiles > 0) tile_of(0, c_b, c_m0, c_n0);
+  int stage = 0;
+  int next_stage = Cfg::STAGES - 1;
+  double afr[2][Cfg::FM], bfr[2][Cfg::FN];
+  for (int64_t st = 0; st < steps; ++st) {
+    cp_async_wait<Cfg::STAGES - 2>();
+    __syncthreads();
+    const double* as = As + stage * Cfg::A_STAGE;
+    const double* bs = Bs + stage * Cfg::B_STAGE;
+    double sc[Cfg::FN];
+    if (g.bscale != nullptr) {
+      const double* srow = g.bscale + c_b * g.s_scale_b + c_ko * g.s_scale_ko;
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) {
+        const int64_t n = c_n0 + wn0 + j * 8 + gq;
+        sc[j] = (n < g.N) ? __ldg(srow + n) : 0.0;
+      }
+    }
+    const double* arow = nullptr;
+    int64_t a_kleft = 0;
+    if (g.ascale != nullptr) {
+      const int64_t ki0 = c_ki * Cfg::BK;
+      arow = g.ascale + c_b * g.s_ascale_b + c_ko * g.s_ascale_ko + ki0;
+      a_kleft = g.Kin - ki0;
+    }
+    auto load_frags = [&](int buf, int kk) {
+      double asc = 1.0;
+      if (g.ascale != nullptr) asc = (kk + tq < a_kleft) ? __ldg(arow + kk + tq) : 0.0;
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i) {
+        const int m = wm0 + i * 8 + gq;
+        afr[buf][i] = Cfg::A_KCONTIG ? as[m * Cfg::LDA + kk + tq] : as[(kk + tq) * Cfg::LDA + m];
+        if (g.ascale != nullptr) afr[buf][i] *= asc;
+      }
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) {
+        const int n = wn0 + j * 8 + gq;
+        bfr[buf][j] = Cfg::B_KCONTIG ? bs[n * Cfg::LDB + kk + tq] : bs[(kk + tq) * Cfg::LDB + n];
+        if (g.bscale != nullptr) bfr[buf][j] *= sc[j];
+      }
+    };
+    load_frags(0, 0);
+#pragma unroll
+    for (int ks = 0; ks < KSTEPS; ++ks) {
+      if (ks + 1 < KSTEPS) load_frags((ks + 1) & 1, (ks + 1) * 4);
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j)
+          dmma884(acc[i][j][0], acc[i][j][1], afr[ks & 1][i], bfr[ks & 1][j]);
+      if (ks == 0) {
+        if (st + Cfg::STAGES - 1 < steps) load_stage(next_stage);
+        cp_async_commit();
+      }
+    }
+    stage = (stage + 1 == Cfg::STAGES) ? 0 : stage + 1;
+    next_stage = (next_stage + 1 == Cfg::STAGES) ? 0 : next_stage + 1;
+    if (++c_ki == ktPerKo) {
+      c_ki = 0;
+      if (++c_ko == g.Kout) {
+        c_ko = 0;
+        // tile done: store (the next tile's first stages are already in flight)
+        double* Cb = g.C + c_b * g.sCb;
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) {
+          const int64_t m = c_m0 + wm0 + i * 8 + gq;
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int64_t n = c_n0 + wn0 + j * 8 + 2 * tq + h;
+              if (m < g.M && n < g.N) {
+                double* c = Cb + m * g.sCm + n * g.sCn;
+                const double v = g.alpha * acc[i][j][h];
+                *c = (g.beta == 0.0) ? v : v + g.beta * (*c);
+              }
+              acc[i][j][h] = 0.0;
+            }
+          }
+        }
+        if (++c_tile < my_tiles) tile_of(c_tile, c_b, c_m0, c_n0);
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
 // Deterministic split-K reduction (fixed order over splits) + mirror for
 // symmetric outputs + alpha/beta.
 __global__ void bt_gemm_reduce_kernel(BtGemmArgs g, int64_t bm, int64_t bn);
