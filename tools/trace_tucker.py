@@ -8,7 +8,27 @@ from torch.profiler import profile, ProfilerActivity
 from paper_2105_01170_b200 import configs, decomp
 
 which = sys.argv[1] if len(sys.argv) > 1 else "c3"
-if which == "c2":
+if which == "c1":
+    import numpy as np
+    import paper_2105_01170_b200 as bt
+    from paper_2105_01170_b200 import reconstruct
+    pat, a = configs.c1_matrix()
+    init = configs.normal_init((32, 32, 32), 8, 0)
+    rhs = torch.from_numpy(np.random.default_rng(1001).standard_normal((1024, 16))).cuda()
+
+    def c1():
+        t = bt.mat_to_tensor(a, pat)
+        saved = decomp._cp_init
+        decomp._cp_init = lambda _t, _r: [torch.from_numpy(f).cuda() for f in init]
+        try:
+            res = decomp.cp_als(t, 8, 50, 0.0)
+        finally:
+            decomp._cp_init = saved
+        ks = reconstruct.kron_sum_from_kruskal(res.rep, pat)
+        err = reconstruct.error_fro(a, ks)
+        return reconstruct.matvec(ks, rhs), err
+    runs = {"c1_pipeline": c1}
+elif which == "c2":
     params = configs.c2_markov()
     pat, t = configs.c2_build(params)
     runs = {"c2_hosvd": lambda: decomp.hosvd(t, [32, 400, 32])}
