@@ -289,6 +289,9 @@ int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need, double tau
                             const double* start, int64_t start_cols, int64_t hint, double* w,
                             double* v, int64_t* bq_out, int64_t* k_out, int* status, void* ws,
                             int64_t ws_bytes, void* stream);
+/* Diagnostic: 13 clock64 values: stamps (9) of sweep 1's phases in the fused one-CTA
+ * small CP-ALS kernel of bt_cp_als_f64, then 4 pinv timings (tools/prof_c1_small.py). */
+int bt_cp_small_clocks(long long* out);
 /* out[0] = trace(m), m n x n row-major (device double out) */
 int bt_trace_f64(const double* m, int64_t n, double* out, void* stream);
 /* SVQB column scaling: dinv = diag(m)^-1/2 (0 for a zero diagonal), out = D (m + m^T)/2 D */

@@ -465,6 +465,404 @@ __global__ void __launch_bounds__(1024) pinv_fast_kernel(const double* __restric
 
 
 // ---------------------------------------------------------------------------
+// Fused small CP-ALS (C1-sized tensors): every sweep of decomp.py:376-401 in
+// ONE launch of one CTA -- factors, P = X x3 C, MTTKRPs, Grams and the pinv
+// (pinv_block) live in shared memory, X streams from L2.  Same arithmetic as
+// the phase kernels (dimension tree for modes 1/2, Cholesky-first pinv, Gram-
+// identity fit with the explicit-residual switch, fixed-order sums); used
+// when the whole problem fits one SM (the multi-kernel sweep is launch-bound
+// there: ~25 kernels of a few microseconds each).
+// ---------------------------------------------------------------------------
+
+constexpr int SMALL_RS = 16;  // register row of R values
+__device__ long long g_small_clk[16];  // phase clocks of sweep 1 (tools/prof_c1_small.py)
+
+struct SmallLayout {
+  int64_t a, b, c, p, m, g, vp, gbuf, nrm, smf, red, total;
+};
+
+__host__ __device__ inline SmallLayout small_layout(int64_t I, int64_t J, int64_t K, int64_t R,
+                                                    int NP) {
+  SmallLayout l{};
+  int64_t o = 0;
+  auto take = [&](int64_t n) {
+    const int64_t at = o;
+    o += (n + 1) / 2 * 2;
+    return at;
+  };
+  l.a = take(I * R);
+  l.b = take(J * R);
+  l.c = take(K * R);
+  // P (I J R); reused for the mode-3 chunk partials [chunks][K][16] (16 warps)
+  const int64_t mt = (K + 7) / 8;
+  const int64_t ch = mt < 15 ? 15 / mt : 1;  // 15 compute warps (warp 0 runs the pinv)
+  l.p = take(I * J * R > ch * K * 16 ? I * J * R : ch * K * 16);
+  const int64_t mx = I > J ? (I > K ? I : K) : (J > K ? J : K);
+  l.m = take(mx * R);
+  l.g = take(3 * R * R);
+  l.vp = take(R * R);
+  l.gbuf = take(R * R + 2);
+  l.nrm = take(R);
+  l.smf = take(3 * NP * (NP + 1));
+  l.red = take(64);
+  l.total = o;
+  return l;
+}
+
+// fixed-order CTA sum (warp shuffles, then warp partials in order); all
+// threads return the total
+__device__ __forceinline__ double small_block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[k];
+  return t;
+}
+
+// Cholesky-first pinv of V = G0 o G1 (R <= 32) by ONE warp (warp-level
+// syncs only): the fast path of pinv_block (V^-1 = L^-T L^-1, accepted when
+// ||V||_1 ||V^-1||_1 <= 1e12).  Returns false (warp-uniform) when the caller
+// must take pinv_block's eigen path.  a, y: R x (R+1) scratch each.
+__device__ bool pinv_warp_chol(const double* __restrict__ g0, const double* __restrict__ g1,
+                               int R, double* __restrict__ vp, double* a, double* y) {
+  const int lane = threadIdx.x & 31;
+  const int ld = R + 1;
+  for (int e = lane; e < R * R; e += 32) {
+    const int r = e / R, c = e % R;
+    a[r * ld + c] = g0[e] * g1[e];
+  }
+  __syncwarp();
+  double cs = 0.0;
+  if (lane < R)
+    for (int r = 0; r < R; ++r) cs += fabs(a[r * ld + lane]);
+  double vn1 = cs;
+  for (int o = 16; o > 0; o >>= 1) vn1 = fmax(vn1, __shfl_xor_sync(0xffffffffu, vn1, o));
+  // in place: lower triangle -> L
+  for (int k = 0; k < R; ++k) {
+    const double d = a[k * ld + k];
+    if (!(d > 0.0)) return false;  // same d in every lane
+    const double lk = sqrt(d);
+    __syncwarp();
+    for (int i = k + 1 + lane; i < R; i += 32) a[i * ld + k] /= lk;
+    if (lane == 0) a[k * ld + k] = lk;
+    __syncwarp();
+    const int t = R - k - 1;
+    for (int e = lane; e < t * t; e += 32) {
+      const int ii = e / t, jj = e - ii * t;
+      if (jj <= ii)
+        a[(k + 1 + ii) * ld + k + 1 + jj] -= a[(k + 1 + ii) * ld + k] * a[(k + 1 + jj) * ld + k];
+    }
+    __syncwarp();
+  }
+  // Y = L^-1, one column per lane
+  if (lane < R) {
+    const int c = lane;
+    for (int i = 0; i < c; ++i) y[i * ld + c] = 0.0;
+    y[c * ld + c] = 1.0 / a[c * ld + c];
+    for (int i = c + 1; i < R; ++i) {
+      double sacc = 0.0;
+      for (int k = c; k < i; ++k) sacc = fma(a[i * ld + k], y[k * ld + c], sacc);
+      y[i * ld + c] = -sacc / a[i * ld + i];
+    }
+  }
+  __syncwarp();
+  // V^-1 = Y^T Y
+  for (int e = lane; e < R * R; e += 32) {
+    const int r = e / R, c = e % R;
+    const int k0 = r > c ? r : c;
+    double v = 0.0;
+    for (int k = k0; k < R; ++k) v = fma(y[k * ld + r], y[k * ld + c], v);
+    vp[e] = v;
+  }
+  __syncwarp();
+  double ic = 0.0;
+  if (lane < R)
+    for (int r = 0; r < R; ++r) ic += fabs(vp[r * R + lane]);
+  for (int o = 16; o > 0; o >>= 1) ic = fmax(ic, __shfl_xor_sync(0xffffffffu, ic, o));
+  return vn1 * ic <= 1e12;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(512)
+    cp_small_kernel(const double* __restrict__ X, int I, int J, int K, int R,
+                    double* __restrict__ ga, double* __restrict__ gb, double* __restrict__ gc,
+                    double* __restrict__ glam, double x2, int max_iters, double tol, int fit_mode,
+                    double* __restrict__ fit_hist, int* __restrict__ out_info) {
+  extern __shared__ __align__(16) double sm[];
+  const SmallLayout L = small_layout(I, J, K, R, NP);
+  double* F[3] = {sm + L.a, sm + L.b, sm + L.c};
+  double* P = sm + L.p;
+  double* M = sm + L.m;
+  double* G[3] = {sm + L.g, sm + L.g + R * R, sm + L.g + 2 * R * R};
+  double* Vp = sm + L.vp;
+  double* gbuf = sm + L.gbuf;
+  double* nrm = sm + L.nrm;
+  double* smf = sm + L.smf;
+  double* red = sm + L.red;
+  __shared__ int stop, pinv_ok;
+  __shared__ double fit_s, explicit_s;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t rows[3] = {I, J, K};
+  int it = 0;
+  for (int e = tid; e < I * R; e += nt) F[0][e] = ga[e];
+  for (int e = tid; e < J * R; e += nt) F[1][e] = gb[e];
+  for (int e = tid; e < K * R; e += nt) F[2][e] = gc[e];
+  if (tid == 0) stop = 0;
+  __syncthreads();
+  for (int k = 0; k < 3; ++k)
+    for (int e = tid; e < R * R; e += nt) {
+      const int a = e / R, b = e % R;
+      double s = 0.0;
+      for (int64_t r = 0; r < rows[k]; ++r) s = fma(F[k][r * R + a], F[k][r * R + b], s);
+      G[k][e] = s;
+    }
+  __syncthreads();
+  // one factor update from M (rows x R): pinv, F_un = M Vp, Gram, norms
+  // warp 0: Cholesky-first pinv of G_o0 o G_o1 while warps 1.. run the
+  // mode's MTTKRP (the Grams it needs are final before that MTTKRP starts)
+  auto pinv_w0 = [&](int go0, int go1) {
+    if ((tid >> 5) == 0) {
+      const long long c0 = clock64();
+      const bool ok = pinv_warp_chol(G[go0], G[go1], R, Vp, smf, smf + R * (R + 1));
+      if (tid == 0) pinv_ok = ok ? 1 : 0;
+      if (it == 1 && tid == 0) g_small_clk[9 + go0 + go1] = clock64() - c0;
+    }
+  };
+  auto solve = [&](int k, int go0, int go1, bool last) {
+    if (!pinv_ok) {
+      pinv_block<NP>(G[go0], G[go1], R, Vp, smf);
+      __syncthreads();
+    }
+    const int64_t nr = rows[k];
+    double* f = F[k];
+    for (int64_t e = tid; e < nr * R; e += nt) {
+      const int64_t row = e / R;
+      const int c = static_cast<int>(e % R);
+      double s = 0.0;
+      for (int q = 0; q < R; ++q) s = fma(M[row * R + q], Vp[q * R + c], s);
+      f[e] = s;
+    }
+    __syncthreads();
+    for (int e = tid; e < R * R; e += nt) {
+      const int a = e / R, b = e % R;
+      double s = 0.0;
+      for (int64_t r = 0; r < nr; ++r) s = fma(f[r * R + a], f[r * R + b], s);
+      gbuf[e] = s;
+    }
+    double inner = 0.0;
+    if (last) {
+      double s = 0.0;
+      for (int64_t e = tid; e < nr * R; e += nt) s = fma(f[e], M[e], s);
+      inner = small_block_sum(s, red);
+    }
+    __syncthreads();
+    for (int r = tid; r < R; r += nt) {
+      double v = sqrt(gbuf[r * R + r]);
+      if (v == 0.0) v = 1.0;
+      nrm[r] = v;
+    }
+    __syncthreads();
+    for (int e = tid; e < R * R; e += nt) G[k][e] = gbuf[e] / (nrm[e / R] * nrm[e % R]);
+    for (int64_t e = tid; e < nr * R; e += nt) f[e] = f[e] / nrm[e % R];
+    __syncthreads();
+    if (last) {
+      double s = 0.0;
+      for (int e = tid; e < R * R; e += nt)
+        s += nrm[e / R] * nrm[e % R] * G[0][e] * G[1][e] * G[2][e];
+      const double xh2 = small_block_sum(s, red);
+      if (tid == 0) {
+        const double res2 = fmax(x2 - 2.0 * inner + xh2, 0.0);
+        const double relres = sqrt(res2 / x2);
+        explicit_s = ((fit_mode == 1) || (fit_mode == 0 && relres < 1e-3)) ? 1.0 : 0.0;
+        fit_s = 1.0 - relres;
+      }
+      __syncthreads();
+    }
+  };
+  double prev = -INFINITY;
+  int conv = 0;
+  for (it = 0; it < max_iters; ++it) {
+    if (it == 1 && tid == 0) g_small_clk[0] = clock64();
+    // P = X x3 C  (P[ij][r] = sum_k X[ij][k] C[k][r]) on DMMA: warp per
+    // 8-row tile of (ij), both 8-wide r tiles, k in steps of 4
+    pinv_w0(1, 2);
+    if (tid >= 32) {
+      const int lane = tid & 31, warp = (tid >> 5) - 1, nw = (nt >> 5) - 1;
+      const int gq = lane >> 2, tq = lane & 3;
+      const int64_t IJ = (int64_t)I * J;
+      for (int64_t m0 = (int64_t)warp * 8; m0 < IJ; m0 += (int64_t)nw * 8) {
+        double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+        const int64_t row = m0 + gq;
+        const double* xr = X + (row < IJ ? row : 0) * K;
+        for (int k0 = 0; k0 < K; k0 += 4) {
+          const int kk = k0 + tq;
+          const double av = (row < IJ && kk < K) ? __ldg(xr + kk) : 0.0;
+          const double b0 = (kk < K && gq < R) ? F[2][kk * R + gq] : 0.0;
+          dmma884(c00, c01, av, b0);
+          if (R > 8) {
+            const double b1 = (kk < K && 8 + gq < R) ? F[2][kk * R + 8 + gq] : 0.0;
+            dmma884(c10, c11, av, b1);
+          }
+        }
+        if (row < IJ) {
+          const int n = 2 * tq;
+          if (n < R) P[row * R + n] = c00;
+          if (n + 1 < R) P[row * R + n + 1] = c01;
+          if (R > 8) {
+            if (8 + n < R) P[row * R + 8 + n] = c10;
+            if (9 + n < R) P[row * R + 9 + n] = c11;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (it == 1 && tid == 0) g_small_clk[1] = clock64();
+    // mode 1: M[i][r] = sum_j P[i][j][r] B[j][r]
+    if (tid >= 32)
+      for (int e = tid - 32; e < I * R; e += nt - 32) {
+        const int i = e / R, r = e % R;
+        double s = 0.0;
+        for (int j = 0; j < J; ++j) s = fma(P[((int64_t)i * J + j) * R + r], F[1][j * R + r], s);
+        M[e] = s;
+      }
+    __syncthreads();
+    if (it == 1 && tid == 0) g_small_clk[2] = clock64();
+    solve(0, 1, 2, false);
+    if (it == 1 && tid == 0) g_small_clk[3] = clock64();
+    // mode 2: M[j][r] = sum_i P[i][j][r] A[i][r]  (A just updated)
+    pinv_w0(0, 2);
+    if (tid >= 32)
+      for (int e = tid - 32; e < J * R; e += nt - 32) {
+        const int j = e / R, r = e % R;
+        double s = 0.0;
+        for (int i = 0; i < I; ++i) s = fma(P[((int64_t)i * J + j) * R + r], F[0][i * R + r], s);
+        M[e] = s;
+      }
+    __syncthreads();
+    if (it == 1 && tid == 0) g_small_clk[4] = clock64();
+    solve(1, 0, 2, false);
+    if (it == 1 && tid == 0) g_small_clk[5] = clock64();
+    // mode 3: M[k][r] = sum_ij X[ij][k] A[i][r] B[j][r] on DMMA: rows k
+    // (8-tiles), cols r, the (ij) reduction split in fixed chunks over the
+    // warps, chunk partials summed in order through shared memory
+    pinv_w0(0, 1);
+    {
+      const int lane = tid & 31, warp = (tid >> 5) - 1, nw = (nt >> 5) - 1;
+      const int gq = lane >> 2, tq = lane & 3;
+      const int64_t IJ = (int64_t)I * J;
+      const int mtiles = (K + 7) / 8;
+      const int chunks = nw / mtiles > 0 ? nw / mtiles : 1;  // as small_layout (nw = 15)
+      const int64_t clen = ((IJ + chunks - 1) / chunks + 3) / 4 * 4;
+      double* part = P;  // P is free again: [chunk][k][16] partials
+      for (int item = warp; warp >= 0 && item < mtiles * chunks; item += nw) {
+        const int mt = item % mtiles, ch = item / mtiles;
+        const int kr = mt * 8 + gq;
+        double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+        const int64_t s0 = ch * clen, s1 = s0 + clen < IJ ? s0 + clen : IJ;
+        int64_t ij = s0 + tq;
+        int64_t ii = ij / J, jj = ij - ii * J;
+        constexpr int UN = 8;  // X loads in flight per lane
+        for (int64_t base = s0; base < s1; base += 4 * UN) {
+          double av[UN];
+          int iu[UN], ju[UN];
+          bool vu[UN];
+#pragma unroll
+          for (int u = 0; u < UN; ++u) {
+            vu[u] = ij < s1;
+            av[u] = (vu[u] && kr < K) ? __ldg(X + ij * K + kr) : 0.0;
+            iu[u] = static_cast<int>(ii);
+            ju[u] = static_cast<int>(jj);
+            ij += 4;
+            jj += 4;
+            while (jj >= J) {
+              jj -= J;
+              ++ii;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < UN; ++u) {
+            double w0 = 0.0, w1 = 0.0;
+            if (vu[u]) {
+              if (gq < R) w0 = F[0][iu[u] * R + gq] * F[1][ju[u] * R + gq];
+              if (8 + gq < R) w1 = F[0][iu[u] * R + 8 + gq] * F[1][ju[u] * R + 8 + gq];
+            }
+            dmma884(c00, c01, av[u], w0);
+            if (R > 8) dmma884(c10, c11, av[u], w1);
+          }
+        }
+        double* pp = part + ((int64_t)ch * K) * 16;
+        if (kr < K) {
+          pp[kr * 16 + 2 * tq] = c00;
+          pp[kr * 16 + 2 * tq + 1] = c01;
+          pp[kr * 16 + 8 + 2 * tq] = c10;
+          pp[kr * 16 + 9 + 2 * tq] = c11;
+        }
+      }
+      __syncthreads();
+      for (int e = tid; e < K * R; e += nt) {
+        const int kk = e / R, r = e % R;
+        double s = 0.0;
+        for (int ch = 0; ch < chunks; ++ch) s += part[((int64_t)ch * K + kk) * 16 + r];
+        M[e] = s;
+      }
+    }
+    __syncthreads();
+    if (it == 1 && tid == 0) g_small_clk[6] = clock64();
+    solve(2, 0, 1, true);   // sets glam-equivalent nrm, fit_s, explicit_s
+    if (it == 1 && tid == 0) g_small_clk[7] = clock64();
+    if (explicit_s != 0.0) {
+      // ||X - [[A lam, B, C]]||^2, one (i, j) row per thread pass
+      double loc = 0.0;
+      for (int64_t ij = tid; ij < (int64_t)I * J; ij += nt) {
+        const int64_t i = ij / J, j = ij % J;
+        double wb[SMALL_RS];
+#pragma unroll
+        for (int r = 0; r < SMALL_RS; ++r)
+          wb[r] = (r < R) ? F[0][i * R + r] * nrm[r] * F[1][j * R + r] : 0.0;
+        const double* xr = X + ij * K;
+        for (int kk = 0; kk < K; ++kk) {
+          double xh = 0.0;
+#pragma unroll
+          for (int r = 0; r < SMALL_RS; ++r)
+            if (r < R) xh = fma(wb[r], F[2][kk * R + r], xh);
+          const double d = __ldg(xr + kk) - xh;
+          loc = fma(d, d, loc);
+        }
+      }
+      const double res2 = small_block_sum(loc, red);
+      if (tid == 0) fit_s = 1.0 - sqrt(res2) / sqrt(x2);
+    }
+    __syncthreads();
+    if (it == 1 && tid == 0) g_small_clk[8] = clock64();
+    if (tid == 0) {
+      const double fit = fit_s;
+      fit_hist[it] = fit;
+      if (tol > 0.0 && fabs(fit - prev) < tol) stop = 1;
+      prev = fit;
+    }
+    __syncthreads();
+    if (stop) {
+      conv = 1;
+      ++it;
+      break;
+    }
+  }
+  if (it > max_iters) it = max_iters;
+  // outputs: x = F0 * lam (KruskalRep.x), normalised F1, F2, lam
+  for (int e = tid; e < I * R; e += nt) ga[e] = F[0][e] * nrm[e % R];
+  for (int e = tid; e < J * R; e += nt) gb[e] = F[1][e];
+  for (int e = tid; e < K * R; e += nt) gc[e] = F[2][e];
+  for (int r = tid; r < R; r += nt) glam[r] = nrm[r];
+  if (tid == 0) {
+    out_info[0] = it;
+    out_info[1] = conv;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // solve: F_un = (sum_s Mpart[s]) @ Vp ; per-CTA Gram + <F_un, M> partials
 // ---------------------------------------------------------------------------
 
@@ -1402,11 +1800,83 @@ extern "C" int bt_cp_state_finish(void* state, int n_iters, double* fit_history)
   return BT_OK;
 }
 
+// Diagnostic: clock64 stamps of sweep 1's phases in the fused small kernel
+// (P, mode 1 MTTKRP, solve 1, mode 2, solve 2, mode 3, solve 3, fit, end).
+extern "C" int bt_cp_small_clocks(long long* out) {
+  BT_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_small_clk, sizeof(long long) * 13));
+  return BT_OK;
+}
+
 // One-GPU driver over the phase API (no cross-rank sums).
+// The fused one-CTA path of bt_cp_als_f64 for tensors that fit one SM.
+// Returns 1 when it ran (outputs written), 0 when the problem is not eligible.
+static int cp_small_try(const bt_cp_problem* pb, double* a, double* b, double* c, double* lam,
+                        int max_iters, double tol, int fit_mode, double* fit_history,
+                        int* n_iters, int* converged, cudaStream_t st, int* rc) {
+  static const bool off = getenv("BT_CP_SMALL") && getenv("BT_CP_SMALL")[0] == '0';
+  *rc = BT_OK;
+  const int64_t I = pb->I, J = pb->J, K = pb->K, R = pb->R;
+  if (off || R > SMALL_RS || I < 1 || J < 1 || K < 1 || I * J * K > (int64_t(1) << 17) ||
+      I > 1024 || J > 1024 || K > 1024 || pb->norm_x <= 0.0)
+    return 0;
+  const int NP = R <= 8 ? 8 : 16;
+  const size_t smem = static_cast<size_t>(small_layout(I, J, K, R, NP).total) * 8;
+  if (smem > 200 * 1024) return 0;
+  double* dbuf = nullptr;
+  cudaError_t e = cudaMallocAsync(&dbuf, sizeof(double) * (max_iters + 2), st);
+  if (e != cudaSuccess) {
+    bt_set_error("cp_als: %s", cudaGetErrorString(e));
+    *rc = BT_E_CUDA;
+    return 1;
+  }
+  int* info = reinterpret_cast<int*>(dbuf + max_iters);
+  const double x2 = pb->norm_x * pb->norm_x;
+  if (NP == 8) {
+    cudaFuncSetAttribute(cp_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    cp_small_kernel<8><<<1, 512, smem, st>>>(pb->x, (int)I, (int)J, (int)K, (int)R, a, b, c, lam,
+                                             x2, max_iters, tol, fit_mode, dbuf, info);
+  } else {
+    cudaFuncSetAttribute(cp_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    cp_small_kernel<16><<<1, 512, smem, st>>>(pb->x, (int)I, (int)J, (int)K, (int)R, a, b, c,
+                                              lam, x2, max_iters, tol, fit_mode, dbuf, info);
+  }
+  cudaError_t le = cudaGetLastError();
+  if (le != cudaSuccess) {
+    bt_set_error("cp_small_kernel: %s", cudaGetErrorString(le));
+    cudaFreeAsync(dbuf, st);
+    *rc = BT_E_CUDA;
+    return 1;
+  }
+  bt_count_launch();
+  int hinfo[2] = {0, 0};
+  cudaMemcpyAsync(hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  if (hinfo[0] > 0 && fit_history)
+    cudaMemcpyAsync(fit_history, dbuf, sizeof(double) * hinfo[0], cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(dbuf, st);
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    bt_set_error("cp_small: %s", cudaGetErrorString(e));
+    *rc = BT_E_CUDA;
+    return 1;
+  }
+  *n_iters = hinfo[0];
+  *converged = hinfo[1];
+  return 1;
+}
+
 extern "C" int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, double* c,
                              double* lam, int max_iters, double tol, int fit_mode,
                              double* fit_history, int* n_iters, int* converged, double* phase_ms,
                              void* wsv, int64_t ws_bytes, void* stream) {
+  if (phase_ms == nullptr && max_iters >= 1) {
+    int rc = BT_OK;
+    if (cp_small_try(pb, a, b, c, lam, max_iters, tol, fit_mode, fit_history, n_iters, converged,
+                     bt_stream(stream), &rc))
+      return rc;
+  }
   void* h = nullptr;
   BT_TRY(bt_cp_state_create(pb, a, b, c, lam, max_iters, fit_mode, wsv, ws_bytes, stream, &h));
   auto* S = static_cast<bt_cp_state*>(h);
