@@ -1102,33 +1102,51 @@ __global__ void __launch_bounds__(Cfg::THREADS)
 // DMMA tile version is latency bound (a K = R reduction per X tile): a warp
 // owns a 32-wide k chunk -- C[k, :] in registers -- and streams (i, j) rows
 // of X with coalesced loads; Xhat[i][j][k] = sum_r (W[i][r] B[j][r]) C[k][r].
-// Fixed-order sums (deterministic); X read once.
+// The row factors W[i] o B[j] of the warp's rows are formed once into
+// shared memory (each lane two products per row instead of 2 R loads per
+// element) and read back as broadcast double2.  Fixed-order sums
+// (deterministic); X read once.
 template <int RS>
 __global__ void __launch_bounds__(256)
     residual_small_kernel(const double* __restrict__ X, const double* __restrict__ W,
                           const double* __restrict__ Bf, const double* __restrict__ Cf, int64_t I,
                           int64_t J, int64_t K, int R, const double* __restrict__ flag,
                           double* __restrict__ part) {
+  constexpr int ROWS = 512 / RS;  // 32 KB of row factors per CTA
+  __shared__ __align__(16) double wbs[8][ROWS * RS];
   __shared__ double red[8];
   if (flag != nullptr && *flag == 0.0) {
     if (threadIdx.x == 0) part[blockIdx.x] = 0.0;
     return;
   }
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* wb = wbs[wid];
   const int64_t kchunks = (K + 31) / 32;
-  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + wid;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   double local = 0.0;
-  // warp work item: (k chunk, row group of 64 (i, j) rows)
+  // warp work item: (k chunk, row group of ROWS (i, j) rows)
   const int64_t rows = I * J;
-  const int64_t groups = (rows + 63) / 64;
+  const int64_t groups = (rows + ROWS - 1) / ROWS;
   for (int64_t item = gw; item < kchunks * groups; item += nwarps) {
     const int64_t kc = item % kchunks, g = item / kchunks;
     const int64_t k = kc * 32 + lane;
     double c[RS];
 #pragma unroll
     for (int r = 0; r < RS; ++r) c[r] = (k < K && r < R) ? __ldg(Cf + k * R + r) : 0.0;
-    const int64_t r0 = g * 64, r1 = r0 + 64 < rows ? r0 + 64 : rows;
+    const int64_t r0 = g * ROWS, r1 = r0 + ROWS < rows ? r0 + ROWS : rows;
+    __syncwarp();
+    for (int e = lane; e < ROWS * RS; e += 32) {
+      const int rr = e / RS, r = e - rr * RS;
+      const int64_t row = r0 + rr;
+      double v = 0.0;
+      if (row < r1 && r < R) {
+        const int64_t i = row / J, j = row - i * J;
+        v = __ldg(W + i * R + r) * __ldg(Bf + j * R + r);
+      }
+      wb[e] = v;
+    }
+    __syncwarp();
     constexpr int UR = 4;  // independent X loads in flight per lane
     for (int64_t row = r0; row < r1; row += UR) {
       double xv[UR];
@@ -1138,11 +1156,14 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int u = 0; u < UR; ++u) {
         if (row + u >= r1) break;
-        const int64_t i = (row + u) / J, j = (row + u) - i * J;
+        const double2* w2 = reinterpret_cast<const double2*>(wb + (row + u - r0) * RS);
         double xh = 0.0;
 #pragma unroll
-        for (int r = 0; r < RS; ++r)
-          if (r < R) xh = fma(__ldg(W + i * R + r) * __ldg(Bf + j * R + r), c[r], xh);
+        for (int r = 0; r < RS / 2; ++r) {
+          const double2 w = w2[r];
+          xh = fma(w.x, c[2 * r], xh);
+          xh = fma(w.y, c[2 * r + 1], xh);
+        }
         if (k < K) {
           const double d = xv[u] - xh;
           local = fma(d, d, local);
