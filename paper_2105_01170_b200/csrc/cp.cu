@@ -385,6 +385,19 @@ __device__ void pinv_block(const double* __restrict__ g0, const double* __restri
     __syncthreads();
   }
   __syncthreads();
+  if (chol_ok && tid == 0) {
+    // kappa_2(V) >= (max l_kk / min l_kk)^2 and kappa_1 >= kappa_2 / R: a
+    // diagonal ratio beyond R * 1e12 fails the test below for sure, so the
+    // inverse is not formed (ill-conditioned V goes straight to the eigen path)
+    double lo = INFINITY, hi = 0.0;
+    for (int k = 0; k < R; ++k) {
+      const double l = x[k * LD + k];
+      lo = fmin(lo, l);
+      hi = fmax(hi, l);
+    }
+    if ((hi / lo) * (hi / lo) > 1e12 * R) chol_ok = 0;
+  }
+  __syncthreads();
   if (chol_ok) {
     // Y = L^-1 by right-looking substitution on the identity, one barrier
     // per step (row k's division is applied one step late, when no thread
@@ -447,8 +460,8 @@ __device__ void pinv_block(const double* __restrict__ g0, const double* __restri
   __syncthreads();
   double fro2 = 0.0;
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) fro2 += fro_red[w];
-  if (NP <= 32)
-    jacobi_warp(a, q, NP, LD, cs, sn, pp, qq, 40, 1e-15 * sqrt(fro2), 1e-15);
+  if constexpr (NP <= 32)
+    jacobi_warp_t<NP>(a, q, LD, cs, sn, pp, qq, 40, 1e-15 * sqrt(fro2), 1e-15);
   else
     jacobi_fast(a, q, NP, LD, cs, sn, pp, qq, 40, 1e-15 * sqrt(fro2), 1e-15);
   __syncthreads();

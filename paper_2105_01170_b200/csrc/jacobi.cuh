@@ -137,6 +137,95 @@ static __device__ __noinline__ int jacobi_fast(double* a, double* qv, int n, int
   return any;
 }
 
+// jacobi_warp with the size known at compile time: every lane's 2x2 blocks
+// and eigenvector entries are fixed across rounds, so their (k1, k2) / (k, i)
+// coordinates are computed once instead of by integer division every round.
+// Same operations per element as jacobi_warp (identical results).
+template <int N>
+static __device__ __noinline__ int jacobi_warp_t(double* a, double* qv, int ld, double* cs,
+                                                 double* sn, int* pp, int* qq, int max_sweeps,
+                                                 double abs_tol, double rel_tol) {
+  static_assert(N % 2 == 0 && N <= 64, "jacobi_warp_t: even N <= 64");
+  constexpr int HALF = N / 2;
+  constexpr int NB = (HALF * HALF + 31) / 32;
+  constexpr int NQ = (HALF * N + 31) / 32;
+  if (threadIdx.x >= 32) return 0;
+  const int lane = threadIdx.x;
+  int b1[NB], b2[NB], qk[NQ], qi[NQ];
+#pragma unroll
+  for (int u = 0; u < NB; ++u) {
+    const int e = lane + 32 * u;
+    b1[u] = e < HALF * HALF ? e / HALF : -1;
+    b2[u] = e < HALF * HALF ? e % HALF : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < NQ; ++u) {
+    const int e = lane + 32 * u;
+    qk[u] = e < HALF * N ? e / N : -1;
+    qi[u] = e < HALF * N ? e % N : 0;
+  }
+  int any = 0;
+  for (int idx = lane; idx < N * N; idx += 32) {
+    const int r = idx / N, c = idx - r * N;
+    qv[r * ld + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    int rotated = 0;
+    for (int rnd = 0; rnd < N - 1; ++rnd) {
+      if (lane < HALF) {
+        int p, q;
+        rr_pair(N, rnd, lane, p, q);
+        const double apq = a[p * ld + q];
+        const double app = a[p * ld + p], aqq = a[q * ld + q];
+        double c = 1.0, s = 0.0;
+        if (apq != 0.0 && fabs(apq) > abs_tol && fabs(apq) > rel_tol * sqrt(fabs(app) * fabs(aqq))) {
+          jacobi_rotation(app, aqq, apq, c, s);
+          rotated = 1;
+        }
+        cs[lane] = c;
+        sn[lane] = s;
+        pp[lane] = p;
+        qq[lane] = q;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        const int k1 = b1[u], k2 = b2[u];
+        if (k1 < 0) continue;
+        const double s1 = sn[k1], s2 = sn[k2];
+        if (s1 == 0.0 && s2 == 0.0) continue;
+        const double c1 = cs[k1], c2 = cs[k2];
+        const int p1 = pp[k1], q1 = qq[k1], p2 = pp[k2], q2 = qq[k2];
+        const double x11 = a[p1 * ld + p2], x12 = a[p1 * ld + q2];
+        const double x21 = a[q1 * ld + p2], x22 = a[q1 * ld + q2];
+        const double y11 = c1 * x11 - s1 * x21, y12 = c1 * x12 - s1 * x22;
+        const double y21 = s1 * x11 + c1 * x21, y22 = s1 * x12 + c1 * x22;
+        a[p1 * ld + p2] = c2 * y11 - s2 * y12;
+        a[q1 * ld + q2] = s2 * y21 + c2 * y22;
+        a[p1 * ld + q2] = (k1 == k2) ? 0.0 : s2 * y11 + c2 * y12;
+        a[q1 * ld + p2] = (k1 == k2) ? 0.0 : c2 * y21 - s2 * y22;
+      }
+#pragma unroll
+      for (int u = 0; u < NQ; ++u) {
+        const int k = qk[u], i = qi[u];
+        if (k < 0) continue;
+        const double s = sn[k];
+        if (s == 0.0) continue;
+        const double c = cs[k];
+        const int p = pp[k], q = qq[k];
+        const double x = qv[i * ld + p], y = qv[i * ld + q];
+        qv[i * ld + p] = c * x - s * y;
+        qv[i * ld + q] = s * x + c * y;
+      }
+      __syncwarp();
+    }
+    if (!__any_sync(0xffffffffu, rotated)) break;
+    any = 1;
+  }
+  return any;
+}
+
 // Warp-synchronous variant for n <= 32 (the CP pinv at R <= 32): executed by
 // warp 0 alone, __syncwarp instead of CTA barriers (a round costs a few
 // hundred cycles instead of two CTA-wide barriers).  Same rotation rule and
