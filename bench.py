@@ -622,6 +622,16 @@ def run_bt200(args, rank, world):
     del x
     ws_cache.clear()
     torch.cuda.empty_cache()
+    # ---- GPU secondary configs first: the host-side numpy work of the CPU
+    # baselines below leaves OpenBLAS threads spinning, which would steal
+    # the host cores the latency-bound configs (C1) launch from
+    ex = None
+    if not args.no_extras and rank == 0:
+        ex = extras_run(torch)
+        for key in ("c3_gram_mode1", "c3_ttm_mode1"):
+            if isinstance(ex.get(key + "_tflops"), float):
+                ex[key + "_frac_dmma"] = ex[key + "_tflops"] / peak
+        result["extras"] = ex
     # ---- CPU baseline (bounded slab, rank 0, N=1)
     if not args.no_cpu and rank == 0 and world == 1:
         try:
@@ -639,19 +649,13 @@ def run_bt200(args, rank, world):
             del host
         except Exception as exc:  # pragma: no cover
             result["cpu_baseline"] = {"value": None, "error": repr(exc)[:300]}
-    if not args.no_extras and rank == 0:
-        ex = extras_run(torch)
-        for key in ("c3_gram_mode1", "c3_ttm_mode1"):
-            if isinstance(ex.get(key + "_tflops"), float):
-                ex[key + "_frac_dmma"] = ex[key + "_tflops"] / peak
-        result["extras"] = ex
-        if not args.no_cpu and world == 1:
-            cpu = extras_cpu()
-            result["extras_cpu_reference"] = cpu
-            result["extras_speedup_vs_cpu"] = {
-                k: cpu[k] / ex[k] for k in ("c1_pipeline_ms", "c2_hosvd_ms", "c2_matvec64_ms",
-                                            "c3_st_hosvd_ms", "c4_cp_ms", "gather_standin_ms")
-                if isinstance(cpu.get(k), float) and isinstance(ex.get(k), float) and ex[k] > 0}
+    if ex is not None and not args.no_cpu and world == 1:
+        cpu = extras_cpu()
+        result["extras_cpu_reference"] = cpu
+        result["extras_speedup_vs_cpu"] = {
+            k: cpu[k] / ex[k] for k in ("c1_pipeline_ms", "c2_hosvd_ms", "c2_matvec64_ms",
+                                        "c3_st_hosvd_ms", "c4_cp_ms", "gather_standin_ms")
+            if isinstance(cpu.get(k), float) and isinstance(ex.get(k), float) and ex[k] > 0}
     if rank == 0:
         print(json.dumps(result), flush=True)
 
