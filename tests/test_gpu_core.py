@@ -270,3 +270,105 @@ def test_qr_thin_vs_numpy(shape, cond):
     assert np.abs(q.T @ q - np.eye(n)).max() < 1e-12
     assert np.linalg.norm(q @ r - a) <= 1e-13 * np.linalg.norm(a)
     assert np.abs(r - ro).max() <= 1e-12 * cond * np.abs(ro).max()
+
+
+# ---------------------------------------------------------------------------
+# fused one-CTA CP-ALS (SM-sized tensors) vs the phase kernels
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dims,r,fit", [((32, 32, 32), 8, "auto"), ((7, 19, 11), 5, "explicit"),
+                                        ((40, 9, 33), 13, "gram"), ((16, 16, 64), 16, "auto"),
+                                        ((5, 6, 7), 1, "auto")])
+def test_cp_fused_small_matches_phase_kernels(dims, r, fit):
+    """cp_als on a tensor that fits one SM runs cp_small_kernel (one launch
+    for all sweeps); the phase C-ABI (bt_cp_*) runs the multi-kernel sweep.
+    Same fit histories, factors and weights (different summation orders)."""
+    from paper_2105_01170_b200 import _dev
+    from paper_2105_01170_b200.parallel import NativeCpOps, cp_als_sharded
+
+    rng = np.random.default_rng(sum(dims) + r)
+    x = rng.standard_normal(dims)
+    init = oc.normal_init(dims, r, 7)
+    iters = 12
+    saved = with_init(init)
+    try:
+        res = bt.cp_als(x, r, iters, 0.0, fit=fit)
+    finally:
+        decomp._cp_init = saved
+    xd = torch.from_numpy(x).cuda()
+    f = [torch.from_numpy(v.copy()).cuda() for v in init]
+    ops = NativeCpOps(xd, r, f[0], f[1], f[2], iters, fit=fit)
+    hist, n, conv = cp_als_sharded(ops, iters, 0.0, lambda b: None)
+    ops.close()
+    np.testing.assert_allclose(res.fit_history, hist, rtol=0, atol=1e-11)
+    ref = port.cp_als(x, r, iters, 0.0, init=lambda _t, _r: [v.copy() for v in init])
+    np.testing.assert_allclose(res.fit_history, ref.fit_history, rtol=0, atol=1e-10)
+    assert res.n_iters == iters and not res.converged
+    assert _dev.is_device(res.rep.x) is False
+
+
+def test_cp_fused_small_tol_stops_like_reference():
+    """tol > 0: the in-kernel |fit - prev| < tol test stops at the same sweep
+    as decomp.py:398-401 (oracle restatement)."""
+    rng = np.random.default_rng(3)
+    a, b, c = (rng.standard_normal((n, 3)) for n in (12, 10, 9))
+    x = np.einsum("ir,jr,kr->ijk", a, b, c) + 1e-3 * rng.standard_normal((12, 10, 9))
+    init = oc.normal_init(x.shape, 3, 11)
+    saved = with_init(init)
+    try:
+        res = bt.cp_als(x, 3, 200, 1e-9)
+    finally:
+        decomp._cp_init = saved
+    ref = port.cp_als(x, 3, 200, 1e-9, init=lambda _t, _r: [v.copy() for v in init])
+    assert res.converged == ref.converged and res.n_iters == ref.n_iters
+    np.testing.assert_allclose(res.fit_history, ref.fit_history, rtol=0, atol=1e-10)
+
+
+# ---------------------------------------------------------------------------
+# leading eigenpairs of a deflation pass (bt_leading_subspace_f64)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,need,decay", [(300, 20, 8.0), (600, 64, 3.0), (257, 5, 14.0)])
+def test_leading_subspace_vs_numpy(n, need, decay):
+    rng = np.random.default_rng(n + need)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = 10.0 ** (-decay * np.linspace(0, 1, n) ** 0.5)
+    g = (q * lam) @ q.T
+    g = (g + g.T) / 2
+    gd = torch.from_numpy(g).cuda()
+    out = L._leading_subspace(gd, need, 1e-6)
+    if out is None:          # predicted too slow: the caller's tridiagonal fallback
+        w, v = L.eigh_dev(gd, nvec=need, tau=1e-6)
+        k = need
+    else:
+        w, v, k = out
+    w, v = w.cpu().numpy(), v.cpu().numpy()
+    assert k >= 1
+    ref_w, ref_v = np.linalg.eigh(g)
+    ref_w, ref_v = ref_w[::-1], ref_v[:, ::-1]
+    np.testing.assert_allclose(w[:k], ref_w[:k], rtol=0, atol=64 * 2.2e-16 * ref_w[0])
+    # accepted vectors: residual-certified, orthonormal, sign rule applied
+    vk = v[:, :k]
+    assert np.abs(vk.T @ vk - np.eye(k)).max() < 1e-12
+    res = np.linalg.norm(g @ vk - vk * w[:k], axis=0)
+    assert res.max() <= 40 * 2.2e-16 * ref_w[0]
+    idx = np.argmax(np.abs(vk), axis=0)
+    assert np.all(vk[idx, np.arange(k)] > 0)
+
+
+def test_leading_subspace_warm_start_and_shape_guard():
+    rng = np.random.default_rng(5)
+    n = 400
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = 10.0 ** (-40 * np.linspace(0, 1, n))   # 10^-0.1 per index: a fast block edge
+    g = (q * lam) @ q.T
+    g = (g + g.T) / 2
+    gd = torch.from_numpy(g).cuda()
+    w0, v0, k0 = L._leading_subspace(gd, 30, 1e-6)
+    # warm start with the answer: converges to the same pairs
+    w1, v1, k1 = L._leading_subspace(gd, 30, 1e-6, start=v0[:, :k0].contiguous())
+    kk = min(k0, k1)
+    assert subspace_angle(v0[:, :kk].cpu().numpy(), v1[:, :kk].cpu().numpy()) < 1e-10
+    # a block wider than n / 2 is not applicable (status 2 -> None)
+    small = torch.from_numpy(g[:40, :40].copy()).cuda()
+    assert L._leading_subspace(small, 30, 1e-6) is None
