@@ -252,6 +252,32 @@ __device__ __forceinline__ void bt_tile_coords(const BtGemmArgs& g, int64_t lin,
   tn = lin - r * (r + 1) / 2;
 }
 
+// Fast epilogue for an interior tile of a row-major C (sCn == 1, beta == 0,
+// 16-byte aligned rows): row pointers formed once per fragment row, the two
+// accumulators of a lane stored as one 16-byte st.global -- no per-element
+// bounds checks or 64-bit address products (the generic path costs ~8
+// integer instructions per element, a quarter of a K = 128 tile's issue).
+// Returns false when the tile needs the generic path.
+template <class Cfg>
+__device__ __forceinline__ bool bt_store_tile_fast(const BtGemmArgs& g, double* Cb, int64_t m0,
+                                                   int64_t n0, int wm0, int wn0, int gq, int tq,
+                                                   double (&acc)[Cfg::FM][Cfg::FN][2]) {
+  if (!(g.sCn == 1 && g.beta == 0.0 && (g.sCm & 1) == 0 && m0 + Cfg::BM <= g.M &&
+        n0 + Cfg::BN <= g.N && (reinterpret_cast<uintptr_t>(Cb) & 15u) == 0))
+    return false;
+  double* base = Cb + (m0 + wm0 + gq) * g.sCm + (n0 + wn0 + 2 * tq);
+  const int64_t row8 = 8 * g.sCm;
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i) {
+    double* row = base + i * row8;
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j)
+      *reinterpret_cast<double2*>(row + j * 8) =
+          make_double2(g.alpha * acc[i][j][0], g.alpha * acc[i][j][1]);
+  }
+  return true;
+}
+
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS) bt_gemm_kernel(BtGemmArgs g) {
   extern __shared__ __align__(16) double smem_dyn[];
@@ -273,6 +299,7 @@ __global__ void __launch_bounds__(Cfg::THREADS) bt_gemm_kernel(BtGemmArgs g) {
   const bool direct = (g.splits == 1) && !g.symmetric;
   double* wsb = g.ws + (batch * g.splits + split) * g.M * g.N;
   double* Cb = g.C + batch * g.sCb;
+  if (direct && bt_store_tile_fast<Cfg>(g, Cb, m0, n0, wm0, wn0, gq, tq, acc)) return;
 #pragma unroll
   for (int i = 0; i < Cfg::FM; ++i) {
     const int64_t m = m0 + wm0 + i * 8 + gq;
@@ -443,6 +470,14 @@ __global__ void __launch_bounds__(Cfg::THREADS) bt_gemm_persist_kernel(BtGemmArg
         c_ko = 0;
         // tile done: store (the next tile's first stages are already in flight)
         double* Cb = g.C + c_b * g.sCb;
+        if (bt_store_tile_fast<Cfg>(g, Cb, c_m0, c_n0, wm0, wn0, gq, tq, acc)) {
+#pragma unroll
+          for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+            for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+          if (++c_tile < my_tiles) tile_of(c_tile, c_b, c_m0, c_n0);
+          continue;
+        }
 #pragma unroll
         for (int i = 0; i < Cfg::FM; ++i) {
           const int64_t m = c_m0 + wm0 + i * 8 + gq;
