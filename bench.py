@@ -622,6 +622,14 @@ def run_bt200(args, rank, world):
     del x
     ws_cache.clear()
     torch.cuda.empty_cache()
+    # ---- N > 1: the C3 ST-HOSVD (+5 HOOI) sharded along the time mode over
+    # all ranks (parallel.tucker_c3_distributed: NCCL allreduce of the mode-1
+    # Grams, allgather of the projected mode-2 slabs), max over ranks
+    if world > 1 and not args.no_extras:
+        try:
+            result["extras_distributed"] = c3_distributed(torch, world, rank)
+        except Exception as exc:  # pragma: no cover
+            result["extras_distributed"] = {"c3_error": repr(exc)[:300]}
     # ---- GPU secondary configs first: the host-side numpy work of the CPU
     # baselines below leaves OpenBLAS threads spinning, which would steal
     # the host cores the latency-bound configs (C1) launch from
@@ -658,6 +666,35 @@ def run_bt200(args, rank, world):
             if isinstance(cpu.get(k), float) and isinstance(ex.get(k), float) and ex[k] > 0}
     if rank == 0:
         print(json.dumps(result), flush=True)
+
+
+def c3_distributed(torch, world, rank):
+    """ST-HOSVD and ST-HOSVD + 5 HOOI of C3 on this rank's lag slab; CUDA
+    events bracketed by barriers, max over ranks."""
+    from paper_2105_01170_b200 import configs
+    from paper_2105_01170_b200.parallel import shard_bounds, tucker_c3_distributed
+
+    _, t = configs.c3_build()
+    p0, p1 = shard_bounds(int(t.shape[1]), world, rank)
+    x_local = t[:, p0:p1, :].contiguous()
+    del t
+    torch.cuda.empty_cache()
+    out = {"workload": f"C3 (1024, 512, 1024) sharded along the 512 lags over {world} GPUs"}
+    for key, sweeps in (("c3_st_hosvd_ms", 0), ("c3_st_hosvd_plus_5_hooi_ms", 5)):
+        tucker_c3_distributed(x_local, 64, 32, hooi_sweeps=sweeps, p_offset=p0)   # warm-up
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        tucker_c3_distributed(x_local, 64, 32, hooi_sweeps=sweeps, p_offset=p0)
+        e1.record()
+        torch.cuda.synchronize()
+        tt = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        out[key] = float(tt.item())
+    del x_local
+    torch.cuda.empty_cache()
+    return out
 
 
 def e2e_run(args, torch, x_dev, init, world, rank, k0, k1):
