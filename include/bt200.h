@@ -292,6 +292,10 @@ int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need, double tau
 /* Diagnostic: 13 clock64 values: stamps (9) of sweep 1's phases in the fused one-CTA
  * small CP-ALS kernel of bt_cp_als_f64, then 4 pinv timings (tools/prof_c1_small.py). */
 int bt_cp_small_clocks(long long* out);
+/* detect_pattern representatives: out[k] (m x n, contiguous) = the block at
+ * cell cells[k] (= i*q + j, device int64) of a (row stride lda). */
+int bt_copy_cells_f64(const double* a, int64_t lda, const int64_t* cells, int64_t p, int64_t q,
+                      int64_t m, int64_t n, double* out, void* stream);
 /* out[0] = trace(m), m n x n row-major (device double out) */
 int bt_trace_f64(const double* m, int64_t n, double* out, void* stream);
 /* SVQB column scaling: dinv = diag(m)^-1/2 (0 for a zero diagonal), out = D (m + m^T)/2 D */

@@ -121,6 +121,7 @@ _SIGS = {
     "bt_inv_sqrt_f64": (C.c_int, [_dp, _i64, _dp, _dp]),
     "bt_sym_scale_f64": (C.c_int, [_dp, _i64, _dp, _dp, _dp]),
     "bt_trace_f64": (C.c_int, [_dp, _i64, _dp, _dp]),
+    "bt_copy_cells_f64": (C.c_int, [_dp, _i64, _dp, _i64, _i64, _i64, _i64, _dp, _dp]),
     "bt_cp_small_clocks": (C.c_int, [_dp]),
     "bt_leading_subspace_ws_bytes": (_i64, [_i64, _i64, _i64]),
     "bt_leading_subspace_f64": (C.c_int, [_dp, _i64, _i64, C.c_double, _dp, _i64, _i64, _dp, _dp,

@@ -422,8 +422,14 @@ def detect_pattern(a, m: int, n: int, tol: float = 0.0):
     pattern = BlockPattern(ell=ell, q=q, m=m, n=n, placements=placements,
                            structure_class=classify_placements(placements, ell, q))
     if _dev.is_device(a):
-        reps = tuple(ad[i * m:(i + 1) * m, j * n:(j + 1) * n].contiguous()
-                     for i, j in (c[0] for c in placements))
+        # every class's first occurrence, copied by one kernel into a (p, m, n)
+        # stack whose slices are the contiguous representatives
+        first = np.array([int(c[0][0]) * q + int(c[0][1]) for c in placements], dtype=np.int64)
+        cd = _dev.to_device(first, dtype=t.int64)
+        stack = _dev.empty((len(placements), m, n))
+        N.call("bt_copy_cells_f64", _dev.ptr(ad), cols, _dev.ptr(cd), len(placements), q, m, n,
+               _dev.ptr(stack), _dev.stream())
+        reps = tuple(stack[k] for k in range(len(placements)))
     else:
         reps = tuple(np.ascontiguousarray(a[i * m:(i + 1) * m, j * n:(j + 1) * n])
                      for i, j in (c[0] for c in placements))

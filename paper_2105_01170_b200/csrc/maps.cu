@@ -566,3 +566,45 @@ extern "C" int bt_scatter_blocks_f64(const double* t, int64_t t_sm, int64_t t_sp
   BT_LAUNCH_CHECK();
   return BT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Representative blocks of detect_pattern (blocks.py:298-306 returns each
+// class's first occurrence as a contiguous array): out[k] (m x n) = the
+// block at cell cells[k] = i*q + j of a.  One launch for all classes, one
+// CTA row per block row, 16-byte copies when the rows allow it.
+// ---------------------------------------------------------------------------
+
+__global__ void copy_cells_kernel(const double* __restrict__ a, int64_t lda,
+                                  const int64_t* __restrict__ cells, int64_t p, int64_t q,
+                                  int64_t m, int64_t n, double* __restrict__ out, int vec2) {
+  const int64_t rows = p * m;
+  for (int64_t rr = blockIdx.x; rr < rows; rr += gridDim.x) {
+    const int64_t k = rr / m, r = rr - k * m;
+    const int64_t c = cells[k];
+    const int64_t i = c / q, j = c - i * q;
+    const double* src = a + (i * m + r) * lda + j * n;
+    double* dst = out + (k * m + r) * n;
+    if (vec2) {
+      const double2* s2 = reinterpret_cast<const double2*>(src);
+      double2* d2 = reinterpret_cast<double2*>(dst);
+      for (int64_t x = threadIdx.x; x < n / 2; x += blockDim.x) d2[x] = s2[x];
+    } else {
+      for (int64_t x = threadIdx.x; x < n; x += blockDim.x) dst[x] = src[x];
+    }
+  }
+}
+
+extern "C" int bt_copy_cells_f64(const double* a, int64_t lda, const int64_t* cells, int64_t p,
+                                 int64_t q, int64_t m, int64_t n, double* out, void* stream) {
+  BT_REQUIRE(p >= 0 && m >= 0 && n >= 0 && q >= 1, BT_E_SHAPE, "copy_cells: bad extents");
+  if (p == 0 || m == 0 || n == 0) return BT_OK;
+  const int vec2 = (n % 2 == 0) && (lda % 2 == 0) &&
+                   (reinterpret_cast<uintptr_t>(a) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  const int threads = n >= 512 ? 256 : 128;
+  const int64_t rows = p * m;
+  copy_cells_kernel<<<static_cast<unsigned>(rows < 65535 ? rows : 65535), threads, 0,
+                      bt_stream(stream)>>>(a, lda, cells, p, q, m, n, out, vec2);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
