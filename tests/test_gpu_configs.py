@@ -88,6 +88,41 @@ def test_c3_reduced_st_hosvd_spsd_vs_oracle():
     assert rel(pr(sp.basis.cpu().numpy(), sp.blocks.cpu().numpy()), pr(u_o, proj_o)) < 1e-10
 
 
+def test_c3_full_size_properties():
+    """C3 at full size (1024 x 512 x 1024, 4.3 GB) through size-independent
+    properties: orthonormal factors; HOOI keeps or raises the captured energy
+    ||core||; the projection identity ||t - t_hat||^2 = ||t||^2 - ||core||^2
+    of an orthonormal Tucker model; the SPSD compression (psd.py:164-187)
+    gives symmetric positive semidefinite reduced blocks U^T C_k U."""
+    from paper_2105_01170_b200.tensor import fro_norm_dev, ttm_dev
+
+    pat, t = configs.c3_build()
+    st = decomp.st_hosvd(t, [64, 32, 64], shared=(1, 3))
+    h = decomp.hooi(t, st, 5, shared=(1, 3))
+    x2 = fro_norm_dev(t) ** 2
+    for rep in (st, h):
+        u, v = rep.factors[0], rep.factors[1]
+        assert rep.factors[2] is u
+        assert (u.T @ u - torch.eye(64, dtype=u.dtype, device=u.device)).abs().max() < 1e-12
+        assert (v.T @ v - torch.eye(32, dtype=v.dtype, device=v.device)).abs().max() < 1e-12
+    c_st, c_h = fro_norm_dev(st.core) ** 2, fro_norm_dev(h.core) ** 2
+    assert c_h >= c_st * (1.0 - 1e-12)
+    u, v = h.factors[0], h.factors[1]
+    that = ttm_dev(ttm_dev(ttm_dev(h.core, 1, u, 1024), 2, v, 512), 3, u, 1024)
+    err2 = fro_norm_dev(t - that) ** 2
+    assert abs(err2 - (x2 - c_h)) <= 1e-9 * x2
+    del that
+    eta = torch.tensor(pat.counts, dtype=torch.float64, device="cuda")
+    blocks = (t.permute(1, 0, 2) / eta.sqrt()[:, None, None]).contiguous()
+    sp = psd.spsd_compress_blocks(pat, blocks, 64)
+    b = sp.basis
+    assert (b.T @ b - torch.eye(64, dtype=b.dtype, device=b.device)).abs().max() < 1e-12
+    sb = sp.blocks
+    assert (sb - sb.transpose(1, 2)).abs().max() <= 1e-12 * sb.abs().max()
+    w = torch.linalg.eigvalsh(0.5 * (sb + sb.transpose(1, 2)))
+    assert w.min() >= -1e-12 * w.max()
+
+
 def test_c4_reduced_cp_and_ml_matvec():
     k, grid, r = 31, 16, 4
     psf = oc.c4_psf(k)
