@@ -58,6 +58,7 @@ __global__ void bt_gemm_reduce_kernel(BtGemmArgs g, int64_t bm, int64_t bn) {
     int64_t src = idx;
     if (g.symmetric && (m / bm < n / bn || (m / bm == n / bn && m < n))) src = n * g.N + m;
     double s = 0.0;
+#pragma unroll 8
     for (int k = 0; k < g.splits; ++k) s += wsb[k * total + src];
     double* c = Cb + m * g.sCm + n * g.sCn;
     const double v = g.alpha * s;
@@ -80,7 +81,10 @@ static int bt_pick_splits(int64_t tiles, int64_t batch, int64_t KT) {
   if (have >= slots || KT < 8) return 1;
   int best = 1;
   double best_eff = static_cast<double>(have) / static_cast<double>(slots);
-  const int64_t smax = std::min<int64_t>(64, KT / 4);
+  // up to one split per slot: a rank's C5 mode-3 GEMM at 8 GPUs is a single
+  // 128x64 output tile over a 16.8M-long reduction (a cap of 64 splits ran
+  // it on 64 of the 296 slots: 8.4 TF/s)
+  const int64_t smax = std::min<int64_t>(slots, KT / 4);
   for (int64_t s = 2; s <= smax; ++s) {
     const int64_t n = have * s;
     const int64_t waves = (n + slots - 1) / slots;
