@@ -27,6 +27,7 @@ from .tensor import fold, fro_norm, mode_multiply, squeeze, twist, unfold
 from .container import container_kind, container_read, container_write
 from .apps import (EraResult, LtiSystem, MarkovSequence, era_identify_compressed,
                    hankel_pattern_from_markov, markov_from_lti)
-from . import apps, container, decomp, multilevel, parallel, psd, reconstruct  # noqa: F401
+from .dropin import install, installed, uninstall
+from . import apps, container, decomp, dropin, multilevel, parallel, psd, reconstruct  # noqa: F401
 
 __version__ = "0.1.0"
