@@ -157,6 +157,12 @@ typedef struct bt_cp_problem {
  * when tol > 0 (convergence test); with tol <= 0 the sweeps run without host
  * synchronisation. */
 int64_t bt_cp_als_ws_bytes(const bt_cp_problem* pb);
+/* Dimension-tree root the CP phases use for this problem: 0 = P = X x3 C
+ * (modes 1/2 from P, mode 3 a full GEMM), 1 = Q = X x1 A (mode 1 a full
+ * GEMM, modes 2/3 from Q; short mode-3 slabs, e.g. a rank's slab at 4-8
+ * GPUs).  Same MTTKRPs as decomp.py:384-388 either way; only the summation
+ * order differs. */
+int bt_cp_tree_variant(const bt_cp_problem* pb);
 int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, double* c, double* lam,
                   int max_iters, double tol, int fit_mode, double* fit_history, int* n_iters,
                   int* converged, double* phase_ms, void* ws, int64_t ws_bytes, void* stream);

@@ -62,6 +62,7 @@ _SIGS = {
     "bt_build_cp_model_f64": (C.c_int, [_dp, _dp, _dp, _i64, _i64, _i64, _i64, _i64, _i64,
                                         C.c_double, C.c_uint64, _dp, _dp, _i64, _dp]),
     "bt_cp_als_ws_bytes": (_i64, [_P(CpProblem)]),
+    "bt_cp_tree_variant": (C.c_int, [_P(CpProblem)]),
     "bt_cp_als_f64": (C.c_int, [_P(CpProblem), _dp, _dp, _dp, _dp, C.c_int, C.c_double, C.c_int,
                                 _P(C.c_double), _P(C.c_int), _P(C.c_int), _P(C.c_double), _dp,
                                 _i64, _dp]),

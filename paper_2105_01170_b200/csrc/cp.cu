@@ -283,6 +283,44 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Q-tree mode 2: m2[j][r] = sum_k Q[j][k][r] C[k][r], one CTA per j; G
+// k-groups of R threads sum k = g, g + G, ... in order, then the groups are
+// added in a fixed order (bit-reproducible)
+__global__ void __launch_bounds__(256)
+    mode2_from_q_kernel(const double* __restrict__ Q, const double* __restrict__ C, int64_t K,
+                        int R, double* __restrict__ m2) {
+  __shared__ double part[256];
+  const int64_t j = blockIdx.x;
+  const double* q = Q + j * K * R;
+  const int groups = R <= 256 ? 256 / R : 1;
+  for (int r0 = 0; r0 < R; r0 += 256) {
+    const int g = R <= 256 ? threadIdx.x / R : 0;
+    const int r = R <= 256 ? threadIdx.x % R : r0 + threadIdx.x;
+    const bool act = (R <= 256) ? (g < groups) : (r < R);
+    double acc0 = 0.0, acc1 = 0.0;
+    if (act) {
+      int64_t k = g;
+      for (; k + groups < K; k += 2 * groups) {
+        acc0 = fma(ld_stream(q + k * R + r), __ldg(C + k * R + r), acc0);
+        acc1 = fma(ld_stream(q + (k + groups) * R + r), __ldg(C + (k + groups) * R + r), acc1);
+      }
+      if (k < K) acc0 = fma(ld_stream(q + k * R + r), __ldg(C + k * R + r), acc0);
+    }
+    part[threadIdx.x] = acc0 + acc1;
+    __syncthreads();
+    if (R <= 256) {
+      if (threadIdx.x < R) {
+        double v = 0.0;
+        for (int gg = 0; gg < groups; ++gg) v += part[gg * R + threadIdx.x];
+        m2[j * R + threadIdx.x] = v;
+      }
+      break;
+    }
+    if (r < R) m2[j * R + r] = part[threadIdx.x];
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // on-chip symmetric Jacobi: pinv of an R x R symmetric matrix
 // ---------------------------------------------------------------------------
@@ -1271,6 +1309,13 @@ struct Plan {
   int64_t off_p, off_m1, off_m2, off_m3, off_m3ws, off_gp, off_ip, off_f, off_state, off_res,
       off_w, off_m1d, off_m2d, off_gbuf, off_init, off_res1, total;
   int64_t m3_ws_elems;
+  // dimension-tree root.  0: P = X x3 C (I x J x R; modes 1 and 2 from P,
+  // mode 3 a full GEMM).  1: Q = X x1 A_new (J x K x R; mode 1 from the tree
+  // kernel's fused epilogue with no P store, modes 2 and 3 from Q) -- chosen
+  // for short mode-3 slabs (a rank's slab at 4-8 GPUs), where P would still
+  // be I*J*R (8.6 GB at C5 written and re-read every sweep) while Q is J*K*R
+  int qtree;
+  int64_t s3, chunk3;  // j-chunks of the mode-3 reduction from Q
 };
 
 BtGemmArgs mode3_args(const Plan& pl, const double* X, const double* A, const double* B,
@@ -1292,6 +1337,31 @@ BtGemmArgs mode3_args(const Plan& pl, const double* X, const double* A, const do
   return g;
 }
 
+// Q[(j,k)][r] = sum_i X[i][j][k] A[i][r]  (rows (j,k) M-contiguous in X)
+BtGemmArgs qtree_args(const Plan& pl, const double* X, const double* A, double* Q) {
+  BtGemmArgs g{};
+  g.M = pl.J * pl.K;
+  g.N = pl.R;
+  g.Kin = pl.I;
+  g.Kout = 1;
+  g.A = BtOperand{X, 1, 0, pl.J * pl.K, 0};
+  g.B = BtOperand{A, 1, 0, pl.R, 0};
+  g.C = Q;
+  g.sCm = pl.R;
+  g.sCn = 1;
+  g.alpha = 1.0;
+  g.beta = 0.0;
+  return g;
+}
+
+int cp_tree_variant(int64_t I, int64_t J, int64_t K, int64_t R) {
+  static const char* e = getenv("BT_CP_TREE");  // A/B switch (tools/scale_proxy.py)
+  if (e && e[0] == 'p') return 0;
+  if (e && e[0] == 'q') return 1;
+  (void)J;
+  return (R > 16 && K <= 256 && 4 * K <= I) ? 1 : 0;
+}
+
 Plan make_plan(const bt_cp_problem* pb) {
   Plan pl;
   pl.I = pb->I;
@@ -1309,8 +1379,17 @@ Plan make_plan(const bt_cp_problem* pb) {
   const int64_t maxrows = std::max(pl.I, std::max(pl.J, pl.K));
   pl.solve_parts_max = bt_cdiv(maxrows, SOLVE_ROWS);
   pl.res_grid = 8 * bt_num_sms();
+  pl.qtree = cp_tree_variant(pl.I, pl.J, pl.K, pl.R);
+  {
+    const int64_t KR = pl.K * pl.R;
+    const int64_t blocks_kr = std::max<int64_t>(1, std::min<int64_t>(bt_cdiv(KR, 256), 2048));
+    pl.s3 = std::max<int64_t>(1, std::min<int64_t>(pl.J, bt_cdiv(4 * bt_num_sms(), blocks_kr)));
+    pl.chunk3 = bt_cdiv(pl.J, pl.s3);
+    pl.s3 = bt_cdiv(pl.J, pl.chunk3);
+  }
   BtGemmArgs g3 = mode3_args(pl, nullptr, nullptr, nullptr, nullptr);
   pl.m3_ws_elems = bt_gemm_ws_elems(g3, 1);
+  if (pl.qtree) pl.m3_ws_elems = bt_gemm_ws_elems(qtree_args(pl, nullptr, nullptr, nullptr), 1);
   const int64_t RR = pl.R * pl.R;
   int64_t o = 0;
   auto take = [&](int64_t n) {
@@ -1318,9 +1397,9 @@ Plan make_plan(const bt_cp_problem* pb) {
     o += (n + 1) / 2 * 2;  // keep 16-byte alignment
     return at;
   };
-  pl.off_p = take(pl.I * pl.J * pl.R);
+  pl.off_p = take(pl.qtree ? pl.J * pl.K * pl.R : pl.I * pl.J * pl.R);   // P or Q
   pl.off_m1 = take(pl.I * pl.jtiles * pl.R);
-  pl.off_m2 = take(pl.s2 * JR);
+  pl.off_m2 = take(pl.qtree ? pl.s3 * pl.K * pl.R : pl.s2 * JR);
   pl.off_m3 = take(pl.K * pl.R);
   pl.off_m3ws = take(pl.m3_ws_elems);
   pl.off_gp = take(std::max<int64_t>(pl.solve_parts_max, 64) * RR);  // also Gram split-K partials
@@ -1621,6 +1700,10 @@ struct bt_cp_state {
 
 static int64_t cp_total_ws(const Plan& pl) { return pl.total + 16; }
 
+extern "C" int bt_cp_tree_variant(const bt_cp_problem* pb) {
+  return pb ? cp_tree_variant(pb->I, pb->J, pb->K, pb->R) : -1;
+}
+
 extern "C" int64_t bt_cp_als_ws_bytes(const bt_cp_problem* pb) {
   Plan pl = make_plan(pb);
   return cp_total_ws(pl) * 8;
@@ -1721,6 +1804,39 @@ extern "C" int bt_cp_mttkrp(void* state, int mode, double* out) {
   const Plan& pl = S->pl;
   double* ws = S->ws;
   cudaStream_t st = S->st;
+  if (pl.qtree && pl.K > 0) {
+    if (mode == 1) {
+      // the tree kernel without its P store: M1 partials per (i, j-tile) from
+      // the fused epilogue (23 TF/s at K = 128 vs 20 for the engine GEMM with
+      // the Khatri-Rao B-scale)
+      BT_TRY(run_tree(pl, S->X, S->F[2], S->F[1], nullptr, ws + pl.off_m1, 0, st));
+      reduce_m1_kernel<<<grid_n(pl.I * pl.R), 256, 0, st>>>(ws + pl.off_m1, pl.I, pl.jtiles, pl.R,
+                                                            out);
+      BT_LAUNCH_CHECK();
+      return BT_OK;
+    }
+    if (mode == 2) {
+      BtGemmArgs g = qtree_args(pl, S->X, S->F[0], ws + pl.off_p);
+      g.ws = ws + pl.off_m3ws;
+      BT_TRY(bt_gemm_run(g, 1, st, 0, pl.m3_ws_elems));
+      mode2_from_q_kernel<<<static_cast<unsigned>(pl.J), 256, 0, st>>>(ws + pl.off_p, S->F[2], pl.K,
+                                                                       static_cast<int>(pl.R), out);
+      BT_LAUNCH_CHECK();
+      return BT_OK;
+    }
+    if (mode == 3) {
+      // m3[k][r] = sum_j Q[j][k][r] B[j][r]: j-chunk partials, fixed-order sum
+      const int64_t KR = pl.K * pl.R;
+      const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(bt_cdiv(KR, 256), 2048));
+      mode2_from_p_kernel<<<dim3(static_cast<unsigned>(bx), static_cast<unsigned>(pl.s3)), 256, 0,
+                            st>>>(ws + pl.off_p, S->F[1], pl.J, KR, pl.R, pl.chunk3,
+                                  ws + pl.off_m2);
+      BT_LAUNCH_CHECK();
+      reduce_parts_kernel<<<grid_n(KR), 256, 0, st>>>(ws + pl.off_m2, pl.s3, KR, KR, out);
+      BT_LAUNCH_CHECK();
+      return BT_OK;
+    }
+  }
   if (mode == 1) {
     if (pl.K > 0) {
       BT_TRY(run_tree(pl, S->X, S->F[2], S->F[1], ws + pl.off_p, ws + pl.off_m1, 1, st));

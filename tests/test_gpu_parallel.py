@@ -140,3 +140,62 @@ def test_matvec_rhs_sharded_concat_equals_full(world):
     parts = [matvec_sharded(rep, x, world, k) for k in range(world)]
     got = np.concatenate(parts, axis=1)
     assert np.linalg.norm(got - full) <= 1e-14 * np.linalg.norm(full)
+
+
+def _variant(x, r):
+    import ctypes as C
+
+    from paper_2105_01170_b200 import _dev
+    from paper_2105_01170_b200 import _native as N
+
+    I, J, K = (int(s) for s in x.shape)
+    pb = N.CpProblem(_dev.ptr(x), I, J, K, r, 0.0)
+    return N.load().bt_cp_tree_variant(C.byref(pb))
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_sharded_native_cp_qtree(world):
+    """Short mode-3 slabs (a rank's slab at 4-8 GPUs) take the Q = X x1 A
+    dimension tree (mode 1 a direct GEMM, modes 2/3 from Q): same fits as the
+    oracle, sharded and not."""
+    I, J, K, r, iters = 160, 48, 40, 20, 6
+    x = configs.c5_build(I, J, K, r)
+    init = oc.normal_init((I, J, K), r, 1003)
+    ops = []
+    for rank in range(world):
+        k0, k1 = shard_bounds(K, world, rank)
+        xs = x[:, :, k0:k1].contiguous()
+        assert _variant(xs, r) == 1
+        f = [torch.from_numpy(init[0]).cuda(), torch.from_numpy(init[1]).cuda(),
+             torch.from_numpy(init[2][k0:k1].copy()).cuda()]
+        ops.append(NativeCpOps(xs, r, f[0], f[1], f[2], iters, fit="explicit"))
+    hists = lockstep(ops, iters)
+    ref = port.cp_als(x.cpu().numpy(), r, iters, 0.0, init=port.cp_init_normal(1003))
+    for h in hists:
+        np.testing.assert_allclose(h, ref.fit_history, rtol=0, atol=1e-11)
+    zc = torch.cat([o.f[2] for o in ops]).cpu().numpy()
+    np.testing.assert_allclose(zc, ref.z, rtol=0, atol=1e-9)
+    np.testing.assert_allclose(ops[0].f[1].cpu().numpy(), ref.y, rtol=0, atol=1e-9)
+    for o in ops:
+        o.close()
+
+
+def test_cp_als_qtree_public_api_and_variant_rule():
+    import paper_2105_01170_b200 as bt
+    from paper_2105_01170_b200 import decomp
+
+    I, J, K, r, iters = 200, 64, 48, 24, 10
+    x = configs.c5_build(I, J, K, r)
+    assert _variant(x, r) == 1
+    assert _variant(configs.c5_build(64, 64, 64, 4), 4) == 0        # R <= 16: P tree
+    assert _variant(configs.c5_build(64, 64, 64, 32), 32) == 0      # K > I / 4: P tree
+    init = oc.normal_init((I, J, K), r, 7)
+    saved = decomp._cp_init
+    decomp._cp_init = lambda _t, _r: [v.copy() for v in init]
+    try:
+        res = bt.cp_als(x.cpu().numpy(), r, iters, 0.0, fit="explicit")
+    finally:
+        decomp._cp_init = saved
+    ref = port.cp_als(x.cpu().numpy(), r, iters, 0.0, init=lambda _t, _r: [v.copy() for v in init])
+    np.testing.assert_allclose(res.fit_history, ref.fit_history, rtol=0, atol=1e-11)
+    np.testing.assert_allclose(res.rep.z, ref.z, rtol=0, atol=1e-9)
