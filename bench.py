@@ -567,11 +567,17 @@ def run_bt200(args, rank, world):
         torch.distributed.barrier()
     ref_flops = ITERS * 6.0 * I_ * J_ * K_ * R_
     value = ref_flops / (ms / 1e3) / 1e9     # whole job: the global tensor, max-over-ranks time
-    tree_ms = phase_tot[0] / (args.steps * ITERS)
-    mode3_ms = phase_tot[2] / (args.steps * ITERS)
     kloc = k1 - k0
+    import ctypes as C
+
+    variant = int(lib.bt_cp_tree_variant(C.byref(N.CpProblem(_dev.ptr(x), I_, J_, kloc, R_, 0.0))))
+    per = args.steps * ITERS
+    tree_ms = phase_tot[0] / per
+    # the second full pass over X: the Q GEMM (+ mode-2 reduction, phase 1) on
+    # the Q tree, the mode-3 GEMM (phase 2) on the P tree
+    gemm2_ms = (phase_tot[1] if variant == 1 else phase_tot[2]) / per
     if tree_ms == 0.0:
-        # sharded run: time this rank's P / mode-1 and mode-3 kernels separately (CUDA events)
+        # sharded run: time this rank's mode-1 tree kernel and second GEMM separately (CUDA events)
         for k in range(3):
             f[k].copy_(init_dev[k])
         ops = NativeCpOps(x, R_, f[0], f[1], f[2], ITERS)
@@ -579,22 +585,36 @@ def run_bt200(args, rank, world):
         allreduce(buf)
         ops.init_finish(buf)
         tree_ms = timed(torch, lambda: ops.mttkrp(1), 3, 1)
-        mode3_ms = timed(torch, lambda: ops.mttkrp(3), 3, 1)
+        gemm2_ms = timed(torch, lambda: ops.mttkrp(2 if variant == 1 else 3), 3, 1)
         ops.close()
     achieved = 2.0 * I_ * J_ * kloc * R_ / (tree_ms / 1e3) / 1e12
     peak = peaks["dmma"]
     fit = hist_holder["h"][-1]
-    log(f"[bench] C5 step {ms:.1f} ms, tree {tree_ms:.2f} ms, mode2 {phase_tot[1] / (args.steps * ITERS):.2f} ms,"
-        f" mode3 {mode3_ms:.2f} ms, solves+fit {phase_tot[3] / (args.steps * ITERS):.2f} ms, fit {fit}")
+    log(f"[bench] C5 step {ms:.1f} ms, tree variant {'Q' if variant else 'P'}, phases/sweep "
+        f"{[round(v / per, 2) for v in phase_tot]} ms, fit {fit}")
     traffic = None
+    ncu_file = "r01_ncu_c5q.json" if variant == 1 else "r01_ncu_c5.json"
     try:
         prof = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
-                                           "profiles", "r01_ncu_c5.json")))
+                                           "profiles", ncu_file)))
         if prof["config"] == {"I": I_, "J": J_, "K": kloc, "R": R_}:
             tk = prof["tree_p_kernel"]
             traffic = tk["dram_bytes_read"] + tk["dram_bytes_write"]
     except (OSError, KeyError, ValueError):
         pass
+    if variant == 1:
+        phases = {"mode1_tree_no_p_store": tree_ms, "q_gemm_plus_mode2": phase_tot[1] / per,
+                  "mode3_from_q": phase_tot[2] / per, "solves_fit": phase_tot[3] / per}
+        kname = ("tree_p_ws_kernel (X x3 C tiles, mode-1 reduction fused, no P store; "
+                 "DMMA) -- Q dimension tree")
+        alg_bytes = 8.0 * I_ * J_ * kloc
+        alg_note = "algorithmic X = "
+    else:
+        phases = {"p_tree": tree_ms, "mode2": phase_tot[1] / per, "mode3": phase_tot[2] / per,
+                  "solves_fit": phase_tot[3] / per}
+        kname = "tree_p_kernel (P = X x3 C, DMMA) -- P dimension tree"
+        alg_bytes = 8.0 * I_ * J_ * (kloc + R_)
+        alg_note = "algorithmic X + P = "
     result = {
         "metric": "CP-ALS MTTKRP GFLOP/s (reference-equivalent 6*I*J*K*R per sweep)",
         "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -609,19 +629,18 @@ def run_bt200(args, rank, world):
                    "l2": "inputs (137 GB) >> L2; no flush needed",
                    "per_sweep_ms": ms / ITERS, "final_fit": fit,
                    "executed_mttkrp_flops_per_sweep": 4.0 * I_ * J_ * K_ * R_,
-                   "phase_ms_per_sweep": {"p_tree": tree_ms,
-                                          "mode2": phase_tot[1] / (args.steps * ITERS),
-                                          "mode3": mode3_ms,
-                                          "solves_fit": phase_tot[3] / (args.steps * ITERS)}},
-        "roofline": {"bound": "tensor", "kernel": "tree_p_kernel (P = X x3 C, DMMA)",
+                   "dimension_tree": "Q = X x1 A" if variant == 1 else "P = X x3 C",
+                   "phase_ms_per_sweep": phases},
+        "roofline": {"bound": "tensor", "kernel": kname,
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "traffic_note": ("bytes per launch, ncu dram__bytes_read+write "
-                                      "(profiles/r01_ncu_c5.json); algorithmic X + P = "
-                                      f"{8.0 * I_ * J_ * (kloc + R_):.4g} B"),
+                                      f"(profiles/{ncu_file}); {alg_note}{alg_bytes:.4g} B"),
                      "peak_source": "measured in this run: DMMA.8x8x4 chains on all SMs "
                                     "(MEASURED_PEAKS.json has no FP64 figure)",
-                     "mode3_gemm_achieved": 2.0 * I_ * J_ * kloc * R_ / (mode3_ms / 1e3) / 1e12},
+                     "second_gemm": ("Q GEMM (+ mode-2 reduction)" if variant == 1 else
+                                     "mode-3 GEMM"),
+                     "second_gemm_achieved": 2.0 * I_ * J_ * kloc * R_ / (gemm2_ms / 1e3) / 1e12},
         "clocks": clk.summary(),
         "gpu_launches": launches,
         "fp64_peaks_tflops": dict(peaks),

@@ -148,8 +148,9 @@ typedef struct bt_cp_problem {
  * the initialisation on entry; on exit a holds KruskalRep.x = F0 * lam
  * (decomp.py:403), b and c the normalised factors, lam (R) the mode-3
  * column norms (decomp.py:391-392).  phase_ms (host, 4 doubles, optional)
- * accumulates CUDA-event times of the phases [P/mode-1 tree kernel,
- * mode-2, mode-3 GEMM, solves + fit].  fit_history (host, max_iters) receives the fit
+ * accumulates CUDA-event times of the phases [mode 1 (tree kernel), mode 2
+ * (P tree: stream P; Q tree: the Q GEMM + reduction), mode 3 (P tree: GEMM;
+ * Q tree: stream Q), solves + fit] (bt_cp_tree_variant).  fit_history (host, max_iters) receives the fit
  * per sweep; *n_iters and *converged follow decomp.py:397-410.
  * fit_mode: 0 auto (Gram identity, explicit residual when the identity loses
  * precision), 1 always explicit (reference semantics decomp.py:395-396),
@@ -158,9 +159,9 @@ typedef struct bt_cp_problem {
  * synchronisation. */
 int64_t bt_cp_als_ws_bytes(const bt_cp_problem* pb);
 /* Dimension-tree root the CP phases use for this problem: 0 = P = X x3 C
- * (modes 1/2 from P, mode 3 a full GEMM), 1 = Q = X x1 A (mode 1 a full
- * GEMM, modes 2/3 from Q; short mode-3 slabs, e.g. a rank's slab at 4-8
- * GPUs).  Same MTTKRPs as decomp.py:384-388 either way; only the summation
+ * (modes 1/2 from P, mode 3 a full GEMM), 1 = Q = X x1 A (mode 1 from the
+ * tree kernel without a P store, Q by one GEMM, modes 2/3 from Q; chosen
+ * when R > 16 and K <= I).  Same MTTKRPs as decomp.py:384-388 either way; only the summation
  * order differs. */
 int bt_cp_tree_variant(const bt_cp_problem* pb);
 int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, double* c, double* lam,

@@ -1312,8 +1312,9 @@ struct Plan {
   // dimension-tree root.  0: P = X x3 C (I x J x R; modes 1 and 2 from P,
   // mode 3 a full GEMM).  1: Q = X x1 A_new (J x K x R; mode 1 from the tree
   // kernel's fused epilogue with no P store, modes 2 and 3 from Q) -- chosen
-  // for short mode-3 slabs (a rank's slab at 4-8 GPUs), where P would still
-  // be I*J*R (8.6 GB at C5 written and re-read every sweep) while Q is J*K*R
+  // whenever K <= I (C5, and a rank's mode-3 slab at any GPU count), where P
+  // would be I*J*R (8.6 GB at C5 written and re-read every sweep) while Q is
+  // J*K*R
   int qtree;
   int64_t s3, chunk3;  // j-chunks of the mode-3 reduction from Q
 };
@@ -1359,10 +1360,16 @@ int cp_tree_variant(int64_t I, int64_t J, int64_t K, int64_t R) {
   if (e && e[0] == 'p') return 0;
   if (e && e[0] == 'q') return 1;
   (void)J;
-  return (R > 16 && K <= 256 && 4 * K <= I) ? 1 : 0;
+  // Q (J*K*R) is no larger than P (I*J*R) and the Q GEMM (X rows
+  // M-contiguous, no operand scale) beats the mode-3 GEMM with its
+  // Khatri-Rao B-scale: C5 sweep 153.4 -> 149.8 ms at K = 1024, 24.1 -> 22.4
+  // ms at a rank's K = 128 slab.  R <= 16 keeps the narrow-tile P tree (C4).
+  return (R > 16 && K <= I) ? 1 : 0;
 }
 
-Plan make_plan(const bt_cp_problem* pb) {
+// variant < 0: the cp_tree_variant rule; the standalone bt_mttkrp_f64
+// (one mode, P layout) passes 0
+Plan make_plan(const bt_cp_problem* pb, int variant = -1) {
   Plan pl;
   pl.I = pb->I;
   pl.J = pb->J;
@@ -1379,7 +1386,7 @@ Plan make_plan(const bt_cp_problem* pb) {
   const int64_t maxrows = std::max(pl.I, std::max(pl.J, pl.K));
   pl.solve_parts_max = bt_cdiv(maxrows, SOLVE_ROWS);
   pl.res_grid = 8 * bt_num_sms();
-  pl.qtree = cp_tree_variant(pl.I, pl.J, pl.K, pl.R);
+  pl.qtree = variant < 0 ? cp_tree_variant(pl.I, pl.J, pl.K, pl.R) : variant;
   {
     const int64_t KR = pl.K * pl.R;
     const int64_t blocks_kr = std::max<int64_t>(1, std::min<int64_t>(bt_cdiv(KR, 256), 2048));
@@ -2172,7 +2179,7 @@ extern "C" int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, doub
 }
 
 extern "C" int64_t bt_mttkrp_ws_bytes(const bt_cp_problem* pb, int mode) {
-  Plan pl = make_plan(pb);
+  Plan pl = make_plan(pb, 0);
   (void)mode;
   return pl.total * 8;
 }
@@ -2182,7 +2189,7 @@ extern "C" int bt_mttkrp_f64(const bt_cp_problem* pb, int mode, const double* a,
                              void* stream) {
   BT_REQUIRE(mode >= 1 && mode <= 3, BT_E_SHAPE, "mttkrp: mode %d out of range", mode);
   cudaStream_t st = bt_stream(stream);
-  Plan pl = make_plan(pb);
+  Plan pl = make_plan(pb, 0);
   BT_REQUIRE(ws_bytes >= pl.total * 8, BT_E_VALUE, "mttkrp: workspace too small");
   double* ws = static_cast<double*>(wsv);
   double* P = ws + pl.off_p;

@@ -188,7 +188,7 @@ def test_cp_als_qtree_public_api_and_variant_rule():
     x = configs.c5_build(I, J, K, r)
     assert _variant(x, r) == 1
     assert _variant(configs.c5_build(64, 64, 64, 4), 4) == 0        # R <= 16: P tree
-    assert _variant(configs.c5_build(64, 64, 64, 32), 32) == 0      # K > I / 4: P tree
+    assert _variant(configs.c5_build(32, 64, 64, 32), 32) == 0      # K > I: P tree
     init = oc.normal_init((I, J, K), r, 7)
     saved = decomp._cp_init
     decomp._cp_init = lambda _t, _r: [v.copy() for v in init]
