@@ -606,7 +606,9 @@ def run_bt200(args, rank, world):
         phases = {"mode1_tree_no_p_store": tree_ms, "q_gemm_plus_mode2": gemm2_ms,
                   "mode3_from_q": phase_tot[2] / per, "solves_fit": phase_tot[3] / per}
         kname = ("tree_p_ws_kernel (X x3 C tiles, mode-1 reduction fused, no P store; "
-                 "DMMA) -- Q dimension tree")
+                 "DMMA) -- Q dimension tree") if kloc > 256 else (
+                 "bt_gemm_kernel (T = X[i]^T B batched over i, DMMA; mode 1 streamed from T) "
+                 "-- Q dimension tree, short mode-3 slab")
         alg_bytes = 8.0 * I_ * J_ * kloc
         alg_note = "algorithmic X = "
     else:

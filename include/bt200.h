@@ -160,8 +160,9 @@ typedef struct bt_cp_problem {
 int64_t bt_cp_als_ws_bytes(const bt_cp_problem* pb);
 /* Dimension-tree root the CP phases use for this problem: 0 = P = X x3 C
  * (modes 1/2 from P, mode 3 a full GEMM), 1 = Q = X x1 A (mode 1 from the
- * tree kernel without a P store, Q by one GEMM, modes 2/3 from Q; chosen
- * when R > 16 and K <= I).  Same MTTKRPs as decomp.py:384-388 either way; only the summation
+ * tree kernel without a P store -- or, for K <= 256, from T[i] = X[i]^T B
+ * batched over i --, Q by one GEMM, modes 2/3 from Q; chosen when R > 16
+ * and K <= I).  Same MTTKRPs as decomp.py:384-388 either way; only the summation
  * order differs. */
 int bt_cp_tree_variant(const bt_cp_problem* pb);
 int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, double* c, double* lam,

@@ -1317,6 +1317,11 @@ struct Plan {
   // J*K*R
   int qtree;
   int64_t s3, chunk3;  // j-chunks of the mode-3 reduction from Q
+  // Q tree with a short mode-3 slab (K <= 256, i.e. <= 16 k-tiles per tree
+  // tile): mode 1 as T[i] = X[i]^T B (batched over i, the reduction over J
+  // is long) then m1[i][r] = sum_k T[i][k][r] C[k][r]
+  int m1_via_t;
+  int64_t off_t;
 };
 
 BtGemmArgs mode3_args(const Plan& pl, const double* X, const double* A, const double* B,
@@ -1350,6 +1355,24 @@ BtGemmArgs qtree_args(const Plan& pl, const double* X, const double* A, double* 
   g.C = Q;
   g.sCm = pl.R;
   g.sCn = 1;
+  g.alpha = 1.0;
+  g.beta = 0.0;
+  return g;
+}
+
+// T[i][k][r] = sum_j X[i][j][k] B[j][r]: batch i, rows k M-contiguous
+BtGemmArgs tslab_args(const Plan& pl, const double* X, const double* B, double* T) {
+  BtGemmArgs g{};
+  g.M = pl.K;
+  g.N = pl.R;
+  g.Kin = pl.J;
+  g.Kout = 1;
+  g.A = BtOperand{X, 1, 0, pl.K, pl.J * pl.K};
+  g.B = BtOperand{B, 1, 0, pl.R, 0};
+  g.C = T;
+  g.sCm = pl.R;
+  g.sCn = 1;
+  g.sCb = pl.K * pl.R;
   g.alpha = 1.0;
   g.beta = 0.0;
   return g;
@@ -1397,6 +1420,7 @@ Plan make_plan(const bt_cp_problem* pb, int variant = -1) {
   BtGemmArgs g3 = mode3_args(pl, nullptr, nullptr, nullptr, nullptr);
   pl.m3_ws_elems = bt_gemm_ws_elems(g3, 1);
   if (pl.qtree) pl.m3_ws_elems = bt_gemm_ws_elems(qtree_args(pl, nullptr, nullptr, nullptr), 1);
+  pl.m1_via_t = pl.qtree && pl.K <= 256 && pl.I <= 65535;
   const int64_t RR = pl.R * pl.R;
   int64_t o = 0;
   auto take = [&](int64_t n) {
@@ -1406,6 +1430,7 @@ Plan make_plan(const bt_cp_problem* pb, int variant = -1) {
   };
   pl.off_p = take(pl.qtree ? pl.J * pl.K * pl.R : pl.I * pl.J * pl.R);   // P or Q
   pl.off_m1 = take(pl.I * pl.jtiles * pl.R);
+  pl.off_t = take(pl.m1_via_t ? pl.I * pl.K * pl.R : 0);
   pl.off_m2 = take(pl.qtree ? pl.s3 * pl.K * pl.R : pl.s2 * JR);
   pl.off_m3 = take(pl.K * pl.R);
   pl.off_m3ws = take(pl.m3_ws_elems);
@@ -1812,6 +1837,15 @@ extern "C" int bt_cp_mttkrp(void* state, int mode, double* out) {
   double* ws = S->ws;
   cudaStream_t st = S->st;
   if (pl.qtree && pl.K > 0) {
+    if (mode == 1 && pl.m1_via_t) {
+      BtGemmArgs g = tslab_args(pl, S->X, S->F[1], ws + pl.off_t);
+      g.ws = ws + pl.off_m3ws;
+      BT_TRY(bt_gemm_run(g, pl.I, st, 1, 0));
+      mode2_from_q_kernel<<<static_cast<unsigned>(pl.I), 256, 0, st>>>(ws + pl.off_t, S->F[2], pl.K,
+                                                                       static_cast<int>(pl.R), out);
+      BT_LAUNCH_CHECK();
+      return BT_OK;
+    }
     if (mode == 1) {
       // the tree kernel without its P store: M1 partials per (i, j-tile) from
       // the fused epilogue (23 TF/s at K = 128 vs 20 for the engine GEMM with

@@ -184,18 +184,21 @@ def test_cp_als_qtree_public_api_and_variant_rule():
     import paper_2105_01170_b200 as bt
     from paper_2105_01170_b200 import decomp
 
-    I, J, K, r, iters = 200, 64, 48, 24, 10
-    x = configs.c5_build(I, J, K, r)
-    assert _variant(x, r) == 1
     assert _variant(configs.c5_build(64, 64, 64, 4), 4) == 0        # R <= 16: P tree
     assert _variant(configs.c5_build(32, 64, 64, 32), 32) == 0      # K > I: P tree
-    init = oc.normal_init((I, J, K), r, 7)
-    saved = decomp._cp_init
-    decomp._cp_init = lambda _t, _r: [v.copy() for v in init]
-    try:
-        res = bt.cp_als(x.cpu().numpy(), r, iters, 0.0, fit="explicit")
-    finally:
-        decomp._cp_init = saved
-    ref = port.cp_als(x.cpu().numpy(), r, iters, 0.0, init=lambda _t, _r: [v.copy() for v in init])
-    np.testing.assert_allclose(res.fit_history, ref.fit_history, rtol=0, atol=1e-11)
-    np.testing.assert_allclose(res.rep.z, ref.z, rtol=0, atol=1e-9)
+    # K <= 256: mode 1 through the batched T = X[i]^T B GEMM; K > 256: the
+    # tree kernel without its P store
+    for I, J, K, r, iters in ((200, 64, 48, 24, 10), (300, 16, 272, 20, 6)):
+        x = configs.c5_build(I, J, K, r)
+        assert _variant(x, r) == 1
+        init = oc.normal_init((I, J, K), r, 7)
+        saved = decomp._cp_init
+        decomp._cp_init = lambda _t, _r: [v.copy() for v in init]
+        try:
+            res = bt.cp_als(x.cpu().numpy(), r, iters, 0.0, fit="explicit")
+        finally:
+            decomp._cp_init = saved
+        ref = port.cp_als(x.cpu().numpy(), r, iters, 0.0,
+                          init=lambda _t, _r: [v.copy() for v in init])
+        np.testing.assert_allclose(res.fit_history, ref.fit_history, rtol=0, atol=1e-11)
+        np.testing.assert_allclose(res.rep.z, ref.z, rtol=0, atol=1e-9)
