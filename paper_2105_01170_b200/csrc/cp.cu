@@ -1000,12 +1000,16 @@ __device__ __forceinline__ double warp_ordered_sum(const double* __restrict__ p,
 __global__ void __launch_bounds__(256)
     gram_reduce_kernel(const double* __restrict__ gram_part, int64_t nparts, int R,
                        const double* __restrict__ inner_part, double* __restrict__ gbuf) {
-  for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
+  // one thread per Gram entry across the grid (was one CTA for all R*R:
+  // 255 us per solve at R = 64, I = 4096); same per-entry summation order
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < R * R;
+       idx += gridDim.x * blockDim.x) {
     double s = 0.0;
+#pragma unroll 4
     for (int64_t p = 0; p < nparts; ++p) s += gram_part[p * R * R + idx];
     gbuf[idx] = s;
   }
-  if (threadIdx.x < 32) {
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
     const double inner = inner_part ? warp_ordered_sum(inner_part, nparts) : 0.0;
     if (threadIdx.x == 0) {
       gbuf[R * R] = inner;
@@ -1599,7 +1603,8 @@ int run_solve_rows(const Plan& pl, const CpState& s, double* ws, const double* m
         mpart, nparts, part_stride, row_stride, s.vp, rows, R, F, gp, with_inner ? ip : nullptr);
     BT_LAUNCH_CHECK();
   }
-  gram_reduce_kernel<<<1, 256, 0, st>>>(gp, parts, R, with_inner ? ip : nullptr, gbuf);
+  gram_reduce_kernel<<<static_cast<unsigned>(bt_cdiv(static_cast<int64_t>(R) * R, 256)), 256, 0,
+                       st>>>(gp, parts, R, with_inner ? ip : nullptr, gbuf);
   BT_LAUNCH_CHECK();
   return BT_OK;
 }
