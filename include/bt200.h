@@ -320,6 +320,9 @@ int bt_sign_fix_pair_f64(double* x, int64_t rows, int64_t cols, double* y, int64
 int bt_reverse_axes_f64(const double* x, const int64_t* dims, int ndim, double* out, void* stream);
 /* out[i] = Philox4x32-10 Box-Muller normal of index i under key. */
 int bt_fill_normal_f64(double* out, int64_t n, uint64_t key, void* stream);
+/* out (cols x rows) = x (rows x cols)^T, row-major, tiled through shared
+ * memory (the RHS layout flips of the batched matvecs). */
+int bt_transpose_f64(const double* x, int64_t rows, int64_t cols, double* out, void* stream);
 /* out[i][j] = left[i] x[i][j] right[j] (left / right may be NULL). */
 int bt_diag_scale_f64(const double* x, int64_t rows, int64_t cols, const double* left,
                       const double* right, double* out, void* stream);

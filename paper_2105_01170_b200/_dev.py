@@ -79,3 +79,13 @@ def to_host(x) -> np.ndarray:
 def like_input(ref, dev_tensor):
     """Return dev_tensor as a CUDA tensor if ref was on device, else numpy."""
     return dev_tensor if is_device(ref) else to_host(dev_tensor)
+
+
+def transpose(x):
+    """x (rows, cols) device tensor -> contiguous (cols, rows) copy, by the
+    library's tiled transpose kernel (layout plumbing of the matvec RHS)."""
+    x = x.contiguous()
+    rows, cols = int(x.shape[0]), int(x.shape[1])
+    out = empty((cols, rows), dtype=x.dtype)
+    _native.call("bt_transpose_f64", ptr(x), rows, cols, ptr(out), stream())
+    return out

@@ -514,6 +514,43 @@ extern "C" int bt_reverse_axes_f64(const double* x, const int64_t* dims, int ndi
   return BT_OK;
 }
 
+// out (cols x rows) = x (rows x cols)^T, both row-major: 32 x 32 tiles staged
+// in shared memory (padded against bank conflicts) so reads and writes are
+// both coalesced -- the right-hand-side layout flip of the batched matvecs
+// ((q*n, nrhs) user layout <-> one contiguous vector per RHS)
+__global__ void __launch_bounds__(256) bt_transpose_kernel(const double* __restrict__ x,
+                                                           int64_t rows, int64_t cols,
+                                                           double* __restrict__ out) {
+  __shared__ double tile[32][33];
+  const int64_t tiles_c = (cols + 31) / 32;
+  const int64_t ntiles = ((rows + 31) / 32) * tiles_c;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t r0 = (t / tiles_c) * 32, c0 = (t % tiles_c) * 32;
+    for (int k = threadIdx.y; k < 32; k += 8) {
+      const int64_t r = r0 + k, c = c0 + threadIdx.x;
+      if (r < rows && c < cols) tile[k][threadIdx.x] = x[r * cols + c];
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += 8) {
+      const int64_t c = c0 + k, r = r0 + threadIdx.x;
+      if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][k];
+    }
+    __syncthreads();
+  }
+}
+
+extern "C" int bt_transpose_f64(const double* x, int64_t rows, int64_t cols, double* out,
+                                void* stream) {
+  BT_REQUIRE(rows >= 0 && cols >= 0, BT_E_SHAPE, "transpose: negative extent");
+  if (rows == 0 || cols == 0) return BT_OK;
+  const int64_t ntiles = ((rows + 31) / 32) * ((cols + 31) / 32);
+  const int64_t blocks = ntiles < 8 * 148 * 4 ? ntiles : 8 * 148 * 4;
+  bt_transpose_kernel<<<static_cast<unsigned>(blocks), dim3(32, 8), 0, bt_stream(stream)>>>(
+      x, rows, cols, out);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
 // out[i][j] = left[i] * x[i][j] * right[j] (either scale may be null) -- the
 // diagonal similarity of the ERA shift solve (apps.py:216-218)
 __global__ void bt_diag_scale_kernel(const double* __restrict__ x, int64_t rows, int64_t cols,

@@ -232,7 +232,7 @@ def ml_matvec(terms, x, stacks=None):
     else:
         if x.shape[0] != ntot:
             raise ShapeError(f"right-hand sides of shape {tuple(x.shape)} != ({ntot}, nrhs)")
-        xd = _dev.to_device(x).T.contiguous()
+        xd = _dev.transpose(_dev.to_device(x))
         nrhs = int(x.shape[1])
     y = _dev.empty((nrhs, nout[0] * nout[1] * nout[2]))
     cin = (C.c_int64 * 3)(*nin)
@@ -240,5 +240,5 @@ def ml_matvec(terms, x, stacks=None):
     ws = _dev.workspace(N.load().bt_ml_matvec_ws_bytes(nterms, cin, cout, nrhs))
     N.call("bt_ml_matvec_f64", nterms, cin, cout, _dev.ptr(s1), _dev.ptr(s2), _dev.ptr(s3),
            _dev.ptr(xd), nrhs, _dev.ptr(y), _dev.ptr(ws), int(ws.numel()) * 8, _dev.stream())
-    out = y[0] if x.ndim == 1 else y.T.contiguous()
+    out = y[0] if x.ndim == 1 else _dev.transpose(y)
     return _dev.like_input(x, out)

@@ -261,7 +261,7 @@ def _rhs_block(x, qn):
     if x.ndim != 2 or x.shape[0] != qn:
         raise ShapeError(f"right-hand sides of shape {tuple(x.shape)} != ({qn}, nrhs)")
     xd = _dev.to_device(x)
-    return xd.T.contiguous(), int(x.shape[1])
+    return _dev.transpose(xd), int(x.shape[1])
 
 
 def flops_kron(pat: BlockPattern, r: int) -> int:
@@ -304,7 +304,7 @@ def matvec(rep, x, counter: FlopCounter | None = None):
             counter.add(nrhs * flops_blr(pat, rl, rr))
     else:
         raise TypeError(f"unsupported representation {type(rep).__name__}")
-    out = y[0] if x.ndim == 1 else y.T.contiguous()
+    out = y[0] if x.ndim == 1 else _dev.transpose(y)
     return _dev.like_input(x, out)
 
 

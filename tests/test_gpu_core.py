@@ -372,3 +372,15 @@ def test_leading_subspace_warm_start_and_shape_guard():
     # a block wider than n / 2 is not applicable (status 2 -> None)
     small = torch.from_numpy(g[:40, :40].copy()).cuda()
     assert L._leading_subspace(small, 30, 1e-6) is None
+
+
+@pytest.mark.parametrize("shape", [(37, 1000), (1, 5), (1025, 33), (4096, 32), (64, 64)])
+def test_transpose_kernel(shape):
+    """bt_transpose_f64 (the matvec RHS layout flip) is an exact transpose,
+    ragged tile edges included."""
+    from paper_2105_01170_b200 import _dev
+
+    x = torch.from_numpy(np.random.default_rng(shape[0]).standard_normal(shape)).cuda()
+    y = _dev.transpose(x)
+    assert tuple(y.shape) == shape[::-1]
+    assert torch.equal(y.cpu(), x.cpu().T)
