@@ -651,16 +651,6 @@ def run_bt200(args, rank, world):
         "gpu_launches": launches,
         "fp64_peaks_tflops": dict(peaks),
     }
-    # ---- e2e: public API with host buffers (H2D of X + init, D2H of factors)
-    ws_cache.clear()
-    torch.cuda.empty_cache()
-    if not args.no_e2e:
-        try:
-            result["e2e"] = e2e_run(args, torch, x, init, world, rank, k0, k1)
-        except Exception as exc:  # pragma: no cover
-            result["e2e"] = {"value": None, "unit": "GFLOP/s", "error": repr(exc)[:300]}
-        x = None
-    del x
     ws_cache.clear()
     torch.cuda.empty_cache()
     # ---- N > 1: the C3 ST-HOSVD (+5 HOOI) sharded along the time mode over
@@ -681,6 +671,21 @@ def run_bt200(args, rank, world):
             if isinstance(ex.get(key + "_tflops"), float):
                 ex[key + "_frac_dmma"] = ex[key + "_tflops"] / peak
         result["extras"] = ex
+    # ---- e2e: public API with host buffers (H2D of X + init, D2H of factors).
+    # After the GPU secondary configs: pinning and unpinning 137 GB of host
+    # memory left single-call latencies of the light configs (C1, C4) 10-30x
+    # slow on some boxes when they ran after it
+    ws_cache.clear()
+    torch.cuda.empty_cache()
+    if not args.no_e2e:
+        try:
+            result["e2e"] = e2e_run(args, torch, x, init, world, rank, k0, k1)
+        except Exception as exc:  # pragma: no cover
+            result["e2e"] = {"value": None, "unit": "GFLOP/s", "error": repr(exc)[:300]}
+        x = None
+    del x
+    ws_cache.clear()
+    torch.cuda.empty_cache()
     # ---- CPU baseline (bounded slab, rank 0, N=1)
     if not args.no_cpu and rank == 0 and world == 1:
         try:
