@@ -520,6 +520,10 @@ def run_bt200(args, rank, world):
     hist_holder = {}
     allreduce = torch_allreduce()
 
+    # the sharded run's phase state (workspace, handle) is built once, outside
+    # the timed steps; each step re-seeds the factors and re-runs init_local
+    ops = NativeCpOps(x, R_, f[0], f[1], f[2], ITERS) if world > 1 else None
+
     def step():
         for k in range(3):
             f[k].copy_(init_dev[k])
@@ -527,9 +531,7 @@ def run_bt200(args, rank, world):
             hist, n_it, conv = cp_als_device(x, R_, f, lam, ITERS, 0.0, "auto", 0.0, ws_holder(),
                                              phase_ms=phase)
         else:
-            ops = NativeCpOps(x, R_, f[0], f[1], f[2], ITERS)
             hist, n_it, conv = cp_als_sharded(ops, ITERS, 0.0, allreduce)
-            ops.close()
         hist_holder["h"] = hist
 
     ws_cache = {}
@@ -580,12 +582,12 @@ def run_bt200(args, rank, world):
         # sharded run: time this rank's mode-1 tree kernel and second GEMM separately (CUDA events)
         for k in range(3):
             f[k].copy_(init_dev[k])
-        ops = NativeCpOps(x, R_, f[0], f[1], f[2], ITERS)
         buf = ops.init_local()
         allreduce(buf)
         ops.init_finish(buf)
         tree_ms = timed(torch, lambda: ops.mttkrp(1), 3, 1)
         gemm2_ms = timed(torch, lambda: ops.mttkrp(2 if variant == 1 else 3), 3, 1)
+    if ops is not None:
         ops.close()
     achieved = 2.0 * I_ * J_ * kloc * R_ / (tree_ms / 1e3) / 1e12
     peak = peaks["dmma"]
@@ -614,13 +616,13 @@ def run_bt200(args, rank, world):
     else:
         phases = {"p_tree": tree_ms, "mode2": phase_tot[1] / per, "mode3": gemm2_ms,
                   "solves_fit": phase_tot[3] / per}
+        kname = "tree_p_ws_kernel (P = X x3 C, mode-1 reduction fused; DMMA) -- P dimension tree"
+        alg_bytes = 8.0 * I_ * J_ * (kloc + R_)
+        alg_note = "algorithmic X + P = "
     if world > 1:
         # sharded: only this rank's two full-pass kernels are timed (separately,
         # CUDA events); the sweep's other phases are not instrumented
         phases = {k: v for k, v in phases.items() if v > 0.0}
-        kname = "tree_p_kernel (P = X x3 C, DMMA) -- P dimension tree"
-        alg_bytes = 8.0 * I_ * J_ * (kloc + R_)
-        alg_note = "algorithmic X + P = "
     result = {
         "metric": "CP-ALS MTTKRP GFLOP/s (reference-equivalent 6*I*J*K*R per sweep)",
         "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -651,6 +653,13 @@ def run_bt200(args, rank, world):
         "gpu_launches": launches,
         "fp64_peaks_tflops": dict(peaks),
     }
+    if world > 1:
+        result["comm"] = {"backend": os.environ.get("BT_DIST_BACKEND", "nccl"), "nranks": world,
+                          "nccl_algo": os.environ.get("NCCL_ALGO"),
+                          "nccl_proto": os.environ.get("NCCL_PROTO")}
+    # the secondary configs get the whole HBM: the headline tensor is released
+    # here and rebuilt on the device for the e2e run
+    x = None
     ws_cache.clear()
     torch.cuda.empty_cache()
     # ---- N > 1: the C3 ST-HOSVD (+5 HOOI) sharded along the time mode over
@@ -679,11 +688,11 @@ def run_bt200(args, rank, world):
     torch.cuda.empty_cache()
     if not args.no_e2e:
         try:
+            x = configs.c5_build(I_, J_, K_, R_, k_slab=(k0, k1))
             result["e2e"] = e2e_run(args, torch, x, init, world, rank, k0, k1)
         except Exception as exc:  # pragma: no cover
             result["e2e"] = {"value": None, "unit": "GFLOP/s", "error": repr(exc)[:300]}
         x = None
-    del x
     ws_cache.clear()
     torch.cuda.empty_cache()
     # ---- CPU baseline (bounded slab, rank 0, N=1)
@@ -772,7 +781,7 @@ def e2e_run(args, torch, x_dev, init, world, rank, k0, k1):
             return decomp.cp_als(host, R_, ITERS, 0.0)
         return parallel.cp_als_distributed(host, R_, ITERS, 0.0, init=init_l)
 
-    steps = max(1, min(args.steps, 2))
+    steps = max(1, min(args.steps, 5))
     try:
         once()  # warm-up
         torch.cuda.synchronize()
@@ -812,13 +821,42 @@ def e2e_run(args, torch, x_dev, init, world, rank, k0, k1):
                     " -> H2D, device ALS, D2H of factors + fit history"}
 
 
+def relaunch(args):
+    """``--gpus N`` (N > 1) without a launcher: re-execute this script under
+    ``torch.distributed.run`` with one process per GPU (the driver's own
+    launch line), so ``n_gpus`` always equals the ranks that ran."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    log(f"[bench] --gpus {args.gpus} without a launcher: {' '.join(cmd)}")
+    return subprocess.call(cmd)
+
+
+def nccl_env():
+    """Fixed reduction order (bit-reproducible sums across
+    runs) and communicator evidence in the log."""
+    os.environ.setdefault("NCCL_ALGO", "Ring")
+    os.environ.setdefault("NCCL_PROTO", "Simple")
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
         os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks")
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -828,7 +866,17 @@ def main():
             # BT_DIST_BACKEND=gloo is a test hook only: it runs the N > 1 code
             # path as several ranks on one GPU (host-mediated sums, so no
             # kernel waits on another rank's); the product path is NCCL
-            dist.init_process_group(os.environ.get("BT_DIST_BACKEND", "nccl"))
+            backend = os.environ.get("BT_DIST_BACKEND", "nccl")
+            if backend == "nccl":
+                nccl_env()
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local_device(torch)))
+            else:
+                dist.init_process_group(backend)
+            probe = torch.ones(1, device="cuda")
+            dist.all_reduce(probe)          # creates the communicator now
+            log(f"[bench] rank {rank}: {backend} communicator nranks={dist.get_world_size()} "
+                f"(allreduce of ones = {int(probe.item())}), device cuda:{local_device(torch)}, "
+                f"NCCL_ALGO={os.environ.get('NCCL_ALGO')} NCCL_PROTO={os.environ.get('NCCL_PROTO')}")
         else:
             dist.init_process_group("gloo")
     if args.impl == "reference":

@@ -274,3 +274,32 @@ def gather_standin(nb=256, ell=128):
 def c1_reference_tensor():
     pat, a = c1_inputs()
     return pat, a, gather(a, pat)
+
+
+def c5_tensor_rows(factors, i0, i1, dims, noise=1e-4):
+    """Mode-1 rows i0:i1 of the C5 tensor of extents ``dims`` (same values as
+    ``c5_tensor``: model + noise * eps(global linear C-order index)), so large
+    instances can be generated chunk by chunk without the full index grids."""
+    a0, b0, c0 = factors
+    _, j, k = dims
+    x = np.einsum("ir,jr,kr->ijk", a0[i0:i1], b0, c0, optimize=True)
+    base = (np.arange(i0, i1, dtype=np.uint64) * np.uint64(j))[:, None] + np.arange(j, dtype=np.uint64)[None, :]
+    lin = base[:, :, None] * np.uint64(k) + np.arange(k, dtype=np.uint64)[None, None, :]
+    x += noise * philox_normal(lin)
+    return x
+
+
+def c5_tensor_threaded(i, j, k, r, noise=1e-4, seed=3, rows=16, threads=8):
+    """``c5_tensor`` for instances too large for its index grids: mode-1 row
+    chunks generated on a thread pool (numpy releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    f = c5_factors(i, j, k, r, seed)
+    out = np.empty((i, j, k))
+
+    def one(i0):
+        out[i0:i0 + rows] = c5_tensor_rows(f, i0, min(i, i0 + rows), (i, j, k), noise)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one, range(0, i, rows)))
+    return out

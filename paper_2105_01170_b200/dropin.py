@@ -23,11 +23,20 @@ from __future__ import annotations
 import importlib
 import sys
 
-# modules of blockten whose namespaces hold hot-path names (blockten/__init__.py:12-89
-# re-exports them; the others import them at module level)
-_MODULES = ("blockten", "blockten.tensor", "blockten.blocks", "blockten.decomp",
-            "blockten.reconstruct", "blockten.psd", "blockten.multilevel", "blockten.apps",
-            "blockten.container", "blockten.cli", "blockten.errors")
+import pkgutil
+
+
+def _modules(package: str) -> list:
+    """The package and every module in it (blockten/__init__.py:12-89
+    re-exports the hot-path names; each other module -- fileio, cli, ... --
+    imports what it uses at module level, errors included), so no consumer
+    keeps a reference binding."""
+    pkg = importlib.import_module(package)
+    names = [package]
+    for info in pkgutil.iter_modules(getattr(pkg, "__path__", [])):
+        if not info.name.startswith("__"):
+            names.append(f"{package}.{info.name}")
+    return names
 
 # name -> "module.attr" inside this package
 _TARGETS = {
@@ -92,7 +101,7 @@ def _resolve(path: str):
 def install(package: str = "blockten") -> dict:
     """Route ``package`` (default: the reference ``blockten``) through bt200.
 
-    Imports every module of ``_MODULES`` that exists (a missing optional one,
+    Imports every module of the package (a module that fails to import,
     e.g. cli, is skipped) and rebinds each name of ``_TARGETS`` it holds.
     Returns ``{module: [rebound names]}``.  Idempotent; ``uninstall()``
     reverts.  Raises ImportError when the package itself is absent."""
@@ -102,8 +111,7 @@ def install(package: str = "blockten") -> dict:
     if _state.get("package") not in (None, package):
         uninstall()
     done: dict = {}
-    for name in _MODULES:
-        modname = package + name[len("blockten"):]
+    for modname in _modules(package):
         try:
             mod = importlib.import_module(modname)
         except ImportError:
@@ -120,13 +128,19 @@ def install(package: str = "blockten") -> dict:
     # seeded-init hook: keep the reference's decomp._cp_init the one users set
     if "bt_cp_init" not in _state:
         ref_decomp = sys.modules.get(package + ".decomp")
-        ref_default = getattr(ref_decomp, "_cp_init", None)
         bt_default = bdecomp._cp_init
         _state["bt_cp_init"] = bt_default
 
+        def _is_ref_default(hook) -> bool:
+            # the reference's own HOSVD init (decomp.py:329-341), recognised by
+            # where it is defined -- a hook the user set before install() is
+            # honoured like one set after it
+            return (getattr(hook, "__module__", None) == ref_decomp.__name__
+                    and getattr(hook, "__qualname__", None) == "_cp_init")
+
         def _cp_init(t, r):
             hook = getattr(ref_decomp, "_cp_init", None)
-            if hook is not None and hook is not ref_default:
+            if hook is not None and not _is_ref_default(hook):
                 return hook(t, r)
             return bt_default(t, r)
 

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
+from functools import reduce
 from itertools import product
 
 import numpy as np
@@ -132,6 +133,18 @@ class MlKronTerm:
 
     level_mats: tuple
     block: object
+
+    def densify(self):
+        """multilevel.py:193-194: level_mats[0] (x) ... (x) block, folded
+        left to right like the reference's reduce(np.kron, ...)."""
+        mats = (*self.level_mats, self.block)
+        if _dev.is_device(self.block):
+            kron = _dev.torch().kron
+            mats = tuple(_dev.to_device(m) for m in mats)
+        else:
+            kron = np.kron
+            mats = tuple(np.asarray(m) for m in mats)
+        return reduce(kron, mats)
 
 
 def psf_weighted_tensor(psf, grid: int | None = None):

@@ -14,8 +14,13 @@ import sys
 import pytest
 
 REF = "/root/reference/pkg/src"
-if os.path.isdir(REF) and REF not in sys.path:
-    sys.path.append(REF)
+# the GPU box has no /root/reference: there the unmodified reference comes
+# from its pip install under baseline/_ref (git-ignored, travels with the repo)
+_BASE = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+for _p in (REF, _BASE):
+    if os.path.isdir(os.path.join(_p, "blockten")) and _p not in sys.path:
+        sys.path.append(_p)
+        break
 blockten = pytest.importorskip("blockten")
 
 import paper_2105_01170_b200 as bt  # noqa: E402
@@ -58,7 +63,7 @@ def test_signatures_and_fields_match_reference():
     """Every rebound function takes the reference's parameters (in order; bt200
     may add keyword-only extensions) and every dataclass has its fields."""
     for attr, path in dropin._TARGETS.items():
-        mods = [m for m in dropin._MODULES if attr in vars(importlib.import_module(m))]
+        mods = [m for m in dropin._modules("blockten") if attr in vars(importlib.import_module(m))]
         if not mods:
             continue
         ref = vars(importlib.import_module(mods[0]))[attr]
@@ -95,3 +100,39 @@ def test_uninstall_restores():
     bt.uninstall()
     assert not bt.installed()
     assert (apps.hosvd, decomp.cp_als, blockten.errors.ShapeError, bt.decomp._cp_init) == before
+
+
+def test_every_module_rebound_including_fileio(installed):
+    """fileio raises ContainerFormatError / ShapeError that the CLI's
+    except clauses (cli.py:385-392) must catch as bt200's classes."""
+    import blockten.fileio as fileio
+
+    assert "blockten.fileio" in installed
+    assert fileio.ContainerFormatError is bt.ContainerFormatError
+    assert fileio.ShapeError is bt.ShapeError
+
+
+def test_cli_malformed_matrix_market_exit_code(installed, tmp_path, capsys):
+    import blockten.cli as cli
+
+    bad = tmp_path / "bad.mtx"
+    bad.write_text("this is not a matrix market file\n1 2 3\n")
+    code = cli.main(["analyze", str(bad), "--block-rows", "2", "--block-cols", "2"])
+    assert code == 2, capsys.readouterr().err
+
+
+def test_hook_set_before_install_is_honoured():
+    import blockten.decomp as decomp
+
+    saved = decomp._cp_init
+    try:
+        decomp._cp_init = lambda t, r: ("pre-install hook", r)
+        bt.install()
+        try:
+            assert bt.decomp._cp_init(None, 5) == ("pre-install hook", 5)
+            decomp._cp_init = saved          # the reference default -> bt200's HOSVD init
+            assert bt.decomp._cp_init is not saved
+        finally:
+            bt.uninstall()
+    finally:
+        decomp._cp_init = saved
