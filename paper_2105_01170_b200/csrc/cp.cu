@@ -25,6 +25,7 @@
 
 #include "gemm.cuh"
 #include "jacobi.cuh"
+#include "tma.cuh"
 
 int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, int64_t ws_elems);
 extern "C" const char* bt_last_error(void);
@@ -256,6 +257,198 @@ __global__ void __launch_bounds__(Cfg::THREADS + 32, 2)
     double sum = 0.0;
 #pragma unroll
     for (int w = 0; w < Cfg::WM; ++w) sum += red[w][c];
+    m1part[(i * jtiles + tm) * R + r] = sum;
+  }
+}
+
+// TMA tree kernel.  Both operand tiles arrive by cp.async.bulk.tensor into
+// dense 128-byte-swizzled stage buffers (16-byte chunk c of a 128-byte row r
+// lands at chunk c ^ (r & 7)): the X tile (128 rows j x 16 k, K-contiguous)
+// as one box, the C tile (16 k x 64 r) as four 16 x 16 boxes.  With no
+// padding, 4 stages of 24 KB fit twice per SM.  There is no producer warp:
+// each of the 4 DMMA warps counts itself out of a stage on a shared counter
+// and the LAST one to leave re-arms the stage's mbarrier and issues its
+// refill (k-tile kt + STAGES), so the CTA is 128 threads and the register
+// budget (255) holds the 64x32 warp tile without spills.
+// Fragment k assignment: a 64-bit LDS is served per half-warp (lanes gq in
+// 4h..4h+3, tq 0..3 -> 16 x 8 B = one pass over the 32 banks), so the 4
+// k values a k-step gives the tq lanes must spread over distinct 8-byte
+// slots for BOTH operands: A wants distinct (bit 0, bit 3) of k (chunk group
+// and half under the row XOR), B wants distinct (bit 1, bit 2) of k (the XOR
+// with k & 7).  k = {0, 3, 12, 15} ^ d with d = {0, 1, 4, 5} per k-step
+// satisfies both and covers the 16 k of a stage.  The products per output
+// are the same; they are added in this fixed order (bit-reproducible).
+struct TreeTma {
+  static constexpr int BM = 128, BN = 64, BK = 16, STAGES = 4;
+  static constexpr int WM = 2, WN = 2, THREADS = WM * WN * 32;
+  static constexpr int TM = BM / WM, TN = BN / WN, FM = TM / 8, FN = TN / 8;
+  static constexpr int A_STAGE = BM * BK;  // doubles
+  static constexpr int B_STAGE = BK * BN;
+  static constexpr int STAGE_BYTES = (A_STAGE + B_STAGE) * 8;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;  // + alignment slack
+};
+
+__device__ __forceinline__ void tree_tma_issue(const CUtensorMap* xmap, const CUtensorMap* cmap,
+                                               double* as, double* bs, uint64_t* bar, int k0, int m0,
+                                               int n0, int i, uint64_t pol_x, uint64_t pol_c) {
+  mbar_arrive_expect_tx(bar, TreeTma::STAGE_BYTES);
+  tma_load_3d(as, xmap, bar, k0, m0, i, pol_x);
+#pragma unroll
+  for (int q = 0; q < TreeTma::BN / 16; ++q)
+    tma_load_2d(bs + q * 16 * TreeTma::BK, cmap, bar, n0 + 16 * q, k0, pol_c);
+}
+
+__global__ void __launch_bounds__(TreeTma::THREADS, 2)
+    tree_p_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap cmap,
+                      BtGemmArgs g, const double* __restrict__ Bf, int64_t R,
+                      double* __restrict__ m1part, int64_t jtiles, int store_p) {
+  using T = TreeTma;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[T::WM][T::BN];
+  __shared__ __align__(8) uint64_t full[T::STAGES];
+  __shared__ int left_cnt[T::STAGES];
+  const int tm = blockIdx.x, tn = blockIdx.y, i = blockIdx.z;
+  const int m0 = tm * T::BM, n0 = tn * T::BN;
+  const int KT = static_cast<int>((g.Kin + T::BK - 1) / T::BK);
+  // offset from smem_raw (not an integer round trip) so the fragment reads
+  // stay LDS instead of generic loads
+  double* As = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  double* Bs = As + T::STAGES * T::A_STAGE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t pol_x = l2_policy_evict_first();
+  const uint64_t pol_c = l2_policy_evict_last();
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&xmap);
+    tma_prefetch_desc(&cmap);
+    for (int s = 0; s < T::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      left_cnt[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < T::STAGES && s < KT; ++s)
+      tree_tma_issue(&xmap, &cmap, As + s * T::A_STAGE, Bs + s * T::B_STAGE, &full[s], s * T::BK, m0,
+                     n0, i, pol_x, pol_c);
+  }
+  __syncthreads();
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wmi = warp % T::WM;
+  const int wm0 = wmi * T::TM;
+  const int wn0 = (warp / T::WM) * T::TN;
+  double acc[T::FM][T::FN][2];
+#pragma unroll
+  for (int a = 0; a < T::FM; ++a)
+#pragma unroll
+    for (int b = 0; b < T::FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  constexpr int KSTEPS = T::BK / 4;
+  const int kq = 3 * (tq & 1) + 12 * (tq >> 1);   // {0, 3, 12, 15}
+  const int g2 = gq >> 1, g1 = gq & 1;
+  double afr[2][T::FM], bfr[2][T::FN];
+  auto load_frags = [&](int buf, const double* as, const double* bs, int ks) {
+    const int k = kq ^ ((ks & 1) + 4 * (ks >> 1));     // ^ {0, 1, 4, 5}
+    const int acol = 2 * ((k >> 1) ^ gq) + (k & 1);
+#pragma unroll
+    for (int a = 0; a < T::FM; ++a) afr[buf][a] = as[(wm0 + a * 8 + gq) * T::BK + acol];
+    const int x = k & 7;
+#pragma unroll
+    for (int b = 0; b < T::FN; ++b) {
+      const int q = (wn0 >> 4) + (b >> 1);
+      const int chunk = (4 * (b & 1) + g2) ^ x;
+      bfr[buf][b] = bs[q * 16 * T::BK + k * 16 + 2 * chunk + g1];
+    }
+  };
+  // fragments are software-pipelined across stages: the last k-step of
+  // stage s issues its DMMAs after the first fragments of stage s + 1 are in
+  // flight, and stage s is released (refilled) as soon as its last
+  // fragments sit in registers
+  if (KT > 0) {
+    mbar_wait(&full[0], 0u);
+    load_frags(0, As, Bs, 0);
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % T::STAGES;
+    const double* as = As + s * T::A_STAGE;
+    const double* bs = Bs + s * T::B_STAGE;
+#pragma unroll
+    for (int ks = 0; ks < KSTEPS; ++ks) {
+      if (ks + 1 < KSTEPS) {
+        load_frags((ks + 1) & 1, as, bs, ks + 1);
+      } else {
+        // leave stage s; the last warp out refills it with k-tile kt + STAGES
+        __syncwarp();
+        if (lane == 0) {
+          int old;
+          asm volatile("atom.release.cta.shared::cta.add.s32 %0, [%1], 1;"
+                       : "=r"(old)
+                       : "r"(smem_u32(&left_cnt[s]))
+                       : "memory");
+          if (old == T::WM * T::WN - 1) {
+            asm volatile("fence.acq_rel.cta;" ::: "memory");
+            left_cnt[s] = 0;
+            const int nk = kt + T::STAGES;
+            if (nk < KT) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              tree_tma_issue(&xmap, &cmap, As + s * T::A_STAGE, Bs + s * T::B_STAGE, &full[s],
+                             nk * T::BK, m0, n0, i, pol_x, pol_c);
+            }
+          }
+        }
+        if (kt + 1 < KT) {
+          const int s1 = (kt + 1) % T::STAGES;
+          mbar_wait(&full[s1], static_cast<unsigned>(((kt + 1) / T::STAGES) & 1));
+          load_frags(0, As + s1 * T::A_STAGE, Bs + s1 * T::B_STAGE, 0);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < T::FM; ++a)
+#pragma unroll
+        for (int b = 0; b < T::FN; ++b) dmma884(acc[a][b][0], acc[a][b][1], afr[ks & 1][a], bfr[ks & 1][b]);
+    }
+  }
+  // epilogue (tree_p_ws_kernel's)
+  double* Pb = g.C + i * g.sCb;
+  double colsum[T::FN][2];
+#pragma unroll
+  for (int j = 0; j < T::FN; ++j) colsum[j][0] = colsum[j][1] = 0.0;
+#pragma unroll
+  for (int fi = 0; fi < T::FM; ++fi) {
+    const int64_t jrow = m0 + wm0 + fi * 8 + gq;
+    const bool rv = jrow < g.M;
+#pragma unroll
+    for (int fj = 0; fj < T::FN; ++fj) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t r = n0 + wn0 + fj * 8 + 2 * tq + h;
+        if (rv && r < g.N) {
+          const double v = acc[fi][fj][h];
+          if (store_p) Pb[jrow * g.sCm + r] = v;
+          colsum[fj][h] = fma(v, __ldg(Bf + jrow * R + r), colsum[fj][h]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int fj = 0; fj < T::FN; ++fj)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double v = colsum[fj][h];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      colsum[fj][h] = v;
+    }
+  if (gq == 0) {
+#pragma unroll
+    for (int fj = 0; fj < T::FN; ++fj)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) red[wmi][wn0 + fj * 8 + 2 * tq + h] = colsum[fj][h];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < T::BN; c += T::THREADS) {
+    const int64_t r = n0 + c;
+    if (r >= g.N) continue;
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < T::WM; ++w) sum += red[w][c];
     m1part[(i * jtiles + tm) * R + r] = sum;
   }
 }
@@ -1285,10 +1478,11 @@ int tree_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("BT_TREE_CFG");
-    // 9 (default): warp-specialised -- 4 DMMA warps of 64x32 + 1 cp.async
-    // producer warp, mbarrier ring, 3 stages: 72.5 ms on C5; 6: the same
-    // tile with all warps loading and computing: 73.5 ms
-    v = e ? atoi(e) : 9;
+    // 11 (default): warp-specialised with the X tile by TMA, 4 unpadded
+    // swizzled stages (tree_p_tma_kernel); 9: the same with a cp.async
+    // producer and 3 padded stages (tree_p_ws_kernel: 72.5 ms on C5); 6:
+    // the same tile with all warps loading and computing: 73.5 ms
+    v = e ? atoi(e) : 11;
   }
   return v;
 }
@@ -1487,6 +1681,41 @@ int launch_tree_ws(const Plan& pl, const double* X, const double* C, const doubl
   return BT_OK;
 }
 
+// TMA tree kernel (default for R > 16 with K even; BT_TREE_CFG=9 keeps the
+// cp.async producer of tree_p_ws_kernel for A/B runs)
+int launch_tree_tma(const Plan& pl, const double* X, const double* C, const double* B, double* P,
+                    double* m1part, int store_p, cudaStream_t st) {
+  using T = TreeTma;
+  BtGemmArgs g{};
+  g.M = pl.J;
+  g.N = pl.R;
+  g.Kin = pl.K;
+  g.Kout = 1;
+  g.A = BtOperand{X, pl.K, 0, 1, pl.J * pl.K};
+  g.B = BtOperand{C, 1, 0, pl.R, 0};
+  g.C = P;
+  g.sCm = pl.R;
+  g.sCn = 1;
+  g.sCb = pl.J * pl.R;
+  g.alpha = 1.0;
+  CUtensorMap xmap, cmap;
+  BT_TRY(bt_tma_map_f64_3d(&xmap, X, pl.K, pl.J, pl.I, pl.K, pl.J * pl.K, T::BK, T::BM, 1));
+  BT_TRY(bt_tma_map_f64_2d(&cmap, C, pl.R, pl.K, pl.R, 16, T::BK));
+  static bool attr = false;
+  if (!attr) {
+    BT_CUDA_CHECK(cudaFuncSetAttribute(tree_p_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       T::SMEM_BYTES));
+    attr = true;
+  }
+  BT_REQUIRE(pl.I <= 65535, BT_E_SHAPE, "cp: mode-1 extent %lld exceeds 65535", (long long)pl.I);
+  dim3 grid(static_cast<unsigned>(bt_cdiv(pl.J, T::BM)), static_cast<unsigned>(bt_cdiv(pl.R, T::BN)),
+            static_cast<unsigned>(pl.I));
+  tree_p_tma_kernel<<<grid, T::THREADS, T::SMEM_BYTES, st>>>(xmap, cmap, g, B, pl.R, m1part, pl.jtiles,
+                                                            store_p);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
 template <int BN, int V, int VAR = 0>
 int launch_tree(const Plan& pl, const double* X, const double* C, const double* B, double* P,
                 double* m1part, int store_p, cudaStream_t st) {
@@ -1533,8 +1762,11 @@ int run_tree(const Plan& pl, const double* X, const double* C, const double* B, 
                 : launch_tree<16, 1>(pl, X, C, B, P, m1part, store_p, st);
     default:
       if (v2) {
-        return tree_variant() == 6 ? launch_tree<64, 2>(pl, X, C, B, P, m1part, store_p, st)
-                                   : launch_tree_ws<2>(pl, X, C, B, P, m1part, store_p, st);
+        const int tv = tree_variant();
+        if (tv == 6) return launch_tree<64, 2>(pl, X, C, B, P, m1part, store_p, st);
+        if (tv == 9 || pl.K > INT32_MAX || pl.J > INT32_MAX)
+          return launch_tree_ws<2>(pl, X, C, B, P, m1part, store_p, st);
+        return launch_tree_tma(pl, X, C, B, P, m1part, store_p, st);
       }
       return launch_tree<64, 1>(pl, X, C, B, P, m1part, store_p, st);
   }
