@@ -28,6 +28,17 @@
 #include "tma.cuh"
 
 int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, int64_t ws_elems);
+int bt_gemm_at_tma(const double* a, int64_t lda, int64_t sAb, const double* b, int64_t ldb, double* c,
+                   int64_t ldc, int64_t sCb, int64_t M, int64_t N, int64_t Kdim, int64_t batch,
+                   cudaStream_t st);
+// BT_GEMM_TMA=0: the Q-tree GEMMs on the cp.async engine (A/B runs)
+static bool use_at_tma() {
+  static const int v = [] {
+    const char* e = getenv("BT_GEMM_TMA");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v != 0;
+}
 extern "C" const char* bt_last_error(void);
 int64_t bt_gemm_ws_elems(BtGemmArgs g, int64_t batch);
 
@@ -2075,9 +2086,15 @@ extern "C" int bt_cp_mttkrp(void* state, int mode, double* out) {
   cudaStream_t st = S->st;
   if (pl.qtree && pl.K > 0) {
     if (mode == 1 && pl.m1_via_t) {
-      BtGemmArgs g = tslab_args(pl, S->X, S->F[1], ws + pl.off_t);
-      g.ws = ws + pl.off_m3ws;
-      BT_TRY(bt_gemm_run(g, pl.I, st, 1, 0));
+      int rc = use_at_tma() ? bt_gemm_at_tma(S->X, pl.K, pl.J * pl.K, S->F[1], pl.R, ws + pl.off_t, pl.R,
+                                             pl.K * pl.R, pl.K, pl.R, pl.J, pl.I, st)
+                            : BT_E_VALUE;
+      if (rc == BT_E_VALUE) {
+        BtGemmArgs g = tslab_args(pl, S->X, S->F[1], ws + pl.off_t);
+        g.ws = ws + pl.off_m3ws;
+        rc = bt_gemm_run(g, pl.I, st, 1, 0);
+      }
+      BT_TRY(rc);
       mode2_from_q_kernel<<<static_cast<unsigned>(pl.I), 256, 0, st>>>(ws + pl.off_t, S->F[2], pl.K,
                                                                        static_cast<int>(pl.R), out);
       BT_LAUNCH_CHECK();
@@ -2094,9 +2111,15 @@ extern "C" int bt_cp_mttkrp(void* state, int mode, double* out) {
       return BT_OK;
     }
     if (mode == 2) {
-      BtGemmArgs g = qtree_args(pl, S->X, S->F[0], ws + pl.off_p);
-      g.ws = ws + pl.off_m3ws;
-      BT_TRY(bt_gemm_run(g, 1, st, 0, pl.m3_ws_elems));
+      int rc = use_at_tma() ? bt_gemm_at_tma(S->X, pl.J * pl.K, 0, S->F[0], pl.R, ws + pl.off_p, pl.R, 0,
+                                             pl.J * pl.K, pl.R, pl.I, 1, st)
+                            : BT_E_VALUE;
+      if (rc == BT_E_VALUE) {
+        BtGemmArgs g = qtree_args(pl, S->X, S->F[0], ws + pl.off_p);
+        g.ws = ws + pl.off_m3ws;
+        rc = bt_gemm_run(g, 1, st, 0, pl.m3_ws_elems);
+      }
+      BT_TRY(rc);
       mode2_from_q_kernel<<<static_cast<unsigned>(pl.J), 256, 0, st>>>(ws + pl.off_p, S->F[2], pl.K,
                                                                        static_cast<int>(pl.R), out);
       BT_LAUNCH_CHECK();
