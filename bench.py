@@ -595,7 +595,7 @@ def run_bt200(args, rank, world):
     log(f"[bench] C5 step {ms:.1f} ms, tree variant {'Q' if variant else 'P'}, phases/sweep "
         f"{[round(v / per, 2) for v in phase_tot]} ms, fit {fit}")
     traffic = None
-    ncu_file = "r01_ncu_c5q.json" if variant == 1 else "r01_ncu_c5.json"
+    ncu_file = "r02_ncu_c5q.json" if variant == 1 else "r01_ncu_c5.json"
     try:
         prof = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                            "profiles", ncu_file)))
@@ -607,16 +607,16 @@ def run_bt200(args, rank, world):
     if variant == 1:
         phases = {"mode1_tree_no_p_store": tree_ms, "q_gemm_plus_mode2": gemm2_ms,
                   "mode3_from_q": phase_tot[2] / per, "solves_fit": phase_tot[3] / per}
-        kname = ("tree_p_ws_kernel (X x3 C tiles, mode-1 reduction fused, no P store; "
+        kname = ("tree_p_tma_kernel (X x3 C tiles by TMA, mode-1 reduction fused, no P store; "
                  "DMMA) -- Q dimension tree") if kloc > 256 else (
-                 "bt_gemm_kernel (T = X[i]^T B batched over i, DMMA; mode 1 streamed from T) "
-                 "-- Q dimension tree, short mode-3 slab")
+                 "gemm_at_tma_kernel (T = X[i]^T B batched over i, TMA + DMMA; mode 1 streamed "
+                 "from T) -- Q dimension tree, short mode-3 slab")
         alg_bytes = 8.0 * I_ * J_ * kloc
         alg_note = "algorithmic X = "
     else:
         phases = {"p_tree": tree_ms, "mode2": phase_tot[1] / per, "mode3": gemm2_ms,
                   "solves_fit": phase_tot[3] / per}
-        kname = "tree_p_ws_kernel (P = X x3 C, mode-1 reduction fused; DMMA) -- P dimension tree"
+        kname = "tree_p_tma_kernel (P = X x3 C by TMA, mode-1 reduction fused; DMMA) -- P dimension tree"
         alg_bytes = 8.0 * I_ * J_ * (kloc + R_)
         alg_note = "algorithmic X + P = "
     if world > 1:
@@ -646,8 +646,8 @@ def run_bt200(args, rank, world):
                                       f"(profiles/{ncu_file}); {alg_note}{alg_bytes:.4g} B"),
                      "peak_source": "measured in this run: DMMA.8x8x4 chains on all SMs "
                                     "(MEASURED_PEAKS.json has no FP64 figure)",
-                     "second_gemm": ("Q GEMM (+ mode-2 reduction)" if variant == 1 else
-                                     "mode-3 GEMM"),
+                     "second_gemm": ("Q GEMM gemm_at_tma_kernel (+ mode-2 reduction)" if variant == 1
+                                     else "mode-3 GEMM"),
                      "second_gemm_achieved": 2.0 * I_ * J_ * kloc * R_ / (gemm2_ms / 1e3) / 1e12},
         "clocks": clk.summary(),
         "gpu_launches": launches,
