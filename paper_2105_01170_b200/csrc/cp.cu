@@ -2510,3 +2510,11 @@ extern "C" int bt_pinv_sym_f64(const double* v, int64_t R, double* vp, void* str
              (long long)R, PINV_MAX_R);
   return run_pinv(v, nullptr, static_cast<int>(R), vp, bt_stream(stream));
 }
+
+// diagnostics: sweeps of the last warp-Jacobi eigen path in this module
+extern "C" int bt_debug_jacobi_sweeps(void) {
+  int v = -1;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&v, g_jacobi_sweeps, sizeof(int));
+  return v;
+}

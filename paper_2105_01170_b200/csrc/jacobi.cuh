@@ -5,6 +5,9 @@
 
 #include "bt_common.cuh"
 
+// sweeps of the last jacobi_warp_t call (diagnostics: bt_debug_jacobi_sweeps)
+static __device__ int g_jacobi_sweeps;
+
 // Circle-method round-robin pair k of round rnd for n (even) players
 // (0 <= rnd, k < n - 1: conditional subtractions instead of integer modulo).
 static __device__ __forceinline__ void rr_pair(int n, int rnd, int k, int& p, int& q) {
@@ -220,8 +223,12 @@ static __device__ __noinline__ int jacobi_warp_t(double* a, double* qv, int ld, 
       }
       __syncwarp();
     }
-    if (!__any_sync(0xffffffffu, rotated)) break;
+    if (!__any_sync(0xffffffffu, rotated)) {
+      if (lane == 0) g_jacobi_sweeps = sweep;
+      break;
+    }
     any = 1;
+    if (lane == 0) g_jacobi_sweeps = sweep + 1;
   }
   return any;
 }
