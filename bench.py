@@ -265,6 +265,23 @@ def extras_run(torch, budget_s=240.0):
         from paper_2105_01170_b200.tensor import fro_norm_dev
 
         out["c3_core_norm_ratio"] = fro_norm_dev(rep.core) / fro_norm_dev(t3)
+        # C3's two outputs: the PSD-preserving SpsdRep from the
+        # unweighted blocks (psd.py:164-187) and the BLR operator of the
+        # (64, 32, 64) Tucker (reconstruct.py:229-240) with its matvec
+        from paper_2105_01170_b200 import psd
+
+        eta3 = torch.tensor(pat3.counts, dtype=torch.float64, device="cuda")
+        blocks3 = (t3.permute(1, 0, 2) / eta3.sqrt()[:, None, None]).contiguous()
+        out["c3_spsd_ms"] = timed(torch, lambda: psd.spsd_compress_blocks(pat3, blocks3, 64), 3, 1)
+        del blocks3
+        torch.cuda.empty_cache()
+        out["c3_blr_from_tucker_ms"] = timed(torch, lambda: reconstruct.blr_from_tucker(rep, pat3), 3, 1)
+        blr3 = reconstruct.blr_from_tucker(rep, pat3)
+        rhs3 = torch.from_numpy(np.random.default_rng(1003).standard_normal((pat3.shape[1], 16))).cuda()
+        ms_mv = timed(torch, lambda: reconstruct.matvec(blr3, rhs3), 3, 1)
+        out["c3_blr_matvec16_ms"] = ms_mv
+        out["c3_blr_matvec_tflops"] = 16 * reconstruct.flops_blr(pat3, 64, 64) / ms_mv / 1e9
+        del blr3, rhs3
         # K7 / K9 kernel rooflines at C3: the mode-1 unfolding Gram (SYRK over
         # the 1024 x 524288 unfolding, unique-half work n(n+1)N/n flops, SURVEY
         # 8d) and the first TTM t x1 U^T (2 r N flops)

@@ -710,6 +710,233 @@ __device__ void pinv_block(const double* __restrict__ g0, const double* __restri
   pinv_from_eig(a, q, R, LD, vp);
 }
 
+// Vp = pinv(V), V = G0 o G1, R <= NP <= 32, by one-sided (Hestenes) Jacobi
+// held in the registers of ONE warp: lane (c + NP h) owns rows
+// [h ROWS, (h+1) ROWS) of column c of W (= V J, starts at V) and of the
+// accumulated rotation J (starts at I).  A round pairs the columns by the
+// circle method (partner of c in round r: (2r - c) mod (NP - 1), with NP - 1
+// meeting r); the two lanes of a pair swap their halves by shuffles, form
+// ||w_p||^2, ||w_q||^2, w_p . w_q (row halves added in a fixed order, so both
+// lanes get the same bits), and apply the same rotation -- no shared memory,
+// no barrier, no data-dependent register index.  At convergence the columns
+// of W are orthogonal: sigma_k = ||W_k|| are V's singular values and
+// pinv(V) = sum_{sigma_k > 1e-15 sigma_max} J_k (W_k / sigma_k^2)^T, numpy's
+// SVD pinv cutoff (decomp.py:387) with the sign of each eigenvalue kept.
+__device__ long long g_pinv1s_dbg[2];  // sweeps, cycles of the last call (diagnostics)
+
+// Warm start (jstore != nullptr, warm != 0): W = V J_prev, J = J_prev with
+// J_prev the rotation this kernel stored for the same mode on its previous
+// call -- ALS changes V little from sweep to sweep, so V J_prev is already
+// nearly column-orthogonal and the sweeps drop from ~8-15 to a few.  The
+// converged factorisation (and the cutoff) is the same up to rounding.
+template <int NP>
+__global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restrict__ g0,
+                                                          const double* __restrict__ g1, int R,
+                                                          double* __restrict__ vp,
+                                                          double* __restrict__ jstore, int warm) {
+  static_assert(NP == 8 || NP == 16 || NP == 32, "NP in {8, 16, 32}");
+  constexpr int HALVES = 32 / NP, ROWS = NP / HALVES;
+  __shared__ double js[NP][NP + 1], ws[NP][NP + 1], isg[NP];
+  const int lane = threadIdx.x;
+  const int col = lane % NP, half = lane / NP, r0 = half * ROWS;
+  double w[ROWS], jv[ROWS];
+  double ss = 0.0;
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) {
+    const int r = r0 + i;
+    double v = 0.0;
+    if (r < R && col < R) v = g1 ? g0[r * R + col] * g1[r * R + col] : g0[r * R + col];
+    w[i] = v;
+    jv[i] = (r == col) ? 1.0 : 0.0;
+    ss = fma(v, v, ss);
+  }
+  // ---- well-conditioned V: Cholesky inverse by this warp in shared memory
+  // (no CTA barriers), accepted on the same test as pinv_block (kappa_1 <=
+  // 1e12, where numpy's pinv is the inverse to ~kappa eps)
+  {
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) ws[r0 + i][col] = w[i];
+    __syncwarp();
+    // ||V||_1 (lanes < R take a column each)
+    double c1 = 0.0;
+    if (lane < R)
+      for (int r = 0; r < R; ++r) c1 += fabs(ws[r][lane]);
+    double vn1 = c1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vn1 = fmax(vn1, __shfl_xor_sync(0xffffffffu, vn1, o));
+    int ok = 1;
+    double lo = INFINITY, hi = 0.0;
+    for (int k = 0; k < R && ok; ++k) {
+      const double d = ws[k][k];
+      if (!(d > 0.0)) {
+        ok = 0;
+        break;
+      }
+      const double rl = rsqrt_nr(d), lkk = d * rl;
+      lo = fmin(lo, lkk);
+      hi = fmax(hi, lkk);
+      __syncwarp();
+      if (lane > k && lane < R) ws[lane][k] *= rl;
+      if (lane == 0) ws[k][k] = lkk;
+      __syncwarp();
+      // trailing lower triangle j <= i, i, j > k
+      const int m = R - 1 - k;
+      for (int idx = lane; idx < m * m; idx += 32) {
+        const int i = k + 1 + idx / m, j = k + 1 + idx % m;
+        if (j <= i) ws[i][j] -= ws[i][k] * ws[j][k];
+      }
+      __syncwarp();
+    }
+    // kappa_2 >= (max l_kk / min l_kk)^2: hopeless cases skip the inverse
+    if (ok && (hi / lo) * (hi / lo) > 1e12 * R) ok = 0;
+    if (ok) {
+      // Y = L^-1, one column per lane (forward substitution on e_lane)
+      if (lane < R) {
+        for (int i = 0; i < R; ++i) {
+          double acc = (i == lane) ? 1.0 : 0.0;
+          for (int k = lane; k < i; ++k) acc -= ws[i][k] * js[k][lane];
+          js[i][lane] = (i < lane) ? 0.0 : acc / ws[i][i];
+        }
+      }
+      __syncwarp();
+      // V^-1 = Y^T Y (into ws: L is no longer needed) and its 1-norm
+      for (int idx = lane; idx < R * R; idx += 32) {
+        const int r = idx / R, c = idx % R;
+        double v = 0.0;
+        for (int k = (r > c ? r : c); k < R; ++k) v = fma(js[k][r], js[k][c], v);
+        ws[r][c] = v;
+        vp[idx] = v;
+      }
+      __syncwarp();
+      double in1 = 0.0;
+      if (lane < R)
+        for (int r = 0; r < R; ++r) in1 += fabs(ws[r][lane]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) in1 = fmax(in1, __shfl_xor_sync(0xffffffffu, in1, o));
+      if (vn1 * in1 <= 1e12) return;   // vp holds V^-1 (== pinv)
+    }
+    __syncwarp();
+  }
+  if (jstore != nullptr && warm) {
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+      ws[r0 + i][col] = w[i];                       // V (symmetric)
+      js[r0 + i][col] = jstore[(r0 + i) * NP + col];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+      double acc = 0.0;
+      for (int k = 0; k < NP; ++k) acc = fma(ws[r0 + i][k], js[k][col], acc);
+      w[i] = acc;
+      jv[i] = js[r0 + i][col];
+    }
+    __syncwarp();
+  }
+  // ||V||_F^2: each element counted once (lanes hold disjoint pieces)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  // columns below 1e-15 ||V||_F sit at numpy's cutoff (1e-15 sigma_max,
+  // sigma_max >= ||V||_F / sqrt(R)) or below it: their mutual orthogonality
+  // is rounding noise and their rotation against a large column is below
+  // eps, so pairs involving one are not rotated (else near-null spaces keep
+  // the sweeps going on noise)
+  const double floor_norm = 1e-15 * sqrt(ss);
+  const double floor2 = floor_norm * floor_norm;
+  // sum over the HALVES row blocks of a column in a fixed order (block 0
+  // first), identical in every lane holding that column
+  auto colsum = [&](double v) {
+#pragma unroll
+    for (int o = NP; o < 32; o <<= 1) {
+      const double u = __shfl_xor_sync(0xffffffffu, v, o);
+      v = (lane & o) ? (u + v) : (v + u);
+    }
+    return v;
+  };
+  const long long t_start = clock64();
+  int sweeps_done = 0;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    int rotated = 0;
+    sweeps_done = sweep + 1;
+    for (int rnd = 0; rnd < NP - 1; ++rnd) {
+      int partner;
+      if (col == NP - 1) {
+        partner = rnd;
+      } else if (col == rnd) {
+        partner = NP - 1;
+      } else {
+        partner = 2 * rnd - col;
+        if (partner < 0) partner += NP - 1;
+        if (partner >= NP - 1) partner -= NP - 1;
+      }
+      const int src = partner + half * NP;
+      double pw[ROWS], pj[ROWS];
+#pragma unroll
+      for (int i = 0; i < ROWS; ++i) {
+        pw[i] = __shfl_sync(0xffffffffu, w[i], src);
+        pj[i] = __shfl_sync(0xffffffffu, jv[i], src);
+      }
+      const bool lo = col < partner;
+      double a = 0.0, b = 0.0, g = 0.0;
+#pragma unroll
+      for (int i = 0; i < ROWS; ++i) {
+        const double wp = lo ? w[i] : pw[i], wq = lo ? pw[i] : w[i];
+        a = fma(wp, wp, a);
+        b = fma(wq, wq, b);
+        g = fma(wp, wq, g);
+      }
+      a = colsum(a);
+      b = colsum(b);
+      g = colsum(g);
+      // rotate unless the pair is orthogonal to working precision
+      // (|g| <= 1e-15 sqrt(a b), compared squared: no IEEE sqrt on the
+      // round's critical path) or a column is below the noise floor
+      if (g * g > 1e-30 * (a * b) && fmin(a, b) > floor2) {
+        double c, s;
+        jacobi_rotation(a, b, g, c, s);
+        rotated = 1;
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) {
+          if (lo) {
+            w[i] = c * w[i] - s * pw[i];
+            jv[i] = c * jv[i] - s * pj[i];
+          } else {
+            w[i] = s * pw[i] + c * w[i];
+            jv[i] = s * pj[i] + c * jv[i];
+          }
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, rotated)) break;
+  }
+  if (lane == 0) {
+    g_pinv1s_dbg[0] = sweeps_done;
+    g_pinv1s_dbg[1] = clock64() - t_start;
+  }
+  // sigma_k = ||W_k||; numpy cutoff 1e-15 * sigma_max
+  double n2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) n2 = fma(w[i], w[i], n2);
+  const double sig = sqrt(colsum(n2));
+  double smax = sig;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+  if (half == 0) isg[col] = (sig > 1e-15 * smax) ? 1.0 / (sig * sig) : 0.0;
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) {
+    js[r0 + i][col] = jv[i];
+    ws[r0 + i][col] = w[i];
+    if (jstore != nullptr) jstore[(r0 + i) * NP + col] = jv[i];
+  }
+  __syncwarp();
+  for (int idx = lane; idx < R * R; idx += 32) {
+    const int r = idx / R, c = idx % R;
+    double v = 0.0;
+    for (int k = 0; k < NP; ++k) v = fma(js[r][k] * isg[k], ws[c][k], v);
+    vp[idx] = v;
+  }
+}
+
 template <int NP>
 __global__ void __launch_bounds__(1024) pinv_fast_kernel(const double* __restrict__ g0,
                                                          const double* __restrict__ g1, int R,
@@ -1531,6 +1758,7 @@ struct Plan {
   // is long) then m1[i][r] = sum_k T[i][k][r] C[k][r]
   int m1_via_t;
   int64_t off_t;
+  int64_t off_jstore;
 };
 
 BtGemmArgs mode3_args(const Plan& pl, const double* X, const double* A, const double* B,
@@ -1654,6 +1882,7 @@ Plan make_plan(const bt_cp_problem* pb, int variant = -1) {
   pl.off_gbuf = take(pl.R * pl.R + 2);
   pl.off_init = take(pl.R * pl.R + 2);
   pl.off_res1 = take(2);
+  pl.off_jstore = take(3 * 16 * 16);   // warm-start rotations of the R <= 16 pinv, per mode
   pl.total = o;
   return pl;
 }
@@ -1815,7 +2044,26 @@ int launch_pinv_fast(const double* g0, const double* g1, int R, double* vp, cuda
   return BT_OK;
 }
 
-int run_pinv(const double* g0, const double* g1, int R, double* vp, cudaStream_t st) {
+// BT_PINV_1S=0: the shared-memory Cholesky-first / two-sided Jacobi pinv for
+// R <= 16 as well (A/B runs)
+static bool use_pinv_1s() {
+  static const int v = [] {
+    const char* e = getenv("BT_PINV_1S");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v != 0;
+}
+
+int run_pinv(const double* g0, const double* g1, int R, double* vp, cudaStream_t st,
+             double* jstore = nullptr, int warm = 0) {
+  if (R <= 16 && use_pinv_1s()) {
+    if (R <= 8)
+      pinv_jacobi1_kernel<8><<<1, 32, 0, st>>>(g0, g1, R, vp, jstore, warm);
+    else
+      pinv_jacobi1_kernel<16><<<1, 32, 0, st>>>(g0, g1, R, vp, jstore, warm);
+    BT_LAUNCH_CHECK();
+    return BT_OK;
+  }
   if (R <= 8) return launch_pinv_fast<8>(g0, g1, R, vp, st);
   if (R <= 16) return launch_pinv_fast<16>(g0, g1, R, vp, st);
   if (R <= 32) return launch_pinv_fast<32>(g0, g1, R, vp, st);
@@ -1827,9 +2075,10 @@ int run_pinv(const double* g0, const double* g1, int R, double* vp, cudaStream_t
 // over nparts partials), gbuf = [F_un^T F_un, <F_un, M>] (summed over CTAs).
 int run_solve_rows(const Plan& pl, const CpState& s, double* ws, const double* mpart,
                    int64_t nparts, int64_t part_stride, int64_t row_stride, int64_t rows, int go0,
-                   int go1, double* F, bool with_inner, double* gbuf, cudaStream_t st) {
+                   int go1, double* F, bool with_inner, double* gbuf, cudaStream_t st,
+                   bool pinv_done = false) {
   const int R = static_cast<int>(pl.R);
-  BT_TRY(run_pinv(s.gram[go0], s.gram[go1], R, s.vp, st));
+  if (!pinv_done) BT_TRY(run_pinv(s.gram[go0], s.gram[go1], R, s.vp, st));
   const int64_t parts = bt_cdiv(rows, SOLVE_ROWS);
   double* gp = ws + pl.off_gp;
   double* ip = ws + pl.off_ip;
@@ -1976,6 +2225,10 @@ struct bt_cp_state {
   const double* X;
   double* F[3];
   double* lam;
+  // single-GPU driver only: the R x R pinv of mode k depends only on the
+  // other modes' Grams, so it runs on `side` while mode k's MTTKRP runs on st
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 static int64_t cp_total_ws(const Plan& pl) { return pl.total + 16; }
@@ -2039,6 +2292,12 @@ extern "C" int bt_cp_state_create(const bt_cp_problem* pb, double* a, double* b,
 extern "C" int bt_cp_state_destroy(void* state) {
   auto* S = static_cast<bt_cp_state*>(state);
   if (!S) return BT_OK;
+  if (S->ev_fork) cudaEventDestroy(S->ev_fork);
+  if (S->ev_join) cudaEventDestroy(S->ev_join);
+  if (S->side) {
+    cudaStreamSynchronize(S->side);
+    cudaStreamDestroy(S->side);
+  }
   cudaFreeAsync(S->dhist, S->st);
   delete S;
   return BT_OK;
@@ -2168,14 +2427,35 @@ extern "C" int bt_cp_mttkrp(void* state, int mode, double* out) {
 
 // Local solve of `mode` from the (summed) MTTKRP m: gbuf = [F_un^T F_un, <F_un, M>, 0].
 // For mode 3 (row-sharded) gbuf must be summed across ranks before finish.
-extern "C" int bt_cp_solve(void* state, int mode, const double* m, double* gbuf) {
-  auto* S = static_cast<bt_cp_state*>(state);
+static int cp_solve_impl(bt_cp_state* S, int mode, const double* m, double* gbuf, bool pinv_done) {
   const Plan& pl = S->pl;
   const int k = mode - 1;
   const int64_t rows[3] = {pl.I, pl.J, pl.K};
   const int go0 = (k == 0) ? 1 : 0, go1 = (k == 2) ? 1 : 2;
   return run_solve_rows(pl, S->s, S->ws, m, 1, 0, pl.R, rows[k], go0, go1, S->F[k], k == 2, gbuf,
-                        S->st);
+                        S->st, pinv_done);
+}
+
+extern "C" int bt_cp_solve(void* state, int mode, const double* m, double* gbuf) {
+  return cp_solve_impl(static_cast<bt_cp_state*>(state), mode, m, gbuf, false);
+}
+
+// fork mode `mode`'s pinv(G_o0 o G_o1) onto the side stream (joined by
+// cp_pinv_join before the solve)
+static int cp_pinv_fork(bt_cp_state* S, int mode, int warm) {
+  const int k = mode - 1;
+  const int go0 = (k == 0) ? 1 : 0, go1 = (k == 2) ? 1 : 2;
+  BT_CUDA_CHECK(cudaEventRecord(S->ev_fork, S->st));
+  BT_CUDA_CHECK(cudaStreamWaitEvent(S->side, S->ev_fork, 0));
+  BT_TRY(run_pinv(S->s.gram[go0], S->s.gram[go1], static_cast<int>(S->pl.R), S->s.vp, S->side,
+                  S->ws + S->pl.off_jstore + k * 256, warm));
+  BT_CUDA_CHECK(cudaEventRecord(S->ev_join, S->side));
+  return BT_OK;
+}
+
+static int cp_pinv_join(bt_cp_state* S) {
+  BT_CUDA_CHECK(cudaStreamWaitEvent(S->st, S->ev_join, 0));
+  return BT_OK;
 }
 
 extern "C" int bt_cp_solve_finish(void* state, int mode, int it, const double* gbuf) {
@@ -2353,22 +2633,37 @@ extern "C" int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, doub
   int it = 0, conv = 0;
   // one ALS sweep; ix < 0: the kernels take the sweep index from the device
   // counter (graph replay), which the sweep then advances
+  // the pinv of each mode overlaps that mode's MTTKRP (side stream; joined
+  // before the solve).  With per-phase events requested it stays inline so
+  // the phase times keep their meaning.
+  const bool overlap = phase_ms == nullptr;
+  if (overlap) {
+    if (cudaStreamCreateWithFlags(&S->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&S->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&S->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      bt_set_error("cp_als: cannot create the pinv side stream");
+      bt_cp_state_destroy(h);
+      return BT_E_CUDA;
+    }
+  }
+  // sweep 1 (eager) factors each mode's V cold; later sweeps (and the graph
+  // captured from sweep 2) warm-start from the stored rotation
+  int warm = 0;
+  auto mode_step = [&](int mode, double* mbuf, int ix) -> int {
+    BT_TRY(mark());
+    if (overlap) BT_TRY(cp_pinv_fork(S, mode, warm));
+    BT_TRY(bt_cp_mttkrp(h, mode, mbuf));
+    BT_TRY(mark());
+    if (overlap) BT_TRY(cp_pinv_join(S));
+    BT_TRY(cp_solve_impl(S, mode, mbuf, gbuf, overlap));
+    BT_TRY(bt_cp_solve_finish(h, mode, ix, gbuf));
+    return BT_OK;
+  };
   auto sweep = [&](int ix) -> int {
-    BT_TRY(mark());
-    BT_TRY(bt_cp_mttkrp(h, 1, m1));
-    BT_TRY(mark());
-    BT_TRY(bt_cp_solve(h, 1, m1, gbuf));
-    BT_TRY(bt_cp_solve_finish(h, 1, ix, gbuf));
-    BT_TRY(mark());
-    BT_TRY(bt_cp_mttkrp(h, 2, m2));
-    BT_TRY(mark());
-    BT_TRY(bt_cp_solve(h, 2, m2, gbuf));
-    BT_TRY(bt_cp_solve_finish(h, 2, ix, gbuf));
-    BT_TRY(mark());
-    BT_TRY(bt_cp_mttkrp(h, 3, m3));
-    BT_TRY(mark());
-    BT_TRY(bt_cp_solve(h, 3, m3, gbuf));
-    BT_TRY(bt_cp_solve_finish(h, 3, ix, gbuf));
+    BT_TRY(mode_step(1, m1, ix));
+    BT_TRY(mode_step(2, m2, ix));
+    BT_TRY(mode_step(3, m3, ix));
+    warm = 1;
     BT_TRY(bt_cp_residual(h, res2));
     BT_TRY(bt_cp_residual_finish(h, ix, res2));
     BT_TRY(mark());
@@ -2517,4 +2812,11 @@ extern "C" int bt_debug_jacobi_sweeps(void) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(&v, g_jacobi_sweeps, sizeof(int));
   return v;
+}
+
+extern "C" int64_t bt_debug_pinv1s(int which) {
+  long long v[2] = {-1, -1};
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(v, g_pinv1s_dbg, sizeof(v));
+  return v[which & 1];
 }

@@ -32,4 +32,9 @@ for R in (8, 16, 64):
         torch.cuda.synchronize()
         v = (v + v.T) / 2
         err = np.abs(out.cpu().numpy() - np.linalg.pinv(v)).max() / np.abs(np.linalg.pinv(v)).max()
-        print(f"R={R:3d} {name:9s} {e0.elapsed_time(e1) * 10:.1f} us/launch  err {err:.1e}")
+        import ctypes
+        lib = N.load()
+        lib.bt_debug_pinv1s.restype = ctypes.c_int64
+        sw, cyc = lib.bt_debug_pinv1s(0), lib.bt_debug_pinv1s(1)
+        print(f"R={R:3d} {name:9s} {e0.elapsed_time(e1) * 10:.1f} us/launch  err {err:.1e}  "
+              f"(1-sided: {sw} sweeps, {cyc} cycles)")
