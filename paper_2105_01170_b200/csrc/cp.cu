@@ -718,10 +718,12 @@ __device__ void pinv_block(const double* __restrict__ g0, const double* __restri
 // meeting r); the two lanes of a pair swap their halves by shuffles, form
 // ||w_p||^2, ||w_q||^2, w_p . w_q (row halves added in a fixed order, so both
 // lanes get the same bits), and apply the same rotation -- no shared memory,
-// no barrier, no data-dependent register index.  At convergence the columns
-// of W are orthogonal: sigma_k = ||W_k|| are V's singular values and
-// pinv(V) = sum_{sigma_k > 1e-15 sigma_max} J_k (W_k / sigma_k^2)^T, numpy's
-// SVD pinv cutoff (decomp.py:387) with the sign of each eigenvalue kept.
+// no barrier, no data-dependent register index.  The rotation is the
+// one-sided one (it orthogonalises W = V J, i.e. diagonalises J^T V^2 J, whose
+// eigenvectors are V's); the stopping rule and the pinv are the two-sided
+// eigen path's: rotate while |(J^T V J)_pq| > 1e-15 ||V||_F, then
+// pinv(V) = sum_{|lambda_k| > 1e-15 max|lambda|} J_k J_k^T / lambda_k with
+// lambda_k = (J^T V J)_kk (numpy's rcond cutoff, decomp.py:387).
 __device__ long long g_pinv1s_dbg[2];  // sweeps, cycles of the last call (diagnostics)
 
 // Warm start (jstore != nullptr, warm != 0): W = V J_prev, J = J_prev with
@@ -813,11 +815,18 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
         for (int r = 0; r < R; ++r) in1 += fabs(ws[r][lane]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) in1 = fmax(in1, __shfl_xor_sync(0xffffffffu, in1, o));
-      if (vn1 * in1 <= 1e12) return;   // vp holds V^-1 (== pinv)
+      if (vn1 * in1 <= 1e12) {
+        // vp holds V^-1 (== pinv).  No rotation was formed: mark the stored
+        // one stale so the next warm call of this mode starts cold
+        if (jstore != nullptr && lane == 0) jstore[0] = __longlong_as_double(0x7ff8dead0000dead);
+        return;
+      }
     }
     __syncwarp();
   }
-  if (jstore != nullptr && warm) {
+  // a stale store (the previous call took the Cholesky path) or a non-finite
+  // one falls back to the cold start
+  if (jstore != nullptr && warm && isfinite(jstore[0])) {
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) {
       ws[r0 + i][col] = w[i];                       // V (symmetric)
@@ -836,13 +845,14 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
   // ||V||_F^2: each element counted once (lanes hold disjoint pieces)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  // columns below 1e-15 ||V||_F sit at numpy's cutoff (1e-15 sigma_max,
-  // sigma_max >= ||V||_F / sqrt(R)) or below it: their mutual orthogonality
-  // is rounding noise and their rotation against a large column is below
-  // eps, so pairs involving one are not rotated (else near-null spaces keep
-  // the sweeps going on noise)
-  const double floor_norm = 1e-15 * sqrt(ss);
-  const double floor2 = floor_norm * floor_norm;
+  // columns below 1e-14 ||V||_F lie within ~10x of numpy's cutoff (1e-15
+  // sigma_max, sigma_max >= ||V||_F / sqrt(R)): their directions are rounding
+  // noise of V (known to ~eps ||V||_F), so pairs involving one are not
+  // rotated (else near-null spaces keep the sweeps going on noise)
+  // stopping rule of the two-sided eigen path (pinv_block): a pair is rotated
+  // while its entry of J^T V J (= J_p . W_q) exceeds 1e-15 ||V||_F -- V is
+  // known only to ~eps ||V||_F, so smaller off-diagonals are noise
+  const double abs_tol = 1e-15 * sqrt(ss);
   // sum over the HALVES row blocks of a column in a fixed order (block 0
   // first), identical in every lane holding that column
   auto colsum = [&](double v) {
@@ -877,21 +887,24 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
         pj[i] = __shfl_sync(0xffffffffu, jv[i], src);
       }
       const bool lo = col < partner;
-      double a = 0.0, b = 0.0, g = 0.0;
+      double a = 0.0, b = 0.0, g = 0.0, e = 0.0;
 #pragma unroll
       for (int i = 0; i < ROWS; ++i) {
         const double wp = lo ? w[i] : pw[i], wq = lo ? pw[i] : w[i];
+        const double jp = lo ? jv[i] : pj[i];
         a = fma(wp, wp, a);
         b = fma(wq, wq, b);
         g = fma(wp, wq, g);
+        e = fma(jp, wq, e);          // (J^T V J)_pq
       }
       a = colsum(a);
       b = colsum(b);
       g = colsum(g);
+      e = colsum(e);
       // rotate unless the pair is orthogonal to working precision
       // (|g| <= 1e-15 sqrt(a b), compared squared: no IEEE sqrt on the
       // round's critical path) or a column is below the noise floor
-      if (g * g > 1e-30 * (a * b) && fmin(a, b) > floor2) {
+      if (g != 0.0 && fabs(e) > abs_tol) {
         double c, s;
         jacobi_rotation(a, b, g, c, s);
         rotated = 1;
@@ -913,26 +926,27 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
     g_pinv1s_dbg[0] = sweeps_done;
     g_pinv1s_dbg[1] = clock64() - t_start;
   }
-  // sigma_k = ||W_k||; numpy cutoff 1e-15 * sigma_max
-  double n2 = 0.0;
+  // eigenvalues lambda_k = J_k . W_k = (J^T V J)_kk; pinv = sum over
+  // |lambda_k| > 1e-15 max |lambda| of J_k J_k^T / lambda_k -- the cutoff and
+  // formula of pinv_from_eig (numpy's rcond on the singular values |lambda|)
+  double lk = 0.0;
 #pragma unroll
-  for (int i = 0; i < ROWS; ++i) n2 = fma(w[i], w[i], n2);
-  const double sig = sqrt(colsum(n2));
-  double smax = sig;
+  for (int i = 0; i < ROWS; ++i) lk = fma(jv[i], w[i], lk);
+  lk = colsum(lk);
+  double lmax = fabs(lk);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
-  if (half == 0) isg[col] = (sig > 1e-15 * smax) ? 1.0 / (sig * sig) : 0.0;
+  for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+  if (half == 0) isg[col] = (fabs(lk) > 1e-15 * lmax) ? 1.0 / lk : 0.0;
 #pragma unroll
   for (int i = 0; i < ROWS; ++i) {
     js[r0 + i][col] = jv[i];
-    ws[r0 + i][col] = w[i];
     if (jstore != nullptr) jstore[(r0 + i) * NP + col] = jv[i];
   }
   __syncwarp();
   for (int idx = lane; idx < R * R; idx += 32) {
     const int r = idx / R, c = idx % R;
     double v = 0.0;
-    for (int k = 0; k < NP; ++k) v = fma(js[r][k] * isg[k], ws[c][k], v);
+    for (int k = 0; k < NP; ++k) v = fma(js[r][k] * isg[k], js[c][k], v);
     vp[idx] = v;
   }
 }
