@@ -779,13 +779,15 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
       hi = fmax(hi, lkk);
       __syncwarp();
       if (lane > k && lane < R) ws[lane][k] *= rl;
-      if (lane == 0) ws[k][k] = lkk;
+      if (lane == 0) {
+        ws[k][k] = lkk;
+        isg[k] = rl;  // 1 / l_kk for the substitution below
+      }
       __syncwarp();
-      // trailing lower triangle j <= i, i, j > k
-      const int m = R - 1 - k;
-      for (int idx = lane; idx < m * m; idx += 32) {
-        const int i = k + 1 + idx / m, j = k + 1 + idx % m;
-        if (j <= i) ws[i][j] -= ws[i][k] * ws[j][k];
+      // trailing lower triangle j <= i, i, j > k: one row per lane
+      if (lane > k && lane < R) {
+        const double lik = ws[lane][k];
+        for (int j = k + 1; j <= lane; ++j) ws[lane][j] -= lik * ws[j][k];
       }
       __syncwarp();
     }
@@ -797,7 +799,7 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
         for (int i = 0; i < R; ++i) {
           double acc = (i == lane) ? 1.0 : 0.0;
           for (int k = lane; k < i; ++k) acc -= ws[i][k] * js[k][lane];
-          js[i][lane] = (i < lane) ? 0.0 : acc / ws[i][i];
+          js[i][lane] = (i < lane) ? 0.0 : acc * isg[i];
         }
       }
       __syncwarp();
@@ -1036,32 +1038,36 @@ __device__ bool pinv_warp_chol(const double* __restrict__ g0, const double* __re
     for (int r = 0; r < R; ++r) cs += fabs(a[r * ld + lane]);
   double vn1 = cs;
   for (int o = 16; o > 0; o >>= 1) vn1 = fmax(vn1, __shfl_xor_sync(0xffffffffu, vn1, o));
-  // in place: lower triangle -> L
+  // in place: lower triangle -> L; the diagonal's reciprocals go to y's
+  // diagonal slots (Newton-refined rsqrt: no IEEE sqrt / division on the
+  // critical path -- this warp runs beside 15 DMMA warps)
   for (int k = 0; k < R; ++k) {
     const double d = a[k * ld + k];
     if (!(d > 0.0)) return false;  // same d in every lane
-    const double lk = sqrt(d);
+    const double rl = rsqrt_nr(d);
     __syncwarp();
-    for (int i = k + 1 + lane; i < R; i += 32) a[i * ld + k] /= lk;
-    if (lane == 0) a[k * ld + k] = lk;
+    for (int i = k + 1 + lane; i < R; i += 32) a[i * ld + k] *= rl;
+    if (lane == 0) {
+      a[k * ld + k] = d * rl;
+      y[k * ld + k] = rl;       // 1 / l_kk
+    }
     __syncwarp();
-    const int t = R - k - 1;
-    for (int e = lane; e < t * t; e += 32) {
-      const int ii = e / t, jj = e - ii * t;
-      if (jj <= ii)
-        a[(k + 1 + ii) * ld + k + 1 + jj] -= a[(k + 1 + ii) * ld + k] * a[(k + 1 + jj) * ld + k];
+    // trailing update, one row per lane (R <= 32: no index division)
+    for (int i = k + 1 + lane; i < R; i += 32) {
+      const double lik = a[i * ld + k];
+      for (int j = k + 1; j <= i; ++j) a[i * ld + j] -= lik * a[j * ld + k];
     }
     __syncwarp();
   }
-  // Y = L^-1, one column per lane
+  // Y = L^-1, one column per lane (reciprocal diagonal from the factorisation)
+  __syncwarp();
   if (lane < R) {
     const int c = lane;
     for (int i = 0; i < c; ++i) y[i * ld + c] = 0.0;
-    y[c * ld + c] = 1.0 / a[c * ld + c];
     for (int i = c + 1; i < R; ++i) {
       double sacc = 0.0;
       for (int k = c; k < i; ++k) sacc = fma(a[i * ld + k], y[k * ld + c], sacc);
-      y[i * ld + c] = -sacc / a[i * ld + i];
+      y[i * ld + c] = -sacc * y[i * ld + i];
     }
   }
   __syncwarp();
