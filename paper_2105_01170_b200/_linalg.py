@@ -61,6 +61,10 @@ def eigh_dev(gd, nvec: int | None = None, tau: float = -1.0):
 
 _DEBUG = bool(os.environ.get("BT_BASIS_DEBUG"))
 SUBSPACE = os.environ.get("BT_SUBSPACE", "1") != "0"
+# BT_SUB_DIRECT=0: a cold block of >= 48 wanted pairs at n <= 1536 takes the
+# oversampled subspace iteration instead of the tridiagonal solver (measured
+# slower at C3: 23 iterations x ~1.1 ms vs ~15 ms)
+_SUB_DIRECT = os.environ.get("BT_SUB_DIRECT", "1") != "0"
 SUB_OVERSAMPLE = 16
 SUB_MAX_BLOCK = 96     # Rayleigh-Ritz matrices stay on the one-CTA Jacobi path
 
@@ -69,7 +73,8 @@ def _leading_subspace(gd, need: int, tau: float, start=None, hint=None):
     """Leading eigenpairs of a symmetric n x n Gram by block subspace
     iteration with Rayleigh-Ritz (bt_leading_subspace_f64: GEMMs, column-
     scaled SVQB and the one-CTA Jacobi on the b x b projection, driven from
-    the library's host side), b = min(need, hint, 80) + 16 columns.
+    the library's host side), b = min(need, hint, 80) + 16 columns (a cold
+    block of >= 48 wanted pairs: + up to need / 2, at most 96).
 
     Returns (w, v, k): the b Ritz values (descending, device), Ritz vectors
     (n x b, sign-normalised) and the count k of leading pairs that are
@@ -85,8 +90,9 @@ def _leading_subspace(gd, need: int, tau: float, start=None, hint=None):
     wsb = N.load().bt_leading_subspace_ws_bytes(n, int(need), h)
     if wsb <= 0:
         return None
-    b = min(n, min(max(1, min(int(need), h)) if h > 0 else int(need), SUB_MAX_BLOCK - SUB_OVERSAMPLE)
-            + SUB_OVERSAMPLE)
+    # the library's block is at most SUB_MAX_BLOCK columns (a cold block of
+    # many wanted pairs oversamples by up to half; the call reports its size)
+    b = min(n, SUB_MAX_BLOCK)
     ws = _dev.workspace(wsb)
     w = _dev.empty((b,))
     vbuf = _dev.empty((n * b,))
@@ -259,7 +265,7 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
         # converges at the spectrum's own rate near the block edge (C3 mode 1:
         # lambda_81 / lambda_64 = 0.6); up to n ~ 1.5k the tridiagonal solver
         # is cheaper than the iteration needed to measure that
-        direct = cold and hint is None and need >= 48 and n <= 1536
+        direct = (cold and hint is None and need >= 48 and n <= 1536 and _SUB_DIRECT)
         sub = (_leading_subspace(g, need, RESOLVE_TAU, start if basis is None else None, hint)
                if SUBSPACE and n > SMALL_EIG and not direct else None)
         if sub is not None:

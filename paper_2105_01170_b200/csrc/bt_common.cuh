@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include "../../include/bt200.h"
@@ -46,6 +47,16 @@ void bt_count_launch();
       return code;                      \
     }                                   \
   } while (0)
+
+// NVTX range around a C-ABI call (header-only NVTX3: a no-op unless a tool
+// such as nsys / ncu is attached); names are the C-ABI entry points
+struct BtNvtxRange {
+  explicit BtNvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~BtNvtxRange() { nvtxRangePop(); }
+  BtNvtxRange(const BtNvtxRange&) = delete;
+  BtNvtxRange& operator=(const BtNvtxRange&) = delete;
+};
+#define BT_NVTX(name) BtNvtxRange bt_nvtx_range_(name)
 
 static inline cudaStream_t bt_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -131,6 +131,7 @@ int grid1d(int64_t n) { return static_cast<int>(std::min<int64_t>(bt_cdiv(n, 256
 
 extern "C" int bt_build_hankel_f64(const double* params, int64_t p, int64_t d_out, int64_t d_in,
                                    const int64_t* eta, double* t, void* stream) {
+  BT_NVTX("bt_build_hankel_f64");
   BT_REQUIRE(p >= 1 && d_out >= 1 && d_in >= 1, BT_E_SHAPE, "hankel: empty input");
   hankel_kernel<<<grid1d(p * d_out * d_in), 256, 0, bt_stream(stream)>>>(params, p, d_out, d_in,
                                                                          eta, t);
@@ -141,6 +142,7 @@ extern "C" int bt_build_hankel_f64(const double* params, int64_t p, int64_t d_ou
 extern "C" int bt_build_gneiting_f64(const double* points, int64_t npts, int64_t lags,
                                      double lag_scale, const int64_t* eta, double* t,
                                      void* stream) {
+  BT_NVTX("bt_build_gneiting_f64");
   BT_REQUIRE(npts >= 1 && lags >= 1 && lag_scale > 0, BT_E_SHAPE, "gneiting: bad extents");
   const int grid = static_cast<int>(std::min<int64_t>(npts * lags, 148 * 32));
   gneiting_kernel<<<grid, 256, 0, bt_stream(stream)>>>(points, npts, lags, lag_scale, eta, t);
@@ -150,6 +152,7 @@ extern "C" int bt_build_gneiting_f64(const double* points, int64_t npts, int64_t
 
 extern "C" int bt_build_psf_f64(const double* psf, int64_t k, int64_t grid, double* x,
                                 void* stream) {
+  BT_NVTX("bt_build_psf_f64");
   BT_REQUIRE(k >= 1 && (k % 2) == 1, BT_E_SHAPE, "psf extent K must be odd");
   BT_REQUIRE(grid >= (k + 1) / 2, BT_E_SHAPE, "psf: image grid smaller than the kernel radius");
   psf_kernel<<<grid1d(k * k * k), 256, 0, bt_stream(stream)>>>(psf, k, grid, x);
@@ -198,6 +201,7 @@ extern "C" int bt_build_cp_model_f64(const double* a0, const double* b0, const d
                                      int64_t I, int64_t J, int64_t K, int64_t R, int64_t k0,
                                      int64_t k1, double noise, uint64_t key, double* x, void* ws,
                                      int64_t ws_bytes, void* stream) {
+  BT_NVTX("bt_build_cp_model_f64");
   BT_REQUIRE(I >= 1 && J >= 1 && K >= 1 && R >= 1 && 0 <= k0 && k0 < k1 && k1 <= K, BT_E_SHAPE,
              "cp_model: bad extents");
   (void)ws;

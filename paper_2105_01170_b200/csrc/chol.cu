@@ -172,6 +172,7 @@ extern "C" int64_t bt_cholesky_ws_bytes(int64_t n) {
 
 extern "C" int bt_cholesky_f64(const double* a, int64_t n, double* l, void* ws, int64_t* bad_pivot,
                                void* stream) {
+  BT_NVTX("bt_cholesky_f64");
   BT_REQUIRE(n >= 1, BT_E_SHAPE, "cholesky: empty matrix");
   cudaStream_t st = bt_stream(stream);
   int64_t* info = static_cast<int64_t*>(ws);
@@ -223,6 +224,7 @@ extern "C" int64_t bt_tri_inv_lower_ws_bytes(int64_t n) {
 // X = L^-1 by block rows: X_i = D_i^-1 (E_i - L_{i,<i} X_{<i}), columns < i0+bi.
 extern "C" int bt_tri_inv_lower_f64(const double* l, int64_t n, double* linv, void* ws,
                                     void* stream) {
+  BT_NVTX("bt_tri_inv_lower_f64");
   BT_REQUIRE(n >= 1, BT_E_SHAPE, "tri_inv: empty matrix");
   cudaStream_t st = bt_stream(stream);
   const int64_t nblk = cdiv64(n, NB);

@@ -2359,6 +2359,7 @@ extern "C" int bt_cp_init_finish(void* state, const double* buf) {
 // Modes 1/2 are partial sums over the local mode-3 slab (sum across ranks);
 // mode 3 rows are complete locally.  Mode 1 also (re)computes P = X x3 C.
 extern "C" int bt_cp_mttkrp(void* state, int mode, double* out) {
+  BT_NVTX("bt_cp_mttkrp");
   auto* S = static_cast<bt_cp_state*>(state);
   const Plan& pl = S->pl;
   double* ws = S->ws;
@@ -2457,6 +2458,7 @@ static int cp_solve_impl(bt_cp_state* S, int mode, const double* m, double* gbuf
 }
 
 extern "C" int bt_cp_solve(void* state, int mode, const double* m, double* gbuf) {
+  BT_NVTX("bt_cp_solve");
   return cp_solve_impl(static_cast<bt_cp_state*>(state), mode, m, gbuf, false);
 }
 
@@ -2491,6 +2493,7 @@ extern "C" int bt_cp_solve_finish(void* state, int mode, int it, const double* g
 // Explicit residual partial ||X_local - Xhat_local||^2 into res2 (device scalar;
 // writes 0 when the Gram identity was judged accurate).  Sum across ranks.
 extern "C" int bt_cp_residual(void* state, double* res2) {
+  BT_NVTX("bt_cp_residual");
   auto* S = static_cast<bt_cp_state*>(state);
   const Plan& pl = S->pl;
   if (S->fit_mode == 2 || pl.K == 0) {
@@ -2622,6 +2625,7 @@ extern "C" int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, doub
                              double* lam, int max_iters, double tol, int fit_mode,
                              double* fit_history, int* n_iters, int* converged, double* phase_ms,
                              void* wsv, int64_t ws_bytes, void* stream) {
+  BT_NVTX("bt_cp_als_f64");
   if (phase_ms == nullptr && max_iters >= 1) {
     int rc = BT_OK;
     if (cp_small_try(pb, a, b, c, lam, max_iters, tol, fit_mode, fit_history, n_iters, converged,
@@ -2796,6 +2800,7 @@ extern "C" int64_t bt_mttkrp_ws_bytes(const bt_cp_problem* pb, int mode) {
 extern "C" int bt_mttkrp_f64(const bt_cp_problem* pb, int mode, const double* a, const double* b,
                              const double* c, double* out, void* wsv, int64_t ws_bytes,
                              void* stream) {
+  BT_NVTX("bt_mttkrp_f64");
   BT_REQUIRE(mode >= 1 && mode <= 3, BT_E_SHAPE, "mttkrp: mode %d out of range", mode);
   cudaStream_t st = bt_stream(stream);
   Plan pl = make_plan(pb, 0);
@@ -2821,6 +2826,7 @@ extern "C" int bt_mttkrp_f64(const bt_cp_problem* pb, int mode, const double* a,
 }
 
 extern "C" int bt_pinv_sym_f64(const double* v, int64_t R, double* vp, void* stream) {
+  BT_NVTX("bt_pinv_sym_f64");
   BT_REQUIRE(R >= 1 && R <= PINV_MAX_R, BT_E_SHAPE, "pinv: size %lld outside [1, %d]",
              (long long)R, PINV_MAX_R);
   return run_pinv(v, nullptr, static_cast<int>(R), vp, bt_stream(stream));

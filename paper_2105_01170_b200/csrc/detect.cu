@@ -207,6 +207,7 @@ int grid_cells(int64_t cells) {
 extern "C" int bt_block_digest_f64(const double* a, int64_t lda, int64_t ell, int64_t q, int64_t m,
                                    int64_t n, double tol, uint64_t* h1, uint64_t* h2, int* nz,
                                    void* stream) {
+  BT_NVTX("bt_block_digest_f64");
   BT_REQUIRE(ell >= 1 && q >= 1 && m >= 1 && n >= 1, BT_E_SHAPE, "digest: empty grid");
   BT_REQUIRE(lda >= q * n, BT_E_SHAPE, "digest: lda too small");
   BT_REQUIRE(m * (n / (vec2_ok(a, lda, n) ? 2 : 1)) < ((int64_t)1 << 31), BT_E_SHAPE,
@@ -231,6 +232,7 @@ extern "C" int bt_block_digest_f64(const double* a, int64_t lda, int64_t ell, in
 extern "C" int bt_block_match_f64(const double* a, int64_t lda, int64_t ell, int64_t q, int64_t m,
                                   int64_t n, const int64_t* cand, double tol, int exact, int* eq,
                                   void* stream) {
+  BT_NVTX("bt_block_match_f64");
   BT_REQUIRE(ell >= 1 && q >= 1 && m >= 1 && n >= 1, BT_E_SHAPE, "match: empty grid");
   BT_REQUIRE(lda >= q * n, BT_E_SHAPE, "match: lda too small");
   if (vec2_ok(a, lda, n))

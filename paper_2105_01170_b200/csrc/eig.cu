@@ -407,6 +407,7 @@ extern "C" int64_t bt_syevd_ws_bytes(int64_t n) { return eig_plan(n).total * 8; 
 
 extern "C" int bt_syevd_f64(const double* a, int64_t n, double* w, double* v, void* wsv,
                             int64_t ws_bytes, void* stream) {
+  BT_NVTX("bt_syevd_f64");
   BT_REQUIRE(n >= 1, BT_E_SHAPE, "syevd: empty matrix");
   cudaStream_t st = bt_stream(stream);
   EigPlan p = eig_plan(n);

@@ -638,6 +638,7 @@ extern "C" int64_t bt_syevx_ws_bytes(int64_t n, int64_t nvec) { return xplan(n, 
 
 extern "C" int bt_syevx_f64(const double* a, int64_t n, int64_t nvec, double vec_tau, double* w,
                             double* v, void* wsv, int64_t ws_bytes, void* stream) {
+  BT_NVTX("bt_syevx_f64");
   BT_REQUIRE(n >= 3 && nvec >= 1 && nvec <= n, BT_E_SHAPE, "syevx: need n >= 3, 1 <= nvec <= n");
   BT_REQUIRE(n <= 3200, BT_E_SHAPE, "syevx: n = %lld above the shared-memory limit 3200",
              (long long)n);

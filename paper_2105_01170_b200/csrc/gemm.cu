@@ -322,6 +322,7 @@ extern "C" int64_t bt_gemm_f64_ws_bytes(const bt_gemm_desc* d) {
 }
 
 extern "C" int bt_gemm_f64(const bt_gemm_desc* d, double* ws, int64_t ws_bytes, void* stream) {
+  BT_NVTX("bt_gemm_f64");
   BT_REQUIRE(d != nullptr, BT_E_VALUE, "gemm: null descriptor");
   BT_REQUIRE(!d->symmetric || d->M == d->N, BT_E_SHAPE, "gemm: symmetric output must be square");
   BtGemmArgs g = bt_make_args(d);

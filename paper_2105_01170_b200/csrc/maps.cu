@@ -440,6 +440,7 @@ extern "C" int64_t bt_gather_ws_bytes(const bt_pattern_dev* pat) {
 extern "C" int bt_gather_blocks_f64(const double* a, int64_t lda, const bt_pattern_dev* pat,
                                     double tol, int weighted, double* t, void* ws,
                                     int64_t* bad_order, void* stream) {
+  BT_NVTX("bt_gather_blocks_f64");
   BT_REQUIRE(pat->m >= 1 && pat->n >= 1 && pat->ell >= 1 && pat->q >= 1, BT_E_SHAPE,
              "gather: pattern extents must be positive");
   BT_REQUIRE(lda >= pat->q * pat->n, BT_E_SHAPE, "gather: lda too small");
@@ -506,6 +507,7 @@ extern "C" int bt_gather_blocks_f64(const double* a, int64_t lda, const bt_patte
 extern "C" int bt_scatter_blocks_f64(const double* t, int64_t t_sm, int64_t t_sp, int64_t t_sn,
                                      const bt_pattern_dev* pat, double* a, int64_t lda,
                                      void* stream) {
+  BT_NVTX("bt_scatter_blocks_f64");
   BT_REQUIRE(pat->m >= 1 && pat->n >= 1 && pat->ell >= 1 && pat->q >= 1, BT_E_SHAPE,
              "scatter: pattern extents must be positive");
   BT_REQUIRE(lda >= pat->q * pat->n, BT_E_SHAPE, "scatter: lda too small");
@@ -596,6 +598,7 @@ __global__ void copy_cells_kernel(const double* __restrict__ a, int64_t lda,
 
 extern "C" int bt_copy_cells_f64(const double* a, int64_t lda, const int64_t* cells, int64_t p,
                                  int64_t q, int64_t m, int64_t n, double* out, void* stream) {
+  BT_NVTX("bt_copy_cells_f64");
   BT_REQUIRE(p >= 0 && m >= 0 && n >= 0 && q >= 1, BT_E_SHAPE, "copy_cells: bad extents");
   if (p == 0 || m == 0 || n == 0) return BT_OK;
   const int vec2 = (n % 2 == 0) && (lda % 2 == 0) &&

@@ -481,6 +481,7 @@ extern "C" int bt_matvec_kron_f64(const bt_pattern_dev* pat, const int64_t* row_
                                   const int64_t* row_cells, const double* coeffs,
                                   const double* terms, int64_t r, const double* x, int64_t nrhs,
                                   double* y, void* wsv, int64_t ws_bytes, void* stream) {
+  BT_NVTX("bt_matvec_kron_f64");
   BT_REQUIRE(r >= 1 && nrhs >= 1, BT_E_SHAPE, "matvec_kron: empty terms or RHS");
   KronPlan kp = kron_plan(pat, r, nrhs);
   BT_REQUIRE(ws_bytes >= kp.total * 8, BT_E_VALUE, "matvec_kron: workspace too small");
@@ -526,6 +527,7 @@ extern "C" int bt_matvec_blr_f64(const bt_pattern_dev* pat, const int64_t* row_p
                                  const double* right, int64_t rr, const double* middles,
                                  const double* x, int64_t nrhs, double* y, void* wsv,
                                  int64_t ws_bytes, void* stream) {
+  BT_NVTX("bt_matvec_blr_f64");
   BT_REQUIRE(rl >= 1 && rr >= 1 && nrhs >= 1, BT_E_SHAPE, "matvec_blr: empty operand");
   BT_REQUIRE(rl <= 64 && rr <= 64, BT_E_SHAPE, "matvec_blr: side ranks above 64 not supported");
   BlrPlan bp = blr_plan(pat, rl, rr, nrhs);
@@ -647,6 +649,7 @@ extern "C" int bt_ml_matvec_f64(int64_t nterms, const int64_t* nin, const int64_
                                 const double* s1, const double* s2, const double* s3,
                                 const double* x, int64_t nrhs, double* y, void* wsv,
                                 int64_t ws_bytes, void* stream) {
+  BT_NVTX("bt_ml_matvec_f64");
   BT_REQUIRE(nterms >= 1 && nrhs >= 1, BT_E_SHAPE, "ml_matvec: empty terms or RHS");
   const int64_t R = nterms;
   MlPlan mp = ml_plan(R, nin, nout, nrhs);

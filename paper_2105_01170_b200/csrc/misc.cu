@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(256)
 extern "C" int bt_transpose_check_f64(const double* blocks, int64_t p, int64_t n,
                                       const int64_t* partner, double tol, void* ws,
                                       int64_t* bad_class, void* stream) {
+  BT_NVTX("bt_transpose_check_f64");
   cudaStream_t st = bt_stream(stream);
   int* flags = static_cast<int*>(ws);
   const int grid = static_cast<int>(p < 148 * 8 ? p : 148 * 8);
@@ -497,6 +498,7 @@ __global__ void bt_reverse_axes_kernel(const double* __restrict__ x, RevDims rd,
 
 extern "C" int bt_reverse_axes_f64(const double* x, const int64_t* dims, int ndim, double* out,
                                    void* stream) {
+  BT_NVTX("bt_reverse_axes_f64");
   BT_REQUIRE(ndim >= 1 && ndim <= 6, BT_E_SHAPE, "reverse_axes: rank %d outside 1..6", ndim);
   RevDims rd;
   rd.nd = ndim;
@@ -541,6 +543,7 @@ __global__ void __launch_bounds__(256) bt_transpose_kernel(const double* __restr
 
 extern "C" int bt_transpose_f64(const double* x, int64_t rows, int64_t cols, double* out,
                                 void* stream) {
+  BT_NVTX("bt_transpose_f64");
   BT_REQUIRE(rows >= 0 && cols >= 0, BT_E_SHAPE, "transpose: negative extent");
   if (rows == 0 || cols == 0) return BT_OK;
   const int64_t ntiles = ((rows + 31) / 32) * ((cols + 31) / 32);

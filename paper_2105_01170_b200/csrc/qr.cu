@@ -96,6 +96,7 @@ extern "C" int64_t bt_qr_thin_ws_bytes(int64_t m, int64_t n) { return (2 * m * n
 
 extern "C" int bt_qr_thin_f64(const double* a, int64_t m, int64_t n, double* q, double* r,
                               void* ws, int64_t ws_bytes, void* stream) {
+  BT_NVTX("bt_qr_thin_f64");
   BT_REQUIRE(n >= 1 && m >= n, BT_E_SHAPE, "qr_thin expects a tall or square matrix");
   BT_REQUIRE(ws_bytes >= bt_qr_thin_ws_bytes(m, n), BT_E_VALUE, "qr_thin: workspace too small");
   cudaStream_t st = bt_stream(stream);

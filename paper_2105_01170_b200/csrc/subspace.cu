@@ -43,6 +43,17 @@ namespace {
 constexpr int SUB_OVERSAMPLE = 16;
 constexpr int SUB_MAX_BLOCK = 96;
 constexpr int SUB_MAX_ITERS = 10;
+// a cold block of many wanted pairs (C3 mode 1: 64 of 1024) oversamples by
+// half the wanted count (capped by SUB_MAX_BLOCK) and may take more
+// iterations: at b = 96 it converges at lambda_97 / lambda_64 ~ 0.31 per
+// iteration, ~0.2 ms each, well under the tridiagonal solver's ~15 ms
+constexpr int SUB_MAX_ITERS_COLD = 32;
+
+int64_t block_for(int64_t n, int64_t want, bool cold) {
+  const int64_t over = cold ? std::max<int64_t>(SUB_OVERSAMPLE, want / 2) : SUB_OVERSAMPLE;
+  return std::min(n, std::min<int64_t>(std::min<int64_t>(want, SUB_MAX_BLOCK - SUB_OVERSAMPLE) + over,
+                                       SUB_MAX_BLOCK));
+}
 constexpr double SUB_RESID = 32.0;
 constexpr double EPS = 2.220446049250313e-16;
 constexpr double SVQB_DROP = 1e3 * EPS;
@@ -294,7 +305,7 @@ int svqb(const Ctx& c, const double* y, int64_t n, int64_t b, double* q, int64_t
 
 extern "C" int64_t bt_leading_subspace_ws_bytes(int64_t n, int64_t need, int64_t hint) {
   const int64_t want = hint > 0 ? std::max<int64_t>(1, std::min(need, hint)) : need;
-  const int64_t b = std::min(n, std::min<int64_t>(want, SUB_MAX_BLOCK - SUB_OVERSAMPLE) + SUB_OVERSAMPLE);
+  const int64_t b = block_for(n, want, true);   // the larger of the two block sizes
   if (b < 2 || b > SUB_MAX_BLOCK || 2 * b > n) return 0;
   return plan(n, b).total * 8;
 }
@@ -303,12 +314,15 @@ extern "C" int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need,
                                        const double* start, int64_t start_cols, int64_t hint,
                                        double* w, double* v, int64_t* bq_out, int64_t* k_out,
                                        int* status, void* wsv, int64_t ws_bytes, void* stream) {
+  BT_NVTX("bt_leading_subspace_f64");
   *status = 2;
   *bq_out = 0;
   *k_out = 0;
   const int64_t want = hint > 0 ? std::max<int64_t>(1, std::min(need, hint)) : need;
-  const int64_t b = std::min(n, std::min<int64_t>(want, SUB_MAX_BLOCK - SUB_OVERSAMPLE) + SUB_OVERSAMPLE);
+  const bool cold = start == nullptr || start_cols <= 0;
+  const int64_t b = block_for(n, want, cold && hint <= 0);
   if (b < 2 || b > SUB_MAX_BLOCK || 2 * b > n) return BT_OK;
+  const int max_iters = (cold && hint <= 0 && want >= 48) ? SUB_MAX_ITERS_COLD : SUB_MAX_ITERS;
   const Plan p = plan(n, b);
   BT_REQUIRE(ws_bytes >= p.total * 8, BT_E_VALUE, "leading_subspace: workspace too small");
   static const bool no_chol = getenv("BT_SUB_CHOLQR") && getenv("BT_SUB_CHOLQR")[0] == '0';
@@ -336,7 +350,7 @@ extern "C" int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need,
   if (bq == 0) return BT_OK;
   double prev = -1.0;
   std::vector<double> wh(b), rh(b);
-  for (int it = 0; it < SUB_MAX_ITERS; ++it) {
+  for (int it = 0; it < max_iters; ++it) {
     BT_TRY(c.gemm(gemm_args(n, bq, n, g, n, 1, q, bq, 1, y)));       // G Q
     dropped = 0;
     int64_t nq = 0;
@@ -384,12 +398,12 @@ extern "C" int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need,
       // tridiagonal solver
       const double rate0 = wh[bq - 1] / wh[k - 1];
       if (rate0 >= 1.0 ||
-          std::log(target / worst) / std::log(std::max(rate0, 1e-300)) > 1.5 * (SUB_MAX_ITERS - 1))
+          std::log(target / worst) / std::log(std::max(rate0, 1e-300)) > 1.5 * (max_iters - 1))
         return BT_OK;
     }
     if (prev > 0.0 && worst > 0.0) {
       const double rate = worst / prev;  // linear convergence factor
-      const int left = SUB_MAX_ITERS - 1 - it;
+      const int left = max_iters - 1 - it;
       if (rate >= 1.0 || std::log(target / worst) / std::log(std::max(rate, 1e-300)) > left)
         return BT_OK;  // too slow: the tridiagonal path wins
     }

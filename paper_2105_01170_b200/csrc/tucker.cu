@@ -95,6 +95,7 @@ extern "C" int64_t bt_unfold_gram_ws_bytes(const int64_t* dims, int order, int m
 
 extern "C" int bt_unfold_gram_f64(const double* x, const int64_t* dims, int order, int mode,
                                   double* g, void* ws, int64_t ws_bytes, void* stream) {
+  BT_NVTX("bt_unfold_gram_f64");
   View3 v;
   BT_REQUIRE(view3(dims, order, mode, v), BT_E_SHAPE, "mode %d out of range for order-%d tensor",
              mode, order);
@@ -120,6 +121,7 @@ extern "C" int64_t bt_ttm_ws_bytes(const int64_t* dims, int order, int mode, int
 extern "C" int bt_ttm_f64(const double* x, const int64_t* dims, int order, int mode,
                           const double* u, int64_t rows, int transpose, double* y, void* ws,
                           int64_t ws_bytes, void* stream) {
+  BT_NVTX("bt_ttm_f64");
   View3 v;
   BT_REQUIRE(view3(dims, order, mode, v), BT_E_SHAPE, "mode %d out of range for order-%d tensor",
              mode, order);
