@@ -61,10 +61,10 @@ def eigh_dev(gd, nvec: int | None = None, tau: float = -1.0):
 
 _DEBUG = bool(os.environ.get("BT_BASIS_DEBUG"))
 SUBSPACE = os.environ.get("BT_SUBSPACE", "1") != "0"
-# BT_SUB_DIRECT=0: a cold block of >= 48 wanted pairs at n <= 1536 takes the
-# oversampled subspace iteration instead of the tridiagonal solver (measured
-# slower at C3: 23 iterations x ~1.1 ms vs ~15 ms)
-_SUB_DIRECT = os.environ.get("BT_SUB_DIRECT", "1") != "0"
+# BT_SUB_DIRECT=1: a cold block of >= 48 wanted pairs at n <= 1536 goes to the
+# tridiagonal solver instead of the oversampled subspace iteration (C3 mode 1:
+# 8.1 ms subspace vs 15.9 ms tridiagonal)
+_SUB_DIRECT = os.environ.get("BT_SUB_DIRECT", "0") == "1"
 SUB_OVERSAMPLE = 16
 SUB_MAX_BLOCK = 96     # Rayleigh-Ritz matrices stay on the one-CTA Jacobi path
 
@@ -261,10 +261,11 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
         if need <= 0:
             break
         cold = start is None or basis is not None
-        # a cold block of >= 48 wanted pairs oversamples by 1/3 at most, so it
-        # converges at the spectrum's own rate near the block edge (C3 mode 1:
-        # lambda_81 / lambda_64 = 0.6); up to n ~ 1.5k the tridiagonal solver
-        # is cheaper than the iteration needed to measure that
+        # a cold block of >= 48 wanted pairs oversamples to 96 columns and
+        # runs simultaneous iteration with two G products per CholeskyQR and
+        # a Rayleigh-Ritz only at the start and the end (subspace.cu); C3 mode
+        # 1 (64 of 1024, lambda_97 / lambda_64 ~ 0.31): 28 steps, 8.1 ms
+        # against 15.9 ms for the tridiagonal solver
         direct = (cold and hint is None and need >= 48 and n <= 1536 and _SUB_DIRECT)
         sub = (_leading_subspace(g, need, RESOLVE_TAU, start if basis is None else None, hint)
                if SUBSPACE and n > SMALL_EIG and not direct else None)

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "gemm.cuh"
+#include "jacobi.cuh"  // rsqrt_nr
 
 int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, int64_t ws_elems);
 int64_t bt_gemm_ws_elems(BtGemmArgs g, int64_t batch);
@@ -48,6 +49,12 @@ constexpr int SUB_MAX_ITERS = 10;
 // iterations: at b = 96 it converges at lambda_97 / lambda_64 ~ 0.31 per
 // iteration, ~0.2 ms each, well under the tridiagonal solver's ~15 ms
 constexpr int SUB_MAX_ITERS_COLD = 32;
+
+// BT_SUB_SKIP_RR=0: a Rayleigh-Ritz every iteration for cold blocks too
+bool no_skip_rr() {
+  static const bool v = getenv("BT_SUB_SKIP_RR") && getenv("BT_SUB_SKIP_RR")[0] == '0';
+  return v;
+}
 
 int64_t block_for(int64_t n, int64_t want, bool cold) {
   const int64_t over = cold ? std::max<int64_t>(SUB_OVERSAMPLE, want / 2) : SUB_OVERSAMPLE;
@@ -94,60 +101,76 @@ __global__ void copy_cols_kernel(const double* __restrict__ src, int64_t ld_src,
 constexpr double CHOL_MIN_PIVOT = 1e-6;
 constexpr int CHOL_MAXB = 96;
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
     chol_rinv_kernel(const double* __restrict__ m, int b, double* __restrict__ rinv,
                      int* __restrict__ status) {
+  // Right-looking Cholesky and right-looking L^-1, both element-parallel per
+  // step (one CTA barrier per step; every thread's loads of a step are issued
+  // before its stores).  a: working matrix (unscaled pivot column read in the
+  // update of its step), l: L by columns, x: L^-1.
   extern __shared__ __align__(16) double chol_sm[];
   const int ld = b + 1;
-  double* a = chol_sm;       // b x ld, lower triangle -> L
-  double* x = a + b * ld;    // b x ld, L^-1
+  double* a = chol_sm;
+  double* x = a + b * ld;
+  __shared__ double rdiag[CHOL_MAXB];
   __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
-  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) bad = 0;
+  for (int e = tid; e < b * b; e += nt) {
     const int i = e / b, j = e - i * b;
-    a[(i) * ld + (j)] = m[e];
+    a[i * ld + j] = m[e];
   }
   __syncthreads();
   for (int k = 0; k < b; ++k) {
-    const double piv = a[(k) * ld + (k)];
+    const double piv = a[k * ld + k];
     if (!(piv > CHOL_MIN_PIVOT)) {
-      if (threadIdx.x == 0) bad = 1;
+      if (tid == 0) bad = 1;
       break;  // uniform: every thread read the same pivot
     }
-    const double lkk = sqrt(piv);
-    for (int i = k + 1 + threadIdx.x; i < b; i += blockDim.x) a[(i) * ld + (k)] /= lkk;
-    __syncthreads();
-    if (threadIdx.x == 0) a[(k) * ld + (k)] = lkk;
-    // trailing update of the lower triangle: a_ij -= l_ik l_jk, k < j <= i
-    const int t = b - k - 1;
-    for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
-      const int ii = e / t, jj = e - ii * t;
-      if (jj <= ii)
-        a[(k + 1 + ii) * ld + k + 1 + jj] -= a[(k + 1 + ii) * ld + k] * a[(k + 1 + jj) * ld + k];
+    const double r = rsqrt_nr(piv), rd = r * r;
+    if (tid == 0) rdiag[k] = r;
+    // trailing lower triangle (i, j), k < j <= i: warps take rows, lanes columns
+    const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+    for (int i = k + 1 + warp; i < b; i += nwarp) {
+      const double f = a[i * ld + k] * rd;
+      for (int j = k + 1 + lane; j <= i; j += 32) a[i * ld + j] -= f * a[j * ld + k];
     }
     __syncthreads();
   }
-  __syncthreads();
   if (bad) {
-    if (threadIdx.x == 0) *status = 1;
+    if (tid == 0) *status = 1;
     return;
   }
-  // X = L^-1 by columns (one thread per column, forward substitution)
-  for (int c = threadIdx.x; c < b; c += blockDim.x) {
-    for (int i = 0; i < c; ++i) x[(i) * ld + (c)] = 0.0;
-    x[(c) * ld + (c)] = 1.0 / a[(c) * ld + (c)];
-    for (int i = c + 1; i < b; ++i) {
-      double s = 0.0;
-      for (int k = c; k < i; ++k) s = fma(a[(i) * ld + (k)], x[(k) * ld + (c)], s);
-      x[(i) * ld + (c)] = -s / a[(i) * ld + (i)];
-    }
+  // L = a's lower triangle scaled column-wise by rdiag (l_ik = a_ik r_k), in
+  // place; the diagonal becomes l_kk = a_kk r_k
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e - i * b;
+    if (j <= i) a[i * ld + j] *= rdiag[j];
+    x[i * ld + j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-    const int i = e / b, j = e - i * b;
-    rinv[e] = x[(j) * ld + (i)];  // L^-T
+  // X = L^-1, right-looking: row k /= l_kk, then rows i > k -= l_ik row k
+  // (columns c <= k are the only nonzeros of row k)
+  for (int k = 0; k < b; ++k) {
+    const double rk = rdiag[k];  // 1 / l_kk
+    // scale row k (columns 0..k) -- read by the update of this step only
+    // through xk below, so it is folded in: x_ic -= l_ik * (x_kc * rk)
+    {
+      const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+      for (int i = k + 1 + warp; i < b; i += nwarp) {
+        const double f = a[i * ld + k] * rk;
+        for (int c = lane; c <= k; c += 32) x[i * ld + c] -= f * x[k * ld + c];
+      }
+    }
+    __syncthreads();
+    for (int c = tid; c <= k; c += nt) x[k * ld + c] *= rk;
+    __syncthreads();
   }
-  if (threadIdx.x == 0) *status = 0;
+  for (int e = tid; e < b * b; e += nt) {
+    const int i = e / b, j = e - i * b;
+    rinv[e] = (j >= i) ? x[j * ld + i] : 0.0;  // L^-T: upper triangular
+  }
+  if (tid == 0) *status = 0;
 }
 
 unsigned grid_for(int64_t n) { return static_cast<unsigned>(std::min<int64_t>(bt_cdiv(n, 256), 4096)); }
@@ -258,7 +281,7 @@ int svqb(const Ctx& c, const double* y, int64_t n, int64_t b, double* q, int64_t
                                                           (CHOL_MAXB + 1))));
       attr = true;
     }
-    chol_rinv_kernel<<<1, 256, smb, c.st>>>(ms, static_cast<int>(b), v2, flag);
+    chol_rinv_kernel<<<1, 1024, smb, c.st>>>(ms, static_cast<int>(b), v2, flag);
     BT_LAUNCH_CHECK();
     int hflag = 1;
     BT_CUDA_CHECK(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, c.st));
@@ -349,6 +372,8 @@ extern "C" int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need,
   BT_TRY(svqb(c, y, n, b, q, &bq, &dropped));
   if (bq == 0) return BT_OK;
   double prev = -1.0;
+  int steps_since_rr = 1;
+  const bool skip_rr = max_iters == SUB_MAX_ITERS_COLD && !no_skip_rr();
   std::vector<double> wh(b), rh(b);
   for (int it = 0; it < max_iters; ++it) {
     BT_TRY(c.gemm(gemm_args(n, bq, n, g, n, 1, q, bq, 1, y)));       // G Q
@@ -402,14 +427,46 @@ extern "C" int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need,
         return BT_OK;
     }
     if (prev > 0.0 && worst > 0.0) {
-      const double rate = worst / prev;  // linear convergence factor
+      // linear convergence factor per step (several steps since the last RR
+      // when Rayleigh-Ritz is skipped)
+      const double rate = std::pow(worst / prev, 1.0 / static_cast<double>(steps_since_rr));
       const int left = max_iters - 1 - it;
       if (rate >= 1.0 || std::log(target / worst) / std::log(std::max(rate, 1e-300)) > left)
         return BT_OK;  // too slow: the tridiagonal path wins
     }
-    prev = worst;
     // next block = the Ritz vectors (v stays the caller's output buffer)
     BT_CUDA_CHECK(cudaMemcpyAsync(q, v, sizeof(double) * n * bq, cudaMemcpyDeviceToDevice, c.st));
+    if (skip_rr && worst > 0.0 && k >= 1) {
+      // cold block of many pairs: plain simultaneous iteration (G Q, then
+      // CholeskyQR -- Q's columns stay near the eigenvectors, so the
+      // column-scaled Gram stays well conditioned) for the predicted number
+      // of steps, and the Rayleigh-Ritz + residual check only after them
+      // before any measured rate: sqrt(theta_b / theta_k) -- the Ritz ratio
+      // itself overestimates the speed (C3 mode 1: 0.155 vs 0.31 measured)
+      double rate = std::sqrt(wh[bq - 1] / wh[k - 1]);
+      if (prev > 0.0) rate = std::pow(worst / prev, 1.0 / static_cast<double>(steps_since_rr));
+      int m = 0;
+      if (rate > 0.0 && rate < 1.0)
+        m = static_cast<int>(std::ceil(std::log(target / worst) / std::log(rate))) - 1;
+      m = std::max(0, std::min(m, max_iters - 2 - it));
+      // two applications of G per orthonormalisation (Q's columns are near
+      // eigenvectors, so the column-scaled G^2 Q stays well conditioned)
+      double* gq2 = c.at(p.off_gq);
+      for (int j = 0; j < m; j += 2) {
+        const bool two = j + 1 < m;
+        BT_TRY(c.gemm(gemm_args(n, bq, n, g, n, 1, q, bq, 1, two ? gq2 : y)));   // G Q
+        if (two) BT_TRY(c.gemm(gemm_args(n, bq, n, g, n, 1, gq2, bq, 1, y)));   // G (G Q)
+        int64_t nq = 0, dr = 0;
+        BT_TRY(svqb(c, y, n, bq, q, &nq, &dr));
+        if (nq != bq) return BT_OK;  // the block lost directions: let the caller fall back
+      }
+      it += m;
+      steps_since_rr = m + 1;
+      if (dbg)
+        fprintf(stderr, "[subspace n=%lld b=%lld] %d power steps without Rayleigh-Ritz (rate %.3f)\n",
+                (long long)n, (long long)b, m, rate);
+    }
+    prev = worst;
   }
   return BT_OK;
 }
