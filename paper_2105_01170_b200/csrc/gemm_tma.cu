@@ -19,8 +19,9 @@
 
 namespace {
 
+template <int BN_>
 struct AtCfg {
-  static constexpr int BM = 128, BN = 64, BK = 16, STAGES = 4;
+  static constexpr int BM = 128, BN = BN_, BK = 16, STAGES = 4;
   static constexpr int WM = 2, WN = 2, THREADS = WM * WN * 32;
   static constexpr int TM = BM / WM, TN = BN / WN, FM = TM / 8, FN = TN / 8;
   static constexpr int A_STAGE = BK * BM, B_STAGE = BK * BN;  // doubles
@@ -28,23 +29,27 @@ struct AtCfg {
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;
 };
 
+template <class T>
 __device__ __forceinline__ void at_issue(const CUtensorMap* amap, const CUtensorMap* bmap, double* as,
                                          double* bs, uint64_t* bar, int k0, int m0, int n0, int b,
                                          uint64_t pol_a, uint64_t pol_b) {
-  mbar_arrive_expect_tx(bar, AtCfg::STAGE_BYTES);
+  mbar_arrive_expect_tx(bar, T::STAGE_BYTES);
 #pragma unroll
-  for (int q = 0; q < AtCfg::BM / 16; ++q)
-    tma_load_3d(as + q * 16 * AtCfg::BK, amap, bar, m0 + 16 * q, k0, b, pol_a);
+  for (int q = 0; q < T::BM / 16; ++q)
+    tma_load_3d(as + q * 16 * T::BK, amap, bar, m0 + 16 * q, k0, b, pol_a);
 #pragma unroll
-  for (int q = 0; q < AtCfg::BN / 16; ++q)
-    tma_load_2d(bs + q * 16 * AtCfg::BK, bmap, bar, n0 + 16 * q, k0, pol_b);
+  for (int q = 0; q < T::BN / 16; ++q)
+    tma_load_2d(bs + q * 16 * T::BK, bmap, bar, n0 + 16 * q, k0, pol_b);
 }
 
-__global__ void __launch_bounds__(AtCfg::THREADS, 2)
+// TOUT: store C^T (C[b][n][m], m contiguous: ldc is the n stride) -- the
+// layout of a mode product x x_k U^T over a non-last mode
+template <int BN, bool TOUT>
+__global__ void __launch_bounds__(AtCfg<BN>::THREADS, 2)
     gemm_at_tma_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                        int64_t M, int64_t N, int64_t Kdim, double* __restrict__ C, int64_t ldc,
                        int64_t sCb) {
-  using T = AtCfg;
+  using T = AtCfg<BN>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[T::STAGES];
   __shared__ int left_cnt[T::STAGES];
@@ -64,8 +69,8 @@ __global__ void __launch_bounds__(AtCfg::THREADS, 2)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < T::STAGES && s < KT; ++s)
-      at_issue(&amap, &bmap, As + s * T::A_STAGE, Bs + s * T::B_STAGE, &full[s], s * T::BK, m0, n0, bz,
-               pol_a, pol_b);
+      at_issue<T>(&amap, &bmap, As + s * T::A_STAGE, Bs + s * T::B_STAGE, &full[s], s * T::BK, m0, n0,
+                  bz, pol_a, pol_b);
   }
   __syncthreads();
   const int gq = lane >> 2, tq = lane & 3;
@@ -120,8 +125,8 @@ __global__ void __launch_bounds__(AtCfg::THREADS, 2)
             const int nk = kt + T::STAGES;
             if (nk < KT) {
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              at_issue(&amap, &bmap, As + s * T::A_STAGE, Bs + s * T::B_STAGE, &full[s], nk * T::BK, m0,
-                       n0, bz, pol_a, pol_b);
+              at_issue<T>(&amap, &bmap, As + s * T::A_STAGE, Bs + s * T::B_STAGE, &full[s], nk * T::BK,
+                          m0, n0, bz, pol_a, pol_b);
             }
           }
         }
@@ -145,44 +150,71 @@ __global__ void __launch_bounds__(AtCfg::THREADS, 2)
 #pragma unroll
     for (int fj = 0; fj < T::FN; ++fj) {
       const int64_t n = n0 + wn0 + fj * 8 + 2 * tq;
-      double* p = Cb + m * ldc + n;
-      if (n + 1 < N) {
-        *reinterpret_cast<double2*>(p) = make_double2(acc[fi][fj][0], acc[fi][fj][1]);
-      } else if (n < N) {
-        p[0] = acc[fi][fj][0];
+      if (TOUT) {
+        // 8 consecutive m per (fj, h) across gq: 64-byte runs
+        if (n < N) Cb[n * ldc + m] = acc[fi][fj][0];
+        if (n + 1 < N) Cb[(n + 1) * ldc + m] = acc[fi][fj][1];
+      } else {
+        double* p = Cb + m * ldc + n;
+        if (n + 1 < N) {
+          *reinterpret_cast<double2*>(p) = make_double2(acc[fi][fj][0], acc[fi][fj][1]);
+        } else if (n < N) {
+          p[0] = acc[fi][fj][0];
+        }
       }
     }
   }
 }
 
-}  // namespace
-
-// C[b] (M x N, row stride ldc, batch stride sCb) = A[b]^T B with A[b] the
-// (Kdim x M) row-major block at a + b * sAb (row stride lda) and B (Kdim x N,
-// row stride ldb).  Returns BT_E_VALUE when the shape is outside what the
-// TMA maps can address (the caller then uses the cp.async engine).
-int bt_gemm_at_tma(const double* a, int64_t lda, int64_t sAb, const double* b, int64_t ldb, double* c,
-                   int64_t ldc, int64_t sCb, int64_t M, int64_t N, int64_t Kdim, int64_t batch,
-                   cudaStream_t st) {
-  using T = AtCfg;
-  const bool ok = M % 2 == 0 && lda % 2 == 0 && ldb % 2 == 0 && ldc % 2 == 0 && N % 2 == 0 &&
-                  (batch == 1 || sAb % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
-                                                    reinterpret_cast<uintptr_t>(c)) & 15u) == 0 &&
-                  M <= INT32_MAX && N <= INT32_MAX && Kdim <= INT32_MAX && batch <= 65535 &&
-                  bt_cdiv(N, T::BN) <= 65535;
-  if (!ok) return BT_E_VALUE;
-  CUtensorMap amap, bmap;
-  BT_TRY(bt_tma_map_f64_3d(&amap, a, M, Kdim, batch, lda, batch > 1 ? sAb : lda * Kdim, 16, T::BK, 1));
-  BT_TRY(bt_tma_map_f64_2d(&bmap, b, N, Kdim, ldb, 16, T::BK));
+template <int BN, bool TOUT>
+int launch_at(const CUtensorMap& amap, const CUtensorMap& bmap, int64_t M, int64_t N, int64_t Kdim,
+              double* c, int64_t ldc, int64_t sCb, int64_t batch, cudaStream_t st) {
+  using T = AtCfg<BN>;
   static bool attr = false;
   if (!attr) {
-    BT_CUDA_CHECK(cudaFuncSetAttribute(gemm_at_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       T::SMEM_BYTES));
+    BT_CUDA_CHECK(cudaFuncSetAttribute(gemm_at_tma_kernel<BN, TOUT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES));
     attr = true;
   }
   dim3 grid(static_cast<unsigned>(bt_cdiv(M, T::BM)), static_cast<unsigned>(bt_cdiv(N, T::BN)),
             static_cast<unsigned>(batch));
-  gemm_at_tma_kernel<<<grid, T::THREADS, T::SMEM_BYTES, st>>>(amap, bmap, M, N, Kdim, c, ldc, sCb);
+  gemm_at_tma_kernel<BN, TOUT><<<grid, T::THREADS, T::SMEM_BYTES, st>>>(amap, bmap, M, N, Kdim, c, ldc,
+                                                                        sCb);
   BT_LAUNCH_CHECK();
   return BT_OK;
+}
+
+}  // namespace
+
+// C[b] = A[b]^T B with A[b] the (Kdim x M) row-major block at a + b * sAb
+// (row stride lda) and B (Kdim x N, row stride ldb).  C[b] is (M x N) with
+// row stride ldc, or with transpose_out (N x M) with row stride ldc; batch
+// stride sCb.  N <= 32 takes the 128 x 32 tile.  Returns BT_E_VALUE when the
+// shape is outside what the TMA maps can address (the caller then uses the
+// cp.async engine).
+int bt_gemm_at_tma_ex(const double* a, int64_t lda, int64_t sAb, const double* b, int64_t ldb,
+                      double* c, int64_t ldc, int64_t sCb, int64_t M, int64_t N, int64_t Kdim,
+                      int64_t batch, int transpose_out, cudaStream_t st) {
+  const bool ok = M % 2 == 0 && lda % 2 == 0 && ldb % 2 == 0 && (transpose_out || ldc % 2 == 0) &&
+                  N % 2 == 0 && (batch == 1 || sAb % 2 == 0) &&
+                  ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+                    reinterpret_cast<uintptr_t>(c)) & 15u) == 0 &&
+                  M <= INT32_MAX && N <= INT32_MAX && Kdim <= INT32_MAX && batch <= 65535 &&
+                  bt_cdiv(N, 32) <= 65535 && Kdim >= 1;
+  if (!ok) return BT_E_VALUE;
+  CUtensorMap amap, bmap;
+  BT_TRY(bt_tma_map_f64_3d(&amap, a, M, Kdim, batch, lda, batch > 1 ? sAb : lda * Kdim, 16,
+                           AtCfg<64>::BK, 1));
+  BT_TRY(bt_tma_map_f64_2d(&bmap, b, N, Kdim, ldb, 16, AtCfg<64>::BK));
+  if (N <= 32)
+    return transpose_out ? launch_at<32, true>(amap, bmap, M, N, Kdim, c, ldc, sCb, batch, st)
+                         : launch_at<32, false>(amap, bmap, M, N, Kdim, c, ldc, sCb, batch, st);
+  return transpose_out ? launch_at<64, true>(amap, bmap, M, N, Kdim, c, ldc, sCb, batch, st)
+                       : launch_at<64, false>(amap, bmap, M, N, Kdim, c, ldc, sCb, batch, st);
+}
+
+int bt_gemm_at_tma(const double* a, int64_t lda, int64_t sAb, const double* b, int64_t ldb, double* c,
+                   int64_t ldc, int64_t sCb, int64_t M, int64_t N, int64_t Kdim, int64_t batch,
+                   cudaStream_t st) {
+  return bt_gemm_at_tma_ex(a, lda, sAb, b, ldb, c, ldc, sCb, M, N, Kdim, batch, 0, st);
 }

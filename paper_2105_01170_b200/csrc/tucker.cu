@@ -5,8 +5,13 @@
 // tensor viewed as (outer, n_mode, inner).
 #include "gemm.cuh"
 
+#include <cstdlib>
+
 int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, int64_t ws_elems);
 int64_t bt_gemm_ws_elems(BtGemmArgs g, int64_t batch);
+int bt_gemm_at_tma_ex(const double* a, int64_t lda, int64_t sAb, const double* b, int64_t ldb,
+                      double* c, int64_t ldc, int64_t sCb, int64_t M, int64_t N, int64_t Kdim,
+                      int64_t batch, int transpose_out, cudaStream_t st);
 
 namespace {
 
@@ -126,6 +131,15 @@ extern "C" int bt_ttm_f64(const double* x, const int64_t* dims, int order, int m
   BT_REQUIRE(view3(dims, order, mode, v), BT_E_SHAPE, "mode %d out of range for order-%d tensor",
              mode, order);
   BT_REQUIRE(rows >= 0, BT_E_SHAPE, "ttm: negative row count");
+  // Y(o, :, :) = U^T X(o, :, :) over a non-last mode with u given as U
+  // (n x rows): the TMA-fed transposed-A kernel, C^T stored -- X(o) is read in
+  // place as (n x inner) with inner contiguous (BT_TTM_TMA=0: the engine)
+  static const bool ttm_tma = !(getenv("BT_TTM_TMA") && getenv("BT_TTM_TMA")[0] == '0');
+  if (ttm_tma && transpose && v.inner > 1 && rows > 0 && v.n > 0 && v.outer <= 65535) {
+    const int rc = bt_gemm_at_tma_ex(x, v.inner, v.n * v.inner, u, rows, y, v.inner, rows * v.inner,
+                                     v.inner, rows, v.n, v.outer, 1, bt_stream(stream));
+    if (rc != BT_E_VALUE) return rc;
+  }
   int64_t batch = 1;
   BtGemmArgs a = ttm_args(x, v, u, rows, transpose, y, batch);
   a.ws = static_cast<double*>(ws);

@@ -303,6 +303,7 @@ def hooi(t, init: TuckerRep, sweeps: int, shared=None) -> TuckerRep:
     xd = _dev.to_device(t)
     factors = [None if f is None else _dev.to_device(f) for f in init.factors]
     order = t.ndim
+    last = None   # (mode, tensor projected on every other mode) of the latest update
     for _ in range(int(sweeps)):
         for k in range(order):
             if factors[k] is None or (shared is not None and k + 1 == shared[1]):
@@ -315,7 +316,17 @@ def hooi(t, init: TuckerRep, sweeps: int, shared=None) -> TuckerRep:
             factors[k] = u
             if shared is not None and k + 1 == shared[0]:
                 factors[shared[1] - 1] = u
-    core = _project_core(xd, factors)
+                last = None   # y's projection on the shared partner is stale
+            else:
+                last = (k, y)
+    if last is not None:
+        # the latest update's y is already projected on every other mode's
+        # final factor: the core is one small product away (no extra pass
+        # over the full tensor; same products, modes in a different order)
+        k, y = last
+        core = ttm_dev(y, k + 1, factors[k], int(factors[k].shape[1]), transpose=True)
+    else:
+        core = _project_core(xd, factors)
     return TuckerRep(core=_dev.like_input(t, core),
                      factors=tuple(None if f is None else _dev.like_input(t, f) for f in factors))
 
