@@ -323,6 +323,18 @@ int bt_fill_normal_f64(double* out, int64_t n, uint64_t key, void* stream);
 /* out (cols x rows) = x (rows x cols)^T, row-major, tiled through shared
  * memory (the RHS layout flips of the batched matvecs). */
 int bt_transpose_f64(const double* x, int64_t rows, int64_t cols, double* out, void* stream);
+/* SVD of a small square matrix m (n x n, n <= 32, row-major) by one-sided
+ * Jacobi in one warp (high relative accuracy for small singular values; the
+ * reference's np.linalg.svd of decomp.py:172 restricted to the projected
+ * factor of a basis refinement): s descending, u (n x n) with the sign rule
+ * of decomp.py:176-179 per column, v (n x n) compensated; m = u diag(s) v^T. */
+int bt_svd_small_f64(const double* m, int64_t n, double* u, double* s, double* v, void* stream);
+/* Tall-skinny Householder QR of x (m x n row-major, n <= 32, m up to ~6.6k
+ * rows): q (m x n) orthonormal, r (n x n) upper triangular with diag >= 0
+ * (decomp.py:182-193's normalisation); two-level TSQR, no Gram. */
+int64_t bt_tsqr_ws_bytes(int64_t m, int64_t n);
+int bt_tsqr_f64(const double* x, int64_t m, int64_t n, double* q, double* r, void* ws,
+                int64_t ws_bytes, void* stream);
 /* out[i][j] = left[i] x[i][j] right[j] (left / right may be NULL). */
 int bt_diag_scale_f64(const double* x, int64_t rows, int64_t cols, const double* left,
                       const double* right, double* out, void* stream);

@@ -65,6 +65,8 @@ SUBSPACE = os.environ.get("BT_SUBSPACE", "1") != "0"
 # tridiagonal solver instead of the oversampled subspace iteration (C3 mode 1:
 # 8.1 ms subspace vs 15.9 ms tridiagonal)
 _SUB_DIRECT = os.environ.get("BT_SUB_DIRECT", "0") == "1"
+# BT_REFINE=0: warm-started bases (HOOI) take the Gram deflation passes too
+REFINE = os.environ.get("BT_REFINE", "1") != "0"
 SUB_OVERSAMPLE = 16
 SUB_MAX_BLOCK = 96     # Rayleigh-Ritz matrices stay on the one-CTA Jacobi path
 
@@ -227,6 +229,78 @@ def _next_pass_hint(wh, k: int):
     return k + 4
 
 
+def tsqr_dev(ad):
+    """Householder-quality thin QR of a tall block with <= 32 columns (TSQR on
+    the GPU; falls back to the one-CTA Householder kernel past its row cap)."""
+    m, n = int(ad.shape[0]), int(ad.shape[1])
+    if n > 32 or m < n or m > 6656:
+        return _householder_qr(ad)
+    q, r = _dev.empty((m, n)), _dev.empty((n, n))
+    ws = _dev.workspace(N.load().bt_tsqr_ws_bytes(m, n))
+    N.call("bt_tsqr_f64", _dev.ptr(ad.contiguous()), m, n, _dev.ptr(q), _dev.ptr(r), _dev.ptr(ws),
+           int(ws.numel()) * 8, _dev.stream())
+    return q, r
+
+
+def svd_small_dev(m):
+    """(u, s, v) of a small square matrix (n <= 32) by one-warp one-sided
+    Jacobi (bt_svd_small_f64): s descending, sign rule on u."""
+    n = int(m.shape[0])
+    u, v, s = _dev.empty((n, n)), _dev.empty((n, n)), _dev.empty((n,))
+    N.call("bt_svd_small_f64", _dev.ptr(m.contiguous()), n, _dev.ptr(u), _dev.ptr(s), _dev.ptr(v),
+           _dev.stream())
+    return u, s, v
+
+
+REFINE_MAX_STEPS = 4
+REFINE_TOL = 1e-12     # max change of a resolved vector between two refinement steps
+REFINE_NUMEL = 1 << 26
+
+
+def _refine_basis_qr(xd, mode: int, r: int, start):
+    """Leading r <= 32 left singular vectors of A = unfold(x, mode) from a
+    close warm start V (HOOI's previous sweep) without a Gram: subspace
+    iteration  Z = A^T V -> Q_Z (Householder) -> W = A Q_Z -> Q_W R_W
+    (Householder) -> R_W = U_R S V_R^T (one-sided Jacobi) -> V = Q_W U_R.
+    Every product is a GEMM of A or A^T with an orthonormal block, so a
+    singular direction is resolved to ~eps sigma_1 / gap instead of the
+    Gram's ~eps sigma_1^2 / gap^2 -- one pass resolves what the Gram needs
+    one deflation pass per ~6 orders of magnitude for (C3 mode 2: 5 passes).
+    Returns None when it does not settle within REFINE_MAX_STEPS steps (the
+    caller then runs the deflation passes)."""
+    t = _dev.torch()
+    dims = tuple(int(v) for v in xd.shape)
+    n = dims[mode - 1]
+    cols = xd.numel() // max(n, 1)
+    if (r > 32 or n < r or cols < 2 * r or xd.numel() > REFINE_NUMEL or start is None
+            or int(start.shape[1]) != r):
+        return None
+    # A = unfold(x, mode) with the other indices in C order as columns
+    a = xd.movedim(mode - 1, 0).reshape(n, -1).contiguous()
+    v = start.contiguous()
+    prev = None
+    for _ in range(REFINE_MAX_STEPS):
+        qz, _ = tsqr_dev(gemm_dev(a, v, ta=True))              # A^T V -> Q_Z
+        qw, rw = tsqr_dev(gemm_dev(a, qz))                     # A Q_Z -> Q_W R_W
+        ur, sv, _ = svd_small_dev(rw)
+        v = gemm_dev(qw, ur)
+        N.call("bt_sign_fix_f64", _dev.ptr(v), n, r, _dev.stream())
+        sh = _dev.to_host(sv)
+        if not sh[0] > 0:
+            return None
+        if prev is not None:
+            # a vector is resolved to ~eps sigma_1 / sigma_k: compare each with
+            # the previous step at that accuracy (REFINE_TOL floor); the ones
+            # below 1e-13 sigma_1 are noise either way
+            diff = _dev.to_host((v - prev).abs().amax(dim=0))
+            live = sh > 1e-13 * sh[0]
+            tol = np.maximum(REFINE_TOL, 64 * 2.2e-16 * sh[0] / np.maximum(sh, 1e-300))
+            if np.all(diff[live] <= tol[live]):
+                return v
+        prev = v
+    return None
+
+
 def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_passes: int = 16,
                    reduce=None, start=None):
     """Leading r left singular vectors of unfold(x, mode) (decomp.py:220-234),
@@ -251,6 +325,18 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
     modes = [mode] if extra_mode is None else [mode, extra_mode]
     t = _dev.torch()
     n = int(xd.shape[mode - 1])
+    if extra_mode is None and reduce is None and REFINE and r <= 32 and n >= 2 * r:
+        # warm start (HOOI's previous basis) or, cold, a Gaussian block: the
+        # Gram-free subspace iteration settles in a few steps when the
+        # spectrum decays fast past r (C3 mode 2: ~1e-3 per index) and hands
+        # back to the deflation passes otherwise
+        s0 = start if start is not None else gaussian_dev(n, r, 97531)
+        v = _refine_basis_qr(xd, mode, r, s0)
+        if v is not None:
+            if _DEBUG:
+                print(f"[mode_basis n={n} r={r}] QR refinement from the "
+                      f"{'warm' if start is not None else 'Gaussian'} start", file=sys.stderr)
+            return v
     g = _gram_modes(xd, modes, reduce)
     basis = None
     top = None
