@@ -333,6 +333,11 @@ int bt_svd_small_f64(const double* m, int64_t n, double* u, double* s, double* v
  * rows): q (m x n) orthonormal, r (n x n) upper triangular with diag >= 0
  * (decomp.py:182-193's normalisation); two-level TSQR, no Gram. */
 int64_t bt_tsqr_ws_bytes(int64_t m, int64_t n);
+/* Cholesky of a small SPD Gram g (n x n, n <= 32) for a CholeskyQR step:
+ * lt = L^T, linvt = L^-T (both upper, row-major); *flag (device int) = 1
+ * when a pivot is not above 1e-12 of the largest diagonal entry. */
+int bt_chol_small_f64(const double* g, int64_t n, double* lt, double* linvt, int* flag,
+                      void* stream);
 int bt_tsqr_f64(const double* x, int64_t m, int64_t n, double* q, double* r, void* ws,
                 int64_t ws_bytes, void* stream);
 /* out[i][j] = left[i] x[i][j] right[j] (left / right may be NULL). */

@@ -242,6 +242,44 @@ def tsqr_dev(ad):
     return q, r
 
 
+def _qr_colscaled(z):
+    """(q, r) of a tall block with <= 32 columns by column-scaled CholeskyQR2:
+    Y = Z D (unit columns), two CholeskyQR passes, R = L2^T L1^T D^-1.
+    Accurate whenever Z's columns are already nearly orthogonal up to their
+    scales (a refinement step near convergence: Z = A^T V ~ W Sigma); None
+    when a pivot says otherwise (the caller takes TSQR)."""
+    m, n = int(z.shape[0]), int(z.shape[1])
+    if n > 32 or m < n:
+        return None
+    nrm = _dev.empty((n,))
+    N.call("bt_col_norms_f64", _dev.ptr(z), m, n, _dev.ptr(nrm), _dev.stream())
+    hn = _dev.to_host(nrm)
+    if not np.all(hn > 0.0):
+        return None
+    dinv = _dev.to_device(1.0 / hn)
+    y = _dev.empty((m, n))
+    N.call("bt_diag_scale_f64", _dev.ptr(z), m, n, None, _dev.ptr(dinv), _dev.ptr(y), _dev.stream())
+    flags = _dev.torch().zeros(2, dtype=_dev.torch().int32, device="cuda")
+    r = None
+    for it in range(2):
+        g = gemm_dev(y, y, ta=True)
+        lt, linvt = _dev.empty((n, n)), _dev.empty((n, n))
+        N.call("bt_chol_small_f64", _dev.ptr(g), n, _dev.ptr(lt), _dev.ptr(linvt),
+               flags.data_ptr() + 4 * it, _dev.stream())
+        y = gemm_dev(y, linvt)
+        r = lt if r is None else gemm_dev(lt, r)
+    if int(_dev.to_host(flags).max()) != 0:
+        return None
+    rr = _dev.empty((n, n))
+    N.call("bt_diag_scale_f64", _dev.ptr(r), n, n, None, _dev.ptr(nrm), _dev.ptr(rr), _dev.stream())
+    return y, rr
+
+
+def _qr_refine(z):
+    out = _qr_colscaled(z)
+    return out if out is not None else tsqr_dev(z)
+
+
 def svd_small_dev(m):
     """(u, s, v) of a small square matrix (n <= 32) by one-warp one-sided
     Jacobi (bt_svd_small_f64): s descending, sign rule on u."""
@@ -280,8 +318,8 @@ def _refine_basis_qr(xd, mode: int, r: int, start):
     v = start.contiguous()
     prev = None
     for _ in range(REFINE_MAX_STEPS):
-        qz, _ = tsqr_dev(gemm_dev(a, v, ta=True))              # A^T V -> Q_Z
-        qw, rw = tsqr_dev(gemm_dev(a, qz))                     # A Q_Z -> Q_W R_W
+        qz, _ = _qr_refine(gemm_dev(a, v, ta=True))            # A^T V -> Q_Z
+        qw, rw = _qr_refine(gemm_dev(a, qz))                   # A Q_Z -> Q_W R_W
         ur, sv, _ = svd_small_dev(rw)
         v = gemm_dev(qw, ur)
         N.call("bt_sign_fix_f64", _dev.ptr(v), n, r, _dev.stream())

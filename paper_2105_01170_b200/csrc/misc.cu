@@ -729,3 +729,88 @@ extern "C" int bt_svd_small_f64(const double* m, int64_t n, double* u, double* s
   BT_LAUNCH_CHECK();
   return BT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Small Cholesky for CholeskyQR steps (n <= 32, one warp): g = L L^T,
+// writes lt = L^T (upper) and linvt = L^-T (upper), flag = 1 when a pivot
+// is not above 1e-12 of the largest diagonal (the caller then takes the
+// Householder route).  The Gram comes from a column-scaled block, so its
+// diagonal is ~1.
+// ---------------------------------------------------------------------------
+
+namespace {
+
+__device__ __forceinline__ double rsqrt_nr_f64(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  return y * fma(-h * y, y, 1.5);
+}
+
+__global__ void __launch_bounds__(32) chol_small_kernel(const double* __restrict__ g, int n,
+                                                        double* __restrict__ lt,
+                                                        double* __restrict__ linvt,
+                                                        int* __restrict__ flag) {
+  __shared__ double a[32][33], y[32][33], rd[32];
+  const int lane = threadIdx.x;
+  for (int e = lane; e < n * n; e += 32) a[e / n][e % n] = g[e];
+  __syncwarp();
+  double dmax = 0.0;
+  for (int i = 0; i < n; ++i) dmax = fmax(dmax, a[i][i]);
+  int bad = 0;
+  for (int k = 0; k < n; ++k) {
+    const double d = a[k][k];
+    if (!(d > 1e-12 * dmax)) {
+      bad = 1;
+      break;
+    }
+    const double r = rsqrt_nr_f64(d);
+    __syncwarp();
+    if (lane > k && lane < n) a[lane][k] *= r;
+    if (lane == 0) {
+      a[k][k] = d * r;
+      rd[k] = r;
+    }
+    __syncwarp();
+    if (lane > k && lane < n) {
+      const double lik = a[lane][k];
+      for (int j = k + 1; j <= lane; ++j) a[lane][j] -= lik * a[j][k];
+    }
+    __syncwarp();
+  }
+  if (lane == 0) *flag = bad;
+  if (bad) return;
+  // Y = L^-1, column per lane
+  if (lane < n) {
+    for (int i = 0; i < n; ++i) {
+      double v;
+      if (i < lane) {
+        v = 0.0;
+      } else if (i == lane) {
+        v = rd[i];
+      } else {
+        double acc = 0.0;
+        for (int k = lane; k < i; ++k) acc = fma(a[i][k], y[k][lane], acc);
+        v = -acc * rd[i];
+      }
+      y[i][lane] = v;
+    }
+  }
+  __syncwarp();
+  for (int e = lane; e < n * n; e += 32) {
+    const int i = e / n, j = e % n;
+    lt[e] = (j >= i) ? a[j][i] : 0.0;       // L^T
+    linvt[e] = (j >= i) ? y[j][i] : 0.0;    // L^-T
+  }
+}
+
+}  // namespace
+
+extern "C" int bt_chol_small_f64(const double* g, int64_t n, double* lt, double* linvt, int* flag,
+                                 void* stream) {
+  BT_REQUIRE(n >= 1 && n <= 32, BT_E_SHAPE, "chol_small: n = %lld outside 1..32", (long long)n);
+  chol_small_kernel<<<1, 32, 0, bt_stream(stream)>>>(g, static_cast<int>(n), lt, linvt, flag);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
