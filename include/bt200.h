@@ -338,6 +338,13 @@ int64_t bt_tsqr_ws_bytes(int64_t m, int64_t n);
  * when a pivot is not above 1e-12 of the largest diagonal entry. */
 int bt_chol_small_f64(const double* g, int64_t n, double* lt, double* linvt, int* flag,
                       void* stream);
+/* `need` (<= 1024) orthonormal columns orthogonal to basis (n x k) into out
+ * (n x need), from a Philox Gaussian block under key: blockwise projection +
+ * column-scaled CholeskyQR2, sign rule per column; *status (host) 1 when a
+ * block was rejected (numerically dependent), 0 otherwise. */
+int64_t bt_complete_basis_ws_bytes(int64_t n, int64_t k, int64_t need);
+int bt_complete_basis_f64(const double* basis, int64_t n, int64_t k, int64_t need, uint64_t key,
+                          double* out, int* status, void* ws, int64_t ws_bytes, void* stream);
 int bt_tsqr_f64(const double* x, int64_t m, int64_t n, double* q, double* r, void* ws,
                 int64_t ws_bytes, void* stream);
 /* out[i][j] = left[i] x[i][j] right[j] (left / right may be NULL). */

@@ -189,7 +189,47 @@ def _complete(basis, g, need: int, block: int = 32):
     Falls back to blockwise Loewdin orthonormalisation for thin blocks."""
     t = _dev.torch()
     n = int(g.shape[0])
+    k = 0 if basis is None else int(basis.shape[1])
+    if need <= 1024 and k + need <= n:
+        out = _dev.empty((n, need))
+        st = C.c_int(1)
+        ws = _dev.workspace(N.load().bt_complete_basis_ws_bytes(n, k, need))
+        N.call("bt_complete_basis_f64", None if basis is None else _dev.ptr(basis.contiguous()), n, k,
+               need, 12345, _dev.ptr(out), C.byref(st), _dev.ptr(ws), int(ws.numel()) * 8,
+               _dev.stream())
+        if st.value == 0:
+            return out
     y = gaussian_dev(n, need, 12345)
+    # blocks of <= 32 Gaussian columns: project out everything accepted so
+    # far (twice), then column-scaled CholeskyQR2 with the one-warp Cholesky
+    # (a Gaussian block is well conditioned); the larger paths below only run
+    # if a block is rejected
+    cur = basis
+    outs = []
+    ok = True
+    for j0 in range(0, need, 32):
+        blk = y[:, j0:j0 + 32].contiguous()
+        for _ in range(2):
+            if cur is not None:
+                blk = _axpby(1.0, blk, -1.0, gemm_dev(cur, gemm_dev(cur, blk, ta=True)))
+        qr = _qr_colscaled(blk) if int(blk.shape[1]) <= n else None
+        if qr is None:
+            ok = False
+            break
+        blk = qr[0]
+        if cur is not None:     # re-orthogonalise against the accepted basis once more
+            blk = _axpby(1.0, blk, -1.0, gemm_dev(cur, gemm_dev(cur, blk, ta=True)))
+            qr = _qr_colscaled(blk)
+            if qr is None:
+                ok = False
+                break
+            blk = qr[0]
+        outs.append(blk)
+        cur = blk if cur is None else t.cat([cur, blk], dim=1).contiguous()
+    if ok and outs:
+        out = t.cat(outs, dim=1).contiguous()
+        N.call("bt_sign_fix_f64", _dev.ptr(out), n, int(need), _dev.stream())
+        return out
     if need >= 8:
         for _ in range(2):
             if basis is not None:

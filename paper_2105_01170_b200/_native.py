@@ -101,6 +101,9 @@ _SIGS = {
     "bt_svd_small_f64": (C.c_int, [_dp, _i64, _dp, _dp, _dp, _dp]),
     "bt_tsqr_ws_bytes": (_i64, [_i64, _i64]),
     "bt_chol_small_f64": (C.c_int, [_dp, _i64, _dp, _dp, _dp, _dp]),
+    "bt_complete_basis_ws_bytes": (_i64, [_i64, _i64, _i64]),
+    "bt_complete_basis_f64": (C.c_int, [_dp, _i64, _i64, _i64, C.c_uint64, _dp, _P(C.c_int), _dp,
+                                        _i64, _dp]),
     "bt_tsqr_f64": (C.c_int, [_dp, _i64, _i64, _dp, _dp, _dp, _i64, _dp]),
     "bt_reverse_axes_f64": (C.c_int, [_dp, _P(_i64), C.c_int, _dp, _dp]),
     "bt_sign_fix_pair_f64": (C.c_int, [_dp, _i64, _i64, _dp, _i64, _dp]),

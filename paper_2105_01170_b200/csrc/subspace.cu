@@ -470,3 +470,123 @@ extern "C" int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need,
   }
   return BT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Orthonormal completion of a basis (decomp.py:220-234 full_matrices branch
+// and the deflation's rounding-level remainder): `need` columns orthogonal to
+// basis (n x k) from a Philox Gaussian block, in blocks of <= 32 columns:
+// project out the basis and the columns already made (twice), then
+// column-scaled CholeskyQR2 with the one-warp Cholesky -- all on the stream,
+// one host read of the failure flags at the end (status 1: a block was
+// rejected and the caller takes its own path).
+// ---------------------------------------------------------------------------
+
+extern "C" int bt_chol_small_f64(const double* g, int64_t n, double* lt, double* linvt, int* flag,
+                                 void* stream);
+extern "C" int bt_sign_fix_f64(double* x, int64_t rows, int64_t cols, void* stream);
+
+namespace {
+
+// gs = D g D with D = diag(g_ii^-1/2) (b x b); d out
+__global__ void scale_gram_kernel(const double* __restrict__ g, int b, double* __restrict__ gs,
+                                  double* __restrict__ d) {
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int i = e / b, j = e % b;
+    const double di = rsqrt(g[i * b + i]), dj = rsqrt(g[j * b + j]);
+    gs[e] = g[e] * di * dj;
+    if (i == j) d[i] = di;
+  }
+}
+
+// m = diag(d) linvt  (b x b)
+__global__ void scale_rows_kernel(const double* __restrict__ linvt, const double* __restrict__ d, int b,
+                                  double* __restrict__ m) {
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) m[e] = d[e / b] * linvt[e];
+}
+
+}  // namespace
+
+extern "C" int64_t bt_complete_basis_ws_bytes(int64_t n, int64_t k, int64_t need) {
+  const int64_t rows = k + need;
+  BtGemmArgs g1 = gemm_args(rows, 32, n, nullptr, 1, rows, nullptr, 32, 1, nullptr);
+  BtGemmArgs g2 = gemm_args(n, 32, rows, nullptr, rows, 1, nullptr, 32, 1, nullptr);
+  BtGemmArgs g3 = gemm_args(32, 32, n, nullptr, 1, 32, nullptr, 32, 1, nullptr);
+  const int64_t gw = std::max(bt_gemm_ws_elems(g1, 1), std::max(bt_gemm_ws_elems(g2, 1),
+                                                                 bt_gemm_ws_elems(g3, 1)));
+  return (2 * n * 32 + rows * 32 + 6 * 32 * 32 + 64 + gw + 64) * 8;
+}
+
+extern "C" int bt_complete_basis_f64(const double* basis, int64_t n, int64_t k, int64_t need,
+                                     uint64_t key, double* out, int* status, void* wsv,
+                                     int64_t ws_bytes, void* stream) {
+  BT_NVTX("bt_complete_basis_f64");
+  *status = 1;
+  BT_REQUIRE(n >= 1 && k >= 0 && need >= 1 && k + need <= n, BT_E_SHAPE,
+             "complete_basis: %lld + %lld columns exceed %lld rows", (long long)k, (long long)need,
+             (long long)n);
+  BT_REQUIRE(ws_bytes >= bt_complete_basis_ws_bytes(n, k, need), BT_E_VALUE,
+             "complete_basis: workspace too small");
+  cudaStream_t st = bt_stream(stream);
+  double* w = static_cast<double*>(wsv);
+  double* t0 = w;                 // n x 32 working block
+  double* t1 = t0 + n * 32;       // n x 32
+  double* cproj = t1 + n * 32;    // (k + need) x 32
+  double* gm = cproj + (k + need) * 32;
+  double* gs = gm + 32 * 32;
+  double* lt = gs + 32 * 32;
+  double* linvt = lt + 32 * 32;
+  double* mm = linvt + 32 * 32;
+  double* dv = mm + 32 * 32 + 32 * 32;
+  int* flags = reinterpret_cast<int*>(dv + 32);
+  double* gws = dv + 64;
+  const int64_t gw_elems = ws_bytes / 8 - (gws - w);
+  auto run = [&](BtGemmArgs g) {
+    g.ws = gws;
+    return bt_gemm_run(g, 1, st, 0, gw_elems);
+  };
+  const int64_t nblk = (need + 31) / 32;
+  BT_REQUIRE(2 * nblk <= 64, BT_E_SHAPE, "complete_basis: %lld columns exceed 1024", (long long)need);
+  BT_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int) * 2 * nblk, st));
+  BT_TRY(bt_fill_normal_f64(out, n * need, key, st));
+  for (int64_t j0 = 0; j0 < need; j0 += 32) {
+    const int64_t b = std::min<int64_t>(32, need - j0);
+    // working copy of the block
+    copy_cols_kernel<<<grid_for(n * b), 256, 0, st>>>(out + j0, need, n, b, t0, b);
+    BT_LAUNCH_CHECK();
+    for (int pass = 0; pass < 2; ++pass) {
+      // against the input basis, then the completed columns 0 .. j0
+      const double* qs[2] = {basis, out};
+      const int64_t qk[2] = {k, j0};
+      const int64_t qld[2] = {k, need};
+      for (int p = 0; p < 2; ++p) {
+        if (qk[p] == 0) continue;
+        BT_TRY(run(gemm_args(qk[p], b, n, qs[p], 1, qld[p], t0, b, 1, cproj)));   // Q^T T
+        BtGemmArgs up = gemm_args(n, b, qk[p], qs[p], qld[p], 1, cproj, b, 1, t0); // T -= Q C
+        up.alpha = -1.0;
+        up.beta = 1.0;
+        BT_TRY(run(up));
+      }
+    }
+    // column-scaled CholeskyQR2: T <- T D L^-T, twice
+    for (int it = 0; it < 2; ++it) {
+      BT_TRY(run(gemm_args(b, b, n, t0, 1, b, t0, b, 1, gm)));                    // T^T T
+      scale_gram_kernel<<<1, 256, 0, st>>>(gm, static_cast<int>(b), gs, dv);
+      BT_LAUNCH_CHECK();
+      BT_TRY(bt_chol_small_f64(gs, b, lt, linvt, flags + 2 * (j0 / 32) + it, st));
+      scale_rows_kernel<<<1, 256, 0, st>>>(linvt, dv, static_cast<int>(b), mm);
+      BT_LAUNCH_CHECK();
+      BT_TRY(run(gemm_args(n, b, b, t0, b, 1, mm, b, 1, t1)));                    // T D L^-T
+      std::swap(t0, t1);
+    }
+    copy_cols_kernel<<<grid_for(n * b), 256, 0, st>>>(t0, b, n, b, out + j0, need);
+    BT_LAUNCH_CHECK();
+  }
+  BT_TRY(bt_sign_fix_f64(out, n, need, st));
+  std::vector<int> hf(2 * nblk);
+  BT_CUDA_CHECK(cudaMemcpyAsync(hf.data(), flags, sizeof(int) * 2 * nblk, cudaMemcpyDeviceToHost, st));
+  BT_CUDA_CHECK(cudaStreamSynchronize(st));
+  int bad = 0;
+  for (int f : hf) bad |= f;
+  *status = bad ? 1 : 0;
+  return BT_OK;
+}
