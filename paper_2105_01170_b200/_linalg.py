@@ -431,7 +431,12 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
         # 1 (64 of 1024, lambda_97 / lambda_64 ~ 0.31): 28 steps, 8.1 ms
         # against 15.9 ms for the tridiagonal solver
         direct = (cold and hint is None and need >= 48 and n <= 1536 and _SUB_DIRECT)
-        sub = (_leading_subspace(g, need, RESOLVE_TAU, start if basis is None else None, hint)
+        # a first pass that cannot hold every wanted pair in one block (C2
+        # mode 2: 400 of 2047) starts with a 32-pair block: a pass keeps only
+        # the pairs above RESOLVE_TAU anyway (16 there), and the next pass's
+        # block is sized from this one's spectrum
+        h0 = 32 if (hint is None and basis is None and start is None and need > SUB_MAX_BLOCK) else hint
+        sub = (_leading_subspace(g, need, RESOLVE_TAU, start if basis is None else None, h0)
                if SUBSPACE and n > SMALL_EIG and not direct else None)
         if sub is not None:
             w, v, k_sub = sub
