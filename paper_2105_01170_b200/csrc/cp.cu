@@ -724,6 +724,10 @@ __device__ void pinv_block(const double* __restrict__ g0, const double* __restri
 // eigen path's: rotate while |(J^T V J)_pq| > 1e-15 ||V||_F, then
 // pinv(V) = sum_{|lambda_k| > 1e-15 max|lambda|} J_k J_k^T / lambda_k with
 // lambda_k = (J^T V J)_kk (numpy's rcond cutoff, decomp.py:387).
+template <int NP>
+__device__ __noinline__ bool chol_inv_reg(const double* __restrict__ g0, const double* __restrict__ g1,
+                                          int R, double* __restrict__ vp, double* sc);
+
 __device__ long long g_pinv1s_dbg[2];  // sweeps, cycles of the last call (diagnostics)
 
 // Warm start (jstore != nullptr, warm != 0): W = V J_prev, J = J_prev with
@@ -752,77 +756,16 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
     jv[i] = (r == col) ? 1.0 : 0.0;
     ss = fma(v, v, ss);
   }
-  // ---- well-conditioned V: Cholesky inverse by this warp in shared memory
-  // (no CTA barriers), accepted on the same test as pinv_block (kappa_1 <=
-  // 1e12, where numpy's pinv is the inverse to ~kappa eps)
+  // ---- well-conditioned V: register-resident Cholesky inverse (chol_inv_reg),
+  // accepted on pinv_block's test (kappa_1 <= 1e12, where numpy's pinv is
+  // the inverse to ~kappa eps)
   {
-#pragma unroll
-    for (int i = 0; i < ROWS; ++i) ws[r0 + i][col] = w[i];
-    __syncwarp();
-    // ||V||_1 (lanes < R take a column each)
-    double c1 = 0.0;
-    if (lane < R)
-      for (int r = 0; r < R; ++r) c1 += fabs(ws[r][lane]);
-    double vn1 = c1;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) vn1 = fmax(vn1, __shfl_xor_sync(0xffffffffu, vn1, o));
-    int ok = 1;
-    double lo = INFINITY, hi = 0.0;
-    for (int k = 0; k < R && ok; ++k) {
-      const double d = ws[k][k];
-      if (!(d > 0.0)) {
-        ok = 0;
-        break;
-      }
-      const double rl = rsqrt_nr(d), lkk = d * rl;
-      lo = fmin(lo, lkk);
-      hi = fmax(hi, lkk);
-      __syncwarp();
-      if (lane > k && lane < R) ws[lane][k] *= rl;
-      if (lane == 0) {
-        ws[k][k] = lkk;
-        isg[k] = rl;  // 1 / l_kk for the substitution below
-      }
-      __syncwarp();
-      // trailing lower triangle j <= i, i, j > k: one row per lane
-      if (lane > k && lane < R) {
-        const double lik = ws[lane][k];
-        for (int j = k + 1; j <= lane; ++j) ws[lane][j] -= lik * ws[j][k];
-      }
-      __syncwarp();
-    }
-    // kappa_2 >= (max l_kk / min l_kk)^2: hopeless cases skip the inverse
-    if (ok && (hi / lo) * (hi / lo) > 1e12 * R) ok = 0;
+    const bool ok = chol_inv_reg<NP == 32 ? 16 : NP>(g0, g1, R, vp, &ws[0][0]);
     if (ok) {
-      // Y = L^-1, one column per lane (forward substitution on e_lane)
-      if (lane < R) {
-        for (int i = 0; i < R; ++i) {
-          double acc = (i == lane) ? 1.0 : 0.0;
-          for (int k = lane; k < i; ++k) acc -= ws[i][k] * js[k][lane];
-          js[i][lane] = (i < lane) ? 0.0 : acc * isg[i];
-        }
-      }
-      __syncwarp();
-      // V^-1 = Y^T Y (into ws: L is no longer needed) and its 1-norm
-      for (int idx = lane; idx < R * R; idx += 32) {
-        const int r = idx / R, c = idx % R;
-        double v = 0.0;
-        for (int k = (r > c ? r : c); k < R; ++k) v = fma(js[k][r], js[k][c], v);
-        ws[r][c] = v;
-        vp[idx] = v;
-      }
-      __syncwarp();
-      double in1 = 0.0;
-      if (lane < R)
-        for (int r = 0; r < R; ++r) in1 += fabs(ws[r][lane]);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) in1 = fmax(in1, __shfl_xor_sync(0xffffffffu, in1, o));
-      if (vn1 * in1 <= 1e12) {
-        // vp holds V^-1 (== pinv).  No rotation was formed: mark the stored
-        // one stale so the next warm call of this mode starts cold
-        if (jstore != nullptr && lane == 0) jstore[0] = __longlong_as_double(0x7ff8dead0000dead);
-        return;
-      }
+      // no rotation was formed: mark the stored one stale so the next warm
+      // call of this mode starts cold
+      if (jstore != nullptr && lane == 0) jstore[0] = __longlong_as_double(0x7ff8dead0000dead);
+      return;
     }
     __syncwarp();
   }
@@ -1024,6 +967,83 @@ __device__ __forceinline__ double small_block_sum(double v, double* red) {
 // syncs only): the fast path of pinv_block (V^-1 = L^-T L^-1, accepted when
 // ||V||_1 ||V^-1||_1 <= 1e12).  Returns false (warp-uniform) when the caller
 // must take pinv_block's eigen path.  a, y: R x (R+1) scratch each.
+// Register-resident variant for R <= NP (8 or 16): lane i holds row i of V
+// (rows past R padded with the identity), the Cholesky steps are unrolled so
+// every row / column index is static -- L's column k reaches the other lanes
+// by shuffles, nothing goes through memory until Y = L^-1 is formed (one row
+// of Y per lane, rows of L by shuffle), and V^-1 = Y^T Y is read back from
+// shared memory.  Same acceptance test as pinv_warp_chol.  sc: >= NP*(NP+1)
+// doubles of shared scratch.
+template <int NP>
+__device__ __noinline__ bool chol_inv_reg(const double* __restrict__ g0, const double* __restrict__ g1,
+                                          int R, double* __restrict__ vp, double* sc) {
+  const int lane = threadIdx.x & 31;
+  const int i = lane < NP ? lane : NP - 1;   // lanes past NP mirror the last row (results unused)
+  double row[NP];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    double v = (i == j) ? 1.0 : 0.0;
+    if (i < R && j < R) v = g1 ? g0[i * R + j] * g1[i * R + j] : g0[i * R + j];
+    row[j] = v;
+  }
+  // ||V||_1 = max column sum = max row sum (symmetric)
+  double rs = 0.0;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) rs += (j < R && i < R) ? fabs(row[j]) : 0.0;
+  double vn1 = rs;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) vn1 = fmax(vn1, __shfl_xor_sync(0xffffffffu, vn1, o));
+  int ok = 1;
+  double lo = INFINITY, hi = 0.0, rdiag[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const double d = __shfl_sync(0xffffffffu, row[k], k);
+    ok &= (d > 0.0);
+    const double r = rsqrt_nr(fmax(d, 1e-300));
+    rdiag[k] = r;
+    lo = fmin(lo, d * r);
+    hi = fmax(hi, d * r);
+    const double lik = (i == k) ? d * r : row[k] * r;   // L[i][k] (lane i > k), L[k][k]
+    row[k] = (i >= k) ? lik : 0.0;
+#pragma unroll
+    for (int j = k + 1; j < NP; ++j) {
+      const double ljk = __shfl_sync(0xffffffffu, lik, j);
+      if (i >= j) row[j] -= lik * ljk;
+    }
+  }
+  if (!ok || (hi / lo) * (hi / lo) > 1e12 * R) return false;   // warp-uniform
+  // Y = L^-1: lane c builds column c, y_m = -(sum_{k<m} L[m][k] y_k) / L[m][m]
+  const int c = i;
+  double y[NP];
+#pragma unroll
+  for (int m = 0; m < NP; ++m) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < m; ++k) acc = fma(__shfl_sync(0xffffffffu, row[k], m), y[k], acc);
+    y[m] = (m < c) ? 0.0 : ((m == c) ? rdiag[m] : -acc * rdiag[m]);
+  }
+  // V^-1 = Y^T Y through shared memory (column c of Y from lane c)
+  __syncwarp();
+  if (lane < NP)
+#pragma unroll
+    for (int m = 0; m < NP; ++m) sc[m * (NP + 1) + lane] = y[m];
+  __syncwarp();
+  double in1 = 0.0;
+  for (int e = lane; e < R * R; e += 32) {
+    const int r0 = e / R, c0 = e % R;
+    double v = 0.0;
+#pragma unroll
+    for (int m = 0; m < NP; ++m) v = fma(sc[m * (NP + 1) + r0], sc[m * (NP + 1) + c0], v);
+    vp[e] = v;
+  }
+  __syncwarp();
+  if (lane < R)
+    for (int r0 = 0; r0 < R; ++r0) in1 += fabs(vp[r0 * R + lane]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) in1 = fmax(in1, __shfl_xor_sync(0xffffffffu, in1, o));
+  return vn1 * in1 <= 1e12;
+}
+
 __device__ bool pinv_warp_chol(const double* __restrict__ g0, const double* __restrict__ g1,
                                int R, double* __restrict__ vp, double* a, double* y) {
   const int lane = threadIdx.x & 31;
@@ -1128,7 +1148,9 @@ __global__ void __launch_bounds__(512)
   auto pinv_w0 = [&](int go0, int go1) {
     if ((tid >> 5) == 0) {
       const long long c0 = clock64();
-      const bool ok = pinv_warp_chol(G[go0], G[go1], R, Vp, smf, smf + R * (R + 1));
+      const bool ok = R <= 8 ? chol_inv_reg<8>(G[go0], G[go1], R, Vp, smf)
+                             : (R <= 16 ? chol_inv_reg<16>(G[go0], G[go1], R, Vp, smf)
+                                        : pinv_warp_chol(G[go0], G[go1], R, Vp, smf, smf + R * (R + 1)));
       if (tid == 0) pinv_ok = ok ? 1 : 0;
       if (it == 1 && tid == 0) g_small_clk[9 + go0 + go1] = clock64() - c0;
     }
@@ -1199,14 +1221,25 @@ __global__ void __launch_bounds__(512)
         double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
         const int64_t row = m0 + gq;
         const double* xr = X + (row < IJ ? row : 0) * K;
-        for (int k0 = 0; k0 < K; k0 += 4) {
-          const int kk = k0 + tq;
-          const double av = (row < IJ && kk < K) ? __ldg(xr + kk) : 0.0;
-          const double b0 = (kk < K && gq < R) ? F[2][kk * R + gq] : 0.0;
-          dmma884(c00, c01, av, b0);
-          if (R > 8) {
-            const double b1 = (kk < K && 8 + gq < R) ? F[2][kk * R + 8 + gq] : 0.0;
-            dmma884(c10, c11, av, b1);
+        // 8 X loads in flight per lane (32 k per chunk): the L2 latency is
+        // paid once per chunk instead of once per k-step
+        constexpr int UK = 8;
+        for (int k0 = 0; k0 < K; k0 += 4 * UK) {
+          double av[UK];
+#pragma unroll
+          for (int u = 0; u < UK; ++u) {
+            const int kk = k0 + 4 * u + tq;
+            av[u] = (row < IJ && kk < K) ? __ldg(xr + kk) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < UK; ++u) {
+            const int kk = k0 + 4 * u + tq;
+            const double b0 = (kk < K && gq < R) ? F[2][kk * R + gq] : 0.0;
+            dmma884(c00, c01, av[u], b0);
+            if (R > 8) {
+              const double b1 = (kk < K && 8 + gq < R) ? F[2][kk * R + 8 + gq] : 0.0;
+              dmma884(c10, c11, av[u], b1);
+            }
           }
         }
         if (row < IJ) {
