@@ -84,8 +84,13 @@ def like_input(ref, dev_tensor):
 def transpose(x):
     """x (rows, cols) device tensor -> contiguous (cols, rows) copy, by the
     library's tiled transpose kernel (layout plumbing of the matvec RHS)."""
-    x = x.contiguous()
+    if x.ndim != 2:
+        raise ValueError(f"transpose expects a matrix, got shape {tuple(x.shape)}")
+    # the kernel moves 8-byte elements: anything but fp64 goes through
+    # to_device's conversion first (an int / fp32 tensor would otherwise be
+    # reinterpreted as doubles)
+    x = to_device(x).contiguous()
     rows, cols = int(x.shape[0]), int(x.shape[1])
-    out = empty((cols, rows), dtype=x.dtype)
+    out = empty((cols, rows))
     _native.call("bt_transpose_f64", ptr(x), rows, cols, ptr(out), stream())
     return out

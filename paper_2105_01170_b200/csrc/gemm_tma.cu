@@ -195,7 +195,8 @@ int launch_at(const CUtensorMap& amap, const CUtensorMap& bmap, int64_t M, int64
 int bt_gemm_at_tma_ex(const double* a, int64_t lda, int64_t sAb, const double* b, int64_t ldb,
                       double* c, int64_t ldc, int64_t sCb, int64_t M, int64_t N, int64_t Kdim,
                       int64_t batch, int transpose_out, cudaStream_t st) {
-  const bool ok = M % 2 == 0 && lda % 2 == 0 && ldb % 2 == 0 && (transpose_out || ldc % 2 == 0) &&
+  const bool ok = M % 2 == 0 && lda % 2 == 0 && ldb % 2 == 0 &&
+                  (transpose_out || (ldc % 2 == 0 && (batch == 1 || sCb % 2 == 0))) &&
                   N % 2 == 0 && (batch == 1 || sAb % 2 == 0) &&
                   ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
                     reinterpret_cast<uintptr_t>(c)) & 15u) == 0 &&

@@ -5,10 +5,19 @@
 // tensor viewed as (outer, n_mode, inner).
 #include "gemm.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, int64_t ws_elems);
 int64_t bt_gemm_ws_elems(BtGemmArgs g, int64_t batch);
+int64_t bt_syrk_tma_ws_elems(int64_t n, int64_t kt_total);
+int bt_syrk_tma(const double* x, int64_t outer, int64_t n, int64_t inner, double* g, double* ws,
+                int64_t ws_elems, cudaStream_t st);
+// BT_SYRK_TMA=0: unfolding Grams on the cp.async engine (A/B runs)
+static bool use_syrk_tma() {
+  static const bool v = !(getenv("BT_SYRK_TMA") && getenv("BT_SYRK_TMA")[0] == '0');
+  return v;
+}
 int bt_gemm_at_tma_ex(const double* a, int64_t lda, int64_t sAb, const double* b, int64_t ldb,
                       double* c, int64_t ldc, int64_t sCb, int64_t M, int64_t N, int64_t Kdim,
                       int64_t batch, int transpose_out, cudaStream_t st);
@@ -95,7 +104,10 @@ BtGemmArgs ttm_args(const double* x, const View3& v, const double* u, int64_t ro
 extern "C" int64_t bt_unfold_gram_ws_bytes(const int64_t* dims, int order, int mode) {
   View3 v;
   if (!view3(dims, order, mode, v)) return 0;
-  return bt_gemm_ws_elems(gram_args(nullptr, v, nullptr), 1) * 8;
+  int64_t e = bt_gemm_ws_elems(gram_args(nullptr, v, nullptr), 1);
+  if (v.inner > 1)
+    e = std::max(e, bt_syrk_tma_ws_elems(v.n, v.outer * ((v.inner + 15) / 16)));
+  return e * 8;
 }
 
 extern "C" int bt_unfold_gram_f64(const double* x, const int64_t* dims, int order, int mode,
@@ -104,6 +116,12 @@ extern "C" int bt_unfold_gram_f64(const double* x, const int64_t* dims, int orde
   View3 v;
   BT_REQUIRE(view3(dims, order, mode, v), BT_E_SHAPE, "mode %d out of range for order-%d tensor",
              mode, order);
+  if (use_syrk_tma() && v.inner > 1 && v.n >= 64) {
+    // K-contiguous rows: the TMA-fed SYRK (lower 128-tiles, split reduction)
+    const int rc = bt_syrk_tma(x, v.outer, v.n, v.inner, g, static_cast<double*>(ws), ws_bytes / 8,
+                               bt_stream(stream));
+    if (rc != BT_E_VALUE) return rc;
+  }
   BtGemmArgs a = gram_args(x, v, g);
   a.ws = static_cast<double*>(ws);
   return bt_gemm_run(a, 1, bt_stream(stream), 0, ws_bytes / 8);
