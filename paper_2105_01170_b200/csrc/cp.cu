@@ -289,8 +289,9 @@ __global__ void __launch_bounds__(Cfg::THREADS + 32, 2)
 // with k & 7).  k = {0, 3, 12, 15} ^ d with d = {0, 1, 4, 5} per k-step
 // satisfies both and covers the 16 k of a stage.  The products per output
 // are the same; they are added in this fixed order (bit-reproducible).
-struct TreeTma {
-  static constexpr int BM = 128, BN = 64, BK = 16, STAGES = 4;
+template <int STAGES_, int MINB_>
+struct TreeTmaT {
+  static constexpr int BM = 128, BN = 64, BK = 16, STAGES = STAGES_, MINB = MINB_;
   static constexpr int WM = 2, WN = 2, THREADS = WM * WN * 32;
   static constexpr int TM = BM / WM, TN = BN / WN, FM = TM / 8, FN = TN / 8;
   static constexpr int A_STAGE = BM * BK;  // doubles
@@ -298,6 +299,7 @@ struct TreeTma {
   static constexpr int STAGE_BYTES = (A_STAGE + B_STAGE) * 8;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;  // + alignment slack
 };
+using TreeTma = TreeTmaT<4, 2>;
 
 __device__ __forceinline__ void tree_tma_issue(const CUtensorMap* xmap, const CUtensorMap* cmap,
                                                double* as, double* bs, uint64_t* bar, int k0, int m0,
@@ -309,11 +311,11 @@ __device__ __forceinline__ void tree_tma_issue(const CUtensorMap* xmap, const CU
     tma_load_2d(bs + q * 16 * TreeTma::BK, cmap, bar, n0 + 16 * q, k0, pol_c);
 }
 
-__global__ void __launch_bounds__(TreeTma::THREADS, 2)
+template <class T>
+__global__ void __launch_bounds__(T::THREADS, T::MINB)
     tree_p_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap cmap,
                       BtGemmArgs g, const double* __restrict__ Bf, int64_t R,
                       double* __restrict__ m1part, int64_t jtiles, int store_p) {
-  using T = TreeTma;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[T::WM][T::BN];
   __shared__ __align__(8) uint64_t full[T::STAGES];
@@ -1976,9 +1978,9 @@ int launch_tree_ws(const Plan& pl, const double* X, const double* C, const doubl
 
 // TMA tree kernel (default for R > 16 with K even; BT_TREE_CFG=9 keeps the
 // cp.async producer of tree_p_ws_kernel for A/B runs)
-int launch_tree_tma(const Plan& pl, const double* X, const double* C, const double* B, double* P,
+template <class T>
+int launch_tree_tma_t(const Plan& pl, const double* X, const double* C, const double* B, double* P,
                     double* m1part, int store_p, cudaStream_t st) {
-  using T = TreeTma;
   BtGemmArgs g{};
   g.M = pl.J;
   g.N = pl.R;
@@ -1996,17 +1998,24 @@ int launch_tree_tma(const Plan& pl, const double* X, const double* C, const doub
   BT_TRY(bt_tma_map_f64_2d(&cmap, C, pl.R, pl.K, pl.R, 16, T::BK));
   static bool attr = false;
   if (!attr) {
-    BT_CUDA_CHECK(cudaFuncSetAttribute(tree_p_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    BT_CUDA_CHECK(cudaFuncSetAttribute(tree_p_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        T::SMEM_BYTES));
     attr = true;
   }
   BT_REQUIRE(pl.I <= 65535, BT_E_SHAPE, "cp: mode-1 extent %lld exceeds 65535", (long long)pl.I);
   dim3 grid(static_cast<unsigned>(bt_cdiv(pl.J, T::BM)), static_cast<unsigned>(bt_cdiv(pl.R, T::BN)),
             static_cast<unsigned>(pl.I));
-  tree_p_tma_kernel<<<grid, T::THREADS, T::SMEM_BYTES, st>>>(xmap, cmap, g, B, pl.R, m1part, pl.jtiles,
+  tree_p_tma_kernel<T><<<grid, T::THREADS, T::SMEM_BYTES, st>>>(xmap, cmap, g, B, pl.R, m1part, pl.jtiles,
                                                             store_p);
   BT_LAUNCH_CHECK();
   return BT_OK;
+}
+
+// (a 3-stage, 3-CTA/SM variant was tried: at the 168-register cap it spills
+// ~300 bytes per thread, so the 4-stage, 2-CTA configuration stays)
+int launch_tree_tma(const Plan& pl, const double* X, const double* C, const double* B, double* P,
+                    double* m1part, int store_p, cudaStream_t st) {
+  return launch_tree_tma_t<TreeTma>(pl, X, C, B, P, m1part, store_p, st);
 }
 
 template <int BN, int V, int VAR = 0>
