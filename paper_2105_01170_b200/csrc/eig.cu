@@ -39,7 +39,7 @@ constexpr int INNER_SWEEPS = 2;  // Jacobi sweeps per 64x64 pair subproblem and 
 
 __global__ void __launch_bounds__(1024)
     syevd_small_kernel(const double* __restrict__ a, int n, const double* __restrict__ sumsq,
-                       double* __restrict__ dout, double* __restrict__ qout, int np) {
+                       double* __restrict__ dout, double* __restrict__ qout, int np, int max_sweeps) {
   extern __shared__ __align__(16) double sm[];
   const int ld = np + 1;
   double* s = sm;
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(1024)
     s[r * ld + c] = (r < n && c < n) ? a[r * n + c] : (r == c ? pad : 0.0);
   }
   __syncthreads();
-  jacobi_fast(s, q, np, ld, cs, sn, pp, qq, 60, ABS_TOL * nrm, 1e-15);
+  jacobi_fast(s, q, np, ld, cs, sn, pp, qq, max_sweeps, ABS_TOL * nrm, 1e-15);
   __syncthreads();
   for (int i = threadIdx.x; i < np; i += blockDim.x) dout[i] = s[i * ld + i];
   for (int idx = threadIdx.x; idx < np * np; idx += blockDim.x)
@@ -405,8 +405,20 @@ EigPlan eig_plan(int64_t n) {
 
 extern "C" int64_t bt_syevd_ws_bytes(int64_t n) { return eig_plan(n).total * 8; }
 
+// max_sweeps caps the one-CTA Jacobi (n <= 96; 60 = run to convergence): a
+// truncated solve still returns an orthogonal V and the Rayleigh quotients of
+// its columns, which is all a first Rayleigh-Ritz of a subspace iteration
+// needs (subspace.cu)
+int bt_syevd_sweeps(const double* a, int64_t n, double* w, double* v, void* wsv, int64_t ws_bytes,
+                    void* stream, int max_sweeps);
+
 extern "C" int bt_syevd_f64(const double* a, int64_t n, double* w, double* v, void* wsv,
                             int64_t ws_bytes, void* stream) {
+  return bt_syevd_sweeps(a, n, w, v, wsv, ws_bytes, stream, 60);
+}
+
+int bt_syevd_sweeps(const double* a, int64_t n, double* w, double* v, void* wsv, int64_t ws_bytes,
+                    void* stream, int max_sweeps) {
   BT_NVTX("bt_syevd_f64");
   BT_REQUIRE(n >= 1, BT_E_SHAPE, "syevd: empty matrix");
   cudaStream_t st = bt_stream(stream);
@@ -427,7 +439,7 @@ extern "C" int bt_syevd_f64(const double* a, int64_t n, double* w, double* v, vo
       attr = true;
     }
     syevd_small_kernel<<<1, 1024, sm, st>>>(a, static_cast<int>(n), ss, d, q,
-                                           static_cast<int>(p.np));
+                                           static_cast<int>(p.np), max_sweeps);
     BT_LAUNCH_CHECK();
   } else {
     static bool attr = false;

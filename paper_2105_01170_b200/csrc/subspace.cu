@@ -25,6 +25,8 @@
 #include "jacobi.cuh"  // rsqrt_nr
 
 int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, int64_t ws_elems);
+int bt_syevd_sweeps(const double* a, int64_t n, double* w, double* v, void* ws, int64_t ws_bytes,
+                    void* stream, int max_sweeps);
 int64_t bt_gemm_ws_elems(BtGemmArgs g, int64_t batch);
 
 extern "C" {
@@ -49,6 +51,7 @@ constexpr int SUB_MAX_ITERS = 10;
 // iterations: at b = 96 it converges at lambda_97 / lambda_64 ~ 0.31 per
 // iteration, ~0.2 ms each, well under the tridiagonal solver's ~15 ms
 constexpr int SUB_MAX_ITERS_COLD = 32;
+constexpr int RR_ROUGH_SWEEPS = 4;
 
 // BT_SUB_SKIP_RR=0: a Rayleigh-Ritz every iteration for cold blocks too
 bool no_skip_rr() {
@@ -97,73 +100,188 @@ __global__ void copy_cols_kernel(const double* __restrict__ src, int64_t ld_src,
 // the inverse of its transposed factor: rinv = L^-T, so Y D rinv has
 // orthonormal columns (CholeskyQR).  status = 0 ok, 1 when a pivot falls
 // below CHOL_MIN_PIVOT (cond(m) too large for one CholeskyQR + Newton-Schulz
-// step: the caller takes the eigenvalue-based SVQB instead).
+// step: the caller takes the eigenvalue-based SVQB instead); a failure also
+// sets *sticky when given (the deferred check of the power steps).
+//
+// Blocked right-looking, 32-column panels (m padded with identity to a
+// multiple of 32): warp 0 factors the diagonal block in registers (lane =
+// row, pivots and L columns by shuffle) and inverts it (lane = column of
+// L11^-1, L11 rows broadcast from shared memory); all warps form
+// L21 = A21 L11^-T and the trailing update.  The off-diagonal blocks of X = L^-1 follow by block
+// distance: X_ij = -X_ii sum_{j <= k < i} L_ik X_kj.  Three panels and
+// ~10 CTA barriers at b = 96: 54 us, where the element-wise version took one
+// barrier per column and ran 131 us (the three one-warp diagonal blocks are
+// most of what is left).
 constexpr double CHOL_MIN_PIVOT = 1e-6;
 constexpr int CHOL_MAXB = 96;
+constexpr int CHOL_CB = 32;
+constexpr int CHOL_THREADS = 256;
 
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(CHOL_THREADS)
     chol_rinv_kernel(const double* __restrict__ m, int b, double* __restrict__ rinv,
-                     int* __restrict__ status) {
-  // Right-looking Cholesky and right-looking L^-1, both element-parallel per
-  // step (one CTA barrier per step; every thread's loads of a step are issued
-  // before its stores).  a: working matrix (unscaled pivot column read in the
-  // update of its step), l: L by columns, x: L^-1.
+                     int* __restrict__ status, int* __restrict__ sticky) {
+  constexpr int CB = CHOL_CB;
+  constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) double chol_sm[];
-  const int ld = b + 1;
-  double* a = chol_sm;
-  double* x = a + b * ld;
+  const int bp = (b + CB - 1) / CB * CB, P = bp / CB, ld = bp + 1;
+  double* a = chol_sm;      // L (lower); upper off-diagonal blocks: scratch T
+  double* x = a + bp * ld;  // X = L^-1 (lower)
   __shared__ double rdiag[CHOL_MAXB];
   __shared__ int bad;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   if (tid == 0) bad = 0;
-  for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e - i * b;
-    a[i * ld + j] = m[e];
+  // m (b x b, in L2) -> a: eight loads in flight per thread
+  for (int e0 = tid; e0 < bp * bp; e0 += 8 * nt) {
+    double vv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * nt, i = e / bp, j = e - i * bp;
+      vv[u] = (e < bp * bp && i < b && j < b) ? m[i * b + j] : (i == j ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * nt, i = e / bp, j = e - i * bp;
+      if (e < bp * bp) {
+        a[i * ld + j] = vv[u];
+        x[i * ld + j] = 0.0;
+      }
+    }
   }
   __syncthreads();
-  for (int k = 0; k < b; ++k) {
-    const double piv = a[k * ld + k];
-    if (!(piv > CHOL_MIN_PIVOT)) {
-      if (tid == 0) bad = 1;
-      break;  // uniform: every thread read the same pivot
+  for (int p = 0; p < P; ++p) {
+    const int o = p * CB;
+    if (warp == 0) {
+      // lane = row; fully unrolled (a rolled k loop with shifted registers
+      // measured 1.7x slower: one warp, latency bound either way)
+      double r[CB];
+#pragma unroll
+      for (int j = 0; j < CB; ++j) r[j] = a[(o + lane) * ld + o + j];
+      bool ok = true;
+      double rdg = 0.0;
+#pragma unroll
+      for (int k = 0; k < CB; ++k) {
+        const double piv = __shfl_sync(FULL, r[k], k);
+        ok = ok && (piv > CHOL_MIN_PIVOT);
+        const double rk = rsqrt_nr(fmax(piv, CHOL_MIN_PIVOT));
+        const double lik = (lane >= k) ? r[k] * rk : 0.0;
+        if (lane == k) rdg = rk;
+        r[k] = lik;
+#pragma unroll
+        for (int j = k + 1; j < CB; ++j) r[j] = fma(-lik, __shfl_sync(FULL, lik, j), r[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < CB; ++j) a[(o + lane) * ld + o + j] = r[j];
+      rdiag[o + lane] = rdg;
+      if (lane == 0 && !ok) bad = 1;
+      __syncwarp();
+      // column `lane` of L11^-1: x_jj = 1 / l_jj, x_ij = -(sum_{j <= k < i} l_ik x_kj) / l_ii
+      // (four partial sums: the chain per row is the last term only)
+      double xc[CB];
+#pragma unroll
+      for (int i = 0; i < CB; ++i) {
+        double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < i - 1; ++k) s4[k & 3] = fma(a[(o + i) * ld + o + k], xc[k], s4[k & 3]);
+        double s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+        if (i >= 1) s = fma(a[(o + i) * ld + o + i - 1], xc[i - 1], s);
+        const double ri = rdiag[o + i];
+        xc[i] = (i == lane) ? ri : ((i > lane) ? -s * ri : 0.0);
+      }
+#pragma unroll
+      for (int i = 0; i < CB; ++i) x[(o + i) * ld + o + lane] = xc[i];
     }
-    const double r = rsqrt_nr(piv), rd = r * r;
-    if (tid == 0) rdiag[k] = r;
-    // trailing lower triangle (i, j), k < j <= i: warps take rows, lanes columns
-    const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
-    for (int i = k + 1 + warp; i < b; i += nwarp) {
-      const double f = a[i * ld + k] * rd;
-      for (int j = k + 1 + lane; j <= i; j += 32) a[i * ld + j] -= f * a[j * ld + k];
+    __syncthreads();
+    if (bad) break;
+    // L21 = A21 L11^-T, a warp per row
+    for (int rr = o + CB + warp; rr < bp; rr += nw) {
+      const double av = a[rr * ld + o + lane];
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < CB; ++k)
+        s4[k & 3] = fma(__shfl_sync(FULL, av, k), x[(o + lane) * ld + o + k], s4[k & 3]);
+      a[rr * ld + o + lane] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    }
+    __syncthreads();
+    // trailing lower triangle: A22 -= L21 L21^T, 4 x 4 blocks per thread
+    const int t0 = o + CB, nq = (bp - t0) / 4;
+    for (int e = tid; e < nq * nq; e += nt) {
+      const int bi = e / nq, bj = e - bi * nq;
+      if (bj > bi) continue;
+      const int i0 = t0 + 4 * bi, j0 = t0 + 4 * bj;
+      double acc[4][4] = {};
+#pragma unroll 4
+      for (int k = 0; k < CB; ++k) {
+        double ai[4], aj[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ai[u] = a[(i0 + u) * ld + o + k];
+          aj[u] = a[(j0 + u) * ld + o + k];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int w = 0; w < 4; ++w) acc[u][w] = fma(ai[u], aj[w], acc[u][w]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          if (j0 + w <= i0 + u) a[(i0 + u) * ld + j0 + w] -= acc[u][w];
     }
     __syncthreads();
   }
   if (bad) {
-    if (tid == 0) *status = 1;
+    if (tid == 0) {
+      *status = 1;
+      if (sticky != nullptr) *sticky = 1;
+    }
     return;
   }
-  // L = a's lower triangle scaled column-wise by rdiag (l_ik = a_ik r_k), in
-  // place; the diagonal becomes l_kk = a_kk r_k
-  for (int e = tid; e < b * b; e += nt) {
-    const int i = e / b, j = e - i * b;
-    if (j <= i) a[i * ld + j] *= rdiag[j];
-    x[i * ld + j] = (i == j) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  // X = L^-1, right-looking: row k /= l_kk, then rows i > k -= l_ik row k
-  // (columns c <= k are the only nonzeros of row k)
-  for (int k = 0; k < b; ++k) {
-    const double rk = rdiag[k];  // 1 / l_kk
-    // scale row k (columns 0..k) -- read by the update of this step only
-    // through xk below, so it is folded in: x_ic -= l_ik * (x_kc * rk)
-    {
-      const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
-      for (int i = k + 1 + warp; i < b; i += nwarp) {
-        const double f = a[i * ld + k] * rk;
-        for (int c = lane; c <= k; c += 32) x[i * ld + c] -= f * x[k * ld + c];
+  // off-diagonal blocks of X by block distance d (4 x 4 register blocks)
+  constexpr int QB = CB / 4;
+  for (int d = 1; d < P; ++d) {
+    const int cnt = (P - d) * QB * QB;
+    for (int e = tid; e < cnt; e += nt) {
+      const int i = d + e / (QB * QB), rc = e % (QB * QB), r0 = 4 * (rc / QB), c0 = 4 * (rc % QB), j = i - d;
+      double acc[4][4] = {};
+      for (int k = j * CB; k < i * CB; ++k) {
+        double ar[4], xk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ar[u] = a[(i * CB + r0 + u) * ld + k];
+          xk[u] = x[k * ld + j * CB + c0 + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int w = 0; w < 4; ++w) acc[u][w] = fma(ar[u], xk[w], acc[u][w]);
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) a[(j * CB + r0 + u) * ld + i * CB + c0 + w] = acc[u][w];  // T_ij in the free upper block (j, i)
     }
     __syncthreads();
-    for (int c = tid; c <= k; c += nt) x[k * ld + c] *= rk;
+    for (int e = tid; e < cnt; e += nt) {
+      const int i = d + e / (QB * QB), rc = e % (QB * QB), r0 = 4 * (rc / QB), c0 = 4 * (rc % QB), j = i - d;
+      double acc[4][4] = {};
+      for (int t = 0; t < r0 + 4; ++t) {
+        double xr[4], tk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          xr[u] = x[(i * CB + r0 + u) * ld + i * CB + t];   // zero above the diagonal
+          tk[u] = a[(j * CB + t) * ld + i * CB + c0 + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int w = 0; w < 4; ++w) acc[u][w] = fma(xr[u], tk[w], acc[u][w]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) x[(i * CB + r0 + u) * ld + j * CB + c0 + w] = -acc[u][w];
+    }
     __syncthreads();
   }
   for (int e = tid; e < b * b; e += nt) {
@@ -250,15 +368,15 @@ struct Ctx {
     g.ws = ws + p.off_gws;
     return bt_gemm_run(g, 1, st, 0, p.gemm_ws);
   }
-  int eig(const double* a, int64_t b, double* w, double* v) const {
-    return bt_syevd_f64(a, b, w, v, ws + p.off_ews, p.eig_ws * 8, st);
+  int eig(const double* a, int64_t b, double* w, double* v, int max_sweeps = 60) const {
+    return bt_syevd_sweeps(a, b, w, v, ws + p.off_ews, p.eig_ws * 8, st, max_sweeps);
   }
 };
 
 // Column-scaled SVQB of y (n x b, row-major) into q (n x keep); returns keep
 // (0 when y is numerically zero) through *keep and the dropped count.
 int svqb(const Ctx& c, const double* y, int64_t n, int64_t b, double* q, int64_t* keep_out,
-         int64_t* dropped) {
+         int64_t* dropped, int* sticky = nullptr) {
   const Plan& p = c.p;
   double* m = c.at(p.off_m);
   double* ms = c.at(p.off_ms);
@@ -273,7 +391,8 @@ int svqb(const Ctx& c, const double* y, int64_t n, int64_t b, double* q, int64_t
     // well-conditioned block (the usual case once Q holds Ritz vectors):
     // CholeskyQR  Q = Y D L^-T  + the Newton-Schulz polish
     int* flag = reinterpret_cast<int*>(c.at(p.off_flag));
-    const size_t smb = sizeof(double) * 2 * b * (b + 1);
+    const int64_t bp = (b + CHOL_CB - 1) / CHOL_CB * CHOL_CB;
+    const size_t smb = sizeof(double) * 2 * bp * (bp + 1);
     static bool attr = false;
     if (!attr) {
       BT_CUDA_CHECK(cudaFuncSetAttribute(chol_rinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -281,11 +400,15 @@ int svqb(const Ctx& c, const double* y, int64_t n, int64_t b, double* q, int64_t
                                                           (CHOL_MAXB + 1))));
       attr = true;
     }
-    chol_rinv_kernel<<<1, 1024, smb, c.st>>>(ms, static_cast<int>(b), v2, flag);
+    chol_rinv_kernel<<<1, CHOL_THREADS, smb, c.st>>>(ms, static_cast<int>(b), v2, flag, sticky);
     BT_LAUNCH_CHECK();
-    int hflag = 1;
-    BT_CUDA_CHECK(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, c.st));
-    BT_CUDA_CHECK(cudaStreamSynchronize(c.st));
+    int hflag = 0;
+    if (sticky == nullptr) {
+      // a deferred check (sticky given) assumes success; the caller reads the
+      // sticky flag once after its run of steps
+      BT_CUDA_CHECK(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+      BT_CUDA_CHECK(cudaStreamSynchronize(c.st));
+    }
     if (hflag == 0) {
       BtGemmArgs g = gemm_args(n, b, b, y, b, 1, v2, b, 1, out);
       g.ascale = dinv;
@@ -386,7 +509,11 @@ extern "C" int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need,
     BT_TRY(c.gemm(gemm_args(bq, bq, n, q, 1, bq, gq, bq, 1, h)));    // Q^T G Q
     sym_kernel<<<grid_for(bq * bq), 256, 0, c.st>>>(h, bq, hs);
     BT_LAUNCH_CHECK();
-    BT_TRY(c.eig(hs, bq, w, sm));                                    // descending
+    // the first Rayleigh-Ritz of a cold many-pair block only orients the
+    // block and estimates the rate: a few Jacobi sweeps (its pairs are never
+    // accepted, see below)
+    const bool rough = skip_rr && it == 0 && start == nullptr;
+    BT_TRY(c.eig(hs, bq, w, sm, rough ? RR_ROUGH_SWEEPS : 60));       // descending
     BT_TRY(c.gemm(gemm_args(n, bq, bq, q, bq, 1, sm, bq, 1, v)));    // V = Q S
     double* gv = c.at(p.off_gv);
     BT_TRY(c.gemm(gemm_args(n, bq, bq, gq, bq, 1, sm, bq, 1, gv)));  // G V = (G Q) S
@@ -408,7 +535,7 @@ extern "C" int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need,
     if (dbg)
       fprintf(stderr, "[subspace n=%lld b=%lld] it %d: k %lld max resid/theta1 %.2e\n",
               (long long)n, (long long)b, it, (long long)k, worst / top);
-    if (worst <= target) {
+    if (worst <= target && !rough) {
       BT_TRY(bt_sign_fix_f64(v, n, bq, c.st));
       *bq_out = bq;
       *k_out = k;
@@ -452,13 +579,22 @@ extern "C" int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need,
       // two applications of G per orthonormalisation (Q's columns are near
       // eigenvectors, so the column-scaled G^2 Q stays well conditioned)
       double* gq2 = c.at(p.off_gq);
+      // CholeskyQR failures are checked once after the run (sticky flag)
+      int* sticky = reinterpret_cast<int*>(c.at(p.off_flag)) + 1;
+      BT_CUDA_CHECK(cudaMemsetAsync(sticky, 0, sizeof(int), c.st));
       for (int j = 0; j < m; j += 2) {
         const bool two = j + 1 < m;
         BT_TRY(c.gemm(gemm_args(n, bq, n, g, n, 1, q, bq, 1, two ? gq2 : y)));   // G Q
         if (two) BT_TRY(c.gemm(gemm_args(n, bq, n, g, n, 1, gq2, bq, 1, y)));   // G (G Q)
         int64_t nq = 0, dr = 0;
-        BT_TRY(svqb(c, y, n, bq, q, &nq, &dr));
+        BT_TRY(svqb(c, y, n, bq, q, &nq, &dr, sticky));
         if (nq != bq) return BT_OK;  // the block lost directions: let the caller fall back
+      }
+      if (m > 0) {
+        int hs = 0;
+        BT_CUDA_CHECK(cudaMemcpyAsync(&hs, sticky, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+        BT_CUDA_CHECK(cudaStreamSynchronize(c.st));
+        if (hs != 0) return BT_OK;  // a step lost conditioning: the caller falls back
       }
       it += m;
       steps_since_rr = m + 1;
