@@ -731,12 +731,12 @@ __device__ __noinline__ bool chol_inv_reg(const double* __restrict__ g0, const d
                                           int R, double* __restrict__ vp, double* sc);
 
 __device__ long long g_pinv1s_dbg[2];  // sweeps, cycles of the last call (diagnostics)
+__device__ long long g_pinv1s_log[512];  // (sweeps << 40 | cycles) per call, ring (diagnostics)
+__device__ unsigned g_pinv1s_n;
 
-// Warm start (jstore != nullptr, warm != 0): W = V J_prev, J = J_prev with
-// J_prev the rotation this kernel stored for the same mode on its previous
-// call -- ALS changes V little from sweep to sweep, so V J_prev is already
-// nearly column-orthogonal and the sweeps drop from ~8-15 to a few.  The
-// converged factorisation (and the cutoff) is the same up to rounding.
+// One-warp pinv of V = g0 o g1 (R <= NP).  jstore / warm are kept for the
+// launch signature (the warm start from the previous sweep's rotation was
+// dropped: ALS changes C4's V too much between sweeps for it to help).
 template <int NP>
 __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restrict__ g0,
                                                           const double* __restrict__ g1, int R,
@@ -747,17 +747,7 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
   __shared__ double js[NP][NP + 1], ws[NP][NP + 1], isg[NP];
   const int lane = threadIdx.x;
   const int col = lane % NP, half = lane / NP, r0 = half * ROWS;
-  double w[ROWS], jv[ROWS];
-  double ss = 0.0;
-#pragma unroll
-  for (int i = 0; i < ROWS; ++i) {
-    const int r = r0 + i;
-    double v = 0.0;
-    if (r < R && col < R) v = g1 ? g0[r * R + col] * g1[r * R + col] : g0[r * R + col];
-    w[i] = v;
-    jv[i] = (r == col) ? 1.0 : 0.0;
-    ss = fma(v, v, ss);
-  }
+  double w[ROWS];
   // ---- well-conditioned V: register-resident Cholesky inverse (chol_inv_reg),
   // accepted on pinv_block's test (kappa_1 <= 1e12, where numpy's pinv is
   // the inverse to ~kappa eps)
@@ -771,35 +761,65 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
     }
     __syncwarp();
   }
-  // a stale store (the previous call took the Cholesky path) or a non-finite
-  // one falls back to the cold start
-  if (jstore != nullptr && warm && isfinite(jstore[0])) {
+  // ---- ill-conditioned / singular V.  Stage 1: Cholesky with diagonal
+  // pivoting in shared memory, V = L L^T with L's columns in pivot order
+  // (rows stay in V's order: no permutation to undo), stopped at the first
+  // pivot below NP eps max(diag V) -- the Schur complement is rounding noise
+  // of V from there on.  Stage 2: one-sided Jacobi on the COLUMNS of L
+  // (L W = U Sigma, so V = U Sigma^2 U^T): L^T L is far closer to diagonal
+  // than V, the columns carry their own scale (a pair is rotated while
+  // |w_p . w_q| > 1e-15 |w_p| |w_q|, no absolute floor needed) and no
+  // eigenvector accumulator is kept -- 5-6 sweeps where Jacobi on V itself
+  // took 10-14 (C4's mode-3 normal matrices, cond ~1e18) and each round
+  // moves half the data.  pinv = sum over sigma_k^2 > 1e-15 max sigma^2 of
+  // w_k w_k^T / sigma_k^4 (numpy's rcond on the eigenvalues sigma^2).
+  (void)warm;
+  if (jstore != nullptr && lane == 0) jstore[0] = __longlong_as_double(0x7ff8dead0000dead);
+  double d0 = 0.0;
+  for (int idx = lane; idx < NP * NP; idx += 32) {
+    const int r = idx / NP, c = idx % NP;
+    double v = 0.0;
+    if (r < R && c < R) v = g1 ? g0[r * R + c] * g1[r * R + c] : g0[r * R + c];
+    ws[r][c] = v;
+    js[r][c] = 0.0;
+    if (r == c) d0 = fmax(d0, v);
+  }
 #pragma unroll
-    for (int i = 0; i < ROWS; ++i) {
-      ws[r0 + i][col] = w[i];                       // V (symmetric)
-      js[r0 + i][col] = jstore[(r0 + i) * NP + col];
+  for (int o = 16; o > 0; o >>= 1) d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
+  __syncwarp();
+  const double piv_floor = NP * 2.220446049250313e-16 * d0;
+  unsigned done = 0u;
+  for (int k = 0; k < R; ++k) {
+    double dv = (lane < NP && !((done >> lane) & 1u)) ? ws[lane][lane] : -1.0;
+    int di = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, dv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, di, o);
+      if (ov > dv || (ov == dv && oi < di)) {
+        dv = ov;
+        di = oi;
+      }
     }
+    if (!(dv > piv_floor)) break;
+    const double piv = sqrt(dv), inv = 1.0 / piv;
+    if (lane < NP) {
+      double l = 0.0;
+      if (lane == di) l = piv;
+      else if (!((done >> lane) & 1u)) l = ws[lane][di] * inv;
+      js[lane][k] = l;
+    }
+    done |= 1u << di;
     __syncwarp();
-#pragma unroll
-    for (int i = 0; i < ROWS; ++i) {
-      double acc = 0.0;
-      for (int k = 0; k < NP; ++k) acc = fma(ws[r0 + i][k], js[k][col], acc);
-      w[i] = acc;
-      jv[i] = js[r0 + i][col];
+    for (int idx = lane; idx < NP * NP; idx += 32) {
+      const int r = idx / NP, c = idx % NP;
+      if (!((done >> r) & 1u) && !((done >> c) & 1u)) ws[r][c] = fma(-js[r][k], js[c][k], ws[r][c]);
     }
     __syncwarp();
   }
-  // ||V||_F^2: each element counted once (lanes hold disjoint pieces)
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  // columns below 1e-14 ||V||_F lie within ~10x of numpy's cutoff (1e-15
-  // sigma_max, sigma_max >= ||V||_F / sqrt(R)): their directions are rounding
-  // noise of V (known to ~eps ||V||_F), so pairs involving one are not
-  // rotated (else near-null spaces keep the sweeps going on noise)
-  // stopping rule of the two-sided eigen path (pinv_block): a pair is rotated
-  // while its entry of J^T V J (= J_p . W_q) exceeds 1e-15 ||V||_F -- V is
-  // known only to ~eps ||V||_F, so smaller off-diagonals are noise
-  const double abs_tol = 1e-15 * sqrt(ss);
+  for (int i = 0; i < ROWS; ++i) w[i] = js[r0 + i][col];
+  __syncwarp();
   // sum over the HALVES row blocks of a column in a fixed order (block 0
   // first), identical in every lane holding that column
   auto colsum = [&](double v) {
@@ -812,8 +832,8 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
   };
   const long long t_start = clock64();
   int sweeps_done = 0;
-  for (int sweep = 0; sweep < 40; ++sweep) {
-    int rotated = 0;
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    int big = 0;
     sweeps_done = sweep + 1;
     for (int rnd = 0; rnd < NP - 1; ++rnd) {
       int partner;
@@ -827,68 +847,50 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
         if (partner >= NP - 1) partner -= NP - 1;
       }
       const int src = partner + half * NP;
-      double pw[ROWS], pj[ROWS];
+      double pw[ROWS];
 #pragma unroll
-      for (int i = 0; i < ROWS; ++i) {
-        pw[i] = __shfl_sync(0xffffffffu, w[i], src);
-        pj[i] = __shfl_sync(0xffffffffu, jv[i], src);
-      }
+      for (int i = 0; i < ROWS; ++i) pw[i] = __shfl_sync(0xffffffffu, w[i], src);
       const bool lo = col < partner;
-      double a = 0.0, b = 0.0, g = 0.0, e = 0.0;
+      double a = 0.0, b = 0.0, g = 0.0;
 #pragma unroll
       for (int i = 0; i < ROWS; ++i) {
         const double wp = lo ? w[i] : pw[i], wq = lo ? pw[i] : w[i];
-        const double jp = lo ? jv[i] : pj[i];
         a = fma(wp, wp, a);
         b = fma(wq, wq, b);
         g = fma(wp, wq, g);
-        e = fma(jp, wq, e);          // (J^T V J)_pq
       }
       a = colsum(a);
       b = colsum(b);
       g = colsum(g);
-      e = colsum(e);
-      // rotate unless the pair is orthogonal to working precision
-      // (|g| <= 1e-15 sqrt(a b), compared squared: no IEEE sqrt on the
-      // round's critical path) or a column is below the noise floor
-      if (g != 0.0 && fabs(e) > abs_tol) {
+      const double g2 = g * g, ab = a * b;
+      if (g2 > 1e-30 * ab) {
         double c, s;
         jacobi_rotation(a, b, g, c, s);
-        rotated = 1;
+        // a sweep whose rotations all had |cos| <= 1e-8 leaves |cos| ~ 1e-16
+        // behind (quadratic convergence): it is the last one
+        if (g2 > 1e-16 * ab) big = 1;
 #pragma unroll
-        for (int i = 0; i < ROWS; ++i) {
-          if (lo) {
-            w[i] = c * w[i] - s * pw[i];
-            jv[i] = c * jv[i] - s * pj[i];
-          } else {
-            w[i] = s * pw[i] + c * w[i];
-            jv[i] = s * pj[i] + c * jv[i];
-          }
-        }
+        for (int i = 0; i < ROWS; ++i) w[i] = lo ? (c * w[i] - s * pw[i]) : (s * pw[i] + c * w[i]);
       }
     }
-    if (!__any_sync(0xffffffffu, rotated)) break;
+    if (!__any_sync(0xffffffffu, big)) break;
   }
   if (lane == 0) {
     g_pinv1s_dbg[0] = sweeps_done;
     g_pinv1s_dbg[1] = clock64() - t_start;
+    const unsigned slot = atomicAdd(&g_pinv1s_n, 1u);
+    g_pinv1s_log[slot & 511u] = ((long long)sweeps_done << 40) | (g_pinv1s_dbg[1] & 0xffffffffffll);
   }
-  // eigenvalues lambda_k = J_k . W_k = (J^T V J)_kk; pinv = sum over
-  // |lambda_k| > 1e-15 max |lambda| of J_k J_k^T / lambda_k -- the cutoff and
-  // formula of pinv_from_eig (numpy's rcond on the singular values |lambda|)
   double lk = 0.0;
 #pragma unroll
-  for (int i = 0; i < ROWS; ++i) lk = fma(jv[i], w[i], lk);
-  lk = colsum(lk);
-  double lmax = fabs(lk);
+  for (int i = 0; i < ROWS; ++i) lk = fma(w[i], w[i], lk);
+  lk = colsum(lk);   // sigma_k^2 = lambda_k
+  double lmax = lk;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-  if (half == 0) isg[col] = (fabs(lk) > 1e-15 * lmax) ? 1.0 / lk : 0.0;
+  if (half == 0) isg[col] = (lk > 1e-15 * lmax) ? 1.0 / (lk * lk) : 0.0;
 #pragma unroll
-  for (int i = 0; i < ROWS; ++i) {
-    js[r0 + i][col] = jv[i];
-    if (jstore != nullptr) jstore[(r0 + i) * NP + col] = jv[i];
-  }
+  for (int i = 0; i < ROWS; ++i) js[r0 + i][col] = w[i];
   __syncwarp();
   for (int idx = lane; idx < R * R; idx += 32) {
     const int r = idx / R, c = idx % R;
@@ -2887,4 +2889,13 @@ extern "C" int64_t bt_debug_pinv1s(int which) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(v, g_pinv1s_dbg, sizeof(v));
   return v[which & 1];
+}
+
+// diagnostics: the ring of (sweeps << 40 | cycles) entries; returns the call count
+extern "C" int64_t bt_debug_pinv1s_log(long long* out512) {
+  unsigned n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out512, g_pinv1s_log, 512 * sizeof(long long));
+  cudaMemcpyFromSymbol(&n, g_pinv1s_n, sizeof(n));
+  return n;
 }
