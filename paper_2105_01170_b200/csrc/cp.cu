@@ -2183,6 +2183,11 @@ int run_solve_finish(const Plan& pl, const CpState& s, const double* gbuf, int64
 
 }  // namespace
 
+// cp_mid.cu: the R <= 16 one-warp pinv of g0 o g1
+int bt_cp_pinv_small(const double* g0, const double* g1, int R, double* vp, cudaStream_t st) {
+  return run_pinv(g0, g1, R, vp, st);
+}
+
 // Explicit residual: Xhat_i = B diag(W_i) C^T with W = A * lam; the per-i
 // diagonal rides on the engine's A-scale (indexed by the reduction index r).
 namespace {
@@ -2665,6 +2670,11 @@ static int cp_small_try(const bt_cp_problem* pb, double* a, double* b, double* c
   return 1;
 }
 
+// cp_mid.cu: two-pass sweep for R <= 16 on tensors larger than one SM
+int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, double* lam,
+                  int max_iters, double tol, int fit_mode, double* fit_history, int* n_iters,
+                  int* converged, cudaStream_t st, int* rc);
+
 extern "C" int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, double* c,
                              double* lam, int max_iters, double tol, int fit_mode,
                              double* fit_history, int* n_iters, int* converged, double* phase_ms,
@@ -2674,6 +2684,9 @@ extern "C" int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, doub
     int rc = BT_OK;
     if (cp_small_try(pb, a, b, c, lam, max_iters, tol, fit_mode, fit_history, n_iters, converged,
                      bt_stream(stream), &rc))
+      return rc;
+    if (bt_cp_mid_try(pb, a, b, c, lam, max_iters, tol, fit_mode, fit_history, n_iters, converged,
+                      bt_stream(stream), &rc))
       return rc;
   }
   void* h = nullptr;
