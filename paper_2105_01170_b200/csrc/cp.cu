@@ -750,15 +750,15 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
   double w[ROWS];
   // ---- well-conditioned V: register-resident Cholesky inverse (chol_inv_reg),
   // accepted on pinv_block's test (kappa_1 <= 1e12, where numpy's pinv is
-  // the inverse to ~kappa eps)
-  {
+  // the inverse to ~kappa eps).  jstore[0] remembers, per mode, that the
+  // previous call needed the eigen path: the attempt (~5 us) is then skipped
+  // until a pivoted Cholesky comes out full rank with a benign pivot ratio.
+  constexpr long long SKIP_CHOL = 0x4a41434f42493031ll;
+  const bool skip_chol = jstore != nullptr && __double_as_longlong(jstore[0]) == SKIP_CHOL;
+  __syncwarp();
+  if (!skip_chol) {
     const bool ok = chol_inv_reg<NP == 32 ? 16 : NP>(g0, g1, R, vp, &ws[0][0]);
-    if (ok) {
-      // no rotation was formed: mark the stored one stale so the next warm
-      // call of this mode starts cold
-      if (jstore != nullptr && lane == 0) jstore[0] = __longlong_as_double(0x7ff8dead0000dead);
-      return;
-    }
+    if (ok) return;
     __syncwarp();
   }
   // ---- ill-conditioned / singular V.  Stage 1: Cholesky with diagonal
@@ -774,7 +774,6 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
   // moves half the data.  pinv = sum over sigma_k^2 > 1e-15 max sigma^2 of
   // w_k w_k^T / sigma_k^4 (numpy's rcond on the eigenvalues sigma^2).
   (void)warm;
-  if (jstore != nullptr && lane == 0) jstore[0] = __longlong_as_double(0x7ff8dead0000dead);
   double d0 = 0.0;
   for (int idx = lane; idx < NP * NP; idx += 32) {
     const int r = idx / NP, c = idx % NP;
@@ -789,6 +788,8 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
   __syncwarp();
   const double piv_floor = NP * 2.220446049250313e-16 * d0;
   unsigned done = 0u;
+  int rank = 0;
+  double dmin = d0;
   for (int k = 0; k < R; ++k) {
     double dv = (lane < NP && !((done >> lane) & 1u)) ? ws[lane][lane] : -1.0;
     int di = lane;
@@ -802,7 +803,9 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
       }
     }
     if (!(dv > piv_floor)) break;
-    const double piv = sqrt(dv), inv = 1.0 / piv;
+    ++rank;
+    dmin = dv;
+    const double inv = rsqrt_nr(dv), piv = dv * inv;
     if (lane < NP) {
       double l = 0.0;
       if (lane == di) l = piv;
@@ -817,6 +820,8 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
     }
     __syncwarp();
   }
+  if (jstore != nullptr && lane == 0)
+    jstore[0] = (rank < R || dmin <= 1e-10 * d0) ? __longlong_as_double(SKIP_CHOL) : 0.0;
 #pragma unroll
   for (int i = 0; i < ROWS; ++i) w[i] = js[r0 + i][col];
   __syncwarp();
@@ -851,21 +856,42 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
 #pragma unroll
       for (int i = 0; i < ROWS; ++i) pw[i] = __shfl_sync(0xffffffffu, w[i], src);
       const bool lo = col < partner;
-      double a = 0.0, b = 0.0, g = 0.0;
+      double a = 0.0, b = 0.0, g = 0.0, a1 = 0.0, b1 = 0.0, g1s = 0.0;
 #pragma unroll
-      for (int i = 0; i < ROWS; ++i) {
+      for (int i = 0; i < ROWS; i += 2) {
         const double wp = lo ? w[i] : pw[i], wq = lo ? pw[i] : w[i];
         a = fma(wp, wp, a);
         b = fma(wq, wq, b);
         g = fma(wp, wq, g);
+        if (i + 1 < ROWS) {
+          const double wp1 = lo ? w[i + 1] : pw[i + 1], wq1 = lo ? pw[i + 1] : w[i + 1];
+          a1 = fma(wp1, wp1, a1);
+          b1 = fma(wq1, wq1, b1);
+          g1s = fma(wp1, wq1, g1s);
+        }
       }
-      a = colsum(a);
-      b = colsum(b);
-      g = colsum(g);
+      a = colsum(a + a1);
+      b = colsum(b + b1);
+      g = colsum(g + g1s);
       const double g2 = g * g, ab = a * b;
       if (g2 > 1e-30 * ab) {
-        double c, s;
-        jacobi_rotation(a, b, g, c, s);
+        // tan of the rotation angle from tan(2 phi) = 2g / (b - a):
+        // t = sgn(d) h / (|d| + sqrt(d^2 + h^2)), d = b - a, h = 2g, with
+        // once-refined rsqrt / rcp (an angle good to ~1e-13 keeps the
+        // quadratic convergence); c = 1/sqrt(1 + t^2) to full precision and
+        // s = t c, so the rotation is orthogonal to rounding whatever t is
+        const double d = b - a, h = 2.0 * g;
+        const double r2 = fma(d, d, h * h);
+        double y;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+        y = y * fma(-0.5 * r2 * y, y, 1.5);
+        const double den = fma(r2, y, fabs(d));
+        double q;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(q) : "d"(den));
+        q = fma(q, fma(-den, q, 1.0), q);
+        const double t = (d < 0.0 ? -h : h) * q;
+        const double c = rsqrt_nr(fma(t, t, 1.0));
+        const double s = t * c;
         // a sweep whose rotations all had |cos| <= 1e-8 leaves |cos| ~ 1e-16
         // behind (quadratic convergence): it is the last one
         if (g2 > 1e-16 * ab) big = 1;
@@ -2183,9 +2209,10 @@ int run_solve_finish(const Plan& pl, const CpState& s, const double* gbuf, int64
 
 }  // namespace
 
-// cp_mid.cu: the R <= 16 one-warp pinv of g0 o g1
-int bt_cp_pinv_small(const double* g0, const double* g1, int R, double* vp, cudaStream_t st) {
-  return run_pinv(g0, g1, R, vp, st);
+// cp_mid.cu: the R <= 16 one-warp pinv of g0 o g1 (state: one double per mode, zero-initialised)
+int bt_cp_pinv_small(const double* g0, const double* g1, int R, double* vp, double* state,
+                     cudaStream_t st) {
+  return run_pinv(g0, g1, R, vp, st, state, 0);
 }
 
 // Explicit residual: Xhat_i = B diag(W_i) C^T with W = A * lam; the per-i

@@ -34,14 +34,15 @@
 #include "bt_common.cuh"
 
 // cp.cu: pinv of g0 o g1 (R <= 16), one warp
-int bt_cp_pinv_small(const double* g0, const double* g1, int R, double* vp, cudaStream_t st);
+int bt_cp_pinv_small(const double* g0, const double* g1, int R, double* vp, double* state,
+                     cudaStream_t st);
 
 namespace {
 
 constexpr int NP = 16;    // padded rank
 constexpr int LDX = 20;   // C copy read as C[k0 + g][4 s + t]: conflict free for ld == 4 (mod 16)
 constexpr int LDP = 18;   // C copy read as C[k0 + 2 t + s][g]: conflict free for 2 ld == 4 (mod 16)
-constexpr int UB = 4;     // 8x8 X blocks per register buffer (two buffers: 8-16 loads in flight per lane)
+constexpr int UB = 8;     // 8x8 X blocks per register buffer (two buffers: 8-16 loads in flight per lane)
 
 __device__ __forceinline__ double ldg_nc(const double* p) {
   double v;
@@ -62,11 +63,24 @@ __global__ void __launch_bounds__(256, 2)
   const int Kp = (K + 7) / 8 * 8;
   double* cx = sm;
   double* cp = sm + (int64_t)Kp * LDX;
-  for (int idx = threadIdx.x; idx < Kp * NP; idx += blockDim.x) {
-    const int k = idx / NP, r = idx % NP;
-    const double v = (k < K && r < R) ? Cf[(int64_t)k * R + r] : 0.0;
-    cx[k * LDX + r] = v;
-    cp[k * LDP + r] = v;
+  // loads batched 8 deep: one global round trip per batch, not per element
+  for (int base = threadIdx.x; base < Kp * NP; base += 8 * blockDim.x) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * blockDim.x;
+      const int k = idx / NP, r = idx % NP;
+      v[u] = (idx < Kp * NP && k < K && r < R) ? __ldg(Cf + (int64_t)k * R + r) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * blockDim.x;
+      if (idx < Kp * NP) {
+        const int k = idx / NP, r = idx % NP;
+        cx[k * LDX + r] = v[u];
+        cp[k * LDP + r] = v[u];
+      }
+    }
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -74,24 +88,17 @@ __global__ void __launch_bounds__(256, 2)
   const int64_t ntiles = (IJ + 7) / 8;
   const int nkb = Kp / 8;
   const bool wide = R > 8;
+  // the ticket of the NEXT tile is drawn while the current one is processed
+  // (a global atomic round trip per tile otherwise)
+  unsigned tk = 0;
+  if (lane == 0) tk = atomicAdd(ticket, 1u);
   for (;;) {
-    unsigned tk = 0;
-    if (lane == 0) tk = atomicAdd(ticket, 1u);
     const int64_t tile = __shfl_sync(0xffffffffu, tk, 0);
     if (tile >= ntiles) break;
+    if (lane == 0) tk = atomicAdd(ticket, 1u);
     const int64_t row = tile * 8 + gq;
     const bool valid = row < IJ;
     const double* xr = X + (valid ? row : 0) * K;
-    double wa[4] = {0.0, 0.0, 0.0, 0.0};
-    if (RESID && valid) {
-      const int64_t i = row / J;
-      const int j = static_cast<int>(row - i * J);
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const int r = 4 * s + tq;
-        if (r < R) wa[s] = W[i * NP + r] * Bf[(int64_t)j * R + r];
-      }
-    }
     double p00 = 0.0, p01 = 0.0, p10 = 0.0, p11 = 0.0, res = 0.0;
     double xc[UB][2], xn[UB][2];
     auto load = [&](double (&dst)[UB][2], int kb0) {
@@ -103,18 +110,27 @@ __global__ void __launch_bounds__(256, 2)
       }
     };
     load(xc, 0);
-    for (int kb0 = 0; kb0 < nkb; kb0 += UB) {
-      if (kb0 + UB < nkb) load(xn, kb0 + UB);
+    double wa[4] = {0.0, 0.0, 0.0, 0.0};
+    if (RESID && valid) {
+      const int64_t i = row / J;
+      const int j = static_cast<int>(row - i * J);
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const int r = 4 * s + tq;
+        if (r < R) wa[s] = __ldg(W + i * NP + r) * __ldg(Bf + (int64_t)j * R + r);
+      }
+    }
+    auto compute = [&](const double (&xv)[UB][2], int kb0) {
 #pragma unroll
       for (int u = 0; u < UB; ++u) {
         if (kb0 + u < nkb) {
           const int kbase = (kb0 + u) * 8;
           const double* c0 = cp + (kbase + 2 * tq) * LDP + gq;
-          dmma884(p00, p01, xc[u][0], c0[0]);
-          dmma884(p00, p01, xc[u][1], c0[LDP]);
+          dmma884(p00, p01, xv[u][0], c0[0]);
+          dmma884(p00, p01, xv[u][1], c0[LDP]);
           if (wide) {
-            dmma884(p10, p11, xc[u][0], c0[8]);
-            dmma884(p10, p11, xc[u][1], c0[LDP + 8]);
+            dmma884(p10, p11, xv[u][0], c0[8]);
+            dmma884(p10, p11, xv[u][1], c0[LDP + 8]);
           }
           if (RESID) {
             const double* c1 = cx + (kbase + gq) * LDX + tq;
@@ -125,17 +141,19 @@ __global__ void __launch_bounds__(256, 2)
               dmma884(d0, d1, wa[2], c1[8]);
               dmma884(d0, d1, wa[3], c1[12]);
             }
-            const double e0 = xc[u][0] - d0, e1 = xc[u][1] - d1;
+            const double e0 = xv[u][0] - d0, e1 = xv[u][1] - d1;
             res = fma(e0, e0, res);
             res = fma(e1, e1, res);
           }
         }
       }
-#pragma unroll
-      for (int u = 0; u < UB; ++u) {
-        xc[u][0] = xn[u][0];
-        xc[u][1] = xn[u][1];
-      }
+    };
+    // ping-pong register buffers: UB blocks (2 UB loads per lane) always in flight
+    for (int kb0 = 0; kb0 < nkb; kb0 += 2 * UB) {
+      if (kb0 + UB < nkb) load(xn, kb0 + UB);
+      compute(xc, kb0);
+      if (kb0 + 2 * UB < nkb) load(xc, kb0 + 2 * UB);
+      if (kb0 + UB < nkb) compute(xn, kb0 + UB);
     }
     if (valid) {
       double* pr = P + row * NP;
@@ -211,16 +229,26 @@ __global__ void __launch_bounds__(256, 2)
   const int rpc4 = (rpc + 7) / 8 * 8;
   const int64_t rbeg = (int64_t)blockIdx.x * rpc;
   const int64_t rend = rbeg + rpc < IJ ? rbeg + rpc : IJ;
-  for (int idx = threadIdx.x; idx < rpc4 * NP; idx += blockDim.x) {
-    const int rr = idx / NP, r = idx % NP;
-    const int64_t row = rbeg + rr;
-    double v = 0.0;
-    if (row < rend && r < R) {
-      const int64_t i = row / J;
-      const int64_t j = row - i * J;
-      v = Af[i * R + r] * Bf[j * R + r];
+  for (int base = threadIdx.x; base < rpc4 * NP; base += 8 * blockDim.x) {
+    double va[8], vb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * blockDim.x;
+      const int rr = idx / NP, r = idx % NP;
+      const int64_t row = rbeg + rr;
+      va[u] = vb[u] = 0.0;
+      if (idx < rpc4 * NP && row < rend && r < R) {
+        const int64_t i = row / J;
+        const int64_t j = row - i * J;
+        va[u] = __ldg(Af + i * R + r);
+        vb[u] = __ldg(Bf + j * R + r);
+      }
     }
-    wb[rr * LDX + r] = v;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * blockDim.x;
+      if (idx < rpc4 * NP) wb[(idx / NP) * LDX + idx % NP] = va[u] * vb[u];
+    }
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -242,18 +270,21 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
       for (int m = 0; m < 8; ++m) dst[m] = (valid && k0 + 8 * m + gq < K) ? ldg_nc(xr + 8 * m) : 0.0;
     };
-    load(xc, rh);
-    for (int st = rh; st < nsteps; st += 2) {
-      if (st + 2 < nsteps) load(xn, st + 2);
+    auto compute = [&](const double (&xv)[8], int st) {
       const double* w0 = wb + (st * 4 + tq) * LDX + gq;
       const double b0 = w0[0], b1 = w0[8];
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
-        dmma884(acc[m][0][0], acc[m][0][1], xc[m], b0);
-        if (wide) dmma884(acc[m][1][0], acc[m][1][1], xc[m], b1);
+        dmma884(acc[m][0][0], acc[m][0][1], xv[m], b0);
+        if (wide) dmma884(acc[m][1][0], acc[m][1][1], xv[m], b1);
       }
-#pragma unroll
-      for (int m = 0; m < 8; ++m) xc[m] = xn[m];
+    };
+    load(xc, rh);
+    for (int st = rh; st < nsteps; st += 4) {
+      if (st + 2 < nsteps) load(xn, st + 2);
+      compute(xc, st);
+      if (st + 4 < nsteps) load(xc, st + 4);
+      if (st + 2 < nsteps) compute(xn, st + 2);
     }
   }
   __syncthreads();
@@ -300,52 +331,100 @@ struct MidFit {
   double x2;
   int I;
   int gram_fit;         // write the Gram-identity fit into fit_hist[*iter]
+  unsigned* ticket;     // pass-1 tile ticket, reset here (a memset node costs a ~4 us gap)
 };
 
-__global__ void __launch_bounds__(512)
+__device__ long long g_mid_clk[12];  // phase clocks of the last solve (diagnostics)
+
+// F_un = M Vp and the Gram F_un^T F_un both on DMMA: the scalar version was
+// bound by its shared-memory loads (two 8-byte LDS per DFMA, 12 us per
+// update).  Fragment reads are conflict free at leading dimension 20.
+constexpr int LDF = 20;
+constexpr int GW = 16;   // warps forming Gram partials
+
+__global__ void __launch_bounds__(1024)
     mid_solve_kernel(const double* __restrict__ M, const double* __restrict__ Vp, int rows, int R,
                      double* __restrict__ F, double* __restrict__ G, int mode3, MidFit fit) {
   extern __shared__ __align__(16) double sm[];
-  double* fs = sm;                               // rows x 17
-  double* ms = sm + (int64_t)rows * 17;          // rows x 17 (M staged: coalesced, independent loads)
-  __shared__ double vs[NP * NP], gpart[2][NP * NP], gun[NP * NP], nrm[NP], red[16];
-  const int tid = threadIdx.x;
-  for (int e = tid; e < R * R; e += blockDim.x) vs[e] = Vp[e];
-  for (int e = tid; e < rows * NP; e += blockDim.x) ms[(e / NP) * 17 + e % NP] = M[e];
+  const int rows8 = (rows + 7) / 8 * 8;
+  double* fs = sm;                                // rows8 x LDF
+  double* ms = sm + (int64_t)rows8 * LDF;         // rows8 x LDF
+  __shared__ double vs[NP * LDF], gw[GW][NP * NP], gun[NP * NP], nrm[NP], red[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  int ck = 0;
+#define MID_CLK() do { if (tid == 0) g_mid_clk[ck] = clock64(); ++ck; } while (0)
+  MID_CLK();
+  for (int e = tid; e < NP * NP; e += blockDim.x) {
+    const int q = e / NP, c = e % NP;
+    vs[q * LDF + c] = (q < R && c < R) ? Vp[q * R + c] : 0.0;
+  }
+  for (int e = tid; e < rows8 * NP; e += blockDim.x)
+    ms[(e / NP) * LDF + e % NP] = e < rows * NP ? M[e] : 0.0;
   __syncthreads();
-  for (int e = tid; e < rows * NP; e += blockDim.x) {
-    const int row = e / NP, c = e % NP;
-    double s = 0.0;
-    if (c < R)
-      for (int q = 0; q < R; ++q) s = fma(ms[row * 17 + q], vs[q * R + c], s);
-    fs[row * 17 + c] = s;
+  MID_CLK();
+  for (int mt = warp; mt * 8 < rows; mt += 32) {
+    const double* mr = ms + (mt * 8 + gq) * LDF + tq;
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4) {
+      const double av = mr[4 * s4];
+      const double* vr = vs + (4 * s4 + tq) * LDF + gq;
+      dmma884(c00, c01, av, vr[0]);
+      dmma884(c10, c11, av, vr[8]);
+    }
+    double* fr = fs + (mt * 8 + gq) * LDF;
+    fr[2 * tq] = c00;
+    fr[2 * tq + 1] = c01;
+    fr[8 + 2 * tq] = c10;
+    fr[9 + 2 * tq] = c11;
   }
   __syncthreads();
-  {
-    const int e = tid & 255, hf = tid >> 8;
-    const int a = e / NP, b = e % NP;
-    double s = 0.0;
-    for (int row = hf; row < rows; row += 2) s = fma(fs[row * 17 + a], fs[row * 17 + b], s);
-    gpart[hf][e] = s;
+  MID_CLK();
+  if (warp < GW) {
+    double g00a = 0.0, g00b = 0.0, g01a = 0.0, g01b = 0.0, g10a = 0.0, g10b = 0.0, g11a = 0.0, g11b = 0.0;
+    for (int ks = warp; ks * 4 < rows8; ks += GW) {
+      const double* fr = fs + (ks * 4 + tq) * LDF + gq;
+      const double a0 = fr[0], a1 = fr[8];
+      dmma884(g00a, g00b, a0, a0);
+      dmma884(g01a, g01b, a0, a1);
+      dmma884(g10a, g10b, a1, a0);
+      dmma884(g11a, g11b, a1, a1);
+    }
+    double* o = gw[warp];
+    o[gq * NP + 2 * tq] = g00a;
+    o[gq * NP + 2 * tq + 1] = g00b;
+    o[gq * NP + 8 + 2 * tq] = g01a;
+    o[gq * NP + 9 + 2 * tq] = g01b;
+    o[(8 + gq) * NP + 2 * tq] = g10a;
+    o[(8 + gq) * NP + 2 * tq + 1] = g10b;
+    o[(8 + gq) * NP + 8 + 2 * tq] = g11a;
+    o[(8 + gq) * NP + 9 + 2 * tq] = g11b;
   }
   double inner = 0.0;
   if (mode3) {
     double s = 0.0;
     for (int e = tid; e < rows * NP; e += blockDim.x) {
       const int row = e / NP, c = e % NP;
-      s = fma(fs[row * 17 + c], ms[row * 17 + c], s);   // padded columns are zero
+      s = fma(fs[row * LDF + c], ms[row * LDF + c], s);   // padded columns are zero
     }
     s = warp_sum(s);
-    if ((tid & 31) == 0) red[tid >> 5] = s;
+    if (lane == 0) red[warp] = s;
   }
   __syncthreads();
-  if (tid < NP * NP) gun[tid] = gpart[0][tid] + gpart[1][tid];
-  if (mode3 && tid == 0) {
+  MID_CLK();
+  if (tid < NP * NP) {
     double t = 0.0;
-    for (int w = 0; w < 16; ++w) t += red[w];
-    red[0] = t;
+#pragma unroll
+    for (int w = 0; w < GW; ++w) t += gw[w][tid];
+    gun[tid] = t;
+  }
+  if (mode3 && tid < 32) {
+    const double t = warp_sum(red[tid]);
+    if (tid == 0) red[0] = t;
   }
   __syncthreads();
+  MID_CLK();
   inner = red[0];
   if (tid < NP) {
     double v = sqrt(gun[tid * NP + tid]);
@@ -353,16 +432,19 @@ __global__ void __launch_bounds__(512)
     nrm[tid] = v;
   }
   __syncthreads();
+  MID_CLK();
   for (int e = tid; e < R * R; e += blockDim.x) {
     const int a = e / R, b = e % R;
     G[e] = gun[a * NP + b] / (nrm[a] * nrm[b]);
   }
   for (int e = tid; e < rows * R; e += blockDim.x) {
     const int row = e / R, c = e % R;
-    F[e] = fs[row * 17 + c] / nrm[c];
+    F[e] = fs[row * LDF + c] / nrm[c];
   }
+  MID_CLK();
   if (!mode3) return;
   for (int r = tid; r < R; r += blockDim.x) fit.lam[r] = nrm[r];
+  if (tid == 0) *fit.ticket = 0u;
   for (int e = tid; e < fit.I * NP; e += blockDim.x) {
     const int i = e / NP, r = e % NP;
     fit.w[e] = r < R ? fit.a[(int64_t)i * R + r] * nrm[r] : 0.0;
@@ -375,14 +457,16 @@ __global__ void __launch_bounds__(512)
     s += nrm[a] * nrm[b] * fit.g0[e] * fit.g1[e] * (gun[a * NP + b] / (nrm[a] * nrm[b]));
   }
   s = warp_sum(s);
-  if ((tid & 31) == 0) red[tid >> 5] = s;
+  if (lane == 0) red[warp] = s;
   __syncthreads();
-  if (tid == 0 && fit.gram_fit) {
-    double xh2 = 0.0;
-    for (int w = 0; w < 16; ++w) xh2 += red[w];
-    const double res2 = fmax(fit.x2 - 2.0 * inner + xh2, 0.0);
-    fit.fit_hist[*fit.iter] = 1.0 - sqrt(res2 / fit.x2);
+  if (tid < 32 && fit.gram_fit) {
+    const double xh2 = warp_sum(red[tid]);
+    if (tid == 0) {
+      const double res2 = fmax(fit.x2 - 2.0 * inner + xh2, 0.0);
+      fit.fit_hist[*fit.iter] = 1.0 - sqrt(res2 / fit.x2);
+    }
   }
+#undef MID_CLK
 }
 
 // sum of the per-tile residual partials (fixed order), explicit fit, sweep counter
@@ -445,6 +529,11 @@ struct MidBuf {
 
 }  // namespace
 
+extern "C" int bt_debug_mid_clocks(long long* out12) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(out12, g_mid_clk, sizeof(long long) * 12);
+}
+
 // Returns 1 when it ran (outputs written, *rc set), 0 when the problem is not eligible.
 int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, double* lam,
                   int max_iters, double tol, int fit_mode, double* fit_history, int* n_iters,
@@ -453,7 +542,7 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
   *rc = BT_OK;
   const int64_t I = pb->I, J = pb->J, K = pb->K;
   const int R = static_cast<int>(pb->R);
-  if (off || pb->R > NP || R < 1 || I < 1 || J < 1 || K < 1 || I > 1024 || J > 1024 || K > 512 ||
+  if (off || pb->R > NP || R < 1 || I < 1 || J < 1 || K < 1 || I > 640 || J > 640 || K > 512 ||
       I * J < 4096 || pb->norm_x <= 0.0 || max_iters < 1)
     return 0;
   const int64_t IJ = I * J;
@@ -462,13 +551,15 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
   const size_t smem1 = sizeof(double) * Kp * (LDX + LDP);
   const int kspans = static_cast<int>(bt_cdiv(K, 256));
   // row chunks of pass 2: two resident CTAs per SM over all k spans
-  const int64_t want_chunks = std::max<int64_t>(1, (2 * nsm) / kspans);
+  // (one CTA slot short of two per SM: the two-CTA register footprint fills an
+  // SM, and the one-warp pinv on the side stream needs a slot to overlap)
+  const int64_t want_chunks = std::max<int64_t>(1, (2 * nsm - 1) / kspans);
   int rpc = static_cast<int>(bt_cdiv(bt_cdiv(IJ, want_chunks), 8) * 8);
   rpc = std::max(rpc, 64);
   const int64_t nchunks = bt_cdiv(IJ, rpc);
   const size_t smem3 = sizeof(double) * std::max<size_t>((size_t)rpc * LDX, 4 * 32 * 33);
   const int64_t maxrows = std::max(I, std::max(J, K));
-  const size_t smem_solve = sizeof(double) * maxrows * 17 * 2;
+  const size_t smem_solve = sizeof(double) * ((maxrows + 7) / 8 * 8) * LDF * 2;
   if (smem1 > 100 * 1024 || smem3 > 100 * 1024 || smem_solve > 220 * 1024) return 0;
   const int64_t ntiles = bt_cdiv(IJ, 8);
   const bool explicit_fit = fit_mode != 2;
@@ -487,7 +578,7 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
   };
   const int64_t oP = take(IJ * NP), oPart = take(nchunks * K * NP), oM = take(maxrows * NP),
                 oRes = take(ntiles), oG = take(3 * NP * NP), oVp = take(3 * NP * NP),
-                oW = take(I * NP), oHist = take(max_iters + 2), oInt = take(4);
+                oW = take(I * NP), oHist = take(max_iters + 2), oInt = take(4), oPst = take(4);
   double* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, sizeof(double) * o, st);
   if (e != cudaSuccess) return fail("workspace", e);
@@ -502,6 +593,7 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
   }
   B.W = ws + oW;
   B.fit_hist = ws + oHist;
+  double* pst = ws + oPst;   // per-mode pinv path memory
   B.iter = reinterpret_cast<int*>(ws + oInt);
   B.ticket = reinterpret_cast<unsigned*>(ws + oInt) + 2;
 
@@ -548,17 +640,17 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
   MID_CHECK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
 
   const double x2 = pb->norm_x * pb->norm_x;
-  const int grid1 = 2 * nsm;
+  const int grid1 = 2 * nsm - 1;   // one slot left for the concurrent pinv warp
   double* F[3] = {a, b, c};
   const int rows[3] = {(int)I, (int)J, (int)K};
 
   // head of sweep 1: Grams of the initial factors, pinv for mode 1, P = X x3 C
-  MID_CHECK(cudaMemsetAsync(B.iter, 0, 16, st), "memset");
+  MID_CHECK(cudaMemsetAsync(B.iter, 0, 64, st), "memset");
   for (int k = 0; k < 3; ++k) {
     mid_gram_kernel<<<1, 1024, sizeof(double) * rows[k] * 17, st>>>(F[k], rows[k], R, B.G[k]);
     MID_LAUNCH("gram");
   }
-  if ((*rc = bt_cp_pinv_small(B.G[1], B.G[2], R, B.vp[0], st)) != BT_OK) {
+  if ((*rc = bt_cp_pinv_small(B.G[1], B.G[2], R, B.vp[0], pst, st)) != BT_OK) {
     cleanup();
     return 1;
   }
@@ -578,7 +670,7 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
   auto fork_pinv = [&](int g0, int g1, int dst) {
     if (cap_e == cudaSuccess) cap_e = cudaEventRecord(ev_fork, cs);
     if (cap_e == cudaSuccess) cap_e = cudaStreamWaitEvent(side, ev_fork, 0);
-    if (cap_rc == BT_OK) cap_rc = bt_cp_pinv_small(B.G[g0], B.G[g1], R, B.vp[dst], side);
+    if (cap_rc == BT_OK) cap_rc = bt_cp_pinv_small(B.G[g0], B.G[g1], R, B.vp[dst], pst + dst, side);
     if (cap_e == cudaSuccess) cap_e = cudaEventRecord(ev_join, side);
   };
   auto join = [&]() {
@@ -588,14 +680,14 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
   // mode 1 (its pinv was forked by the previous sweep / the head above)
   mid_contract_kernel<<<(unsigned)I, 256, 0, cs>>>(B.P, J, 1, (int)J, b, R, B.M);
   note();
-  mid_solve_kernel<<<1, 512, smem_solve, cs>>>(B.M, B.vp[0], (int)I, R, a, B.G[0], 0, nofit);
+  mid_solve_kernel<<<1, 1024, smem_solve, cs>>>(B.M, B.vp[0], (int)I, R, a, B.G[0], 0, nofit);
   note();
   // mode 2
   fork_pinv(0, 2, 1);
   mid_contract_kernel<<<(unsigned)J, 256, 0, cs>>>(B.P, 1, J, (int)I, a, R, B.M);
   note();
   join();
-  mid_solve_kernel<<<1, 512, smem_solve, cs>>>(B.M, B.vp[1], (int)J, R, b, B.G[1], 0, nofit);
+  mid_solve_kernel<<<1, 1024, smem_solve, cs>>>(B.M, B.vp[1], (int)J, R, b, B.G[1], 0, nofit);
   note();
   // mode 3
   fork_pinv(0, 1, 2);
@@ -605,12 +697,11 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
   mid_contract_kernel<<<(unsigned)K, 256, 0, cs>>>(B.part, 1, K, (int)nchunks, nullptr, R, B.M);
   note();
   join();
-  MidFit fit{B.G[0], B.G[1], a, B.W, lam, B.fit_hist, B.iter, x2, (int)I, explicit_fit ? 0 : 1};
-  mid_solve_kernel<<<1, 512, smem_solve, cs>>>(B.M, B.vp[2], (int)K, R, c, B.G[2], 1, fit);
+  MidFit fit{B.G[0], B.G[1], a, B.W, lam, B.fit_hist, B.iter, x2, (int)I, explicit_fit ? 0 : 1, B.ticket};
+  mid_solve_kernel<<<1, 1024, smem_solve, cs>>>(B.M, B.vp[2], (int)K, R, c, B.G[2], 1, fit);
   note();
   // head of the next sweep: pinv for mode 1, P and this sweep's residual
   fork_pinv(1, 2, 0);
-  if (cap_e == cudaSuccess) cap_e = cudaMemsetAsync(B.ticket, 0, sizeof(unsigned), cs);
   if (explicit_fit)
     mid_pass1_kernel<true><<<grid1, 256, smem1, cs>>>(pb->x, IJ, (int)J, (int)K, R, B.W, b, c, B.P,
                                                       B.res_part, B.ticket);
