@@ -23,6 +23,8 @@
 #include <cmath>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "gemm.cuh"
 #include "jacobi.cuh"
 #include "tma.cuh"
@@ -1427,6 +1429,8 @@ __global__ void __launch_bounds__(512)
   }
 }
 
+#include "cp_cluster.cuh"
+
 // ---------------------------------------------------------------------------
 // solve: F_un = (sum_s Mpart[s]) @ Vp ; per-CTA Gram + <F_un, M> partials
 // ---------------------------------------------------------------------------
@@ -2632,9 +2636,88 @@ extern "C" int bt_cp_state_finish(void* state, int n_iters, double* fit_history)
 
 // Diagnostic: clock64 stamps of sweep 1's phases in the fused small kernel
 // (P, mode 1 MTTKRP, solve 1, mode 2, solve 2, mode 3, solve 3, fit, end).
+extern "C" int bt_cp_cluster_clocks(long long* out16) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(out16, g_cluster_clk, sizeof(long long) * 16);
+}
+
 extern "C" int bt_cp_small_clocks(long long* out) {
   BT_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_small_clk, sizeof(long long) * 13));
   return BT_OK;
+}
+
+// The cluster path of bt_cp_als_f64 (cp_cluster.cuh): X resident in the
+// distributed shared memory of 8 CTAs.  Returns 1 when it ran, 0 when the
+// problem is not eligible (the one-CTA kernel is tried next).
+static int cp_cluster_try(const bt_cp_problem* pb, double* a, double* b, double* c, double* lam,
+                          int max_iters, double tol, int fit_mode, double* fit_history,
+                          int* n_iters, int* converged, cudaStream_t st, int* rc) {
+  static const bool off = getenv("BT_CP_CLUSTER") && getenv("BT_CP_CLUSTER")[0] == '0';
+  *rc = BT_OK;
+  const int64_t I = pb->I, J = pb->J, K = pb->K, R = pb->R;
+  if (off || R > SMALL_RS || I < 1 || J < 1 || K < 1 || I * J * K > (int64_t(1) << 17) ||
+      I > 1024 || J > 1024 || K > 1024 || pb->norm_x <= 0.0)
+    return 0;
+  const int NP = R <= 8 ? 8 : 16;
+  const size_t smem = static_cast<size_t>(cluster_layout(I, J, K, R, NP).total) * 8;
+  if (smem > 200 * 1024) return 0;
+  double* dbuf = nullptr;
+  cudaError_t e = cudaMallocAsync(&dbuf, sizeof(double) * (max_iters + 2), st);
+  if (e != cudaSuccess) {
+    bt_set_error("cp_als: %s", cudaGetErrorString(e));
+    *rc = BT_E_CUDA;
+    return 1;
+  }
+  int* info = reinterpret_cast<int*>(dbuf + max_iters);
+  const double x2 = pb->norm_x * pb->norm_x;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL_CS);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL_CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const double* xp = pb->x;
+  const int Ii = (int)I, Ji = (int)J, Ki = (int)K, Ri = (int)R;
+  cudaError_t le;
+  if (NP == 8) {
+    cudaFuncSetAttribute(cp_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    le = cudaLaunchKernelEx(&cfg, cp_cluster_kernel<8>, xp, Ii, Ji, Ki, Ri, a, b, c, lam, x2,
+                            max_iters, tol, fit_mode, dbuf, info);
+  } else {
+    cudaFuncSetAttribute(cp_cluster_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    le = cudaLaunchKernelEx(&cfg, cp_cluster_kernel<16>, xp, Ii, Ji, Ki, Ri, a, b, c, lam, x2,
+                            max_iters, tol, fit_mode, dbuf, info);
+  }
+  if (le != cudaSuccess) {
+    // a cluster that cannot be placed is not an error: the one-CTA kernel runs instead
+    cudaGetLastError();
+    cudaFreeAsync(dbuf, st);
+    return 0;
+  }
+  bt_count_launch();
+  int hinfo[2] = {0, 0};
+  cudaMemcpyAsync(hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, st);
+  e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess && hinfo[0] > 0 && fit_history)
+    cudaMemcpyAsync(fit_history, dbuf, sizeof(double) * hinfo[0], cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(dbuf, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    bt_set_error("cp_cluster: %s", cudaGetErrorString(e));
+    *rc = BT_E_CUDA;
+    return 1;
+  }
+  *n_iters = hinfo[0];
+  *converged = hinfo[1];
+  return 1;
 }
 
 // One-GPU driver over the phase API (no cross-rank sums).
@@ -2709,6 +2792,9 @@ extern "C" int bt_cp_als_f64(const bt_cp_problem* pb, double* a, double* b, doub
   BT_NVTX("bt_cp_als_f64");
   if (phase_ms == nullptr && max_iters >= 1) {
     int rc = BT_OK;
+    if (cp_cluster_try(pb, a, b, c, lam, max_iters, tol, fit_mode, fit_history, n_iters, converged,
+                       bt_stream(stream), &rc))
+      return rc;
     if (cp_small_try(pb, a, b, c, lam, max_iters, tol, fit_mode, fit_history, n_iters, converged,
                      bt_stream(stream), &rc))
       return rc;
