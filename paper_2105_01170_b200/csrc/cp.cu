@@ -2652,7 +2652,8 @@ extern "C" int bt_cp_small_clocks(long long* out) {
 static int cp_cluster_try(const bt_cp_problem* pb, double* a, double* b, double* c, double* lam,
                           int max_iters, double tol, int fit_mode, double* fit_history,
                           int* n_iters, int* converged, cudaStream_t st, int* rc) {
-  static const bool off = getenv("BT_CP_CLUSTER") && getenv("BT_CP_CLUSTER")[0] == '0';
+  // read per call: the parity tests switch paths in-process
+  const bool off = getenv("BT_CP_CLUSTER") && getenv("BT_CP_CLUSTER")[0] == '0';
   *rc = BT_OK;
   const int64_t I = pb->I, J = pb->J, K = pb->K, R = pb->R;
   if (off || R > SMALL_RS || I < 1 || J < 1 || K < 1 || I * J * K > (int64_t(1) << 17) ||
@@ -2726,7 +2727,7 @@ static int cp_cluster_try(const bt_cp_problem* pb, double* a, double* b, double*
 static int cp_small_try(const bt_cp_problem* pb, double* a, double* b, double* c, double* lam,
                         int max_iters, double tol, int fit_mode, double* fit_history,
                         int* n_iters, int* converged, cudaStream_t st, int* rc) {
-  static const bool off = getenv("BT_CP_SMALL") && getenv("BT_CP_SMALL")[0] == '0';
+  const bool off = getenv("BT_CP_SMALL") && getenv("BT_CP_SMALL")[0] == '0';
   *rc = BT_OK;
   const int64_t I = pb->I, J = pb->J, K = pb->K, R = pb->R;
   if (off || R > SMALL_RS || I < 1 || J < 1 || K < 1 || I * J * K > (int64_t(1) << 17) ||

@@ -538,7 +538,8 @@ extern "C" int bt_debug_mid_clocks(long long* out12) {
 int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, double* lam,
                   int max_iters, double tol, int fit_mode, double* fit_history, int* n_iters,
                   int* converged, cudaStream_t st, int* rc) {
-  static const bool off = getenv("BT_CP_MID") && getenv("BT_CP_MID")[0] == '0';
+  // read per call: the parity tests switch paths in-process
+  const bool off = getenv("BT_CP_MID") && getenv("BT_CP_MID")[0] == '0';
   *rc = BT_OK;
   const int64_t I = pb->I, J = pb->J, K = pb->K;
   const int R = static_cast<int>(pb->R);
