@@ -732,6 +732,85 @@ template <int NP>
 __device__ __noinline__ bool chol_inv_reg(const double* __restrict__ g0, const double* __restrict__ g1,
                                           int R, double* __restrict__ vp, double* sc);
 
+// In-place Gauss-Jordan inverse of V = g0 o g1 (SPD: no pivoting needed) by
+// one warp, the matrix spread over the lanes' registers (NP = 8: lane holds
+// 2 entries of a row, NP = 16: 8).  One step per column: the pivot row and
+// the lane's own column-k entry arrive by shuffles, one refined reciprocal,
+// one fused update -- ~170 cycles of dependent latency per step where the
+// Cholesky route (factor, triangular inverse, Y^T Y through shared memory)
+// took ~6k cycles at NP = 8.  Accepted when every pivot is positive,
+// max / min pivot <= 1e14 R and ||V||_1 ||V^-1||_1 <= 1e14: numpy's pinv
+// (rcond 1e-15) is the plain inverse up to kappa_2 = 1e15, and both are
+// accurate to ~kappa eps there; beyond, the eigen path decides the cutoff.
+template <int NP>
+__device__ __forceinline__ bool spd_inv_gj(const double* __restrict__ g0,
+                                           const double* __restrict__ g1, int R,
+                                           double* __restrict__ vp) {
+  static_assert(NP == 8 || NP == 16, "NP in {8, 16}");
+  constexpr int EPL = NP * NP / 32;   // entries per lane
+  constexpr int LPR = NP / EPL;       // lanes per row
+  const int lane = threadIdx.x & 31;
+  const int i = lane / LPR, sub = lane % LPR, jb = sub * EPL;
+  double a[EPL];
+  double rs = 0.0;
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    const int j = jb + e;
+    double v = (i == j) ? 1.0 : 0.0;
+    if (i < R && j < R) {
+      v = g1 ? g0[i * R + j] * g1[i * R + j] : g0[i * R + j];
+      rs += fabs(v);
+    }
+    a[e] = v;
+  }
+  auto row_max = [&](double v) {   // sum over the row's lanes, then max over rows
+#pragma unroll
+    for (int o = 1; o < LPR; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+  };
+  const double vn1 = row_max(rs);
+  bool ok = true;
+  double lo = INFINITY, hi = 0.0;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const int ck = k / EPL, ek = k % EPL;
+    const double f = __shfl_sync(0xffffffffu, a[ek], i * LPR + ck);
+    const double p = __shfl_sync(0xffffffffu, a[ek], k * LPR + ck);
+    double prow[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) prow[e] = __shfl_sync(0xffffffffu, a[e], k * LPR + sub);
+    ok = ok && (p > 0.0);
+    lo = fmin(lo, p);
+    hi = fmax(hi, p);
+    const double ip = rcp_nr(fmax(p, 1e-300));
+    const double fi = -f * ip;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      const bool colk = (jb + e == k);
+      if (i == k)
+        a[e] = colk ? ip : a[e] * ip;
+      else
+        a[e] = colk ? fi : fma(fi, prow[e], a[e]);
+    }
+  }
+  if (!ok || hi > 1e14 * R * lo) return false;   // warp-uniform
+  double is = 0.0;
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    const int j = jb + e;
+    if (i < R && j < R) {
+      vp[i * R + j] = a[e];
+      is += fabs(a[e]);
+    }
+  }
+  const double in1 = row_max(is);
+  __syncwarp();
+  return vn1 * in1 <= 1e14;
+}
+
+
 __device__ long long g_pinv1s_dbg[2];  // sweeps, cycles of the last call (diagnostics)
 __device__ long long g_pinv1s_log[512];  // (sweeps << 40 | cycles) per call, ring (diagnostics)
 __device__ unsigned g_pinv1s_n;
@@ -752,14 +831,9 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
   double w[ROWS];
   // ---- well-conditioned V: register-resident Cholesky inverse (chol_inv_reg),
   // accepted on pinv_block's test (kappa_1 <= 1e12, where numpy's pinv is
-  // the inverse to ~kappa eps).  jstore[0] remembers, per mode, that the
-  // previous call needed the eigen path: the attempt (~5 us) is then skipped
-  // until a pivoted Cholesky comes out full rank with a benign pivot ratio.
-  constexpr long long SKIP_CHOL = 0x4a41434f42493031ll;
-  const bool skip_chol = jstore != nullptr && __double_as_longlong(jstore[0]) == SKIP_CHOL;
-  __syncwarp();
-  if (!skip_chol) {
-    const bool ok = chol_inv_reg<NP == 32 ? 16 : NP>(g0, g1, R, vp, &ws[0][0]);
+  // the inverse to ~kappa eps)
+  {
+    const bool ok = spd_inv_gj<NP == 32 ? 16 : NP>(g0, g1, R, vp);
     if (ok) return;
     __syncwarp();
   }
@@ -776,6 +850,7 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
   // moves half the data.  pinv = sum over sigma_k^2 > 1e-15 max sigma^2 of
   // w_k w_k^T / sigma_k^4 (numpy's rcond on the eigenvalues sigma^2).
   (void)warm;
+  (void)jstore;
   double d0 = 0.0;
   for (int idx = lane; idx < NP * NP; idx += 32) {
     const int r = idx / NP, c = idx % NP;
@@ -822,8 +897,6 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
     }
     __syncwarp();
   }
-  if (jstore != nullptr && lane == 0)
-    jstore[0] = (rank < R || dmin <= 1e-10 * d0) ? __longlong_as_double(SKIP_CHOL) : 0.0;
 #pragma unroll
   for (int i = 0; i < ROWS; ++i) w[i] = js[r0 + i][col];
   __syncwarp();
@@ -907,7 +980,10 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
     g_pinv1s_dbg[0] = sweeps_done;
     g_pinv1s_dbg[1] = clock64() - t_start;
     const unsigned slot = atomicAdd(&g_pinv1s_n, 1u);
-    g_pinv1s_log[slot & 511u] = ((long long)sweeps_done << 40) | (g_pinv1s_dbg[1] & 0xffffffffffll);
+    // sweeps (8 bits) | rank (8 bits) | -log10(dmin / d0) (8 bits) | cycles (32 bits)
+    const long long lg = dmin > 0.0 && d0 > 0.0 ? (long long)fmin(255.0, -log10(dmin / d0)) : 255;
+    g_pinv1s_log[slot & 511u] = ((long long)sweeps_done << 56) | ((long long)rank << 48) | (lg << 40) |
+                                (g_pinv1s_dbg[1] & 0xffffffffll);
   }
   double lk = 0.0;
 #pragma unroll
@@ -1180,8 +1256,8 @@ __global__ void __launch_bounds__(512)
   auto pinv_w0 = [&](int go0, int go1) {
     if ((tid >> 5) == 0) {
       const long long c0 = clock64();
-      const bool ok = R <= 8 ? chol_inv_reg<8>(G[go0], G[go1], R, Vp, smf)
-                             : (R <= 16 ? chol_inv_reg<16>(G[go0], G[go1], R, Vp, smf)
+      const bool ok = R <= 8 ? spd_inv_gj<8>(G[go0], G[go1], R, Vp)
+                             : (R <= 16 ? spd_inv_gj<16>(G[go0], G[go1], R, Vp)
                                         : pinv_warp_chol(G[go0], G[go1], R, Vp, smf, smf + R * (R + 1)));
       if (tid == 0) pinv_ok = ok ? 1 : 0;
       if (it == 1 && tid == 0) g_small_clk[9 + go0 + go1] = clock64() - c0;

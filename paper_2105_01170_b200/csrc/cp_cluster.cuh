@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(512)
 
   auto pinv_w0 = [&](int go0, int go1) {
     if (warp == 0) {
-      const bool ok = chol_inv_reg<NP>(G[go0], G[go1], R, Vp, smf);
+      const bool ok = spd_inv_gj<NP>(G[go0], G[go1], R, Vp);
       if (tid == 0) pinv_ok = ok ? 1 : 0;
     }
   };

@@ -18,4 +18,4 @@ n1 = lib.bt_debug_pinv1s_log(buf)
 print("calls", n1 - n0, "fit", res.fit)
 ent = [buf[i & 511] for i in range(n0, n1)]
 for i, e in enumerate(ent):
-    print(f"call {i:3d} (sweep {i // 3 + 1}, mode {i % 3 + 1}): jacobi sweeps {e >> 40:3d}, {(e & 0xffffffffff) / 1.965e3:7.1f} us")
+    print(f"jacobi call {i:3d}: sweeps {e >> 56:3d}, rank {(e >> 48) & 255:2d}, dmin/d0 1e-{(e >> 40) & 255:<3d} {(e & 0xffffffff) / 1.965e3:7.1f} us")
