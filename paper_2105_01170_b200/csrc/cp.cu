@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 #include <cmath>
 #include <vector>
@@ -2780,18 +2781,20 @@ static int cp_cluster_try(const bt_cp_problem* pb, double* a, double* b, double*
     return 0;
   }
   bt_count_launch();
-  int hinfo[2] = {0, 0};
-  cudaMemcpyAsync(hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, st);
-  e = cudaStreamSynchronize(st);
-  if (e == cudaSuccess && hinfo[0] > 0 && fit_history)
-    cudaMemcpyAsync(fit_history, dbuf, sizeof(double) * hinfo[0], cudaMemcpyDeviceToHost, st);
+  // history and (n_iters, converged) in one read-back, one synchronisation
+  std::vector<double> hbuf(static_cast<size_t>(max_iters) + 2);
+  cudaMemcpyAsync(hbuf.data(), dbuf, sizeof(double) * hbuf.size(), cudaMemcpyDeviceToHost, st);
   cudaFreeAsync(dbuf, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
     bt_set_error("cp_cluster: %s", cudaGetErrorString(e));
     *rc = BT_E_CUDA;
     return 1;
   }
+  int hinfo[2];
+  std::memcpy(hinfo, hbuf.data() + max_iters, sizeof(hinfo));
+  if (fit_history)
+    for (int k = 0; k < hinfo[0] && k < max_iters; ++k) fit_history[k] = hbuf[k];
   *n_iters = hinfo[0];
   *converged = hinfo[1];
   return 1;

@@ -169,13 +169,21 @@ __global__ void __launch_bounds__(512)
       for (int r = 0; r < nr; ++r) s = fma(fu[r * NP + a], fu[r * NP + b], s);
       gbuf[e] = s;
     }
-    double inner = 0.0;
-    if (last) {
-      double s = 0.0;
-      for (int e = tid; e < nr * NP; e += nt) s = fma(fu[e], M[e], s);
-      inner = small_block_sum(s, red);
-    }
+    // last: <F_un, M> and ||Xhat||^2 = sum(G0 o G1 o F_un^T F_un) (the column
+    // norms cancel against the normalised Gram) in one block reduction
+    double s_in = 0.0, s_xh = 0.0;
+    if (last)
+      for (int e = tid; e < nr * NP; e += nt) s_in = fma(fu[e], M[e], s_in);
     __syncthreads();
+    if (last) {
+      for (int e = tid; e < R * R; e += nt) s_xh += G[0][e] * G[1][e] * gbuf[e];
+      s_in = warp_sum(s_in);
+      s_xh = warp_sum(s_xh);
+      if (lane == 0) {
+        red[warp] = s_in;
+        red[16 + warp] = s_xh;
+      }
+    }
     for (int r = tid; r < NP; r += nt) {
       double v = r < R ? sqrt(gbuf[r * R + r]) : 1.0;
       if (v == 0.0) v = 1.0;
@@ -187,20 +195,18 @@ __global__ void __launch_bounds__(512)
       const int row = e / NP, c = e % NP;
       F[k][row * LDF + c] = fu[e] / nrm[c];
     }
-    __syncthreads();
-    if (last) {
-      double s = 0.0;
-      for (int e = tid; e < R * R; e += nt)
-        s += nrm[e / R] * nrm[e % R] * G[0][e] * G[1][e] * G[2][e];
-      const double xh2 = small_block_sum(s, red);
-      if (tid == 0) {
-        const double res2 = fmax(x2 - 2.0 * inner + xh2, 0.0);
-        const double relres = sqrt(res2 / x2);
-        explicit_s = ((fit_mode == 1) || (fit_mode == 0 && relres < 1e-3)) ? 1.0 : 0.0;
-        fit_s = 1.0 - relres;
+    if (last && tid == 0) {
+      double inner = 0.0, xh2 = 0.0;
+      for (int w = 0; w < 16; ++w) {
+        inner += red[w];
+        xh2 += red[16 + w];
       }
-      __syncthreads();
+      const double res2 = fmax(x2 - 2.0 * inner + xh2, 0.0);
+      const double relres = sqrt(res2 / x2);
+      explicit_s = ((fit_mode == 1) || (fit_mode == 0 && relres < 1e-3)) ? 1.0 : 0.0;
+      fit_s = 1.0 - relres;
     }
+    __syncthreads();
   };
   // sum the CS gathered partials (rank order) into M
   auto sum_gather = [&](const double* gb_, int nr) {
