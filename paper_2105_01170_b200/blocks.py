@@ -37,6 +37,12 @@ __all__ = [
 ]
 
 
+# detect_pattern's own partitions skip the per-class validation scan (128
+# classes of a 128 x 128 grid: ~1 ms of numpy calls next to 3.3 ms of device
+# passes); user-built patterns are always validated
+_TRUSTED_PLACEMENTS: dict = {}
+
+
 @dataclass(frozen=True, eq=False)
 class BlockPattern:
     """Placement structure of a block matrix with repeated blocks
@@ -65,6 +71,11 @@ class BlockPattern:
     def __post_init__(self) -> None:
         if min(self.ell, self.q, self.m, self.n) < 1:
             raise ShapeError("pattern extents must be positive")
+        if _TRUSTED_PLACEMENTS.get("on"):
+            # built by detect_pattern from a partition of the grid's cells
+            # (int64 (eta, 2) arrays, disjoint and in range by construction)
+            object.__setattr__(self, "_dev_cache", None)
+            return
         norm = tuple(np.asarray(c, dtype=np.int64) for c in self.placements)
         # class-level checks in class order (blocks.py:86-96); the first
         # failing class wins, a duplicate cell is reported at its second
@@ -361,16 +372,18 @@ def detect_pattern(a, m: int, n: int, tol: float = 0.0):
     t = _dev.torch()
     ad = _dev.to_device(a).contiguous()
     cells_n = ell * q
-    h1 = t.empty(cells_n, dtype=t.int64, device="cuda")
-    h2 = t.empty(cells_n, dtype=t.int64, device="cuda")
-    nz = t.empty(cells_n, dtype=t.int32, device="cuda")
+    # [h1 | h2 | nz (int32 pairs)] in one buffer: one read-back, one synchronisation
+    dig = t.empty(2 * cells_n + (cells_n + 1) // 2, dtype=t.int64, device="cuda")
+    h1, h2 = dig[:cells_n], dig[cells_n:2 * cells_n]
+    nz = dig[2 * cells_n:].view(t.int32)[:cells_n]
     N.call("bt_block_digest_f64", _dev.ptr(ad), cols, ell, q, m, n, float(tol), _dev.ptr(h1),
            _dev.ptr(h2), _dev.ptr(nz), _dev.stream())
-    keep = np.flatnonzero(nz.cpu().numpy())
+    dig_h = dig.cpu().numpy()
+    keep = np.flatnonzero(dig_h[2 * cells_n:].view(np.int32)[:cells_n])
     if keep.size == 0:
         raise PatternMismatchError("matrix is identically zero; nothing to detect")
     # group on (h1, h2): sort by both, mark key changes -> first-occurrence ids
-    k1, k2 = h1.cpu().numpy()[keep], h2.cpu().numpy()[keep]
+    k1, k2 = dig_h[:cells_n][keep], dig_h[cells_n:2 * cells_n][keep]
     srt = np.lexsort((np.arange(len(keep)), k2, k1))
     new = np.ones(len(keep), dtype=bool)
     new[1:] = (k1[srt][1:] != k1[srt][:-1]) | (k2[srt][1:] != k2[srt][:-1])
@@ -418,9 +431,17 @@ def detect_pattern(a, m: int, n: int, tol: float = 0.0):
                 rest = [g for g in rest if eq[leaders[g]] != 1]
             classes.append(np.sort(np.concatenate([members[g] for g in claim])))
             unclaimed = rest
-    placements = tuple(np.stack(np.divmod(c, q), axis=1).astype(np.int64) for c in classes)
-    pattern = BlockPattern(ell=ell, q=q, m=m, n=n, placements=placements,
-                           structure_class=classify_placements(placements, ell, q))
+    # one divmod / stack over every cell in class order, split into per-class views
+    flat = np.concatenate(classes).astype(np.int64, copy=False)
+    rc = np.stack(np.divmod(flat, q), axis=1)
+    bounds = np.cumsum([len(c) for c in classes])[:-1]
+    placements = tuple(np.ascontiguousarray(x) for x in np.split(rc, bounds))
+    _TRUSTED_PLACEMENTS["on"] = True
+    try:
+        pattern = BlockPattern(ell=ell, q=q, m=m, n=n, placements=placements,
+                               structure_class=classify_placements(placements, ell, q))
+    finally:
+        _TRUSTED_PLACEMENTS["on"] = False
     if _dev.is_device(a):
         # every class's first occurrence, copied by one kernel into a (p, m, n)
         # stack whose slices are the contiguous representatives
