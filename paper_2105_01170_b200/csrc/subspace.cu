@@ -496,7 +496,12 @@ extern "C" int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need,
   if (bq == 0) return BT_OK;
   double prev = -1.0;
   int steps_since_rr = 1;
-  const bool skip_rr = max_iters == SUB_MAX_ITERS_COLD && !no_skip_rr();
+  // silent power steps between Rayleigh-Ritz checks: for the cold many-pair
+  // block (C3 mode 1) and, since C2's deflation passes spent 8 full
+  // Rayleigh-Ritz iterations of ~300 us on a block that converges 10x per
+  // 18 us G product, for every cold block (BT_SUB_SKIP_RR_ALL=0: only the former)
+  static const bool skip_all = !(getenv("BT_SUB_SKIP_RR_ALL") && getenv("BT_SUB_SKIP_RR_ALL")[0] == '0');
+  const bool skip_rr = (max_iters == SUB_MAX_ITERS_COLD || (cold && skip_all)) && !no_skip_rr();
   std::vector<double> wh(b), rh(b);
   for (int it = 0; it < max_iters; ++it) {
     BT_TRY(c.gemm(gemm_args(n, bq, n, g, n, 1, q, bq, 1, y)));       // G Q
@@ -642,14 +647,19 @@ __global__ void scale_rows_kernel(const double* __restrict__ linvt, const double
 
 }  // namespace
 
+// columns per completion block: the one-CTA blocked CholeskyQR factor
+// (chol_rinv_kernel, 54 us at 96 columns) instead of 32-column blocks on the
+// one-warp Cholesky (37 us each, three times as many projections)
+constexpr int64_t COMP_BS = CHOL_MAXB;
+
 extern "C" int64_t bt_complete_basis_ws_bytes(int64_t n, int64_t k, int64_t need) {
-  const int64_t rows = k + need;
-  BtGemmArgs g1 = gemm_args(rows, 32, n, nullptr, 1, rows, nullptr, 32, 1, nullptr);
-  BtGemmArgs g2 = gemm_args(n, 32, rows, nullptr, rows, 1, nullptr, 32, 1, nullptr);
-  BtGemmArgs g3 = gemm_args(32, 32, n, nullptr, 1, 32, nullptr, 32, 1, nullptr);
+  const int64_t rows = k + need, B = COMP_BS;
+  BtGemmArgs g1 = gemm_args(rows, B, n, nullptr, 1, rows, nullptr, B, 1, nullptr);
+  BtGemmArgs g2 = gemm_args(n, B, rows, nullptr, rows, 1, nullptr, B, 1, nullptr);
+  BtGemmArgs g3 = gemm_args(B, B, n, nullptr, 1, B, nullptr, B, 1, nullptr);
   const int64_t gw = std::max(bt_gemm_ws_elems(g1, 1), std::max(bt_gemm_ws_elems(g2, 1),
                                                                  bt_gemm_ws_elems(g3, 1)));
-  return (2 * n * 32 + rows * 32 + 6 * 32 * 32 + 64 + gw + 64) * 8;
+  return (2 * n * B + rows * B + 4 * B * B + B + 64 + gw + 64) * 8;
 }
 
 extern "C" int bt_complete_basis_f64(const double* basis, int64_t n, int64_t k, int64_t need,
@@ -663,29 +673,32 @@ extern "C" int bt_complete_basis_f64(const double* basis, int64_t n, int64_t k, 
   BT_REQUIRE(ws_bytes >= bt_complete_basis_ws_bytes(n, k, need), BT_E_VALUE,
              "complete_basis: workspace too small");
   cudaStream_t st = bt_stream(stream);
+  const int64_t B = COMP_BS;
   double* w = static_cast<double*>(wsv);
-  double* t0 = w;                 // n x 32 working block
-  double* t1 = t0 + n * 32;       // n x 32
-  double* cproj = t1 + n * 32;    // (k + need) x 32
-  double* gm = cproj + (k + need) * 32;
-  double* gs = gm + 32 * 32;
-  double* lt = gs + 32 * 32;
-  double* linvt = lt + 32 * 32;
-  double* mm = linvt + 32 * 32;
-  double* dv = mm + 32 * 32 + 32 * 32;
-  int* flags = reinterpret_cast<int*>(dv + 32);
-  double* gws = dv + 64;
+  double* t0 = w;                 // n x B working block
+  double* t1 = t0 + n * B;        // n x B
+  double* cproj = t1 + n * B;     // (k + need) x B
+  double* gm = cproj + (k + need) * B;
+  double* gs = gm + B * B;
+  double* rinv = gs + B * B;
+  double* mm = rinv + B * B;
+  double* dv = mm + B * B;
+  int* flags = reinterpret_cast<int*>(dv + B);
+  double* gws = dv + B + 64;
   const int64_t gw_elems = ws_bytes / 8 - (gws - w);
   auto run = [&](BtGemmArgs g) {
     g.ws = gws;
     return bt_gemm_run(g, 1, st, 0, gw_elems);
   };
-  const int64_t nblk = (need + 31) / 32;
-  BT_REQUIRE(2 * nblk <= 64, BT_E_SHAPE, "complete_basis: %lld columns exceed 1024", (long long)need);
+  const int64_t nblk = (need + B - 1) / B;
+  BT_REQUIRE(2 * nblk <= 64, BT_E_SHAPE, "complete_basis: %lld columns exceed %lld", (long long)need,
+             (long long)(32 * B));
+  BT_CUDA_CHECK(cudaFuncSetAttribute(chol_rinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sizeof(double) * 2 * CHOL_MAXB * (CHOL_MAXB + 1))));
   BT_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int) * 2 * nblk, st));
   BT_TRY(bt_fill_normal_f64(out, n * need, key, st));
-  for (int64_t j0 = 0; j0 < need; j0 += 32) {
-    const int64_t b = std::min<int64_t>(32, need - j0);
+  for (int64_t j0 = 0; j0 < need; j0 += B) {
+    const int64_t b = std::min<int64_t>(B, need - j0);
     // working copy of the block
     copy_cols_kernel<<<grid_for(n * b), 256, 0, st>>>(out + j0, need, n, b, t0, b);
     BT_LAUNCH_CHECK();
@@ -704,12 +717,16 @@ extern "C" int bt_complete_basis_f64(const double* basis, int64_t n, int64_t k, 
       }
     }
     // column-scaled CholeskyQR2: T <- T D L^-T, twice
+    const int64_t bp = (b + CHOL_CB - 1) / CHOL_CB * CHOL_CB;
+    const size_t smb = sizeof(double) * 2 * bp * (bp + 1);
     for (int it = 0; it < 2; ++it) {
       BT_TRY(run(gemm_args(b, b, n, t0, 1, b, t0, b, 1, gm)));                    // T^T T
-      scale_gram_kernel<<<1, 256, 0, st>>>(gm, static_cast<int>(b), gs, dv);
+      scale_gram_kernel<<<1, 1024, 0, st>>>(gm, static_cast<int>(b), gs, dv);
       BT_LAUNCH_CHECK();
-      BT_TRY(bt_chol_small_f64(gs, b, lt, linvt, flags + 2 * (j0 / 32) + it, st));
-      scale_rows_kernel<<<1, 256, 0, st>>>(linvt, dv, static_cast<int>(b), mm);
+      chol_rinv_kernel<<<1, CHOL_THREADS, smb, st>>>(gs, static_cast<int>(b), rinv,
+                                                     flags + 2 * (j0 / B) + it, nullptr);
+      BT_LAUNCH_CHECK();
+      scale_rows_kernel<<<1, 1024, 0, st>>>(rinv, dv, static_cast<int>(b), mm);
       BT_LAUNCH_CHECK();
       BT_TRY(run(gemm_args(n, b, b, t0, b, 1, mm, b, 1, t1)));                    // T D L^-T
       std::swap(t0, t1);
