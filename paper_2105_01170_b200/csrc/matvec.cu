@@ -19,6 +19,10 @@
 #include "gemm.cuh"
 
 int bt_gemm_run(BtGemmArgs g, int64_t batch, cudaStream_t st, int want_splits, int64_t ws_elems);
+// gemm_tma.cu: C[b] = A[b]^T B on the TMA-fed DMMA kernel (BT_E_VALUE: shape not addressable)
+int bt_gemm_at_tma_ex(const double* a, int64_t lda, int64_t sAb, const double* b, int64_t ldb,
+                      double* c, int64_t ldc, int64_t sCb, int64_t M, int64_t N, int64_t Kdim,
+                      int64_t batch, int transpose_out, cudaStream_t st);
 int64_t bt_gemm_ws_elems(BtGemmArgs g, int64_t batch);
 
 namespace {
@@ -597,13 +601,31 @@ extern "C" int bt_matvec_blr_f64(const bt_pattern_dev* pat, const int64_t* row_p
 namespace {
 
 struct MlPlan {
-  int64_t chunk, off_u, off_w2, off_gws, total;
+  int64_t chunk, off_u, off_w2, off_gws, off_fac, total;
 };
+
+// out[(i d1 + j) d2 + k] = in[i s0 + j s1 + k s2]: the level matrices restacked
+// K-major for the TMA kernel (a few hundred KB per call)
+__global__ void restack_kernel(const double* __restrict__ in, double* __restrict__ out, int64_t d0,
+                               int64_t d1, int64_t d2, int64_t s0, int64_t s1, int64_t s2) {
+  const int64_t n = d0 * d1 * d2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e % d2, j = (e / d2) % d1, i = e / (d1 * d2);
+    out[e] = in[i * s0 + j * s1 + k * s2];
+  }
+}
+
+bool ml_use_tma() {
+  static const bool on = !(getenv("BT_ML_TMA") && getenv("BT_ML_TMA")[0] == '0');
+  return on;
+}
 
 MlPlan ml_plan(int64_t R, const int64_t* nin, const int64_t* nout, int64_t nrhs) {
   // nin = (N3i, N2i, N1i), nout = (N3o, N2o, N1o)
   MlPlan m;
-  const int64_t per_u = nin[0] * nin[1] * R * nout[2];
+  // U of the engine route ([a3][a2][r][i1]) or of the TMA route ([a3][a1][r][i2])
+  const int64_t per_u = std::max(nin[0] * nin[1] * R * nout[2], nin[0] * nin[2] * R * nout[1]);
   const int64_t per_w = nin[0] * R * nout[1] * nout[2];
   const int64_t budget = int64_t(1) << 28;  // ~2 GiB per intermediate
   m.chunk = std::max<int64_t>(1, std::min<int64_t>(nrhs, budget / std::max(per_u, per_w)));
@@ -634,6 +656,7 @@ MlPlan ml_plan(int64_t R, const int64_t* nin, const int64_t* nout, int64_t nrhs)
   g3.Kout = R;
   int64_t w3 = bt_gemm_ws_elems(g3, m.chunk);
   m.off_gws = take(std::max(w1, std::max(w2, w3)));
+  m.off_fac = take(R * (nin[1] * nout[1] + nin[2] * nout[2] + nin[0] * nout[0]));
   m.total = o;
   return m;
 }
@@ -662,6 +685,49 @@ extern "C" int bt_ml_matvec_f64(int64_t nterms, const int64_t* nin, const int64_
   const int64_t gws_n = mp.total - mp.off_gws;
   const int64_t N3i = nin[0], N2i = nin[1], N1i = nin[2];
   const int64_t N3o = nout[0], N2o = nout[1], N1o = nout[2];
+  // ---- TMA route: the three mode products as C[b] = A[b]^T B with the
+  // tensor slab as A (its inner extent is M) and a K-major restack of the
+  // level matrices as B -- no product contracts the innermost index of its
+  // input, because each store rotates the layout:
+  //   1. over a2:  U[(s,a3)][a1][(r,i2)]   = x[(s,a3)][a2][a1]^T S2T[a2][(r,i2)]
+  //   2. over a1:  W[(s,a3)][r][i2][i1]    = U[(s,a3)][a1][r,i2]^T S3T_r[a1][i1]     (per r)
+  //   3. over (a3,r), transposed store:  y[s][i3][(i2,i1)] = (W[s][(a3,r)][(i2,i1)]^T S1K[(a3,r)][i3])^T
+  // C4 (128^3, 16 terms, 32 volumes): see DESIGN.md K11.  Even extents and
+  // 16-byte aligned buffers only; anything else takes the engine route below.
+  const bool even = !((N3i | N2i | N1i | N3o | N2o | N1o) & 1);
+  if (ml_use_tma() && even && mp.chunk * N3i <= 65535 &&
+      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+        reinterpret_cast<uintptr_t>(ws)) & 15u) == 0) {
+    double* S2T = ws + mp.off_fac;                 // [a2][(r,i2)]
+    double* S3T = S2T + R * N2i * N2o;             // [r][a1][i1]
+    double* S1K = S3T + R * N1i * N1o;             // [(a3,r)][i3]
+    restack_kernel<<<grid1d(R * N2i * N2o), 256, 0, st>>>(s2, S2T, N2i, R, N2o, 1, N2o * N2i, N2i);
+    BT_LAUNCH_CHECK();
+    restack_kernel<<<grid1d(R * N1i * N1o), 256, 0, st>>>(s3, S3T, R, N1i, N1o, N1o * N1i, 1, N1i);
+    BT_LAUNCH_CHECK();
+    restack_kernel<<<grid1d(R * N3i * N3o), 256, 0, st>>>(s1, S1K, N3i, R, N3o, 1, N3o * N3i, N3i);
+    BT_LAUNCH_CHECK();
+    bool fell_back = false;
+    for (int64_t s0 = 0; s0 < nrhs && !fell_back; s0 += mp.chunk) {
+      const int64_t ns = std::min(mp.chunk, nrhs - s0);
+      const double* xs = x + s0 * N3i * N2i * N1i;
+      double* ys = y + s0 * N3o * N2o * N1o;
+      int rc = bt_gemm_at_tma_ex(xs, N1i, N2i * N1i, S2T, R * N2o, U, R * N2o, N1i * R * N2o, N1i,
+                                 R * N2o, N2i, ns * N3i, 0, st);
+      if (rc == BT_E_VALUE && s0 == 0) {
+        fell_back = true;   // nothing of y written yet: the engine route runs instead
+        break;
+      }
+      BT_TRY(rc);
+      for (int64_t r = 0; r < R; ++r)
+        BT_TRY(bt_gemm_at_tma_ex(U + r * N2o, R * N2o, N1i * R * N2o, S3T + r * N1i * N1o, N1o,
+                                 W2 + r * N2o * N1o, N1o, R * N2o * N1o, N2o, N1o, N1i, ns * N3i, 0,
+                                 st));
+      BT_TRY(bt_gemm_at_tma_ex(W2, N2o * N1o, N3i * R * N2o * N1o, S1K, N3o, ys, N2o * N1o,
+                               N3o * N2o * N1o, N2o * N1o, N3o, N3i * R, ns, 1, st));
+    }
+    if (!fell_back) return BT_OK;
+  }
   for (int64_t s0 = 0; s0 < nrhs; s0 += mp.chunk) {
     const int64_t ns = std::min(mp.chunk, nrhs - s0);
     const double* xs = x + s0 * N3i * N2i * N1i;
