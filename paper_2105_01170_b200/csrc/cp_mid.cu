@@ -543,7 +543,7 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
   *rc = BT_OK;
   const int64_t I = pb->I, J = pb->J, K = pb->K;
   const int R = static_cast<int>(pb->R);
-  if (off || pb->R > NP || R < 1 || I < 1 || J < 1 || K < 1 || I > 640 || J > 640 || K > 512 ||
+  if (off || pb->R > NP || R < 1 || I < 1 || J < 1 || K < 1 || I > 576 || J > 576 || K > 512 ||
       I * J < 4096 || pb->norm_x <= 0.0 || max_iters < 1)
     return 0;
   const int64_t IJ = I * J;
@@ -561,7 +561,7 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
   const size_t smem3 = sizeof(double) * std::max<size_t>((size_t)rpc * LDX, 4 * 32 * 33);
   const int64_t maxrows = std::max(I, std::max(J, K));
   const size_t smem_solve = sizeof(double) * ((maxrows + 7) / 8 * 8) * LDF * 2;
-  if (smem1 > 100 * 1024 || smem3 > 100 * 1024 || smem_solve > 220 * 1024) return 0;
+  if (smem1 > 100 * 1024 || smem3 > 100 * 1024 || smem_solve > 184 * 1024 /* + ~38 KB static in mid_solve_kernel */) return 0;
   const int64_t ntiles = bt_cdiv(IJ, 8);
   const bool explicit_fit = fit_mode != 2;
 

@@ -71,6 +71,10 @@ def _check(res, ref, tol_hist=1e-10, tol_fac=1e-9):
     ((20, 12, 30), 16, "gram", 1e-2),     # R = 16 (two column tiles)
     ((24, 16, 18), 6, "auto", 1e-6),      # near-exact: the explicit residual takes over
     ((9, 130, 7), 2, "auto", 1e-2),       # long mode 2
+    ((1, 60, 50), 3, "auto", 1e-2),       # a single mode-1 row: seven empty slabs
+    ((40, 1, 33), 2, "explicit", 1e-2),   # J = 1
+    ((30, 44, 2), 2, "auto", 1e-2),       # K = 2 (one padded k-step)
+    ((6, 7, 5), 1, "auto", 1e-2),         # R = 1
 ])
 def test_cluster_and_one_cta_paths_match_oracle(shape, r, fit, noise):
     x = _low_rank(shape, r, sum(shape) + r, noise)
@@ -107,6 +111,11 @@ def test_cluster_tol_stops_like_reference_and_is_deterministic():
     ((100, 90, 300), 12, "auto", 1e-2),    # K > 256: two k spans in pass 2
     ((65, 64, 257), 9, "auto", 1e-2),      # K = 257: ragged 8-blocks
     ((128, 33, 40), 16, "auto", 1e-6),     # near-exact fit
+    ((520, 300, 1), 2, "auto", 1e-2),      # K = 1: one padded 8-block per row
+    ((400, 400, 3), 1, "explicit", 1e-2),  # R = 1, K = 3
+    ((576, 70, 5), 3, "auto", 1e-2),       # the largest mode-1 extent the one-CTA update holds
+    ((600, 70, 5), 3, "auto", 1e-2),       # one past it: the general path
+    ((9, 470, 33), 4, "auto", 1e-2),       # short mode 1, long mode 2
 ])
 def test_small_rank_path_matches_oracle(shape, r, fit, noise):
     x = _low_rank(shape, r, sum(shape) + r, noise)
