@@ -181,3 +181,6 @@ __host__ __device__ constexpr int bt_ld(int x) { return x + ((4 - (x % 16)) % 16
 // number of SMs, cached per process (device 0 semantics of the caller's
 // current device)
 int bt_num_sms();
+
+// keep cudaMallocAsync scratch cached in the device's default pool (gemm.cu)
+void bt_keep_async_pool();

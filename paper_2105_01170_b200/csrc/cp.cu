@@ -2455,6 +2455,7 @@ extern "C" int bt_cp_state_create(const bt_cp_problem* pb, double* a, double* b,
   S->s.lam = lam;
   S->s.scal = sb + 4 * RR + S->pl.R;
   S->s.iter = reinterpret_cast<int*>(S->s.scal + 6);
+  bt_keep_async_pool();
   cudaError_t e = cudaMallocAsync(&S->dhist, sizeof(double) * max_iters, S->st);
   if (e != cudaSuccess) {
     delete S;
@@ -2740,6 +2741,7 @@ static int cp_cluster_try(const bt_cp_problem* pb, double* a, double* b, double*
   const size_t smem = static_cast<size_t>(cluster_layout(I, J, K, R, NP).total) * 8;
   if (smem > 200 * 1024) return 0;
   double* dbuf = nullptr;
+  bt_keep_async_pool();
   cudaError_t e = cudaMallocAsync(&dbuf, sizeof(double) * (max_iters + 2), st);
   if (e != cudaSuccess) {
     bt_set_error("cp_als: %s", cudaGetErrorString(e));
@@ -2816,6 +2818,7 @@ static int cp_small_try(const bt_cp_problem* pb, double* a, double* b, double* c
   const size_t smem = static_cast<size_t>(small_layout(I, J, K, R, NP).total) * 8;
   if (smem > 200 * 1024) return 0;
   double* dbuf = nullptr;
+  bt_keep_async_pool();
   cudaError_t e = cudaMallocAsync(&dbuf, sizeof(double) * (max_iters + 2), st);
   if (e != cudaSuccess) {
     bt_set_error("cp_als: %s", cudaGetErrorString(e));

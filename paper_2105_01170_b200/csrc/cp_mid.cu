@@ -581,6 +581,7 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
                 oRes = take(ntiles), oG = take(3 * NP * NP), oVp = take(3 * NP * NP),
                 oW = take(I * NP), oHist = take(max_iters + 2), oInt = take(4), oPst = take(4);
   double* ws = nullptr;
+  bt_keep_async_pool();
   cudaError_t e = cudaMallocAsync(&ws, sizeof(double) * o, st);
   if (e != cudaSuccess) return fail("workspace", e);
   MidBuf B;
