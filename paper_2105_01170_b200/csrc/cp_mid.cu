@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 
 #include "bt_common.cuh"
 
@@ -534,6 +535,46 @@ extern "C" int bt_debug_mid_clocks(long long* out12) {
   return (int)cudaMemcpyFromSymbol(out12, g_mid_clk, sizeof(long long) * 12);
 }
 
+namespace {
+
+// The sweep graph of the last call, kept for the next one: a repeated call on
+// the same buffers (same X, factor, lambda and scratch addresses, shape, fit
+// mode and ||X||) replays it instead of capturing and instantiating again
+// (~0.4 ms of host time per call at C4).  Every pointer and scalar baked into
+// the graph's kernel arguments is part of the key; the streams and events
+// used for capturing live for the process.
+struct MidGraphKey {
+  const void *x, *a, *b, *c, *lam, *ws;
+  int64_t I, J, K, ws_elems;
+  int R, explicit_fit, dev;
+  double x2;
+  bool operator==(const MidGraphKey& o) const {
+    return x == o.x && a == o.a && b == o.b && c == o.c && lam == o.lam && ws == o.ws && I == o.I &&
+           J == o.J && K == o.K && ws_elems == o.ws_elems && R == o.R &&
+           explicit_fit == o.explicit_fit && dev == o.dev && x2 == o.x2;
+  }
+};
+struct MidGraphCache {
+  std::mutex mu;
+  bool valid = false;
+  MidGraphKey key{};
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t side = nullptr, cs = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int stream_dev = -1;
+  void drop() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
+    gexec = nullptr;
+    graph = nullptr;
+    valid = false;
+  }
+};
+MidGraphCache g_mid_cache;
+
+}  // namespace
+
 // Returns 1 when it ran (outputs written, *rc set), 0 when the problem is not eligible.
 int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, double* lam,
                   int max_iters, double tol, int fit_mode, double* fit_history, int* n_iters,
@@ -599,17 +640,13 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
   B.iter = reinterpret_cast<int*>(ws + oInt);
   B.ticket = reinterpret_cast<unsigned*>(ws + oInt) + 2;
 
-  cudaStream_t side = nullptr, cs = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t gexec = nullptr;
+  MidGraphCache& gc = g_mid_cache;
+  std::lock_guard<std::mutex> lock(gc.mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  // an error path drops the cached graph (it may be half built) and frees the scratch
   auto cleanup = [&]() {
-    if (gexec) cudaGraphExecDestroy(gexec);
-    if (graph) cudaGraphDestroy(graph);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
-    if (side) cudaStreamDestroy(side);
-    if (cs) cudaStreamDestroy(cs);
+    gc.drop();
     cudaFreeAsync(ws, st);
   };
 #define MID_CHECK(x, what)          \
@@ -636,10 +673,18 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
                                  (int)smem_solve), "solve attr");
   MID_CHECK(cudaFuncSetAttribute(mid_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sizeof(double) * maxrows * 17)), "gram attr");
-  MID_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "side stream");
-  MID_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "capture stream");
-  MID_CHECK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
-  MID_CHECK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
+  if (gc.stream_dev != dev) {
+    gc.drop();
+    gc.side = gc.cs = nullptr;       // streams of another device are left to the driver
+    gc.ev_fork = gc.ev_join = nullptr;
+    MID_CHECK(cudaStreamCreateWithFlags(&gc.side, cudaStreamNonBlocking), "side stream");
+    MID_CHECK(cudaStreamCreateWithFlags(&gc.cs, cudaStreamNonBlocking), "capture stream");
+    MID_CHECK(cudaEventCreateWithFlags(&gc.ev_fork, cudaEventDisableTiming), "event");
+    MID_CHECK(cudaEventCreateWithFlags(&gc.ev_join, cudaEventDisableTiming), "event");
+    gc.stream_dev = dev;
+  }
+  cudaStream_t side = gc.side, cs = gc.cs;
+  cudaEvent_t ev_fork = gc.ev_fork, ev_join = gc.ev_join;
 
   const double x2 = pb->norm_x * pb->norm_x;
   const int grid1 = 2 * nsm - 1;   // one slot left for the concurrent pinv warp
@@ -660,7 +705,11 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
                                                      B.P, B.res_part, B.ticket);
   MID_LAUNCH("pass1");
 
-  // the sweep graph: tail of sweep t (three updates) + head of sweep t + 1
+  // the sweep graph: tail of sweep t (three updates) + head of sweep t + 1;
+  // replayed from the cache when every baked-in argument is unchanged
+  const MidGraphKey key{pb->x, a, b, c, lam, ws, I, J, K, o, R, explicit_fit ? 1 : 0, dev, x2};
+  if (!(gc.valid && gc.key == key)) {
+  gc.drop();
   MID_CHECK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
   int cap_rc = BT_OK;
   cudaError_t cap_e = cudaSuccess;
@@ -714,7 +763,7 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
   mid_fit_kernel<<<1, 1024, 0, cs>>>(B.res_part, ntiles, x2, B.fit_hist, B.iter, explicit_fit ? 1 : 0);
   note();
   join();
-  const cudaError_t end_e = cudaStreamEndCapture(cs, &graph);
+  const cudaError_t end_e = cudaStreamEndCapture(cs, &gc.graph);
   if (cap_rc != BT_OK || cap_e != cudaSuccess || end_e != cudaSuccess) {
     cudaGetLastError();
     cleanup();
@@ -724,12 +773,15 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
     }
     return fail("sweep graph capture", cap_e != cudaSuccess ? cap_e : end_e);
   }
-  MID_CHECK(cudaGraphInstantiate(&gexec, graph, 0), "graph instantiate");
+  MID_CHECK(cudaGraphInstantiate(&gc.gexec, gc.graph, 0), "graph instantiate");
+  gc.key = key;
+  gc.valid = true;
+  }
 
   int it = 0, conv = 0;
   double prev = -INFINITY;
   for (it = 1; it <= max_iters; ++it) {
-    MID_CHECK(cudaGraphLaunch(gexec, st), "graph launch");
+    MID_CHECK(cudaGraphLaunch(gc.gexec, st), "graph launch");
     if (tol > 0.0) {
       double fitv = 0.0;
       MID_CHECK(cudaMemcpyAsync(&fitv, B.fit_hist + (it - 1), sizeof(double), cudaMemcpyDeviceToHost, st),
@@ -751,7 +803,7 @@ int bt_cp_mid_try(const bt_cp_problem* pb, double* a, double* b, double* c, doub
   MID_CHECK(cudaStreamSynchronize(st), "sync");
   *n_iters = it;
   *converged = conv;
-  cleanup();
+  cudaFreeAsync(ws, st);   // the cached graph is only replayed if the next call gets this block again
   e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return fail("sync", e);
 #undef MID_CHECK
