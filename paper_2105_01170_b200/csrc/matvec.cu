@@ -184,28 +184,40 @@ __global__ void __launch_bounds__(256)
 // the rows' middles S_{class(i, j)} (zero for uncovered cells); BK = 16 over
 // the rr columns.  The block columns are split over gridDim.z with partials
 // reduced in a fixed order (deterministic).
-namespace blrrows {
-constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, THREADS = 128;
-constexpr int LDA = bt_ld(BK), LDB = bt_ld(BK);
-constexpr int A_STAGE = BM * LDA, B_STAGE = BN * LDB;
-constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * 8;
-constexpr int TM = 64, TN = 32, FM = TM / 8, FN = TN / 8;
-}  // namespace blrrows
+// BN = 64: 4 warps of 64x32 (2 x 2); BN = 32 / 16 (few right-hand sides: C3's
+// 16): 4 warps of 32 x BN stacked along the rows, so the tile carries no
+// all-zero RHS columns (the 64-wide tile ran 16 RHS at 7.6 TF/s, 3/4 of its
+// DMMAs on padding).
+template <int BN_>
+struct BlrRows {
+  static constexpr int BM = 128, BN = BN_, BK = 16, STAGES = 3, THREADS = 128;
+  static constexpr int LDA = bt_ld(BK), LDB = bt_ld(BK);
+  static constexpr int A_STAGE = BM * LDA, B_STAGE = BN * LDB;
+  static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * 8;
+  static constexpr int WM = BN_ >= 64 ? 2 : 4;                 // warps along the rows
+  static constexpr int TM = BM / WM, TN = BN / (4 / WM), FM = TM / 8, FN = TN / 8;
+  static constexpr int BCH = BN * 8 / THREADS;                // 16-byte B chunks per thread
+  static_assert(BN_ == 16 || BN_ == 32 || BN_ == 64, "RHS tile of 16, 32 or 64");
+};
+inline int blr_rows_bn(int64_t nrhs) { return nrhs <= 16 ? 16 : (nrhs <= 32 ? 32 : 64); }
 
-template <int RLP>
-__global__ void __launch_bounds__(blrrows::THREADS)
+template <int RLP, int BN_>
+__global__ void __launch_bounds__(BlrRows<BN_>::THREADS)
     blr_rows_kernel(const double* __restrict__ shat, const double* __restrict__ z,
                     const int32_t* __restrict__ cell_class, int64_t rl, int64_t rr, int64_t q,
                     int64_t nrhs, int64_t ell, int64_t jchunk, double* __restrict__ out,
                     int64_t out_split_stride) {
-  using namespace blrrows;
+  using Cfg = BlrRows<BN_>;
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES, THREADS = Cfg::THREADS;
+  constexpr int LDA = Cfg::LDA, LDB = Cfg::LDB, A_STAGE = Cfg::A_STAGE, B_STAGE = Cfg::B_STAGE;
+  constexpr int TM = Cfg::TM, TN = Cfg::TN, FM = Cfg::FM, FN = Cfg::FN, BCH = Cfg::BCH;
   constexpr int R = BM / RLP;  // block rows per CTA
   extern __shared__ __align__(16) double sm[];
   double* As = sm;
   double* Bs = sm + STAGES * A_STAGE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;
-  const int wm0 = (warp & 1) * TM, wn0 = (warp >> 1) * TN;
+  const int wm0 = (warp % Cfg::WM) * TM, wn0 = (warp / Cfg::WM) * TN;
   const int64_t i0 = blockIdx.x * (int64_t)R;
   const int64_t s0 = blockIdx.y * (int64_t)BN;
   const int64_t j0 = blockIdx.z * jchunk;
@@ -223,9 +235,9 @@ __global__ void __launch_bounds__(blrrows::THREADS)
     a_r[it] = idx >> 3;
     a_c[it] = (idx & 7) * 2;
   }
-  int b_r[4], b_c[4];
+  int b_r[BCH], b_c[BCH];
 #pragma unroll
-  for (int it = 0; it < 4; ++it) {
+  for (int it = 0; it < BCH; ++it) {
     const int idx = threadIdx.x + it * THREADS;
     b_r[it] = idx >> 3;
     b_c[it] = (idx & 7) * 2;
@@ -254,7 +266,7 @@ __global__ void __launch_bounds__(blrrows::THREADS)
       cp_async16(as + m * LDA + a_c[it], src, valid);
     }
 #pragma unroll
-    for (int it = 0; it < 4; ++it) {
+    for (int it = 0; it < BCH; ++it) {
       const int n = b_r[it];
       const int64_t s = s0 + n;
       const int64_t cl = rr - k0 - b_c[it];
@@ -353,24 +365,24 @@ int blr_rows_splits(int64_t ctas, int64_t q, int resident) {
   return best;
 }
 
-template <int RLP>
-int launch_blr_rows(const double* shat, const double* z, const int32_t* cell_class, int64_t rl,
-                    int64_t rr, int64_t q, int64_t nrhs, int64_t ell, double* yb, double* part,
-                    int splits, cudaStream_t st) {
-  using namespace blrrows;
+template <int RLP, int BN_>
+int launch_blr_rows_t(const double* shat, const double* z, const int32_t* cell_class, int64_t rl,
+                      int64_t rr, int64_t q, int64_t nrhs, int64_t ell, double* yb, double* part,
+                      int splits, cudaStream_t st) {
+  using Cfg = BlrRows<BN_>;
   static bool attr = false;
   if (!attr) {
-    BT_CUDA_CHECK(cudaFuncSetAttribute(blr_rows_kernel<RLP>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    BT_CUDA_CHECK(cudaFuncSetAttribute(blr_rows_kernel<RLP, BN_>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
     attr = true;
   }
-  constexpr int R = BM / RLP;
+  constexpr int R = Cfg::BM / RLP;
   const int64_t jchunk = bt_cdiv(q, splits);
-  dim3 grid(static_cast<unsigned>(bt_cdiv(ell, R)), static_cast<unsigned>(bt_cdiv(nrhs, BN)),
+  dim3 grid(static_cast<unsigned>(bt_cdiv(ell, R)), static_cast<unsigned>(bt_cdiv(nrhs, Cfg::BN)),
             static_cast<unsigned>(splits));
   const int64_t nout = nrhs * ell * rl;
-  blr_rows_kernel<RLP><<<grid, THREADS, SMEM, st>>>(shat, z, cell_class, rl, rr, q, nrhs, ell,
-                                                    jchunk, splits > 1 ? part : yb, nout);
+  blr_rows_kernel<RLP, BN_><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(
+      shat, z, cell_class, rl, rr, q, nrhs, ell, jchunk, splits > 1 ? part : yb, nout);
   BT_LAUNCH_CHECK();
   if (splits > 1) {
     split_sum_kernel<<<grid1d(nout), 256, 0, st>>>(part, nout, splits, yb);
@@ -380,14 +392,34 @@ int launch_blr_rows(const double* shat, const double* z, const int32_t* cell_cla
 }
 
 template <int RLP>
-int blr_rows_resident() {
+int launch_blr_rows(const double* shat, const double* z, const int32_t* cell_class, int64_t rl,
+                    int64_t rr, int64_t q, int64_t nrhs, int64_t ell, double* yb, double* part,
+                    int splits, cudaStream_t st) {
+  const int bn = blr_rows_bn(nrhs);
+  if (bn == 16)
+    return launch_blr_rows_t<RLP, 16>(shat, z, cell_class, rl, rr, q, nrhs, ell, yb, part, splits, st);
+  if (bn == 32)
+    return launch_blr_rows_t<RLP, 32>(shat, z, cell_class, rl, rr, q, nrhs, ell, yb, part, splits, st);
+  return launch_blr_rows_t<RLP, 64>(shat, z, cell_class, rl, rr, q, nrhs, ell, yb, part, splits, st);
+}
+
+template <int RLP, int BN_>
+int blr_rows_resident_t() {
+  using Cfg = BlrRows<BN_>;
   int per_sm = 0;
-  cudaFuncSetAttribute(blr_rows_kernel<RLP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)blrrows::SMEM);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blr_rows_kernel<RLP>,
-                                                    blrrows::THREADS, blrrows::SMEM) != cudaSuccess)
+  cudaFuncSetAttribute(blr_rows_kernel<RLP, BN_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)Cfg::SMEM);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blr_rows_kernel<RLP, BN_>, Cfg::THREADS,
+                                                    Cfg::SMEM) != cudaSuccess)
     per_sm = 1;
   return per_sm;
+}
+
+template <int RLP>
+int blr_rows_resident(int64_t nrhs) {
+  const int bn = blr_rows_bn(nrhs);
+  return bn == 16 ? blr_rows_resident_t<RLP, 16>()
+                  : (bn == 32 ? blr_rows_resident_t<RLP, 32>() : blr_rows_resident_t<RLP, 64>());
 }
 
 template <int RLP, int RRP, int NB>
@@ -446,8 +478,8 @@ BlrPlan blr_plan(const bt_pattern_dev* pat, int64_t rl, int64_t rr, int64_t nrhs
   b.splits = 1;
   if (b.rows) {
     const int rlp = rl <= 32 ? 32 : 64;
-    const int resident = rlp == 32 ? blr_rows_resident<32>() : blr_rows_resident<64>();
-    const int64_t ctas = bt_cdiv(pat->ell, blrrows::BM / rlp) * bt_cdiv(nrhs, blrrows::BN);
+    const int resident = rlp == 32 ? blr_rows_resident<32>(nrhs) : blr_rows_resident<64>(nrhs);
+    const int64_t ctas = bt_cdiv(pat->ell, 128 / rlp) * bt_cdiv(nrhs, blr_rows_bn(nrhs));
     b.splits = blr_rows_splits(ctas, pat->q, resident);
   }
   int64_t o = 0;
