@@ -729,9 +729,6 @@ __device__ void pinv_block(const double* __restrict__ g0, const double* __restri
 // eigen path's: rotate while |(J^T V J)_pq| > 1e-15 ||V||_F, then
 // pinv(V) = sum_{|lambda_k| > 1e-15 max|lambda|} J_k J_k^T / lambda_k with
 // lambda_k = (J^T V J)_kk (numpy's rcond cutoff, decomp.py:387).
-template <int NP>
-__device__ __noinline__ bool chol_inv_reg(const double* __restrict__ g0, const double* __restrict__ g1,
-                                          int R, double* __restrict__ vp, double* sc);
 
 // In-place Gauss-Jordan inverse of V = g0 o g1 (SPD: no pivoting needed) by
 // one warp, the matrix spread over the lanes' registers (NP = 8: lane holds
@@ -830,7 +827,7 @@ __global__ void __launch_bounds__(32) pinv_jacobi1_kernel(const double* __restri
   const int lane = threadIdx.x;
   const int col = lane % NP, half = lane / NP, r0 = half * ROWS;
   double w[ROWS];
-  // ---- well-conditioned V: register-resident Cholesky inverse (chol_inv_reg),
+  // ---- well-conditioned V: in-register Gauss-Jordan inverse (spd_inv_gj),
   // accepted on pinv_block's test (kappa_1 <= 1e12, where numpy's pinv is
   // the inverse to ~kappa eps)
   {
@@ -1076,83 +1073,6 @@ __device__ __forceinline__ double small_block_sum(double v, double* red) {
 // syncs only): the fast path of pinv_block (V^-1 = L^-T L^-1, accepted when
 // ||V||_1 ||V^-1||_1 <= 1e12).  Returns false (warp-uniform) when the caller
 // must take pinv_block's eigen path.  a, y: R x (R+1) scratch each.
-// Register-resident variant for R <= NP (8 or 16): lane i holds row i of V
-// (rows past R padded with the identity), the Cholesky steps are unrolled so
-// every row / column index is static -- L's column k reaches the other lanes
-// by shuffles, nothing goes through memory until Y = L^-1 is formed (one row
-// of Y per lane, rows of L by shuffle), and V^-1 = Y^T Y is read back from
-// shared memory.  Same acceptance test as pinv_warp_chol.  sc: >= NP*(NP+1)
-// doubles of shared scratch.
-template <int NP>
-__device__ __noinline__ bool chol_inv_reg(const double* __restrict__ g0, const double* __restrict__ g1,
-                                          int R, double* __restrict__ vp, double* sc) {
-  const int lane = threadIdx.x & 31;
-  const int i = lane < NP ? lane : NP - 1;   // lanes past NP mirror the last row (results unused)
-  double row[NP];
-#pragma unroll
-  for (int j = 0; j < NP; ++j) {
-    double v = (i == j) ? 1.0 : 0.0;
-    if (i < R && j < R) v = g1 ? g0[i * R + j] * g1[i * R + j] : g0[i * R + j];
-    row[j] = v;
-  }
-  // ||V||_1 = max column sum = max row sum (symmetric)
-  double rs = 0.0;
-#pragma unroll
-  for (int j = 0; j < NP; ++j) rs += (j < R && i < R) ? fabs(row[j]) : 0.0;
-  double vn1 = rs;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) vn1 = fmax(vn1, __shfl_xor_sync(0xffffffffu, vn1, o));
-  int ok = 1;
-  double lo = INFINITY, hi = 0.0, rdiag[NP];
-#pragma unroll
-  for (int k = 0; k < NP; ++k) {
-    const double d = __shfl_sync(0xffffffffu, row[k], k);
-    ok &= (d > 0.0);
-    const double r = rsqrt_nr(fmax(d, 1e-300));
-    rdiag[k] = r;
-    lo = fmin(lo, d * r);
-    hi = fmax(hi, d * r);
-    const double lik = (i == k) ? d * r : row[k] * r;   // L[i][k] (lane i > k), L[k][k]
-    row[k] = (i >= k) ? lik : 0.0;
-#pragma unroll
-    for (int j = k + 1; j < NP; ++j) {
-      const double ljk = __shfl_sync(0xffffffffu, lik, j);
-      if (i >= j) row[j] -= lik * ljk;
-    }
-  }
-  if (!ok || (hi / lo) * (hi / lo) > 1e12 * R) return false;   // warp-uniform
-  // Y = L^-1: lane c builds column c, y_m = -(sum_{k<m} L[m][k] y_k) / L[m][m]
-  const int c = i;
-  double y[NP];
-#pragma unroll
-  for (int m = 0; m < NP; ++m) {
-    double acc = 0.0;
-#pragma unroll
-    for (int k = 0; k < m; ++k) acc = fma(__shfl_sync(0xffffffffu, row[k], m), y[k], acc);
-    y[m] = (m < c) ? 0.0 : ((m == c) ? rdiag[m] : -acc * rdiag[m]);
-  }
-  // V^-1 = Y^T Y through shared memory (column c of Y from lane c)
-  __syncwarp();
-  if (lane < NP)
-#pragma unroll
-    for (int m = 0; m < NP; ++m) sc[m * (NP + 1) + lane] = y[m];
-  __syncwarp();
-  double in1 = 0.0;
-  for (int e = lane; e < R * R; e += 32) {
-    const int r0 = e / R, c0 = e % R;
-    double v = 0.0;
-#pragma unroll
-    for (int m = 0; m < NP; ++m) v = fma(sc[m * (NP + 1) + r0], sc[m * (NP + 1) + c0], v);
-    vp[e] = v;
-  }
-  __syncwarp();
-  if (lane < R)
-    for (int r0 = 0; r0 < R; ++r0) in1 += fabs(vp[r0 * R + lane]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) in1 = fmax(in1, __shfl_xor_sync(0xffffffffu, in1, o));
-  return vn1 * in1 <= 1e12;
-}
-
 __device__ bool pinv_warp_chol(const double* __restrict__ g0, const double* __restrict__ g1,
                                int R, double* __restrict__ vp, double* a, double* y) {
   const int lane = threadIdx.x & 31;

@@ -1,6 +1,6 @@
 // bt200 -- CP-ALS of an SM-sized tensor on a thread-block cluster (C1: 32^3,
 // R = 8; decomp.py:344-410).  Included by cp.cu inside its anonymous
-// namespace (it uses chol_inv_reg / pinv_block / small_block_sum).
+// namespace (it uses spd_inv_gj / pinv_block / small_block_sum).
 //
 // The one-CTA kernel (cp_small_kernel) re-reads X from L2 twice per sweep
 // and runs on one SM.  Here a cluster of CS = 8 CTAs keeps X in distributed
