@@ -156,7 +156,13 @@ typedef struct bt_cp_problem {
  * precision), 1 always explicit (reference semantics decomp.py:395-396),
  * 2 Gram identity only.  The host loop reads the fit back once per sweep only
  * when tol > 0 (convergence test); with tol <= 0 the sweeps run without host
- * synchronisation. */
+ * synchronisation.
+ * Without phase_ms the call picks the path by size: a tensor that fits the
+ * shared memory of 8 SMs (I*J*K <= 2^17, R <= 16) runs every sweep in ONE
+ * launch on a thread-block cluster (cp_cluster.cuh; one-CTA fallback); R <= 16
+ * beyond that (I, J <= 576, K <= 512) runs the two-pass sweep of cp_mid.cu,
+ * where fit_mode 0 and 1 both report the explicit fit (its residual rides on
+ * the X x3 C pass); everything else the dimension-tree phases below. */
 int64_t bt_cp_als_ws_bytes(const bt_cp_problem* pb);
 /* Dimension-tree root the CP phases use for this problem: 0 = P = X x3 C
  * (modes 1/2 from P, mode 3 a full GEMM), 1 = Q = X x1 A (mode 1 from the
