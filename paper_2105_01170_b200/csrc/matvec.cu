@@ -648,9 +648,8 @@ __global__ void restack_kernel(const double* __restrict__ in, double* __restrict
   }
 }
 
-bool ml_use_tma() {
-  static const bool on = !(getenv("BT_ML_TMA") && getenv("BT_ML_TMA")[0] == '0');
-  return on;
+bool ml_use_tma() {   // read per call: the route-against-route test switches it in-process
+  return !(getenv("BT_ML_TMA") && getenv("BT_ML_TMA")[0] == '0');
 }
 
 MlPlan ml_plan(int64_t R, const int64_t* nin, const int64_t* nout, int64_t nrhs) {

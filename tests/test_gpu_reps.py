@@ -113,6 +113,59 @@ def test_blr_matvec_wide_ranks_and_partial_patterns():
         assert rel(got, ref) < 1e-12, (kind, rl, rr)
 
 
+@pytest.mark.parametrize("nrhs", [1, 3, 16, 17, 32, 33, 64, 70])
+def test_blr_matvec_every_rhs_tile_width(nrhs):
+    """The row-group kernel's RHS tile is 16, 32 or 64 wide by the number of
+    right-hand sides (reconstruct.py:300-315 semantics): every width, its
+    ragged edges and the > 64 RHS grid against densify @ x."""
+    rng = np.random.default_rng(100 + nrhs)
+    pat = bt.build_pattern("toeplitz", 11, 11, 40, 40, block_symmetric=True)
+    rl = rr = 24
+    left = rng.standard_normal((pat.m, rl))
+    right = rng.standard_normal((pat.n, rr))
+    mids = rng.standard_normal((pat.p, rl, rr))
+    rep = reconstruct.BlockLowRankRep(pattern=pat, left=left, right=right, middles=mids)
+    xs = rng.standard_normal((pat.shape[1], nrhs))
+    ref = port.expand(pat, np.einsum("ma,kab,nb->kmn", left, mids, right)) @ xs
+    got = reconstruct.matvec(rep, xs)
+    assert rel(got, ref) < 1e-12
+
+
+@pytest.mark.parametrize("nin,nout", [((8, 6, 10), (8, 6, 10)), ((12, 10, 8), (6, 14, 16)),
+                                      ((7, 6, 10), (8, 6, 10)), ((4, 4, 4), (4, 4, 5))])
+def test_ml_matvec_tma_route_equals_engine_route(nin, nout):
+    """The multilevel matvec's TMA route (three rotated mode products on the
+    transposed-A kernel; even extents) and the cp.async engine route (the
+    fallback for odd extents) against each other and against the dense
+    Kronecker sum, on cubic, non-cubic and odd level sizes."""
+    import os
+
+    rng = np.random.default_rng(sum(nin) + sum(nout))
+
+    class T:
+        def __init__(self, mats):
+            self.level_mats = mats
+            self.block = np.ones((1, 1))
+
+    terms = [T([rng.standard_normal((nout[l], nin[l])) for l in range(3)]) for _ in range(5)]
+    vols = rng.standard_normal((int(np.prod(nin)), 6))
+    dense = sum(np.kron(np.kron(t.level_mats[0], t.level_mats[1]), t.level_mats[2]) for t in terms)
+    ref = dense @ vols
+    got = multilevel.ml_matvec(terms, vols)
+    assert rel(got, ref) < 1e-12
+    saved = os.environ.get("BT_ML_TMA")
+    os.environ["BT_ML_TMA"] = "0"
+    try:
+        eng = multilevel.ml_matvec(terms, vols)
+    finally:
+        if saved is None:
+            os.environ.pop("BT_ML_TMA", None)
+        else:
+            os.environ["BT_ML_TMA"] = saved
+    assert rel(eng, ref) < 1e-12
+    assert rel(got, eng) < 1e-13
+
+
 def test_flop_count_linear_in_terms():
     """test_reconstruct.py:152-165 / acceptance 9: r * (2mnq + 2m nnz)."""
     rng = np.random.default_rng(8)
