@@ -373,6 +373,11 @@ struct Ctx {
   }
 };
 
+bool skip_polish() {
+  static const bool on = !(getenv("BT_SUB_POLISH_ALL") && getenv("BT_SUB_POLISH_ALL")[0] == '1');
+  return on;
+}
+
 // Column-scaled SVQB of y (n x b, row-major) into q (n x keep); returns keep
 // (0 when y is numerically zero) through *keep and the dropped count.
 int svqb(const Ctx& c, const double* y, int64_t n, int64_t b, double* q, int64_t* keep_out,
@@ -410,9 +415,17 @@ int svqb(const Ctx& c, const double* y, int64_t n, int64_t b, double* q, int64_t
       BT_CUDA_CHECK(cudaStreamSynchronize(c.st));
     }
     if (hflag == 0) {
-      BtGemmArgs g = gemm_args(n, b, b, y, b, 1, v2, b, 1, out);
+      // the silent power steps (sticky given) skip the Newton-Schulz polish:
+      // their block is re-orthonormalised by the next step anyway, and the
+      // last iteration before the Rayleigh-Ritz check polishes
+      const bool polish = sticky == nullptr || !skip_polish();
+      BtGemmArgs g = gemm_args(n, b, b, y, b, 1, v2, b, 1, polish ? out : q);
       g.ascale = dinv;
       BT_TRY(c.gemm(g));
+      if (!polish) {
+        *keep_out = b;
+        return BT_OK;
+      }
       BT_TRY(c.gemm(gemm_args(b, b, n, out, 1, b, out, b, 1, m)));
       ns_kernel<<<grid_for(b * b), 256, 0, c.st>>>(m, b, ms);
       BT_LAUNCH_CHECK();
@@ -651,6 +664,8 @@ __global__ void scale_rows_kernel(const double* __restrict__ linvt, const double
 // (chol_rinv_kernel, 54 us at 96 columns) instead of 32-column blocks on the
 // one-warp Cholesky (37 us each, three times as many projections)
 constexpr int64_t COMP_BS = CHOL_MAXB;
+constexpr int COMP_PASSES = 2;   // projection passes per block (twice is enough: one pass leaves ~eps of the
+                                 // block along the basis, which the ERA rank test at n eps sigma_1 sees)
 
 extern "C" int64_t bt_complete_basis_ws_bytes(int64_t n, int64_t k, int64_t need) {
   const int64_t rows = k + need, B = COMP_BS;
@@ -702,7 +717,7 @@ extern "C" int bt_complete_basis_f64(const double* basis, int64_t n, int64_t k, 
     // working copy of the block
     copy_cols_kernel<<<grid_for(n * b), 256, 0, st>>>(out + j0, need, n, b, t0, b);
     BT_LAUNCH_CHECK();
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = 0; pass < COMP_PASSES; ++pass) {
       // against the input basis, then the completed columns 0 .. j0
       const double* qs[2] = {basis, out};
       const int64_t qk[2] = {k, j0};
