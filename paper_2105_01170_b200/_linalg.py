@@ -483,6 +483,33 @@ def mode_basis_dev(xd, mode: int, r: int, extra_mode: int | None = None, max_pas
     return basis[:, :r].contiguous()
 
 
+def small_mode_basis_enqueue(xd, mode: int, r: int):
+    """First pass of mode_basis_dev for a mode whose extent fits the one-CTA
+    Jacobi (n <= SMALL_EIG), enqueued on the current stream without a host
+    read: Gram + full eigensolve.  None when mode_basis_dev would start with
+    the Gram-free refinement instead.  hosvd runs this for its short modes
+    on a side stream beside the long mode's deflation passes (the bases of
+    the original unfoldings are independent, decomp.py:247-256)."""
+    n = int(xd.shape[mode - 1])
+    if n > SMALL_EIG or (REFINE and r <= 32 and n >= 2 * r):
+        return None
+    g = unfold_gram_dev(xd, mode)
+    w, v = eigh_dev(g, nvec=r, tau=RESOLVE_TAU)
+    return g, w, v
+
+
+def small_mode_basis_finish(handle, xd, mode: int, r: int):
+    """The host side of that first pass: the basis when the pass resolved
+    every wanted pair (the same test mode_basis_dev applies), else the full
+    deflation loop from scratch."""
+    _, w, v = handle
+    wh = _dev.to_host(w)
+    top = max(float(wh[0]), 0.0)
+    if top > 0.0 and int(np.sum(wh[:r] > RESOLVE_TAU * wh[0])) >= r:
+        return v[:, :r].contiguous()
+    return mode_basis_dev(xd, mode, r)
+
+
 def _scaled_gemm(a, b, scale, ta=False):
     """op(a) @ b @ diag(scale) on the engine (the diagonal rides on B's
     per-column scale)."""

@@ -21,6 +21,7 @@ Inputs may be numpy (outputs numpy, reference semantics) or CUDA tensors.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -197,6 +198,17 @@ def _mode_basis(mat, r: int):
 # ---------------------------------------------------------------------------
 
 
+_SIDE_MODES = os.environ.get("BT_HOSVD_SIDE", "1") != "0"
+_side = {}
+
+
+def _side_stream():
+    dev = _dev.torch().cuda.current_device()
+    if dev not in _side:
+        _side[dev] = _dev.torch().cuda.Stream()
+    return _side[dev]
+
+
 def _project_core(xd, factors):
     core = xd
     for k, u in enumerate(factors):
@@ -210,12 +222,34 @@ def hosvd(t, ranks) -> TuckerRep:
     sequential projection in mode order."""
     if len(ranks) != t.ndim:
         raise ShapeError(f"expected {t.ndim} ranks, got {len(ranks)}")
-    xd = _dev.to_device(t)
-    factors = []
     for k, r in enumerate(ranks):
         if not 1 <= r <= t.shape[k]:
             raise ShapeError(f"mode-{k + 1} rank {r} out of range for extent {t.shape[k]}")
-        factors.append(L.mode_basis_dev(xd, k + 1, int(r)))
+    xd = _dev.to_device(t)
+    tc = _dev.torch().cuda
+    # the bases come from the original unfoldings, so the modes are
+    # independent: the short ones (one Gram + one one-CTA eigensolve, no host
+    # read) go to a side stream and run beside the long modes' passes
+    main, side, pending = tc.current_stream(), None, {}
+    if _SIDE_MODES and max(int(s) for s in t.shape) > L.SMALL_EIG:
+        for k, r in enumerate(ranks):
+            if int(t.shape[k]) > L.SMALL_EIG:
+                continue
+            if side is None:
+                side = _side_stream()
+                side.wait_stream(main)
+            with tc.stream(side):
+                h = L.small_mode_basis_enqueue(xd, k + 1, int(r))
+            if h is not None:
+                pending[k] = h
+    factors = [None if k in pending else L.mode_basis_dev(xd, k + 1, int(r))
+               for k, r in enumerate(ranks)]
+    if side is not None:
+        main.wait_stream(side)
+    for k, h in pending.items():
+        for buf in h:
+            buf.record_stream(main)
+        factors[k] = L.small_mode_basis_finish(h, xd, k + 1, int(ranks[k]))
     core = _project_core(xd, factors)
     return TuckerRep(core=_dev.like_input(t, core),
                      factors=tuple(_dev.like_input(t, f) for f in factors))
