@@ -110,7 +110,16 @@ int bt_scatter_blocks_f64(const double* t, int64_t t_sm, int64_t t_sp, int64_t t
  * entry not +-0.0, i.e. blk.any(); tol > 0: NOT max|blk| <= tol, NaN kept).
  * Match: for every cell with cand[cell] >= 0, eq[cell] = 1 iff the block
  * equals block cand[cell] (exact != 0: bit for bit; else max|d| <= tol,
- * NaN failing).  Asynchronous. */
+ * NaN failing).  Group: leader[cell] = the row-major first cell with the same
+ * (h1, h2) among the cells with nz != 0 (-1 for a cell with nz == 0) and
+ * cand[cell] = leader[cell] if another cell leads, else -1 -- the host's
+ * first-occurrence grouping (blocks.py:300-318) on the device, so digest,
+ * grouping and match queue without a host round trip.  ws: at least
+ * bt_block_group_ws_bytes(cells) bytes (-1: cell count out of range).
+ * Asynchronous. */
+int64_t bt_block_group_ws_bytes(int64_t cells);
+int bt_block_group(const uint64_t* h1, const uint64_t* h2, const int* nz, int64_t cells,
+                   int64_t* leader, int64_t* cand, void* ws, int64_t ws_bytes, void* stream);
 int bt_block_digest_f64(const double* a, int64_t lda, int64_t ell, int64_t q, int64_t m, int64_t n,
                         double tol, uint64_t* h1, uint64_t* h2, int* nz, void* stream);
 int bt_block_match_f64(const double* a, int64_t lda, int64_t ell, int64_t q, int64_t m, int64_t n,

@@ -92,6 +92,8 @@ _SIGS = {
     "bt_qr_thin_f64": (C.c_int, [_dp, _i64, _i64, _dp, _dp, _dp, _i64, _dp]),
     "bt_block_digest_f64": (C.c_int, [_dp, _i64, _i64, _i64, _i64, _i64, C.c_double, _dp, _dp,
                                       _dp, _dp]),
+    "bt_block_group_ws_bytes": (_i64, [_i64]),
+    "bt_block_group": (C.c_int, [_dp, _dp, _dp, _i64, _dp, _dp, _dp, _i64, _dp]),
     "bt_block_match_f64": (C.c_int, [_dp, _i64, _i64, _i64, _i64, _i64, _dp, C.c_double, C.c_int,
                                      _dp, _dp]),
     "bt_fill_normal_f64": (C.c_int, [_dp, _i64, C.c_uint64, _dp]),

@@ -269,12 +269,6 @@ def kernel_level_pattern(k: int, bm: int, bn: int, grid: int | None = None) -> B
     return _make(grid, grid, bm, bn, [_diag(grid, h - i) for i in range(k)], f"toeplitz:{h}")
 
 
-def _class_segments(placements):
-    counts = np.array([len(c) for c in placements], dtype=np.int64)
-    starts = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
-    return counts, starts
-
-
 def _one_or_two_values(v, counts, starts):
     """Per class: (min, max, every value is min or max) of the segment."""
     lo = np.minimum.reduceat(v, starts)
@@ -290,10 +284,17 @@ def classify_placements(placements, ell: int, q: int) -> str:
     set logic: one offset covering a full diagonal, or a +-d pair covering
     both; one anti-diagonal sum covering it fully; else the bandwidth)."""
     allc = np.vstack(placements) if placements else np.zeros((0, 2), dtype=np.int64)
+    counts = np.array([len(c) for c in placements], dtype=np.int64)
+    return _classify_cells(allc, counts, ell, q)
+
+
+def _classify_cells(allc, counts, ell: int, q: int) -> str:
+    """classify_placements on the stacked (cells, 2) array + per-class counts."""
     if len(allc) and np.all(allc[:, 0] == allc[:, 1]):
         return "diagonal"
-    if placements and ell == q:
-        counts, starts = _class_segments(placements)
+    if len(counts) and ell == q:
+        counts = np.asarray(counts, dtype=np.int64)
+        starts = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
         off = allc[:, 1] - allc[:, 0]
         lo, hi, two = _one_or_two_values(off, counts, starts)
         single = lo == hi
@@ -355,9 +356,10 @@ def detect_pattern(a, m: int, n: int, tol: float = 0.0):
 
     One device pass digests every block (128-bit, order independent) and
     evaluates the reference's skip predicate; equal digests are grouped on
-    the host in row-major first-occurrence order; a second pass checks every
-    cell bit for bit against its group's first cell (a digest collision is
-    split off, never merged).  tol > 0 keeps the reference's linear-scan
+    the device in row-major first-occurrence order (bt_block_group); a second
+    pass checks every cell bit for bit against its group's first cell (a
+    digest collision is split off, never merged); the three launches queue
+    back to back and one read brings leaders and verdicts to the host.  tol > 0 keeps the reference's linear-scan
     semantics -- a block joins the first earlier representative within tol --
     as a greedy over the distinct blocks: representative k is the first
     unclaimed block, and one device pass claims every unclaimed block within
@@ -372,31 +374,34 @@ def detect_pattern(a, m: int, n: int, tol: float = 0.0):
     t = _dev.torch()
     ad = _dev.to_device(a).contiguous()
     cells_n = ell * q
-    # [h1 | h2 | nz (int32 pairs)] in one buffer: one read-back, one synchronisation
+    wsb = int(N.load().bt_block_group_ws_bytes(cells_n))
+    if wsb < 0:
+        raise ShapeError(f"detect_pattern: a {ell} x {q} block grid is out of range")
+    # digest -> grouping -> verify queue back to back; [leader | eq (int32
+    # pairs)] come back in one read, the only synchronisation of the call
     dig = t.empty(2 * cells_n + (cells_n + 1) // 2, dtype=t.int64, device="cuda")
     h1, h2 = dig[:cells_n], dig[cells_n:2 * cells_n]
     nz = dig[2 * cells_n:].view(t.int32)[:cells_n]
+    out = t.zeros(cells_n + (cells_n + 1) // 2, dtype=t.int64, device="cuda")
+    lead_d = out[:cells_n]
+    eq_d = out[cells_n:].view(t.int32)[:cells_n]
+    cand_d = t.empty(cells_n, dtype=t.int64, device="cuda")
+    ws = _dev.workspace(wsb)
+    st = _dev.stream()
     N.call("bt_block_digest_f64", _dev.ptr(ad), cols, ell, q, m, n, float(tol), _dev.ptr(h1),
-           _dev.ptr(h2), _dev.ptr(nz), _dev.stream())
-    dig_h = dig.cpu().numpy()
-    keep = np.flatnonzero(dig_h[2 * cells_n:].view(np.int32)[:cells_n])
+           _dev.ptr(h2), _dev.ptr(nz), st)
+    N.call("bt_block_group", _dev.ptr(h1), _dev.ptr(h2), _dev.ptr(nz), cells_n, _dev.ptr(lead_d),
+           _dev.ptr(cand_d), _dev.ptr(ws), int(ws.numel()) * 8, st)
+    N.call("bt_block_match_f64", _dev.ptr(ad), cols, ell, q, m, n, _dev.ptr(cand_d), 0.0, 1,
+           _dev.ptr(eq_d), st)
+    out_h = out.cpu().numpy()
+    lead_h = out_h[:cells_n]
+    eq = out_h[cells_n:].view(np.int32)[:cells_n]
+    keep = np.flatnonzero(lead_h >= 0)
     if keep.size == 0:
         raise PatternMismatchError("matrix is identically zero; nothing to detect")
-    # group on (h1, h2): sort by both, mark key changes -> first-occurrence ids
-    k1, k2 = dig_h[:cells_n][keep], dig_h[cells_n:2 * cells_n][keep]
-    srt = np.lexsort((np.arange(len(keep)), k2, k1))
-    new = np.ones(len(keep), dtype=bool)
-    new[1:] = (k1[srt][1:] != k1[srt][:-1]) | (k2[srt][1:] != k2[srt][:-1])
-    gid = np.cumsum(new) - 1
-    first_of_gid = srt[new]                        # earliest kept index of each key
-    inv = np.empty(len(keep), dtype=np.int64)
-    inv[srt] = gid
-    first = first_of_gid
-    leader = keep[first][inv]                      # group's first cell, per kept cell
-    cand = np.full(cells_n, -1, dtype=np.int64)
-    cand[keep] = np.where(leader == keep, -1, leader)
-    eq = _cells_match(ad, ell, q, m, n, cand, 0.0, True)
-    bad = keep[(cand[keep] >= 0) & (eq[keep] == 0)]
+    leader = lead_h[keep]                          # group's first cell, per kept cell
+    bad = keep[(leader != keep) & (eq[keep] == 0)]
     group_of = np.full(cells_n, -1, dtype=np.int64)
     group_of[keep] = leader
     while bad.size:                                # digest collisions (never expected)
@@ -409,14 +414,19 @@ def detect_pattern(a, m: int, n: int, tol: float = 0.0):
         hit = rest[eq[rest] == 1]
         group_of[hit] = c0
         bad = rest[eq[rest] == 0]
-    # distinct blocks: leaders in row-major order, members sorted
-    order = np.argsort(group_of[keep], kind="stable")
-    gk = group_of[keep][order]
-    leaders, starts = np.unique(gk, return_index=True)
-    members = np.split(keep[order], starts[1:])
-    if tol == 0.0:
-        classes = members
-    else:
+    # distinct blocks: leaders in row-major order, members sorted.  A leader
+    # is a kept cell that leads itself; keep is ascending, so are the leaders.
+    gl = group_of[keep]
+    leaders = keep[gl == keep]
+    lut = np.empty(cells_n, dtype=np.int64)
+    lut[leaders] = np.arange(len(leaders))
+    cid = lut[gl]                                  # class index per kept cell
+    # stable sort by class index: numpy radix-sorts 16-bit keys
+    key = cid.astype(np.uint16) if len(leaders) <= 65536 else cid
+    flat = keep[np.argsort(key, kind="stable")]
+    counts = np.bincount(cid, minlength=len(leaders))
+    if tol != 0.0:
+        members = np.split(flat, np.cumsum(counts)[:-1])
         classes = []
         unclaimed = list(range(len(leaders)))
         while unclaimed:
@@ -431,21 +441,23 @@ def detect_pattern(a, m: int, n: int, tol: float = 0.0):
                 rest = [g for g in rest if eq[leaders[g]] != 1]
             classes.append(np.sort(np.concatenate([members[g] for g in claim])))
             unclaimed = rest
-    # one divmod / stack over every cell in class order, split into per-class views
-    flat = np.concatenate(classes).astype(np.int64, copy=False)
-    rc = np.stack(np.divmod(flat, q), axis=1)
-    bounds = np.cumsum([len(c) for c in classes])[:-1]
-    placements = tuple(np.ascontiguousarray(x) for x in np.split(rc, bounds))
+        flat = np.concatenate(classes).astype(np.int64, copy=False)
+        counts = np.array([len(c) for c in classes], dtype=np.int64)
+    # (row, col) of every cell in class order, split into per-class views
+    rc = np.empty((len(flat), 2), dtype=np.int64)
+    np.floor_divide(flat, q, out=rc[:, 0])
+    np.subtract(flat, rc[:, 0] * q, out=rc[:, 1])
+    placements = tuple(np.split(rc, np.cumsum(counts)[:-1]))
     _TRUSTED_PLACEMENTS["on"] = True
     try:
         pattern = BlockPattern(ell=ell, q=q, m=m, n=n, placements=placements,
-                               structure_class=classify_placements(placements, ell, q))
+                               structure_class=_classify_cells(rc, counts, ell, q))
     finally:
         _TRUSTED_PLACEMENTS["on"] = False
     if _dev.is_device(a):
         # every class's first occurrence, copied by one kernel into a (p, m, n)
         # stack whose slices are the contiguous representatives
-        first = np.array([int(c[0][0]) * q + int(c[0][1]) for c in placements], dtype=np.int64)
+        first = flat[np.concatenate([[0], np.cumsum(counts)[:-1]])]
         cd = _dev.to_device(first, dtype=t.int64)
         stack = _dev.empty((len(placements), m, n))
         N.call("bt_copy_cells_f64", _dev.ptr(ad), cols, _dev.ptr(cd), len(placements), q, m, n,

@@ -79,3 +79,70 @@ def test_detect_large_matches_oracle():
         assert np.array_equal(x, y)
     for x, y in zip(reps, reps_o):
         assert np.array_equal(x, y)
+
+
+def _group_dev(h1, h2, nz):
+    from paper_2105_01170_b200 import _dev
+    from paper_2105_01170_b200 import _native as N
+
+    cells = len(h1)
+    d1 = torch.from_numpy(h1.view(np.int64)).cuda()
+    d2 = torch.from_numpy(h2.view(np.int64)).cuda()
+    dz = torch.from_numpy(nz.astype(np.int32)).cuda()
+    lead = torch.empty(cells, dtype=torch.int64, device="cuda")
+    cand = torch.empty(cells, dtype=torch.int64, device="cuda")
+    ws = _dev.workspace(int(N.load().bt_block_group_ws_bytes(cells)))
+    N.call("bt_block_group", _dev.ptr(d1), _dev.ptr(d2), _dev.ptr(dz), cells, _dev.ptr(lead),
+           _dev.ptr(cand), _dev.ptr(ws), int(ws.numel()) * 8, _dev.stream())
+    return lead.cpu().numpy(), cand.cpu().numpy()
+
+
+@pytest.mark.parametrize("cells,distinct", [(1, 1), (7, 1), (1000, 3), (5000, 5000), (40000, 257)])
+def test_block_group_first_occurrence(cells, distinct):
+    """bt_block_group against a host dictionary: the leader of a kept cell is
+    the first kept cell with the same 128-bit key (keys that share h1 or h2
+    alone stay apart), skipped cells get -1, cand is -1 for leaders."""
+    rng = np.random.default_rng(cells + distinct)
+    pool1 = rng.integers(0, 2**63, size=distinct, dtype=np.int64).astype(np.uint64)
+    pool2 = rng.integers(0, 2**63, size=distinct, dtype=np.int64).astype(np.uint64)
+    if distinct >= 3:            # same h1 / different h2 and the other way round
+        pool1[1] = pool1[0]
+        pool2[2] = pool2[0]
+    pick = rng.integers(0, distinct, size=cells)
+    h1, h2 = pool1[pick].copy(), pool2[pick].copy()
+    nz = (rng.random(cells) > 0.2).astype(np.int32)
+    if cells == 1:
+        nz[:] = 1
+    lead, cand = _group_dev(h1, h2, nz)
+    seen, want = {}, np.full(cells, -1, dtype=np.int64)
+    for c in range(cells):
+        if nz[c]:
+            want[c] = seen.setdefault((int(h1[c]), int(h2[c])), c)
+    assert np.array_equal(lead, want)
+    assert np.array_equal(cand, np.where(want == np.arange(cells), -1, want))
+
+
+@pytest.mark.parametrize("m,n,ell,q", [(5, 3, 7, 9), (33, 6, 4, 5), (70, 34, 3, 3), (2, 2, 40, 40),
+                                       (64, 1030, 2, 2)])
+def test_detect_ragged_block_shapes_match_oracle(m, n, ell, q):
+    """Block shapes off the digest kernel's fast walk: odd widths (8-byte
+    accesses), rows that do not divide the CTA, ragged tails, a row wider
+    than the CTA -- placements and representatives against the oracle."""
+    rng = np.random.default_rng(m * 131 + n)
+    pool = [rng.standard_normal((m, n)) for _ in range(5)]
+    pool.append(np.zeros((m, n)))
+    pool.append(-pool[0])                       # sign flips only
+    swapped = pool[1].copy()
+    swapped[0, 0], swapped[-1, -1] = swapped[-1, -1], swapped[0, 0]
+    pool.append(swapped)                        # same multiset of entries
+    pick = rng.integers(0, len(pool), size=(ell, q))
+    a = np.block([[pool[pick[i, j]] for j in range(q)] for i in range(ell)])
+    got, reps = bt.detect_pattern(a, m, n)
+    pl, reps_o, cls = port.detect_pattern(a, m, n)
+    assert got.p == len(pl) and got.structure_class == cls
+    for x, y in zip(got.placements, pl):
+        assert np.array_equal(x, y)
+    for x, y in zip(reps, reps_o):
+        assert np.array_equal(x, y)
+    gd, rd = bt.detect_pattern(torch.from_numpy(a).cuda()[:, :], m, n)
+    assert all(np.array_equal(x, y) for x, y in zip(gd.placements, pl))
