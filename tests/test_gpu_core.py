@@ -229,6 +229,34 @@ def test_hosvd_golden(golden):
             np.testing.assert_allclose(rep.factors[k], z[f"h{n}_u{k}"], atol=1e-12)
 
 
+@pytest.mark.parametrize("shape,ranks", [((20, 130, 12), (20, 40, 12)), ((8, 12, 200), (5, 12, 30)),
+                                         ((120, 9, 110), (30, 9, 25))])
+def test_hosvd_side_stream_modes_match_serial_and_oracle(shape, ranks, monkeypatch):
+    """hosvd (decomp.py:237-259) with short and long modes mixed: the short
+    modes' first pass runs on a side stream beside the long modes; factors and
+    core are bit-identical to the serial order (BT_HOSVD_SIDE=0 path) and
+    match the oracle's HOSVD (numpy and device input)."""
+    from paper_2105_01170_b200 import decomp
+
+    rng = np.random.default_rng(sum(shape))
+    g = rng.standard_normal(ranks)
+    us = [np.linalg.qr(rng.standard_normal((n, r)))[0] for n, r in zip(shape, ranks)]
+    t = np.einsum("abc,ia,jb,kc->ijk", g, *us) + 1e-3 * rng.standard_normal(shape)
+    rep = bt.hosvd(t, list(ranks))
+    monkeypatch.setattr(decomp, "_SIDE_MODES", False)
+    ser = bt.hosvd(t, list(ranks))
+    monkeypatch.setattr(decomp, "_SIDE_MODES", True)
+    dev = bt.hosvd(torch.from_numpy(t).cuda(), list(ranks))
+    assert np.array_equal(rep.core, ser.core)
+    assert np.array_equal(dev.core.cpu().numpy(), ser.core)
+    for a, b in zip(rep.factors, ser.factors):
+        assert np.array_equal(a, b)
+    core_o, fac_o = port.hosvd(t, list(ranks))
+    np.testing.assert_allclose(rep.core, core_o, atol=1e-8)
+    for a, b in zip(rep.factors, fac_o):
+        np.testing.assert_allclose(a, b, atol=1e-8)
+
+
 @pytest.mark.parametrize("R", [3, 8, 16, 33, 64, 96])
 def test_pinv_sym_vs_numpy(R):
     """bt_pinv_sym_f64 (decomp.py:387 np.linalg.pinv of the Hadamard Gram):
