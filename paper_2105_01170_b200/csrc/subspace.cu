@@ -52,6 +52,15 @@ constexpr int SUB_MAX_ITERS = 10;
 // iteration, ~0.2 ms each, well under the tridiagonal solver's ~15 ms
 constexpr int SUB_MAX_ITERS_COLD = 32;
 constexpr int RR_ROUGH_SWEEPS = 4;
+// BT_RR_ROUGH=<n>: Jacobi sweeps of a cold block's first (rough) Rayleigh-Ritz (A/B switch)
+static int rr_rough_sweeps() {
+  static const int v = [] {
+    const char* e = std::getenv("BT_RR_ROUGH");
+    const int n = e ? std::atoi(e) : RR_ROUGH_SWEEPS;
+    return n >= 1 ? n : RR_ROUGH_SWEEPS;
+  }();
+  return v;
+}
 
 // BT_SUB_SKIP_RR=0: a Rayleigh-Ritz every iteration for cold blocks too
 bool no_skip_rr() {
@@ -531,7 +540,7 @@ extern "C" int bt_leading_subspace_f64(const double* g, int64_t n, int64_t need,
     // block and estimates the rate: a few Jacobi sweeps (its pairs are never
     // accepted, see below)
     const bool rough = skip_rr && it == 0 && start == nullptr;
-    BT_TRY(c.eig(hs, bq, w, sm, rough ? RR_ROUGH_SWEEPS : 60));       // descending
+    BT_TRY(c.eig(hs, bq, w, sm, rough ? rr_rough_sweeps() : 60));       // descending
     BT_TRY(c.gemm(gemm_args(n, bq, bq, q, bq, 1, sm, bq, 1, v)));    // V = Q S
     double* gv = c.at(p.off_gv);
     BT_TRY(c.gemm(gemm_args(n, bq, bq, gq, bq, 1, sm, bq, 1, gv)));  // G V = (G Q) S
