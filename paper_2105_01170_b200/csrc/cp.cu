@@ -314,7 +314,9 @@ __device__ __forceinline__ void tree_tma_issue(const CUtensorMap* xmap, const CU
     tma_load_2d(bs + q * 16 * TreeTma::BK, cmap, bar, n0 + 16 * q, k0, pol_c);
 }
 
-template <class T>
+// REDUCE = false: the plain product (store_p ignored, P always stored, no
+// mode-1 reduction): the last-mode tensor-times-matrix of tucker.cu
+template <class T, bool REDUCE = true>
 __global__ void __launch_bounds__(T::THREADS, T::MINB)
     tree_p_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap cmap,
                       BtGemmArgs g, const double* __restrict__ Bf, int64_t R,
@@ -436,12 +438,13 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         const int64_t r = n0 + wn0 + fj * 8 + 2 * tq + h;
         if (rv && r < g.N) {
           const double v = acc[fi][fj][h];
-          if (store_p) Pb[jrow * g.sCm + r] = v;
-          colsum[fj][h] = fma(v, __ldg(Bf + jrow * R + r), colsum[fj][h]);
+          if (!REDUCE || store_p) Pb[jrow * g.sCm + r] = v;
+          if (REDUCE) colsum[fj][h] = fma(v, __ldg(Bf + jrow * R + r), colsum[fj][h]);
         }
       }
     }
   }
+  if (!REDUCE) return;
 #pragma unroll
   for (int fj = 0; fj < T::FN; ++fj)
 #pragma unroll
@@ -2040,6 +2043,40 @@ int launch_tree_tma_t(const Plan& pl, const double* X, const double* C, const do
   return BT_OK;
 }
 
+// Y (rows x R) = X (rows x K, row-major) U (K x R, row-major) on the TMA tree
+// kernel without its reduction epilogue: the tensor-times-matrix over the
+// LAST mode (tucker.cu bt_ttm_f64; K and R even for the 16-byte TMA strides)
+int ttm_last_tma_impl(const double* x, int64_t rows, int64_t K, const double* u, int64_t R,
+                      double* y, cudaStream_t st) {
+  using T = TreeTma;
+  BtGemmArgs g{};
+  g.M = rows;
+  g.N = R;
+  g.Kin = K;
+  g.Kout = 1;
+  g.A = BtOperand{x, K, 0, 1, rows * K};
+  g.B = BtOperand{u, 1, 0, R, 0};
+  g.C = y;
+  g.sCm = R;
+  g.sCn = 1;
+  g.sCb = rows * R;
+  g.alpha = 1.0;
+  CUtensorMap xmap, cmap;
+  BT_TRY(bt_tma_map_f64_3d(&xmap, x, K, rows, 1, K, rows * K, T::BK, T::BM, 1));
+  BT_TRY(bt_tma_map_f64_2d(&cmap, u, R, K, R, 16, T::BK));
+  static bool attr = false;
+  if (!attr) {
+    BT_CUDA_CHECK(cudaFuncSetAttribute(tree_p_tma_kernel<T, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES));
+    attr = true;
+  }
+  dim3 grid(static_cast<unsigned>(bt_cdiv(rows, T::BM)), static_cast<unsigned>(bt_cdiv(R, T::BN)), 1);
+  tree_p_tma_kernel<T, false><<<grid, T::THREADS, T::SMEM_BYTES, st>>>(xmap, cmap, g, nullptr, R,
+                                                                       nullptr, 1, 1);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
 // (a 3-stage, 3-CTA/SM variant was tried: at the 168-register cap it spills
 // ~300 bytes per thread, so the 4-stage, 2-CTA configuration stays)
 int launch_tree_tma(const Plan& pl, const double* X, const double* C, const double* B, double* P,
@@ -2209,6 +2246,18 @@ int run_solve_finish(const Plan& pl, const CpState& s, const double* gbuf, int64
 }
 
 }  // namespace
+
+// tucker.cu: last-mode tensor-times-matrix on the TMA tree kernel (see
+// ttm_last_tma_impl); BT_E_VALUE when the operands do not meet TMA's
+// 16-byte address / stride rules (the caller takes the engine route)
+int bt_ttm_last_tma(const double* x, int64_t rows, int64_t K, const double* u, int64_t R, double* y,
+                    cudaStream_t st) {
+  if ((K & 1) || (R & 1) || rows < 1 || K < 1 || R < 1 || rows >= ((int64_t)1 << 31) ||
+      K >= ((int64_t)1 << 31) || rows * K >= ((int64_t)1 << 36) ||
+      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(u)) & 15u))
+    return BT_E_VALUE;
+  return ttm_last_tma_impl(x, rows, K, u, R, y, st);
+}
 
 // cp_mid.cu: the R <= 16 one-warp pinv of g0 o g1 (state: one double per mode, zero-initialised)
 int bt_cp_pinv_small(const double* g0, const double* g1, int R, double* vp, double* state,

@@ -141,6 +141,9 @@ extern "C" int64_t bt_ttm_ws_bytes(const int64_t* dims, int order, int mode, int
   return total * 8;
 }
 
+int bt_ttm_last_tma(const double* x, int64_t rows, int64_t K, const double* u, int64_t R, double* y,
+                    cudaStream_t st);
+
 extern "C" int bt_ttm_f64(const double* x, const int64_t* dims, int order, int mode,
                           const double* u, int64_t rows, int transpose, double* y, void* ws,
                           int64_t ws_bytes, void* stream) {
@@ -156,6 +159,15 @@ extern "C" int bt_ttm_f64(const double* x, const int64_t* dims, int order, int m
   if (ttm_tma && transpose && v.inner > 1 && rows > 0 && v.n > 0 && v.outer <= 65535) {
     const int rc = bt_gemm_at_tma_ex(x, v.inner, v.n * v.inner, u, rows, y, v.inner, rows * v.inner,
                                      v.inner, rows, v.n, v.outer, 1, bt_stream(stream));
+    if (rc != BT_E_VALUE) return rc;
+  }
+  // last mode, u given as U (n x rows) with more than 32 columns: the C5
+  // tree kernel without its reduction epilogue (TMA-staged X and U tiles,
+  // 128 x 64 output tiles); narrower outputs stay on the engine's 128 x 32 /
+  // 128 x 16 tile classes
+  static const bool last_tma = !(getenv("BT_TTM_LAST_TMA") && getenv("BT_TTM_LAST_TMA")[0] == '0');
+  if (ttm_tma && last_tma && transpose && v.inner == 1 && rows > 32 && v.n > 0 && v.outer > 0) {
+    const int rc = bt_ttm_last_tma(x, v.outer, v.n, u, rows, y, bt_stream(stream));
     if (rc != BT_E_VALUE) return rc;
   }
   int64_t batch = 1;

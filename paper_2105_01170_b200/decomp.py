@@ -338,6 +338,9 @@ def hooi(t, init: TuckerRep, sweeps: int, shared=None) -> TuckerRep:
     factors = [None if f is None else _dev.to_device(f) for f in init.factors]
     order = t.ndim
     last = None   # (mode, tensor projected on every other mode) of the latest update
+    if (_HOOI_SHARE and shared is not None and order == 3 and all(f is not None for f in factors)
+            and int(sweeps) >= 1):
+        return _hooi_shared3(t, xd, factors, int(sweeps), shared[0] - 1, shared[1] - 1)
     for _ in range(int(sweeps)):
         for k in range(order):
             if factors[k] is None or (shared is not None and k + 1 == shared[1]):
@@ -363,6 +366,38 @@ def hooi(t, init: TuckerRep, sweeps: int, shared=None) -> TuckerRep:
         core = _project_core(xd, factors)
     return TuckerRep(core=_dev.like_input(t, core),
                      factors=tuple(None if f is None else _dev.like_input(t, f) for f in factors))
+
+
+_HOOI_SHARE = os.environ.get("BT_HOOI_SHARE", "1") != "0"
+
+
+def _hooi_shared3(t, xd, factors, sweeps: int, a: int, b: int) -> TuckerRep:
+    """hooi for an order-3 tensor whose modes a and b share one basis U (the
+    third mode c has V).  The same updates as the generic loop -- U from the
+    tensor projected on (V, U), then V from the tensor projected on (U, U)
+    -- with the products ordered so that one full pass serves two updates:
+    T = X x_b U^T is taken once per sweep, right after U changes; the V-step
+    is T x_a U^T and the NEXT sweep's U-step is T x_c V^T.  One full-tensor
+    product per sweep instead of two (C3: 69 instead of 103 GFLOP)."""
+    c = 3 - a - b
+    ru, rv = int(factors[a].shape[1]), int(factors[c].shape[1])
+    tb = None     # X x_b U^T for the current U
+    y = None
+    for _ in range(sweeps):
+        if tb is None:
+            y = ttm_dev(xd, c + 1, factors[c], rv, transpose=True)
+            y = ttm_dev(y, b + 1, factors[b], ru, transpose=True)
+        else:
+            y = ttm_dev(tb, c + 1, factors[c], rv, transpose=True)
+        u = L.mode_basis_dev(y, a + 1, ru, start=factors[a])
+        factors[a] = u
+        factors[b] = u
+        tb = ttm_dev(xd, b + 1, u, ru, transpose=True)
+        y = ttm_dev(tb, a + 1, u, ru, transpose=True)
+        factors[c] = L.mode_basis_dev(y, c + 1, rv, start=factors[c])
+    core = ttm_dev(y, c + 1, factors[c], rv, transpose=True)
+    return TuckerRep(core=_dev.like_input(t, core),
+                     factors=tuple(_dev.like_input(t, f) for f in factors))
 
 
 # ---------------------------------------------------------------------------

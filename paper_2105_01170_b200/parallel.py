@@ -247,11 +247,17 @@ def hooi_sharded(ops, x_local, u, v, sweeps: int, p0: int, p1: int, allreduce, a
     [p0, p1) of V is summed across ranks (I x r2 x r13); V-step: the projected
     (r13, P_local, r13) slabs are all-gathered.  Returns (U, V, core)."""
     y = None
+    tb = None   # x_local x3 U^T for the current U: one full pass per sweep serves
+                # this sweep's V-step and the next sweep's U-step (decomp._hooi_shared3)
     for _ in range(int(sweeps)):
-        z = ops.ttm_t(ops.ttm_t(x_local, 2, ops.rows(v, p0, p1)), 3, u)
+        if tb is None:
+            z = ops.ttm_t(ops.ttm_t(x_local, 2, ops.rows(v, p0, p1)), 3, u)
+        else:
+            z = ops.ttm_t(tb, 2, ops.rows(v, p0, p1))
         allreduce(z)
         u = ops.mode_basis(z, 1, int(u.shape[1]), start=u)
-        y = allgather(ops.ttm_t(ops.ttm_t(x_local, 1, u), 3, u))
+        tb = ops.ttm_t(x_local, 3, u)
+        y = allgather(ops.ttm_t(tb, 1, u))
         v = ops.mode_basis(y, 2, int(v.shape[1]), start=v)
     if y is None:
         y = allgather(ops.ttm_t(ops.ttm_t(x_local, 1, u), 3, u))

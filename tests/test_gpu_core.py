@@ -64,6 +64,31 @@ def test_mode_multiply(dims, mode, rows):
                                atol=1e-12 * np.abs(got).max())
 
 
+@pytest.mark.parametrize("dims,rows", [((9, 31, 64), 34), ((5, 130, 48), 64), ((3, 77, 250), 70),
+                                       ((2, 300, 18), 96), ((4, 50, 33), 64), ((1, 1, 16), 40)])
+def test_last_mode_product_on_tree_kernel_matches_oracle_and_engine(dims, rows, monkeypatch):
+    """x x_3 u^T with u given as (K, rows), rows > 32 (tensor.py:75-90): the
+    TMA tree kernel without its reduction epilogue for even K and rows, the
+    cp.async engine otherwise (odd K: (4, 50, 33)) -- both against the
+    oracle, ragged row counts and a K below one k-tile included."""
+    from paper_2105_01170_b200.tensor import ttm_dev
+
+    rng = np.random.default_rng(sum(dims) + rows)
+    x = rng.standard_normal(dims)
+    u = rng.standard_normal((dims[2], rows))
+    want = port.mode_multiply(x, 3, u.T)
+    xd, ud = torch.from_numpy(x).cuda(), torch.from_numpy(u).cuda()
+    got = ttm_dev(xd, 3, ud, rows, transpose=True).cpu().numpy()
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-12 * np.abs(want).max())
+    # a (rows, K) factor (no transpose flag) and a view at an odd offset take the engine
+    got2 = ttm_dev(xd, 3, ud.t().contiguous(), rows).cpu().numpy()
+    np.testing.assert_allclose(got2, want, rtol=0, atol=1e-12 * np.abs(want).max())
+    pad = torch.zeros(x.size + 1, dtype=torch.float64, device="cuda")
+    pad[1:] = xd.reshape(-1)
+    got3 = ttm_dev(pad[1:].view(*dims), 3, ud, rows, transpose=True).cpu().numpy()
+    np.testing.assert_allclose(got3, want, rtol=0, atol=1e-12 * np.abs(want).max())
+
+
 # ---------------------------------------------------------------------------
 # K1 / K2 maps: bit-exact against the reference's golden vectors
 # ---------------------------------------------------------------------------
