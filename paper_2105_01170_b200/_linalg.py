@@ -282,24 +282,25 @@ def tsqr_dev(ad):
     return q, r
 
 
-def _qr_colscaled(z):
-    """(q, r) of a tall block with <= 32 columns by column-scaled CholeskyQR2:
-    Y = Z D (unit columns), two CholeskyQR passes, R = L2^T L1^T D^-1.
-    Accurate whenever Z's columns are already nearly orthogonal up to their
-    scales (a refinement step near convergence: Z = A^T V ~ W Sigma); None
-    when a pivot says otherwise (the caller takes TSQR)."""
+def _qr_colscaled_lazy(z):
+    """(q, r, chk) of a tall block with <= 32 columns by column-scaled
+    CholeskyQR2: Y = Z D (unit columns), two CholeskyQR passes,
+    R = L2^T L1^T D^-1.  Accurate whenever Z's columns are already nearly
+    orthogonal up to their scales (a refinement step near convergence:
+    Z = A^T V ~ W Sigma).  No host read: chk is a device vector [pivot flag
+    of pass 1, of pass 2, smallest column norm] and the factors are valid iff
+    it reads [0, 0, > 0] (_colscaled_ok).  None when the shape is not
+    eligible."""
     m, n = int(z.shape[0]), int(z.shape[1])
     if n > 32 or m < n:
         return None
+    t = _dev.torch()
     nrm = _dev.empty((n,))
     N.call("bt_col_norms_f64", _dev.ptr(z), m, n, _dev.ptr(nrm), _dev.stream())
-    hn = _dev.to_host(nrm)
-    if not np.all(hn > 0.0):
-        return None
-    dinv = _dev.to_device(1.0 / hn)
+    dinv = 1.0 / nrm
     y = _dev.empty((m, n))
     N.call("bt_diag_scale_f64", _dev.ptr(z), m, n, None, _dev.ptr(dinv), _dev.ptr(y), _dev.stream())
-    flags = _dev.torch().zeros(2, dtype=_dev.torch().int32, device="cuda")
+    flags = t.zeros(2, dtype=t.int32, device="cuda")
     r = None
     for it in range(2):
         g = gemm_dev(y, y, ta=True)
@@ -308,16 +309,38 @@ def _qr_colscaled(z):
                flags.data_ptr() + 4 * it, _dev.stream())
         y = gemm_dev(y, linvt)
         r = lt if r is None else gemm_dev(lt, r)
-    if int(_dev.to_host(flags).max()) != 0:
-        return None
     rr = _dev.empty((n, n))
     N.call("bt_diag_scale_f64", _dev.ptr(r), n, n, None, _dev.ptr(nrm), _dev.ptr(rr), _dev.stream())
-    return y, rr
+    chk = t.cat([flags.to(t.float64), nrm.min().reshape(1)])
+    return y, rr, chk
+
+
+def _colscaled_ok(chk3) -> bool:
+    return chk3[0] == 0.0 and chk3[1] == 0.0 and chk3[2] > 0.0
+
+
+def _qr_colscaled(z):
+    """_qr_colscaled_lazy with its check read here: (q, r), or None when a
+    pivot or a zero column rejects the block (the caller takes TSQR)."""
+    out = _qr_colscaled_lazy(z)
+    if out is None or not _colscaled_ok(_dev.to_host(out[2])):
+        return None
+    return out[0], out[1]
 
 
 def _qr_refine(z):
     out = _qr_colscaled(z)
     return out if out is not None else tsqr_dev(z)
+
+
+def _qr_refine_lazy(z):
+    """(q, r, chk): the column-scaled CholeskyQR2 with its check left on the
+    device, or TSQR (chk None) for shapes it does not take."""
+    out = _qr_colscaled_lazy(z)
+    if out is not None:
+        return out
+    q, r = tsqr_dev(z)
+    return q, r, None
 
 
 def svd_small_dev(m):
@@ -358,19 +381,38 @@ def _refine_basis_qr(xd, mode: int, r: int, start):
     v = start.contiguous()
     prev = None
     for _ in range(REFINE_MAX_STEPS):
-        qz, _ = _qr_refine(gemm_dev(a, v, ta=True))            # A^T V -> Q_Z
-        qw, rw = _qr_refine(gemm_dev(a, qz))                   # A Q_Z -> Q_W R_W
-        ur, sv, _ = svd_small_dev(rw)
-        v = gemm_dev(qw, ur)
-        N.call("bt_sign_fix_f64", _dev.ptr(v), n, r, _dev.stream())
-        sh = _dev.to_host(sv)
+        # one host read per step: the QR checks, the singular values and the
+        # change against the previous step come back together
+        zq = _qr_refine_lazy(gemm_dev(a, v, ta=True))          # A^T V -> Q_Z
+        wq = _qr_refine_lazy(gemm_dev(a, zq[0]))               # A Q_Z -> Q_W R_W
+        ur, sv, _ = svd_small_dev(wq[1])
+        vn = gemm_dev(wq[0], ur)
+        N.call("bt_sign_fix_f64", _dev.ptr(vn), n, r, _dev.stream())
+        parts = [c for c in (zq[2], wq[2]) if c is not None]
+        nchk = len(parts)
+        parts.append(sv)
+        if prev is not None:
+            parts.append((vn - prev).abs().amax(dim=0))
+        host = _dev.to_host(t.cat(parts))
+        if not all(_colscaled_ok(host[3 * i:3 * i + 3]) for i in range(nchk)):
+            # a CholeskyQR pivot rejected its block: redo the step on TSQR
+            qz, _ = _qr_refine(gemm_dev(a, v, ta=True))
+            qw, rw = _qr_refine(gemm_dev(a, qz))
+            ur, sv, _ = svd_small_dev(rw)
+            vn = gemm_dev(qw, ur)
+            N.call("bt_sign_fix_f64", _dev.ptr(vn), n, r, _dev.stream())
+            sh = _dev.to_host(sv)
+            diff = None if prev is None else _dev.to_host((vn - prev).abs().amax(dim=0))
+        else:
+            sh = host[3 * nchk:3 * nchk + r]
+            diff = None if prev is None else host[3 * nchk + r:]
+        v = vn
         if not sh[0] > 0:
             return None
-        if prev is not None:
+        if diff is not None:
             # a vector is resolved to ~eps sigma_1 / sigma_k: compare each with
             # the previous step at that accuracy (REFINE_TOL floor); the ones
             # below 1e-13 sigma_1 are noise either way
-            diff = _dev.to_host((v - prev).abs().amax(dim=0))
             live = sh > 1e-13 * sh[0]
             tol = np.maximum(REFINE_TOL, 64 * 2.2e-16 * sh[0] / np.maximum(sh, 1e-300))
             if np.all(diff[live] <= tol[live]):
