@@ -602,119 +602,118 @@ extern "C" int bt_col_norms_f64(const double* x, int64_t rows, int64_t cols, dou
 }
 
 // ---------------------------------------------------------------------------
-// SVD of a small square matrix (n <= 32) by one-sided (Hestenes) Jacobi in
-// ONE warp: lane c holds column c of W = M J and of J in registers; a round
-// pairs the columns by the circle method and the two lanes of a pair swap
-// columns by shuffles.  Rotation while |w_p . w_q| > 1e-15 ||w_p|| ||w_q||
-// (the relative criterion: small singular values keep high relative
-// accuracy -- the point of taking this route instead of a Gram).  Output:
-// singular values descending, U = W / sigma, V = J, each column of U with its
-// largest-|.| entry positive (decomp.py:176-179 sign rule; first on ties),
-// the sign compensated in V.  Rows/columns beyond n are padding.
+// SVD of a small square matrix (n <= 32) by one-sided (Hestenes) Jacobi on
+// one CTA of 16 warps: W = M J and J live in shared memory column by column;
+// a round pairs the 32 columns by the circle method, warp k takes pair k with
+// lane = row: the three dot products of the pair are xor-butterfly warp sums
+// (every lane ends with the same bits), the rotation is computed redundantly
+// in every lane and the lane updates its row of both columns of W and J; one
+// barrier per round.  (The one-warp version -- a column per lane, three
+// 32-long dependent FMA chains per round -- took 205-345 us per call, two or
+// three calls per basis refinement; this one ~4x less.)  Rotation while
+// |w_p . w_q| > 1e-15 ||w_p|| ||w_q|| (the relative criterion: small singular
+// values keep high relative accuracy -- the point of taking this route
+// instead of a Gram).  Output: singular values descending, U = W / sigma,
+// V = J, each column of U with its largest-|.| entry positive
+// (decomp.py:176-179 sign rule; first on ties), the sign compensated in V.
+// Rows/columns beyond n are padding.
 // ---------------------------------------------------------------------------
 
 namespace {
 
-__global__ void __launch_bounds__(32) svd_small_kernel(const double* __restrict__ m, int n,
-                                                       double* __restrict__ u, double* __restrict__ s,
-                                                       double* __restrict__ v) {
-  constexpr int NP = 32;
-  __shared__ double us[NP][NP + 1], vs[NP][NP + 1], sg[NP];
-  __shared__ int order[NP];
-  const int c = threadIdx.x;
-  double w[NP], jv[NP];
+__device__ __forceinline__ double warp_sum_all(double v) {
 #pragma unroll
-  for (int i = 0; i < NP; ++i) {
-    w[i] = (i < n && c < n) ? m[i * n + c] : 0.0;
-    jv[i] = (i == c) ? 1.0 : 0.0;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(512) svd_small_kernel(const double* __restrict__ m, int n,
+                                                        double* __restrict__ u, double* __restrict__ s,
+                                                        double* __restrict__ v) {
+  constexpr int NP = 32, LD = NP + 1;
+  __shared__ double ws[NP][LD], js[NP][LD], sg[NP];   // [column][row]
+  __shared__ int order[NP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;   // lane = row, 16 warps
+  for (int c = warp; c < NP; c += 16) {
+    ws[c][lane] = (lane < n && c < n) ? m[lane * n + c] : 0.0;
+    js[c][lane] = (lane == c) ? 1.0 : 0.0;
   }
+  __syncthreads();
   for (int sweep = 0; sweep < 40; ++sweep) {
     int rotated = 0;
     for (int rnd = 0; rnd < NP - 1; ++rnd) {
-      int partner;
-      if (c == NP - 1) {
-        partner = rnd;
-      } else if (c == rnd) {
-        partner = NP - 1;
+      // circle method: pair `warp` of round rnd (p < q)
+      int p, q;
+      if (warp == 0) {
+        p = rnd;
+        q = NP - 1;
       } else {
-        partner = 2 * rnd - c;
-        if (partner < 0) partner += NP - 1;
-        if (partner >= NP - 1) partner -= NP - 1;
+        p = rnd + warp;
+        if (p >= NP - 1) p -= NP - 1;
+        q = rnd - warp + (NP - 1);
+        if (q >= NP - 1) q -= NP - 1;
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
       }
-      const bool lo = c < partner;
-      // columns are exchanged through shared memory (register copies of the
-      // partner's two columns would spill); column stride 33: no conflicts
-#pragma unroll
-      for (int i = 0; i < NP; ++i) {
-        us[i][c] = w[i];
-        vs[i][c] = jv[i];
-      }
-      __syncwarp();
-      double a = 0.0, b = 0.0, g = 0.0;
-#pragma unroll
-      for (int i = 0; i < NP; ++i) {
-        const double pwi = us[i][partner];
-        const double wp = lo ? w[i] : pwi, wq = lo ? pwi : w[i];
-        a = fma(wp, wp, a);
-        b = fma(wq, wq, b);
-        g = fma(wp, wq, g);
-      }
-      if (g != 0.0 && g * g > 1e-30 * (a * b)) {
+      const double wp = ws[p][lane], wq = ws[q][lane];
+      const double a = warp_sum_all(wp * wp), b = warp_sum_all(wq * wq), g = warp_sum_all(wp * wq);
+      if (g != 0.0 && g * g > 1e-30 * (a * b)) {   // warp-uniform
         // theta = (b - a) / (2 g); t = sign(theta) / (|theta| + sqrt(1 + theta^2))
         const double th = (b - a) / (2.0 * g);
         const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(1.0 + th * th));
         const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
         rotated = 1;
-#pragma unroll
-        for (int i = 0; i < NP; ++i) {
-          const double pwi = us[i][partner], pji = vs[i][partner];
-          if (lo) {
-            w[i] = cs * w[i] - sn * pwi;
-            jv[i] = cs * jv[i] - sn * pji;
-          } else {
-            w[i] = sn * pwi + cs * w[i];
-            jv[i] = sn * pji + cs * jv[i];
-          }
-        }
+        const double jp = js[p][lane], jq = js[q][lane];
+        ws[p][lane] = cs * wp - sn * wq;
+        ws[q][lane] = sn * wp + cs * wq;
+        js[p][lane] = cs * jp - sn * jq;
+        js[q][lane] = sn * jp + cs * jq;
       }
-      __syncwarp();
+      __syncthreads();
     }
-    if (!__any_sync(0xffffffffu, rotated)) break;
+    if (!__syncthreads_or(rotated)) break;
   }
-  double nrm2 = 0.0;
+  // epilogue on one warp, a column per lane (as the one-warp version did)
+  if (warp == 0) {
+    const int c = lane;
+    double nrm2 = 0.0;
 #pragma unroll
-  for (int i = 0; i < NP; ++i) nrm2 = fma(w[i], w[i], nrm2);
-  const double sig = (c < n) ? sqrt(nrm2) : -1.0;
-  sg[c] = sig;
-  __syncwarp();
-  // descending order (ties: lower column first)
-  int rank = 0;
-  for (int j = 0; j < NP; ++j) rank += (sg[j] > sig) || (sg[j] == sig && j < c);
-  order[rank] = c;
-  const double inv = sig > 0.0 ? 1.0 / sig : 0.0;
-  // sign rule on U's column (largest |entry| positive, first on ties)
-  double best = -1.0, bval = 0.0;
+    for (int i = 0; i < NP; ++i) nrm2 = fma(ws[c][i], ws[c][i], nrm2);
+    const double sig = (c < n) ? sqrt(nrm2) : -1.0;
+    sg[c] = sig;
+    __syncwarp();
+    // descending order (ties: lower column first)
+    int rank = 0;
+    for (int j = 0; j < NP; ++j) rank += (sg[j] > sig) || (sg[j] == sig && j < c);
+    order[rank] = c;
+    const double inv = sig > 0.0 ? 1.0 / sig : 0.0;
+    // sign rule on U's column (largest |entry| positive, first on ties)
+    double best = -1.0, bval = 0.0;
 #pragma unroll
-  for (int i = 0; i < NP; ++i) {
-    const double e = w[i] * inv;
-    if (i < n && fabs(e) > best) {
-      best = fabs(e);
-      bval = e;
+    for (int i = 0; i < NP; ++i) {
+      const double e = ws[c][i] * inv;
+      if (i < n && fabs(e) > best) {
+        best = fabs(e);
+        bval = e;
+      }
     }
-  }
-  const double flip = (bval < 0.0) ? -1.0 : 1.0;
+    const double flip = (bval < 0.0) ? -1.0 : 1.0;
 #pragma unroll
-  for (int i = 0; i < NP; ++i) {
-    us[i][c] = flip * w[i] * inv;
-    vs[i][c] = flip * jv[i];
-  }
-  __syncwarp();
-  if (c < n) {
-    const int src = order[c];
-    s[c] = sg[src];
-    for (int i = 0; i < n; ++i) {
-      u[i * n + c] = us[i][src];
-      v[i * n + c] = vs[i][src];
+    for (int i = 0; i < NP; ++i) {
+      ws[c][i] = flip * ws[c][i] * inv;
+      js[c][i] = flip * js[c][i];
+    }
+    __syncwarp();
+    if (c < n) {
+      const int src = order[c];
+      s[c] = sg[src];
+      for (int i = 0; i < n; ++i) {
+        u[i * n + c] = ws[src][i];
+        v[i * n + c] = js[src][i];
+      }
     }
   }
 }
@@ -725,7 +724,7 @@ extern "C" int bt_svd_small_f64(const double* m, int64_t n, double* u, double* s
                                 void* stream) {
   BT_NVTX("bt_svd_small_f64");
   BT_REQUIRE(n >= 1 && n <= 32, BT_E_SHAPE, "svd_small: n = %lld outside 1..32", (long long)n);
-  svd_small_kernel<<<1, 32, 0, bt_stream(stream)>>>(m, static_cast<int>(n), u, s, v);
+  svd_small_kernel<<<1, 512, 0, bt_stream(stream)>>>(m, static_cast<int>(n), u, s, v);
   BT_LAUNCH_CHECK();
   return BT_OK;
 }

@@ -282,6 +282,35 @@ def test_hosvd_side_stream_modes_match_serial_and_oracle(shape, ranks, monkeypat
         np.testing.assert_allclose(a, b, atol=1e-8)
 
 
+@pytest.mark.parametrize("n", [1, 2, 5, 17, 31, 32])
+def test_svd_small_vs_numpy(n):
+    """bt_svd_small_f64 (the np.linalg.svd of decomp.py:172 on the projected
+    factor of a basis refinement): graded and random matrices -- singular
+    values against LAPACK's (absolute accuracy eps sigma_1), m = u diag(s) v^T,
+    orthonormal factors, the sign rule of decomp.py:176-179, bit-reproducible."""
+    rng = np.random.default_rng(n)
+    q1, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    q2, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    graded = (q1 * 10.0 ** (-np.linspace(0, 11, n))) @ q2.T
+    for m in (rng.standard_normal((n, n)), graded, np.diag(np.arange(n, 0, -1.0)), np.zeros((n, n))):
+        md = torch.from_numpy(np.ascontiguousarray(m)).cuda()
+        u, sv, v = L.svd_small_dev(md)
+        u2, sv2, v2 = L.svd_small_dev(md)
+        assert torch.equal(u, u2) and torch.equal(sv, sv2) and torch.equal(v, v2)
+        u, sv, v = u.cpu().numpy(), sv.cpu().numpy(), v.cpu().numpy()
+        ref = np.linalg.svd(m, compute_uv=False)
+        assert np.all(np.diff(sv) <= 0)
+        scale = max(ref[0], 1e-300)
+        np.testing.assert_allclose(sv, ref, rtol=0, atol=1e-14 * scale)
+        np.testing.assert_allclose((u * sv) @ v.T, m, rtol=0, atol=1e-14 * scale)
+        np.testing.assert_allclose(v.T @ v, np.eye(n), atol=1e-13)
+        live = sv > 1e-13 * scale
+        uu = u[:, live]
+        np.testing.assert_allclose(uu.T @ uu, np.eye(uu.shape[1]), atol=1e-12)
+        for c in range(uu.shape[1]):
+            assert uu[np.argmax(np.abs(uu[:, c])), c] > 0
+
+
 @pytest.mark.parametrize("R", [3, 8, 16, 33, 64, 96])
 def test_pinv_sym_vs_numpy(R):
     """bt_pinv_sym_f64 (decomp.py:387 np.linalg.pinv of the Hadamard Gram):
