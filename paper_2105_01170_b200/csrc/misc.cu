@@ -1,5 +1,6 @@
 // Deterministic reductions and the FP64 peak microbenchmarks.
 #include "bt_common.cuh"
+#include "jacobi.cuh"  // jacobi_rotation
 
 // ---------------------------------------------------------------------------
 // sum of squares (fro_norm, tensor.py:107-109) -- two-pass fixed tree
@@ -662,9 +663,18 @@ __global__ void __launch_bounds__(512) svd_small_kernel(const double* __restrict
       const double a = warp_sum_all(wp * wp), b = warp_sum_all(wq * wq), g = warp_sum_all(wp * wq);
       if (g != 0.0 && g * g > 1e-30 * (a * b)) {   // warp-uniform
         // theta = (b - a) / (2 g); t = sign(theta) / (|theta| + sqrt(1 + theta^2))
-        const double th = (b - a) / (2.0 * g);
-        const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(1.0 + th * th));
-        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        // from refined rcp / rsqrt (jacobi.cuh, ~1 ulp): the IEEE divisions
+        // and square roots were ~1500 of the round's ~1700 dependent cycles;
+        // the exact formula only where 1 / (2 g) would overflow the approximation
+        double cs, sn;
+        if (fabs(g) > 1e-290) {
+          jacobi_rotation(a, b, g, cs, sn);
+        } else {
+          const double th = (b - a) / (2.0 * g);
+          const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(1.0 + th * th));
+          cs = 1.0 / sqrt(1.0 + t * t);
+          sn = cs * t;
+        }
         rotated = 1;
         const double jp = js[p][lane], jq = js[q][lane];
         ws[p][lane] = cs * wp - sn * wq;
