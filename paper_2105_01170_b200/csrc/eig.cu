@@ -379,7 +379,13 @@ struct EigPlan {
 EigPlan eig_plan(int64_t n) {
   EigPlan p;
   p.n = n;
-  p.small = n <= SMALL_N;
+  // BT_EIG_SMALL_N=<n> (<= 96): sizes above n take the multi-CTA block-Jacobi path (A/B switch)
+  static const int small_n = [] {
+    const char* e = getenv("BT_EIG_SMALL_N");
+    const int v = e ? atoi(e) : SMALL_N;
+    return (v >= 2 && v <= SMALL_N) ? v : SMALL_N;
+  }();
+  p.small = n <= small_n;
   p.np = p.small ? n + (n & 1) : bt_cdiv(n, EP) * EP;
   int64_t o = 0;
   auto take = [&](int64_t k) {
